@@ -1,0 +1,221 @@
+/*
+ * hdg_b200.h — C ABI of the B200-native element-local HDG engine.
+ *
+ * Drop-in boundary for the element-local half of the reference HDG library
+ * (/root/reference/proj, namespace hdg). Every entry point below names the
+ * reference interface it replaces (file:line). Conventions:
+ *   - plain pointers and sizes, no C++ or torch types; no exceptions cross;
+ *   - every call returns HDG_OK or an HDG_E* status; hdg_b200_last_error()
+ *     holds the message of the calling thread's last failure;
+ *   - d_* arguments are caller-owned DEVICE buffers, h_* are HOST buffers;
+ *   - arrays keep the reference (Eigen, column-major) layouts: an Nelt x c
+ *     matrix stores entry (K, j) at j*Nelt + K; Batch3 slice K of an r x c
+ *     batch starts at K*r*c (proj/include/hdg/batch.hpp:14-38);
+ *   - indices are 0-based, permutation codes 1..6 (proj/include/hdg/mesh.hpp:6-9);
+ *   - device work is stream-ordered on the context's stream.
+ */
+#ifndef HDG_B200_H
+#define HDG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HDG_B200_ABI_VERSION 1
+
+/* status codes */
+#define HDG_OK 0
+#define HDG_ESINGULAR 1 /* singular local system; *bad_element = lowest index (LocalSolverError, local_solver.hpp:45-49) */
+#define HDG_EINVAL 2    /* bad argument (std::invalid_argument in the reference) */
+#define HDG_ECUDA 3     /* CUDA runtime failure */
+#define HDG_ENCCL 4     /* NCCL failure */
+#define HDG_EMESH 5     /* MeshError (mesh.hpp:75-78) */
+#define HDG_ESTATE 6    /* call order (e.g. no degree set) */
+
+/* boundary classifiers for generated box meshes (mesh.cpp:173-183) */
+#define HDG_BC_ALL_DIRICHLET 0
+#define HDG_BC_DIRICHLET_TOP_BOTTOM 1
+#define HDG_BC_DIRICHLET_X 2 /* |nu_x| > 0.5 */
+
+/* ---------------------------------------------------------------- fields
+ * Coefficient fields replace the reference ScalarField callbacks
+ * (proj/include/hdg/coefficient.hpp:13-14): either a constant, samples at the
+ * physical quadrature nodes (what the callback returns, nq x nelt, element's
+ * nodes contiguous, device memory), or a postfix program over (x,y,z) the
+ * kernels evaluate at each node.                                           */
+#define HDG_FIELD_CONST 0
+#define HDG_FIELD_SAMPLED 1
+#define HDG_FIELD_PROGRAM 2
+#define HDG_FIELD_MAX_OPS 128
+#define HDG_FIELD_MAX_CONSTS 48
+#define HDG_FIELD_MAX_STACK 16
+enum {
+  HDG_OP_X = 0, HDG_OP_Y, HDG_OP_Z, HDG_OP_CONST, HDG_OP_ADD, HDG_OP_SUB, HDG_OP_MUL,
+  HDG_OP_DIV, HDG_OP_NEG, HDG_OP_SIN, HDG_OP_COS, HDG_OP_EXP, HDG_OP_SQRT, HDG_OP_ABS,
+  HDG_OP_LT, HDG_OP_POW
+};
+typedef struct {
+  int kind;               /* HDG_FIELD_* */
+  double value;           /* CONST */
+  const double* samples;  /* SAMPLED: device, nq x nelt */
+  const int* ops;         /* PROGRAM: host, nops opcodes (copied at call) */
+  int nops;
+  const double* consts;   /* PROGRAM: host, nconst literals in order of HDG_OP_CONST */
+  int nconst;
+} hdg_field;
+
+typedef struct hdg_ctx hdg_ctx;   /* device, stream, reference tables */
+typedef struct hdg_mesh hdg_mesh; /* host mesh (setup layer) */
+
+const char* hdg_b200_version(void);
+const char* hdg_b200_last_error(void);
+
+/* ------------------------------------------------------------ host mesh
+ * Replaces box_mesh (mesh.cpp:185-253) and expand (mesh.cpp:74-171): the
+ * face numbering (Dirichlet rows, Neumann rows, then interior faces in
+ * sorted-vertex-triple order) is bit-exact with the reference.            */
+int hdg_b200_mesh_box(int nx, int ny, int nz, int bc_rule, double perturb_frac, uint64_t seed,
+                      double keep_plane_z, hdg_mesh** out);
+int hdg_b200_mesh_create(int nver, const double* h_coords, int nelt, const int* h_elements,
+                         int ndir, const int* h_dirichlet, int nneu, const int* h_neumann,
+                         hdg_mesh** out);
+int hdg_b200_mesh_expand(hdg_mesh* m);
+/* dims: nver, nelt, nfc, ndir, nneu, expanded */
+int hdg_b200_mesh_dims(const hdg_mesh* m, int64_t dims[6]);
+#define HDG_MESH_COORDS 0    /* double nver x 3 */
+#define HDG_MESH_ELEMENTS 1  /* int nelt x 4 */
+#define HDG_MESH_DIRICHLET 2 /* int ndir x 3 */
+#define HDG_MESH_NEUMANN 3   /* int nneu x 3 */
+#define HDG_MESH_FACES 4     /* int nfc x 3 */
+#define HDG_MESH_FACETYPE 5  /* uint8 nfc (0 interior, 1 Dirichlet, 2 Neumann) */
+#define HDG_MESH_FACEBYELE 6 /* int nelt x 4 */
+int hdg_b200_mesh_copy(const hdg_mesh* m, int what, void* h_dst);
+void hdg_b200_mesh_free(hdg_mesh* m);
+
+/* Skeleton sparsity (global_system.cpp:31-56): per face the sorted faces it
+ * couples to, and per element the slot of each (l1,l2) pair in row-face l1's
+ * list. nnbr_total = sum of list lengths; nnz = nnbr_total * d2 * d2.      */
+int hdg_b200_pattern_dims(const hdg_mesh* m, int64_t* nnbr_total);
+int hdg_b200_pattern_build(const hdg_mesh* m, int64_t* h_facebase /* nfc+1 */,
+                           int* h_nbr /* nfc x 8 row-major, -1 padded */,
+                           uint8_t* h_slot /* nelt x 16 */);
+
+/* ------------------------------------------------------------- context */
+int hdg_b200_create(int device, void* cuda_stream, hdg_ctx** out);
+void hdg_b200_destroy(hdg_ctx* ctx);
+int hdg_b200_set_stream(hdg_ctx* ctx, void* cuda_stream);
+/* Tables for degree k on tet_rule(tet_deg) / tri_rule(tri_deg)
+ * (quadrature.cpp:43-90, basis.cpp:151-165; study.cpp:13-15 uses 2k+2).   */
+int hdg_b200_set_degree(hdg_ctx* ctx, int k, int tet_deg, int tri_deg);
+/* Degree k+1 tables on tet_rule(tet_deg) for postprocess_star (study.cpp:33-34). */
+int hdg_b200_set_postprocess_rule(hdg_ctx* ctx, int tet_deg);
+/* dims: k, d3, d2, nq, nqd, factor_doubles_per_element, nq_post, d3_post */
+int hdg_b200_dims(const hdg_ctx* ctx, int64_t dims[8]);
+#define HDG_TABLE_TET_BARY 0
+#define HDG_TABLE_TET_W 1
+#define HDG_TABLE_P 2
+#define HDG_TABLE_CHAT 3
+#define HDG_TABLE_WLM 4
+#define HDG_TABLE_PP 5
+#define HDG_TABLE_DD 6
+#define HDG_TABLE_TRI_BARY 7
+#define HDG_TABLE_TRI_W 8
+int hdg_b200_copy_table(const hdg_ctx* ctx, int which, double* h_dst, int64_t capacity);
+/* Same tables built on the host only (no device needed). */
+int hdg_b200_host_table(int k, int tet_deg, int tri_deg, int which, double* h_dst, int64_t capacity);
+
+/* ------------------------------------------------------ K1: geometry
+ * Replaces geometry (mesh.cpp:43-66), the per-element part of expand
+ * (mesh.cpp:153-169), piola_coefficients (element_matrices.cpp:48-57),
+ * normal_weights (:59-64) and StabilizationField::scaled (:31-36).        */
+typedef struct {
+  double* volume;  /* nelt */
+  double* piola;   /* nelt x 9: a_xx a_xy a_xz a_yx ... (detB * B^{-T}) */
+  double* normals; /* nelt x 12: outward n_l, |n_l| = |e_l| */
+  int* perm;       /* nelt x 4, 1..6 */
+  double* T;       /* nelt x 4: tau(K,l) * |e_{f(K,l)}| */
+  double* verts;   /* nelt x 12: vertex coordinates x1..x4, y1..y4, z1..z4 */
+  double* area;    /* nfc */
+} hdg_geometry;
+int hdg_b200_geometry(hdg_ctx* ctx, int nver, int nelt, int nfc, const double* d_coords,
+                      const int* d_elements, const int* d_faces, const int* d_facebyele,
+                      const double* d_tau /* nelt x 4 or NULL */, double tau_const,
+                      hdg_geometry* g);
+/* tau(K,l) = 1 + |beta(x_e) . nu_{K,l}| at face centroids (config C4 upwinding). */
+int hdg_b200_upwind_tau(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_field bx,
+                        hdg_field by, hdg_field bz, double* d_tau);
+
+/* --------------------------------------------- K2+K3: build + condense
+ * Replaces build_element_matrices (element_matrices.cpp:282-309) ->
+ * local_blocks (local_solver.cpp:124-126) -> condense (local_solver.cpp:71-100)
+ * as one call returning the same CondensedSystem: C (m x m x nelt Batch3) and
+ * Cf (m x nelt), m = 4*d2. d_factors (nullable) receives the per-element
+ * recovery cache used by hdg_b200_recover (dims[5] doubles per element).
+ * d_work: scratch of hdg_b200_work_size() bytes.                           */
+int64_t hdg_b200_work_size(const hdg_ctx* ctx, int nelt);
+int hdg_b200_build_condense(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_field kappa,
+                            hdg_field c, hdg_field f, double* d_C, double* d_Cf,
+                            double* d_factors, void* d_work, int64_t* bad_element);
+
+/* ------------------------------------------ K5: gather + local recover
+ * Replaces gather_traces (global_system.cpp:167-175) + local_recover
+ * (local_solver.cpp:102-135): [q;u] = A1^{-1}(Af - A2 lambda_K) with lambda_K
+ * gathered from the skeleton vector uhat (dof = face*d2 + i). Uses the cache
+ * written by build_condense. Outputs d3 x nelt each.                         */
+int hdg_b200_recover(hdg_ctx* ctx, int nelt, const hdg_geometry* g, const int* d_facebyele,
+                     const double* d_factors, const double* d_uhat, double* d_qx, double* d_qy,
+                     double* d_qz, double* d_u);
+
+/* ------------------------------------------------------ K4: scatter
+ * Replaces assemble (global_system.cpp:31-56): CSR values of H (pattern from
+ * hdg_b200_pattern_fill; structurally symmetric so CSR == Eigen's CSC
+ * pattern) and b += Cf. d_vals and d_b must be zeroed by the caller.       */
+int hdg_b200_pattern_fill(hdg_ctx* ctx, int nfc, int d2, const int64_t* d_facebase,
+                          const int* d_nbr, int64_t* d_rowptr, int* d_colidx);
+int hdg_b200_scatter(hdg_ctx* ctx, int nelt, int d2, const int* d_facebyele,
+                     const uint8_t* d_slot, const int64_t* d_facebase, const double* d_C,
+                     const double* d_Cf, double* d_vals, double* d_b);
+
+/* --------------------------------------------------- K6: postprocess
+ * Replaces postprocess_star (postprocess.cpp:33-74) with stiffness_matrices
+ * (element_matrices.cpp:258-280): u* of degree k+1, d3(k+1) x nelt.        */
+int hdg_b200_postprocess(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_field kappa,
+                         const double* d_qx, const double* d_qy, const double* d_qz,
+                         const double* d_u, double* d_ustar);
+
+/* --------------------------------------------- K7: convection block
+ * Replaces convection_bilinear_matrices (convdiff.cpp:5-28): vol d3 x d3,
+ * dp 4d2 x d3, dd 4d2 x 4d2 per element (Batch3 layout).                   */
+int hdg_b200_convection_block(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_field bx,
+                              hdg_field by, hdg_field bz, double* d_vol, double* d_dp,
+                              double* d_dd);
+
+/* ----------------------------------- materialised element matrices
+ * The ElementMatrixSet of build_element_matrices (element_matrices.hpp:86-93)
+ * in Batch3 layout, for matrix-level parity; any output may be NULL.       */
+typedef struct {
+  double *Mkinv, *Mc, *Cx, *Cy, *Cz, *tauPP; /* d3 x d3 x nelt */
+  double *tauDP, *nxDP, *nyDP, *nzDP;        /* 4d2 x d3 x nelt */
+  double* tauDD;                             /* 4d2 x 4d2 x nelt */
+  double* fvec;                              /* d3 x nelt */
+} hdg_element_matrices;
+int hdg_b200_element_matrices(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_field kappa,
+                              hdg_field c, hdg_field f, hdg_element_matrices* out);
+
+/* Physical images of the volume quadrature nodes (quad_points_physical,
+ * element_matrices.cpp:66-70), nq x nelt each — for callers that sample
+ * their own callbacks into HDG_FIELD_SAMPLED arrays. which: 0 = degree-k
+ * rule, 1 = postprocess rule.                                              */
+int hdg_b200_quad_points(hdg_ctx* ctx, int nelt, const hdg_geometry* g, int which, double* d_X,
+                         double* d_Y, double* d_Z);
+
+/* Block until the context's stream is idle and report any deferred error. */
+int hdg_b200_synchronize(hdg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDG_B200_H */

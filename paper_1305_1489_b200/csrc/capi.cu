@@ -1,0 +1,698 @@
+// C ABI of the engine (include/hdg_b200.h): context, table upload, launch
+// dispatch over the polynomial degree, host mesh setup. No exceptions cross
+// the ABI; every failure becomes an HDG_E* status plus a thread-local message.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hdg_b200.h"
+#include "dev_common.cuh"
+#include "host_internal.hpp"
+#include "kernels_local.cuh"
+#include "kernels_misc.cuh"
+#include "kernels_post.cuh"
+
+using namespace hdgb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct HdgError {
+  int code;
+  std::string msg;
+};
+
+#define CUDA_OK(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw HdgError{HDG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};    \
+  } while (0)
+
+template <class F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return HDG_OK;
+  } catch (const HdgError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const MeshError& e) {
+    g_err = e.what();
+    return HDG_EMESH;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return HDG_EINVAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HDG_EINVAL;
+  }
+}
+
+void require(bool cond, int code, const std::string& msg) {
+  if (!cond) throw HdgError{code, msg};
+}
+
+// Device copy of one degree's tables (one allocation, offsets into it).
+struct TabSet {
+  bool ready = false;
+  HostTables host;
+  DevTab dev{};
+  double* buf = nullptr;
+  size_t doubles = 0;
+};
+
+// DMMA fragment order: fragment (mt, kk) = 32 doubles, lane -> A(mt*8 + lane/4, kk*4 + lane%4).
+std::vector<double> to_fragments(const std::vector<double>& A, int rows, int cols) {
+  std::vector<double> out(size_t(rows) * cols, 0.0);
+  const int kc = cols / 4;
+  for (int mt = 0; mt < rows / 8; ++mt)
+    for (int kk = 0; kk < kc; ++kk)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int r = mt * 8 + lane / 4, c = kk * 4 + lane % 4;
+        out[(size_t(mt) * kc + kk) * 32 + lane] = A[size_t(r) * cols + c];  // A row-major
+      }
+  return out;
+}
+
+void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
+  if (ts.buf) { cudaFree(ts.buf); ts.buf = nullptr; }
+  ts.ready = false;
+  ts.host = build_host_tables(k, tet_deg, tri_deg);
+  const HostTables& h = ts.host;
+  const int d3 = h.d3, d2 = h.d2, nq = h.nq, nqd = h.nqd;
+  const int nqp = round_up(nq, 4), nsym = d3 * (d3 + 1) / 2, nsymp = round_up(nsym, 8), d3p = round_up(d3, 8);
+  // Asym: rows = sym pairs (i >= j), cols = nqp node columns + 4 PP columns (row-major)
+  std::vector<double> Asym(size_t(nsymp) * (nqp + 4), 0.0), Af(size_t(d3p) * nqp, 0.0);
+  for (int j = 0; j < d3; ++j)
+    for (int i = j; i < d3; ++i) {
+      const int r = sym_idx(i, j, d3);
+      for (int q = 0; q < nq; ++q) Asym[size_t(r) * (nqp + 4) + q] = h.P[q + size_t(i) * nq] * h.P[q + size_t(j) * nq];
+      for (int l = 0; l < 4; ++l) Asym[size_t(r) * (nqp + 4) + nqp + l] = h.PP[l][i + size_t(j) * d3];
+    }
+  for (int i = 0; i < d3; ++i)
+    for (int q = 0; q < nq; ++q) Af[size_t(i) * nqp + q] = h.P[q + size_t(i) * nq];
+  const std::vector<double> Asym_f = to_fragments(Asym, nsymp, nqp + 4);
+  const std::vector<double> Af_f = to_fragments(Af, d3p, nqp);
+
+  std::vector<double> all;
+  std::vector<size_t> off;
+  auto push = [&](const std::vector<double>& v) {
+    off.push_back(all.size());
+    all.insert(all.end(), v.begin(), v.end());
+    all.resize(round_up(int(all.size()), 32), 0.0);  // 256 B alignment
+  };
+  auto cat = [](std::initializer_list<const std::vector<double>*> parts) {
+    std::vector<double> o;
+    for (auto* p : parts) o.insert(o.end(), p->begin(), p->end());
+    return o;
+  };
+  push(h.tet_bary);                                              // 0
+  push(h.tet_w);                                                 // 1
+  push(h.P);                                                     // 2
+  push(cat({&h.Pd[0], &h.Pd[1], &h.Pd[2]}));                     // 3
+  push(cat({&h.Chat[0], &h.Chat[1], &h.Chat[2]}));               // 4
+  {
+    std::vector<double> s;
+    for (auto& m : h.Shat) s.insert(s.end(), m.begin(), m.end());
+    push(s);                                                     // 5
+  }
+  {
+    std::vector<double> s;
+    for (auto& m : h.Wlm) s.insert(s.end(), m.begin(), m.end());
+    push(s);                                                     // 6
+  }
+  push(cat({&h.PP[0], &h.PP[1], &h.PP[2], &h.PP[3]}));           // 7
+  push(h.DD);                                                    // 8
+  push(h.tri_bary);                                              // 9
+  push(h.tri_w);                                                 // 10
+  push(cat({&h.Pface[0], &h.Pface[1], &h.Pface[2], &h.Pface[3]}));  // 11
+  {
+    std::vector<double> s;
+    for (auto& m : h.Dperm) s.insert(s.end(), m.begin(), m.end());
+    push(s);                                                     // 12
+  }
+  push(Asym_f);                                                  // 13
+  push(Af_f);                                                    // 14
+  CUDA_OK(cudaMalloc(&ts.buf, all.size() * sizeof(double)));
+  CUDA_OK(cudaMemcpy(ts.buf, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice));
+  ts.doubles = all.size();
+  DevTab& t = ts.dev;
+  t.k = k; t.d3 = d3; t.d2 = d2; t.nq = nq; t.nqd = nqd; t.nqp = nqp;
+  t.nsym = nsym; t.nsymp = nsymp; t.d3p = d3p;
+  const double* b = ts.buf;
+  t.bary = b + off[0]; t.w = b + off[1]; t.P = b + off[2]; t.Pd = b + off[3]; t.Chat = b + off[4];
+  t.Shat = b + off[5]; t.Wlm = b + off[6]; t.PP = b + off[7]; t.DD = b + off[8];
+  t.tri_bary = b + off[9]; t.tri_w = b + off[10]; t.Pface = b + off[11]; t.Dperm = b + off[12];
+  t.Asym = b + off[13]; t.Af = b + off[14];
+  ts.ready = true;
+}
+
+FieldDev to_dev(const hdg_field& f, const char* name) {
+  FieldDev d{};
+  d.kind = f.kind;
+  d.value = f.value;
+  d.samples = f.samples;
+  if (f.kind == HDG_FIELD_PROGRAM) {
+    require(f.nops > 0 && f.nops <= HDG_FIELD_MAX_OPS && f.nconst >= 0 &&
+                f.nconst <= HDG_FIELD_MAX_CONSTS && f.ops,
+            HDG_EINVAL, std::string("field program too large or empty: ") + name);
+    int depth = 0, maxd = 0, nc = 0;
+    for (int i = 0; i < f.nops; ++i) {
+      const int op = f.ops[i];
+      require(op >= HDG_OP_X && op <= HDG_OP_POW, HDG_EINVAL, std::string("bad opcode in ") + name);
+      if (op <= HDG_OP_CONST) ++depth;
+      else if (op == HDG_OP_ADD || op == HDG_OP_SUB || op == HDG_OP_MUL || op == HDG_OP_DIV ||
+               op == HDG_OP_LT || op == HDG_OP_POW) --depth;
+      if (op == HDG_OP_CONST) ++nc;
+      require(depth >= 1, HDG_EINVAL, std::string("stack underflow in ") + name);
+      maxd = std::max(maxd, depth);
+      d.ops[i] = static_cast<unsigned char>(op);
+    }
+    require(depth == 1 && maxd <= HDG_FIELD_MAX_STACK && nc == f.nconst, HDG_EINVAL,
+            std::string("malformed field program: ") + name);
+    for (int i = 0; i < f.nconst; ++i) d.consts[i] = f.consts[i];
+    d.nops = f.nops;
+  } else if (f.kind == HDG_FIELD_SAMPLED) {
+    require(f.samples != nullptr, HDG_EINVAL, std::string("sampled field without samples: ") + name);
+  } else {
+    require(f.kind == HDG_FIELD_CONST, HDG_EINVAL, std::string("bad field kind: ") + name);
+  }
+  return d;
+}
+
+GeoDev to_geo(const hdg_geometry* g) {
+  require(g && g->volume && g->piola && g->normals && g->perm && g->T && g->verts, HDG_EINVAL,
+          "incomplete hdg_geometry");
+  return GeoDev{g->volume, g->piola, g->normals, g->perm, g->T, g->verts};
+}
+
+}  // namespace
+
+struct hdg_mesh {
+  HostMesh m;
+  bool pattern_ready = false;
+  SkeletonPattern pat;
+};
+
+struct hdg_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  TabSet tab[2];  // [0] degree k, [1] postprocess degree k+1
+  int post_tet_deg = -1;
+  int tri_deg = 0;
+  void* work = nullptr;
+  size_t work_bytes = 0;
+  long long* d_bad = nullptr;
+  long long* h_bad = nullptr;
+  int* d_status = nullptr;
+  int* h_status = nullptr;
+};
+
+namespace {
+
+void set_device(hdg_ctx* c) { CUDA_OK(cudaSetDevice(c->device)); }
+
+void* ctx_work(hdg_ctx* c, size_t bytes) {
+  if (bytes > c->work_bytes) {
+    if (c->work) cudaFree(c->work);
+    c->work = nullptr;
+    CUDA_OK(cudaMalloc(&c->work, bytes));
+    c->work_bytes = bytes;
+  }
+  return c->work;
+}
+
+size_t work_doubles(const DevTab& t, long nelt) { return size_t(nelt) * (2 * t.nsym + t.d3); }
+
+int factor_doubles(int k) {
+  const int d3 = hdgb::pdim3(k), m = 4 * hdgb::pdim2(k);
+  return d3 * (d3 + 1) + d3 * m + d3;
+}
+
+template <int K_>
+void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, const double* Ds,
+                     const double* fv, double* C, double* Cf, double* F) {
+  using Dm = CondDims<K_>;
+  using Cg = CondCfg<K_>;
+  const size_t smem = size_t(Cg::EPB) * Dm::PER_ELT * sizeof(double);
+  auto kern = condense_kernel<K_>;
+  CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int occ = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cg::NW * 32 * Cg::EPB, smem));
+  require(occ > 0, HDG_ECUDA, "condense kernel does not fit on an SM");
+  const long need = (long(nelt) + Cg::EPB - 1) / Cg::EPB;
+  const int grid = int(std::min<long>(need, long(c->sms) * occ));
+  kern<<<grid, Cg::NW * 32 * Cg::EPB, smem, c->stream>>>(c->tab[0].dev, nelt, geo, Ms, Ds, fv, C, Cf, F,
+                                                          c->d_bad);
+  CUDA_OK(cudaGetLastError());
+}
+
+template <int K_>
+void launch_recover(hdg_ctx* c, int nelt, const GeoDev& geo, const int* fbe, const double* F,
+                    const double* uhat, double* qx, double* qy, double* qz, double* u) {
+  const int grid = (nelt + kRecWarps - 1) / kRecWarps;
+  recover_kernel<K_><<<grid, kRecWarps * 32, 0, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat, qx,
+                                                              qy, qz, u);
+  CUDA_OK(cudaGetLastError());
+}
+
+#define DISPATCH_K(k, FN, ...)                              \
+  switch (k) {                                              \
+    case 0: FN<0>(__VA_ARGS__); break;                      \
+    case 1: FN<1>(__VA_ARGS__); break;                      \
+    case 2: FN<2>(__VA_ARGS__); break;                      \
+    case 3: FN<3>(__VA_ARGS__); break;                      \
+    case 4: FN<4>(__VA_ARGS__); break;                      \
+    case 5: FN<5>(__VA_ARGS__); break;                      \
+    default: throw HdgError{HDG_EINVAL, "degree not compiled (k <= 5)"}; \
+  }
+
+void check_bad(hdg_ctx* c, int64_t* bad_element) {
+  if (!bad_element) return;
+  CUDA_OK(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  *bad_element = *c->h_bad == LLONG_MAX ? -1 : *c->h_bad;
+  if (*c->h_bad != LLONG_MAX)
+    throw HdgError{HDG_ESINGULAR, "singular local system on element " + std::to_string(*c->h_bad)};
+}
+
+int warps_for(size_t per_warp_bytes) {
+  const size_t cap = 200 * 1024;
+  int w = int(std::min<size_t>(8, cap / std::max<size_t>(per_warp_bytes, 1)));
+  return std::max(1, w);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hdg_b200_version(void) { return "hdg_b200 1.0 (sm_100a)"; }
+const char* hdg_b200_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ mesh
+int hdg_b200_mesh_box(int nx, int ny, int nz, int bc_rule, double perturb_frac, uint64_t seed,
+                      double keep_plane_z, hdg_mesh** out) {
+  return guarded([&] {
+    require(out != nullptr, HDG_EINVAL, "out is NULL");
+    require(bc_rule >= 0 && bc_rule <= 2, HDG_EINVAL, "unknown boundary rule");
+    auto m = std::make_unique<hdg_mesh>();
+    box_mesh(nx, ny, nz, BoundaryRule(bc_rule), m->m);
+    if (perturb_frac > 0) perturb_interior(m->m, nx, ny, nz, perturb_frac, seed, keep_plane_z);
+    *out = m.release();
+  });
+}
+
+int hdg_b200_mesh_create(int nver, const double* h_coords, int nelt, const int* h_elements, int ndir,
+                         const int* h_dirichlet, int nneu, const int* h_neumann, hdg_mesh** out) {
+  return guarded([&] {
+    require(out && nver > 0 && nelt > 0 && ndir >= 0 && nneu >= 0 && h_coords && h_elements,
+            HDG_EINVAL, "bad raw mesh arguments");
+    auto m = std::make_unique<hdg_mesh>();
+    HostMesh& r = m->m;
+    r.nver = nver; r.nelt = nelt; r.ndir = ndir; r.nneu = nneu;
+    r.coords.assign(h_coords, h_coords + size_t(nver) * 3);
+    r.elements.assign(h_elements, h_elements + size_t(nelt) * 4);
+    for (int v : r.elements) require(v >= 0 && v < nver, HDG_EMESH, "vertex index out of range");
+    if (ndir) r.dirichlet.assign(h_dirichlet, h_dirichlet + size_t(ndir) * 3);
+    if (nneu) r.neumann.assign(h_neumann, h_neumann + size_t(nneu) * 3);
+    *out = m.release();
+  });
+}
+
+int hdg_b200_mesh_expand(hdg_mesh* m) {
+  return guarded([&] {
+    require(m != nullptr, HDG_EINVAL, "mesh is NULL");
+    expand_mesh(m->m);
+    m->pattern_ready = false;
+  });
+}
+
+int hdg_b200_mesh_dims(const hdg_mesh* m, int64_t dims[6]) {
+  return guarded([&] {
+    require(m && dims, HDG_EINVAL, "NULL argument");
+    const HostMesh& r = m->m;
+    dims[0] = r.nver; dims[1] = r.nelt; dims[2] = r.nfc; dims[3] = r.ndir; dims[4] = r.nneu;
+    dims[5] = r.expanded;
+  });
+}
+
+int hdg_b200_mesh_copy(const hdg_mesh* m, int what, void* dst) {
+  return guarded([&] {
+    require(m && dst, HDG_EINVAL, "NULL argument");
+    const HostMesh& r = m->m;
+    auto cp = [&](const auto& v) { std::memcpy(dst, v.data(), v.size() * sizeof(v[0])); };
+    switch (what) {
+      case HDG_MESH_COORDS: cp(r.coords); break;
+      case HDG_MESH_ELEMENTS: cp(r.elements); break;
+      case HDG_MESH_DIRICHLET: cp(r.dirichlet); break;
+      case HDG_MESH_NEUMANN: cp(r.neumann); break;
+      case HDG_MESH_FACES: require(r.expanded, HDG_ESTATE, "mesh not expanded"); cp(r.faces); break;
+      case HDG_MESH_FACETYPE: require(r.expanded, HDG_ESTATE, "mesh not expanded"); cp(r.facetype); break;
+      case HDG_MESH_FACEBYELE: require(r.expanded, HDG_ESTATE, "mesh not expanded"); cp(r.facebyele); break;
+      default: throw HdgError{HDG_EINVAL, "unknown mesh array"};
+    }
+  });
+}
+
+void hdg_b200_mesh_free(hdg_mesh* m) { delete m; }
+
+int hdg_b200_pattern_dims(const hdg_mesh* mc, int64_t* nnbr_total) {
+  return guarded([&] {
+    require(mc && nnbr_total, HDG_EINVAL, "NULL argument");
+    auto* m = const_cast<hdg_mesh*>(mc);
+    require(m->m.expanded, HDG_ESTATE, "mesh not expanded");
+    if (!m->pattern_ready) { build_pattern(m->m, m->pat); m->pattern_ready = true; }
+    *nnbr_total = m->pat.facebase.back();
+  });
+}
+
+int hdg_b200_pattern_build(const hdg_mesh* mc, int64_t* h_facebase, int* h_nbr, uint8_t* h_slot) {
+  return guarded([&] {
+    require(mc, HDG_EINVAL, "NULL mesh");
+    auto* m = const_cast<hdg_mesh*>(mc);
+    require(m->m.expanded, HDG_ESTATE, "mesh not expanded");
+    if (!m->pattern_ready) { build_pattern(m->m, m->pat); m->pattern_ready = true; }
+    if (h_facebase) std::memcpy(h_facebase, m->pat.facebase.data(), m->pat.facebase.size() * 8);
+    if (h_nbr) std::memcpy(h_nbr, m->pat.nbr.data(), m->pat.nbr.size() * 4);
+    if (h_slot) std::memcpy(h_slot, m->pat.slot.data(), m->pat.slot.size());
+  });
+}
+
+// --------------------------------------------------------------- context
+int hdg_b200_create(int device, void* stream, hdg_ctx** out) {
+  return guarded([&] {
+    require(out != nullptr, HDG_EINVAL, "out is NULL");
+    auto c = std::make_unique<hdg_ctx>();
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(stream);
+    set_device(c.get());
+    CUDA_OK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+    CUDA_OK(cudaMalloc(&c->d_bad, sizeof(long long)));
+    CUDA_OK(cudaMallocHost(&c->h_bad, sizeof(long long)));
+    CUDA_OK(cudaMalloc(&c->d_status, 2 * sizeof(int)));
+    CUDA_OK(cudaMallocHost(&c->h_status, 2 * sizeof(int)));
+    c->h_status[0] = c->h_status[1] = INT_MAX;
+    CUDA_OK(cudaMemcpy(c->d_status, c->h_status, 2 * sizeof(int), cudaMemcpyHostToDevice));
+    *out = c.release();
+  });
+}
+
+void hdg_b200_destroy(hdg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (auto& t : c->tab)
+    if (t.buf) cudaFree(t.buf);
+  if (c->work) cudaFree(c->work);
+  if (c->d_bad) cudaFree(c->d_bad);
+  if (c->h_bad) cudaFreeHost(c->h_bad);
+  if (c->d_status) cudaFree(c->d_status);
+  if (c->h_status) cudaFreeHost(c->h_status);
+  delete c;
+}
+
+int hdg_b200_set_stream(hdg_ctx* c, void* stream) {
+  return guarded([&] {
+    require(c != nullptr, HDG_EINVAL, "ctx is NULL");
+    c->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int hdg_b200_set_degree(hdg_ctx* c, int k, int tet_deg, int tri_deg) {
+  return guarded([&] {
+    require(c != nullptr, HDG_EINVAL, "ctx is NULL");
+    require(k >= 0 && k <= 5, HDG_EINVAL, "degree must be in 0..5");
+    set_device(c);
+    upload_tables(c->tab[0], k, tet_deg, tri_deg);
+    c->tri_deg = tri_deg;
+    c->tab[1].ready = false;
+    if (c->post_tet_deg >= 0) upload_tables(c->tab[1], k + 1, c->post_tet_deg, tri_deg);
+  });
+}
+
+int hdg_b200_set_postprocess_rule(hdg_ctx* c, int tet_deg) {
+  return guarded([&] {
+    require(c && c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    set_device(c);
+    c->post_tet_deg = tet_deg;
+    // degree k+1 tables on the postprocess tet rule; the level's tri rule is
+    // reused as in study.cpp:34
+    upload_tables(c->tab[1], c->tab[0].host.k + 1, tet_deg, c->tri_deg);
+  });
+}
+
+int hdg_b200_dims(const hdg_ctx* c, int64_t dims[8]) {
+  return guarded([&] {
+    require(c && dims && c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    const DevTab& t = c->tab[0].dev;
+    dims[0] = t.k; dims[1] = t.d3; dims[2] = t.d2; dims[3] = t.nq; dims[4] = t.nqd;
+    dims[5] = factor_doubles(t.k);
+    dims[6] = c->tab[1].ready ? c->tab[1].dev.nq : 0;
+    dims[7] = c->tab[1].ready ? c->tab[1].dev.d3 : 0;
+  });
+}
+
+namespace {
+void copy_table(const HostTables& h, int which, double* dst, int64_t cap) {
+    std::vector<double> v;
+    auto cat = [&](const auto& arr) { for (auto& m : arr) v.insert(v.end(), m.begin(), m.end()); };
+    switch (which) {
+      case HDG_TABLE_TET_BARY: v = h.tet_bary; break;
+      case HDG_TABLE_TET_W: v = h.tet_w; break;
+      case HDG_TABLE_P: v = h.P; break;
+      case HDG_TABLE_CHAT: cat(h.Chat); break;
+      case HDG_TABLE_WLM: cat(h.Wlm); break;
+      case HDG_TABLE_PP: cat(h.PP); break;
+      case HDG_TABLE_DD: v = h.DD; break;
+      case HDG_TABLE_TRI_BARY: v = h.tri_bary; break;
+      case HDG_TABLE_TRI_W: v = h.tri_w; break;
+      default: throw HdgError{HDG_EINVAL, "unknown table"};
+    }
+    require(int64_t(v.size()) <= cap, HDG_EINVAL, "destination too small");
+    std::memcpy(dst, v.data(), v.size() * sizeof(double));
+}
+}  // namespace
+
+int hdg_b200_copy_table(const hdg_ctx* c, int which, double* dst, int64_t cap) {
+  return guarded([&] {
+    require(c && dst && c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    copy_table(c->tab[0].host, which, dst, cap);
+  });
+}
+
+int hdg_b200_host_table(int k, int tet_deg, int tri_deg, int which, double* dst, int64_t cap) {
+  return guarded([&] {
+    require(dst != nullptr, HDG_EINVAL, "dst is NULL");
+    copy_table(build_host_tables(k, tet_deg, tri_deg), which, dst, cap);
+  });
+}
+
+// ------------------------------------------------------------------- K1
+int hdg_b200_geometry(hdg_ctx* c, int nver, int nelt, int nfc, const double* d_coords,
+                      const int* d_elements, const int* d_faces, const int* d_facebyele,
+                      const double* d_tau, double tau_const, hdg_geometry* g) {
+  return guarded([&] {
+    require(c && g && d_coords && d_elements && d_faces && d_facebyele && g->area, HDG_EINVAL,
+            "NULL argument");
+    require(nver > 0 && nelt > 0 && nfc > 0, HDG_EINVAL, "empty mesh");
+    to_geo(g);
+    set_device(c);
+    const int init[2] = {INT_MAX, INT_MAX};
+    std::memcpy(c->h_status, init, sizeof(init));
+    CUDA_OK(cudaMemcpyAsync(c->d_status, c->h_status, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    face_area_kernel<<<(nfc + 255) / 256, 256, 0, c->stream>>>(nver, nfc, d_coords, d_faces, g->area);
+    geometry_kernel<<<(nelt + 127) / 128, 128, 0, c->stream>>>(
+        nver, nelt, nfc, d_coords, d_elements, d_faces, d_facebyele, d_tau, tau_const, g->area,
+        g->volume, g->piola, g->normals, g->perm, g->T, g->verts, c->d_status);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_upwind_tau(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field bx, hdg_field by,
+                        hdg_field bz, double* d_tau) {
+  return guarded([&] {
+    require(c && d_tau && nelt > 0, HDG_EINVAL, "bad argument");
+    const GeoDev geo = to_geo(g);
+    require(bx.kind != HDG_FIELD_SAMPLED && by.kind != HDG_FIELD_SAMPLED && bz.kind != HDG_FIELD_SAMPLED,
+            HDG_EINVAL, "upwind tau needs CONST or PROGRAM fields");
+    set_device(c);
+    upwind_tau_kernel<<<(nelt + 127) / 128, 128, 0, c->stream>>>(nelt, geo, to_dev(bx, "bx"),
+                                                                  to_dev(by, "by"), to_dev(bz, "bz"), d_tau);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_quad_points(hdg_ctx* c, int nelt, const hdg_geometry* g, int which, double* X, double* Y,
+                         double* Z) {
+  return guarded([&] {
+    require(c && X && Y && Z && (which == 0 || which == 1), HDG_EINVAL, "bad argument");
+    require(c->tab[which].ready, HDG_ESTATE, "tables not set");
+    const GeoDev geo = to_geo(g);
+    set_device(c);
+    const DevTab& t = c->tab[which].dev;
+    const long n = long(nelt) * t.nq;
+    quad_points_kernel<<<int((n + 255) / 256), 256, 0, c->stream>>>(nelt, t.nq, t.bary, geo.verts, X, Y, Z);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+// ---------------------------------------------------------------- K2 + K3
+int64_t hdg_b200_work_size(const hdg_ctx* c, int nelt) {
+  if (!c || !c->tab[0].ready) return -1;
+  return int64_t(work_doubles(c->tab[0].dev, nelt) * sizeof(double));
+}
+
+int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field kappa, hdg_field cf,
+                            hdg_field f, double* d_C, double* d_Cf, double* d_factors, void* d_work,
+                            int64_t* bad_element) {
+  return guarded([&] {
+    require(c && d_C && d_Cf && nelt > 0, HDG_EINVAL, "bad argument");
+    require(c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    const GeoDev geo = to_geo(g);
+    const FieldDev fk = to_dev(kappa, "kappa"), fc = to_dev(cf, "c"), ff = to_dev(f, "f");
+    set_device(c);
+    const DevTab& t = c->tab[0].dev;
+    double* work = static_cast<double*>(d_work ? d_work : ctx_work(c, work_doubles(t, nelt) * sizeof(double)));
+    double* Ms = work;
+    double* Ds = Ms + size_t(nelt) * t.nsym;
+    double* fv = Ds + size_t(nelt) * t.nsym;
+    const size_t qsmem = size_t(3) * (t.nqp + 4) * kQuadLDB * sizeof(double);
+    CUDA_OK(cudaFuncSetAttribute(quad_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
+    quad_build_kernel<<<(nelt + kQuadEB - 1) / kQuadEB, kQuadThreads, qsmem, c->stream>>>(t, nelt, geo, fk, fc,
+                                                                                          ff, Ms, Ds, fv);
+    CUDA_OK(cudaGetLastError());
+    set_ll_kernel<<<1, 1, 0, c->stream>>>(c->d_bad, LLONG_MAX);
+    DISPATCH_K(t.k, launch_condense, c, nelt, geo, Ms, Ds, fv, d_C, d_Cf, d_factors);
+    check_bad(c, bad_element);
+  });
+}
+
+// ------------------------------------------------------------------- K5
+int hdg_b200_recover(hdg_ctx* c, int nelt, const hdg_geometry* g, const int* d_facebyele,
+                     const double* d_factors, const double* d_uhat, double* d_qx, double* d_qy,
+                     double* d_qz, double* d_u) {
+  return guarded([&] {
+    require(c && d_facebyele && d_factors && d_uhat && d_qx && d_qy && d_qz && d_u && nelt > 0,
+            HDG_EINVAL, "bad argument");
+    require(c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    const GeoDev geo = to_geo(g);
+    set_device(c);
+    DISPATCH_K(c->tab[0].dev.k, launch_recover, c, nelt, geo, d_facebyele, d_factors, d_uhat, d_qx, d_qy,
+               d_qz, d_u);
+  });
+}
+
+// ------------------------------------------------------------------- K4
+int hdg_b200_pattern_fill(hdg_ctx* c, int nfc, int d2, const int64_t* d_facebase, const int* d_nbr,
+                          int64_t* d_rowptr, int* d_colidx) {
+  return guarded([&] {
+    require(c && d_facebase && d_nbr && d_rowptr && d_colidx && nfc > 0 && d2 > 0, HDG_EINVAL,
+            "bad argument");
+    set_device(c);
+    const long rows = long(nfc) * d2 + 1;
+    pattern_fill_kernel<<<int((rows + 255) / 256), 256, 0, c->stream>>>(nfc, d2, d_facebase, d_nbr, d_rowptr,
+                                                                      d_colidx);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_scatter(hdg_ctx* c, int nelt, int d2, const int* d_facebyele, const uint8_t* d_slot,
+                     const int64_t* d_facebase, const double* d_C, const double* d_Cf, double* d_vals,
+                     double* d_b) {
+  return guarded([&] {
+    require(c && d_facebyele && d_slot && d_facebase && d_C && d_Cf && d_vals && d_b && nelt > 0 && d2 > 0,
+            HDG_EINVAL, "bad argument");
+    set_device(c);
+    scatter_kernel<<<(nelt + 7) / 8, 256, 0, c->stream>>>(nelt, d2, d_facebyele, d_slot, d_facebase, d_C,
+                                                         d_Cf, d_vals, d_b);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+// ------------------------------------------------------------------- K6
+int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field kappa, const double* qx,
+                         const double* qy, const double* qz, const double* u, double* ustar) {
+  return guarded([&] {
+    require(c && qx && qy && qz && u && ustar && nelt > 0, HDG_EINVAL, "bad argument");
+    require(c->tab[0].ready && c->tab[1].ready, HDG_ESTATE, "set_postprocess_rule first");
+    const GeoDev geo = to_geo(g);
+    const FieldDev fk = to_dev(kappa, "kappa");
+    set_device(c);
+    const DevTab& tp = c->tab[1].dev;
+    const int n = tp.d3;
+    const int per_warp = n * (n + 1) + round_up(n, 8) + 3 * tp.nq + 32 + round_up(n, 8);
+    const int nw = warps_for(size_t(per_warp) * 8);
+    const size_t smem = size_t(nw) * per_warp * sizeof(double);
+    CUDA_OK(cudaFuncSetAttribute(postprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const long need = (long(nelt) + nw - 1) / nw;
+    const int grid = int(std::min<long>(need, long(c->sms) * 8));
+    postprocess_kernel<<<grid, nw * 32, smem, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, qx, qy, qz, u,
+                                                          ustar, per_warp);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+// ------------------------------------------------------------------- K7
+int hdg_b200_convection_block(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field bx, hdg_field by,
+                              hdg_field bz, double* vol, double* dp, double* dd) {
+  return guarded([&] {
+    require(c && vol && dp && dd && nelt > 0, HDG_EINVAL, "bad argument");
+    require(c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    require(bx.kind != HDG_FIELD_SAMPLED && by.kind != HDG_FIELD_SAMPLED && bz.kind != HDG_FIELD_SAMPLED,
+            HDG_EINVAL, "convection block needs CONST or PROGRAM fields (face nodes are not sampled)");
+    const GeoDev geo = to_geo(g);
+    set_device(c);
+    const DevTab& t = c->tab[0].dev;
+    const int per_warp = 3 * t.nq + 4 * t.nqd + 32;
+    const int nw = warps_for(size_t(per_warp) * 8);
+    const size_t smem = size_t(nw) * per_warp * sizeof(double);
+    CUDA_OK(cudaFuncSetAttribute(convection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int grid = int(std::min<long>((long(nelt) + nw - 1) / nw, long(c->sms) * 8));
+    convection_kernel<<<grid, nw * 32, smem, c->stream>>>(t, nelt, geo, to_dev(bx, "bx"), to_dev(by, "by"),
+                                                         to_dev(bz, "bz"), vol, dp, dd, per_warp);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_element_matrices(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field kappa, hdg_field cf,
+                              hdg_field f, hdg_element_matrices* out) {
+  return guarded([&] {
+    require(c && out && nelt > 0, HDG_EINVAL, "bad argument");
+    require(c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    const GeoDev geo = to_geo(g);
+    set_device(c);
+    const DevTab& t = c->tab[0].dev;
+    const int per_warp = 3 * t.nq + 32;
+    const int nw = warps_for(size_t(per_warp) * 8);
+    const size_t smem = size_t(nw) * per_warp * sizeof(double);
+    CUDA_OK(cudaFuncSetAttribute(element_matrices_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    EmsOut o{out->Mkinv, out->Mc, out->Cx, out->Cy, out->Cz, out->tauPP, out->tauDP,
+             out->nxDP, out->nyDP, out->nzDP, out->tauDD, out->fvec};
+    const int grid = int(std::min<long>((long(nelt) + nw - 1) / nw, long(c->sms) * 8));
+    element_matrices_kernel<<<grid, nw * 32, smem, c->stream>>>(t, nelt, geo, to_dev(kappa, "kappa"),
+                                                               to_dev(cf, "c"), to_dev(f, "f"), o, per_warp);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_synchronize(hdg_ctx* c) {
+  return guarded([&] {
+    require(c != nullptr, HDG_EINVAL, "ctx is NULL");
+    set_device(c);
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpy(c->h_status, c->d_status, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+    require(c->h_status[0] == INT_MAX, HDG_EMESH,
+            "element " + std::to_string(c->h_status[0]) + " has non-positive orientation");
+    require(c->h_status[1] == INT_MAX, HDG_EMESH, "face vertex triples do not match as sets");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+// Device-side building blocks shared by the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hdg_b200.h"
+
+namespace hdgb {
+
+// ------------------------------------------------------------ compile-time dims
+__host__ __device__ constexpr int cdim3(int k) { return (k + 1) * (k + 2) * (k + 3) / 6; }
+__host__ __device__ constexpr int cdim2(int k) { return (k + 1) * (k + 2) / 2; }
+__host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
+__host__ __device__ constexpr int cnq(int deg) { return (deg / 2 + 1) * (deg / 2 + 1) * (deg / 2 + 1); }
+__host__ __device__ constexpr int cnqd(int deg) { return (deg / 2 + 1) * (deg / 2 + 1); }
+// packed lower-triangle (column-major) index of (i >= j) in an n x n matrix
+__host__ __device__ constexpr int sym_idx(int i, int j, int n) { return j * (2 * n - j + 1) / 2 + (i - j); }
+
+// ------------------------------------------------------------------ tables
+// One degree's reference-element tables in device memory (host_tables.cpp).
+struct DevTab {
+  int k, d3, d2, nq, nqd, nqp, nsym, nsymp, d3p;
+  const double* bary;   // nq x 4
+  const double* w;      // nq
+  const double* P;      // nq x d3
+  const double* Pd;     // 3 x (nq x d3)
+  const double* Chat;   // 3 x (d3 x d3)
+  const double* Shat;   // 9 x (d3 x d3)
+  const double* Wlm;    // 24 x (d2 x d3), index 6*l + (mu-1)
+  const double* PP;     // 4 x (d3 x d3)
+  const double* DD;     // d2 x d2
+  const double* tri_bary;  // nqd x 3
+  const double* tri_w;     // nqd
+  const double* Pface;     // 4 x (nqd x d3)
+  const double* Dperm;     // 6 x (nqd x d2)
+  const double* Asym;   // fragment-ordered [Wsym | PPsym]: nsymp x (nqp + 4)
+  const double* Af;     // fragment-ordered P^T: d3p x nqp
+};
+
+// ------------------------------------------------------------------ fields
+struct FieldDev {
+  int kind;  // HDG_FIELD_*
+  int nops;
+  double value;
+  const double* samples;  // nq x nelt (element's nodes contiguous)
+  unsigned char ops[HDG_FIELD_MAX_OPS];
+  double consts[HDG_FIELD_MAX_CONSTS];
+};
+
+// Postfix VM (opcodes in include/hdg_b200.h). Control flow is uniform across a
+// warp (every lane runs the same program), so the switch never diverges.
+__device__ __forceinline__ double run_program(const FieldDev& F, double x, double y, double z) {
+  double st[HDG_FIELD_MAX_STACK];
+  int sp = 0, ci = 0;
+  for (int i = 0; i < F.nops; ++i) {
+    switch (F.ops[i]) {
+      case HDG_OP_X: st[sp++] = x; break;
+      case HDG_OP_Y: st[sp++] = y; break;
+      case HDG_OP_Z: st[sp++] = z; break;
+      case HDG_OP_CONST: st[sp++] = F.consts[ci++]; break;
+      case HDG_OP_ADD: --sp; st[sp - 1] = st[sp - 1] + st[sp]; break;
+      case HDG_OP_SUB: --sp; st[sp - 1] = st[sp - 1] - st[sp]; break;
+      case HDG_OP_MUL: --sp; st[sp - 1] = st[sp - 1] * st[sp]; break;
+      case HDG_OP_DIV: --sp; st[sp - 1] = st[sp - 1] / st[sp]; break;
+      case HDG_OP_NEG: st[sp - 1] = -st[sp - 1]; break;
+      case HDG_OP_SIN: st[sp - 1] = sin(st[sp - 1]); break;
+      case HDG_OP_COS: st[sp - 1] = cos(st[sp - 1]); break;
+      case HDG_OP_EXP: st[sp - 1] = exp(st[sp - 1]); break;
+      case HDG_OP_SQRT: st[sp - 1] = sqrt(st[sp - 1]); break;
+      case HDG_OP_ABS: st[sp - 1] = fabs(st[sp - 1]); break;
+      case HDG_OP_LT: --sp; st[sp - 1] = st[sp - 1] < st[sp] ? 1.0 : 0.0; break;
+      case HDG_OP_POW: --sp; st[sp - 1] = pow(st[sp - 1], st[sp]); break;
+      default: break;
+    }
+  }
+  return st[0];
+}
+
+// Value of field F at quadrature node q of element K (physical point x,y,z).
+__device__ __forceinline__ double eval_field(const FieldDev& F, double x, double y, double z,
+                                             int q, long K, int nq) {
+  if (F.kind == HDG_FIELD_CONST) return F.value;
+  if (F.kind == HDG_FIELD_SAMPLED) return __ldg(F.samples + K * nq + q);
+  return run_program(F, x, y, z);
+}
+
+// ------------------------------------------------------------------ DMMA
+// D(8x8) += A(8x4, row) * B(4x8, col), fp64 tensor-core MMA (SASS DMMA.8x8x4).
+// Lane layout: a = A[g][t], b = B[t][g], c = {C[g][2t], C[g][2t+1]}, g = lane/4, t = lane%4.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Named barrier for a team of `nthreads` threads (ids 1..15; 0 is __syncthreads).
+__device__ __forceinline__ void team_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Lowest singular element (reference reports the first detected; with one
+// thread that is the lowest, local_solver.cpp:89-98).
+__device__ __forceinline__ void flag_bad(long long* bad, long long K) {
+  atomicMin(reinterpret_cast<unsigned long long*>(bad), static_cast<unsigned long long>(K));
+}
+
+}  // namespace hdgb

@@ -1,0 +1,198 @@
+// K1 (geometry), K4 (skeleton pattern + scatter) and small helper kernels.
+// All are HBM-bound streaming kernels: one thread per element / face row,
+// element index fastest in every SoA array so loads and stores coalesce.
+#pragma once
+
+#include "dev_common.cuh"
+#include "kernels_local.cuh"
+
+namespace hdgb {
+
+__constant__ int c_local_face[4][3] = {{0, 1, 2}, {0, 1, 3}, {0, 2, 3}, {3, 1, 2}};
+__constant__ double c_face_sign[4] = {-1.0, 1.0, -1.0, 1.0};
+__constant__ int c_vertex_image[6][3] = {{0, 1, 2}, {0, 2, 1}, {2, 0, 1}, {2, 1, 0}, {1, 2, 0}, {1, 0, 2}};
+
+// |e| = |1/2 (w2-w1) x (w3-w1)| of the global face triple (mesh.cpp:153-154).
+__global__ void face_area_kernel(int nver, int nfc, const double* __restrict__ X,
+                                 const int* __restrict__ faces, double* __restrict__ area) {
+  const long f = long(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (f >= nfc) return;
+  const int v0 = faces[f], v1 = faces[nfc + f], v2 = faces[2L * nfc + f];
+  double u[3], w[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    u[c] = X[v1 + long(c) * nver] - X[v0 + long(c) * nver];
+    w[c] = X[v2 + long(c) * nver] - X[v0 + long(c) * nver];
+  }
+  const double n0 = 0.5 * (u[1] * w[2] - u[2] * w[1]);
+  const double n1 = 0.5 * (u[2] * w[0] - u[0] * w[2]);
+  const double n2 = 0.5 * (u[0] * w[1] - u[1] * w[0]);
+  area[f] = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+}
+
+// K1: per-element geometry (mesh.cpp:43-66, :156-169; element_matrices.cpp:31-36).
+__global__ void geometry_kernel(int nver, int nelt, int nfc, const double* __restrict__ X,
+                                const int* __restrict__ elements, const int* __restrict__ faces,
+                                const int* __restrict__ facebyele, const double* __restrict__ tau,
+                                double tau_const, const double* __restrict__ area,
+                                double* __restrict__ volume, double* __restrict__ piola,
+                                double* __restrict__ normals, int* __restrict__ perm,
+                                double* __restrict__ T, double* __restrict__ verts,
+                                int* __restrict__ status) {
+  const long K = long(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (K >= nelt) return;
+  int v[4];
+  double x[4], y[4], z[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[i] = elements[long(i) * nelt + K];
+    x[i] = X[v[i]];
+    y[i] = X[long(nver) + v[i]];
+    z[i] = X[2L * nver + v[i]];
+  }
+  // cofactors a = detB B^{-T} (mesh.cpp:56-64)
+  double a[9];
+  a[0] = (y[2] - y[0]) * (z[3] - z[0]) - (y[3] - y[0]) * (z[2] - z[0]);
+  a[1] = (y[3] - y[0]) * (z[1] - z[0]) - (y[1] - y[0]) * (z[3] - z[0]);
+  a[2] = (y[1] - y[0]) * (z[2] - z[0]) - (y[2] - y[0]) * (z[1] - z[0]);
+  a[3] = (x[3] - x[0]) * (z[2] - z[0]) - (x[2] - x[0]) * (z[3] - z[0]);
+  a[4] = (x[1] - x[0]) * (z[3] - z[0]) - (x[3] - x[0]) * (z[1] - z[0]);
+  a[5] = (x[2] - x[0]) * (z[1] - z[0]) - (x[1] - x[0]) * (z[2] - z[0]);
+  a[6] = (x[2] - x[0]) * (y[3] - y[0]) - (x[3] - x[0]) * (y[2] - y[0]);
+  a[7] = (x[3] - x[0]) * (y[1] - y[0]) - (x[1] - x[0]) * (y[3] - y[0]);
+  a[8] = (x[1] - x[0]) * (y[2] - y[0]) - (x[2] - x[0]) * (y[1] - y[0]);
+  // det B by expansion along B's first column (x2-x1, y2-y1, z2-z1)
+  const double detB = (x[1] - x[0]) * a[0] + (y[1] - y[0]) * a[3] + (z[1] - z[0]) * a[6];
+  if (!(detB > 0)) atomicMin(status, int(K < 0x7fffffff ? K : 0x7fffffff));
+  volume[K] = detB / 6.0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) piola[long(i) * nelt + K] = a[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    verts[long(i) * nelt + K] = x[i];
+    verts[long(4 + i) * nelt + K] = y[i];
+    verts[long(8 + i) * nelt + K] = z[i];
+  }
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int i0 = c_local_face[l][0], i1 = c_local_face[l][1], i2 = c_local_face[l][2];
+    const double ux = x[i1] - x[i0], uy = y[i1] - y[i0], uz = z[i1] - z[i0];
+    const double wx = x[i2] - x[i0], wy = y[i2] - y[i0], wz = z[i2] - z[i0];
+    const double sg = c_face_sign[l];
+    normals[long(3 * l) * nelt + K] = sg * (0.5 * (uy * wz - uz * wy));
+    normals[long(3 * l + 1) * nelt + K] = sg * (0.5 * (uz * wx - ux * wz));
+    normals[long(3 * l + 2) * nelt + K] = sg * (0.5 * (ux * wy - uy * wx));
+    const int f = facebyele[long(l) * nelt + K];
+    const int gv[3] = {faces[f], faces[long(nfc) + f], faces[2L * nfc + f]};
+    const int lv[3] = {v[i0], v[i1], v[i2]};
+    int mu = 0;
+    for (int m = 1; m <= 6 && mu == 0; ++m)
+      if (gv[c_vertex_image[m - 1][0]] == lv[0] && gv[c_vertex_image[m - 1][1]] == lv[1] &&
+          gv[c_vertex_image[m - 1][2]] == lv[2])
+        mu = m;
+    if (mu == 0) atomicMin(status + 1, int(K));
+    perm[long(l) * nelt + K] = mu == 0 ? 1 : mu;
+    const double tv = tau ? tau[long(l) * nelt + K] : tau_const;
+    T[long(l) * nelt + K] = tv * area[f];
+  }
+}
+
+// tau(K,l) = 1 + |beta(xbar_e) . nu_{K,l}| (config C4 upwind stabilisation).
+__global__ void upwind_tau_kernel(int nelt, GeoDev geo, FieldDev bx, FieldDev by, FieldDev bz,
+                                  double* __restrict__ tau) {
+  const long K = long(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (K >= nelt) return;
+  for (int l = 0; l < 4; ++l) {
+    double c[3];
+    for (int d = 0; d < 3; ++d)
+      c[d] = (geo.verts[long(4 * d + c_local_face[l][0]) * nelt + K] +
+              geo.verts[long(4 * d + c_local_face[l][1]) * nelt + K] +
+              geo.verts[long(4 * d + c_local_face[l][2]) * nelt + K]) / 3.0;
+    const double nx = geo.normals[long(3 * l) * nelt + K], ny = geo.normals[long(3 * l + 1) * nelt + K],
+                 nz = geo.normals[long(3 * l + 2) * nelt + K];
+    const double nn = sqrt(nx * nx + ny * ny + nz * nz);
+    const double b0 = eval_field(bx, c[0], c[1], c[2], 0, K, 1);
+    const double b1 = eval_field(by, c[0], c[1], c[2], 0, K, 1);
+    const double b2 = eval_field(bz, c[0], c[1], c[2], 0, K, 1);
+    tau[long(l) * nelt + K] = 1.0 + fabs((b0 * nx + b1 * ny + b2 * nz) / nn);
+  }
+}
+
+// Physical quadrature nodes X = bary * verts (element_matrices.cpp:66-70).
+__global__ void quad_points_kernel(int nelt, int nq, const double* __restrict__ bary,
+                                   const double* __restrict__ verts, double* __restrict__ X,
+                                   double* __restrict__ Y, double* __restrict__ Z) {
+  const long idx = long(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= long(nelt) * nq) return;
+  const long K = idx / nq;
+  const int q = int(idx - K * nq);
+  double p[3];
+  for (int d = 0; d < 3; ++d) {
+    double s = 0.0;
+    for (int v = 0; v < 4; ++v) s += bary[long(v) * nq + q] * verts[long(4 * d + v) * nelt + K];
+    p[d] = s;
+  }
+  X[idx] = p[0];
+  Y[idx] = p[1];
+  Z[idx] = p[2];
+}
+
+__global__ void set_ll_kernel(long long* p, long long v) { *p = v; }
+
+// ================================================================ K4
+// CSR of the skeleton matrix H: row (f, i) holds, for every neighbour face g of
+// f in ascending order, the d2 columns g*d2 + j (global_system.cpp:43-54).
+__global__ void pattern_fill_kernel(int nfc, int d2, const int64_t* __restrict__ facebase,
+                                    const int* __restrict__ nbr, int64_t* __restrict__ rowptr,
+                                    int* __restrict__ colidx) {
+  const long row = long(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long ndof = long(nfc) * d2;
+  if (row > ndof) return;
+  if (row == ndof) { rowptr[ndof] = facebase[nfc] * d2 * d2; return; }
+  const long f = row / d2;
+  const int i = int(row - f * d2);
+  const int nb = int(facebase[f + 1] - facebase[f]);
+  const int64_t start = facebase[f] * d2 * d2 + int64_t(i) * nb * d2;
+  rowptr[row] = start;
+  for (int s = 0; s < nb; ++s) {
+    const int gcol = nbr[f * 8 + s] * d2;
+    for (int j = 0; j < d2; ++j) colidx[start + s * d2 + j] = gcol + j;
+  }
+}
+
+// One warp per element. Off-diagonal face blocks have exactly one owner (two
+// tets share at most one face) -> plain stores; diagonal blocks and b receive
+// one or two contributions -> fp64 atomics onto zero, which is bit-exact (a+b
+// is commutative, 0+a exact).
+__global__ void scatter_kernel(int nelt, int d2, const int* __restrict__ facebyele,
+                               const uint8_t* __restrict__ slot, const int64_t* __restrict__ facebase,
+                               const double* __restrict__ C, const double* __restrict__ Cf,
+                               double* __restrict__ vals, double* __restrict__ b) {
+  const int lane = threadIdx.x & 31;
+  const long K = long(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (K >= nelt) return;
+  const int m = 4 * d2;
+  const double* Ck = C + K * m * m;
+  int f[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) f[l] = facebyele[long(l) * nelt + K];
+  for (int task = lane; task < 16 * d2; task += 32) {
+    // task -> (l2, l1, i) with i fastest so lanes read consecutive rows of C
+    const int i = task % d2, l1 = (task / d2) % 4, l2 = task / (4 * d2);
+    const int f1 = f[l1];
+    const int nb = int(facebase[f1 + 1] - facebase[f1]);
+    const int64_t pos = facebase[f1] * d2 * d2 + int64_t(i) * nb * d2 + int64_t(slot[K * 16 + l1 * 4 + l2]) * d2;
+    const int r = l1 * d2 + i;
+    if (l1 == l2) {
+      for (int j = 0; j < d2; ++j) atomicAdd(vals + pos + j, Ck[r + (l2 * d2 + j) * m]);
+    } else {
+      for (int j = 0; j < d2; ++j) vals[pos + j] = Ck[r + (l2 * d2 + j) * m];
+    }
+  }
+  for (int r = lane; r < m; r += 32) {
+    const int l = r / d2;
+    atomicAdd(b + long(f[l]) * d2 + (r - l * d2), Cf[K * m + r]);
+  }
+}
+
+}  // namespace hdgb

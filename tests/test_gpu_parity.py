@@ -1,0 +1,279 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs. Tolerance (BASELINE north star): numbering,
+perm codes and the CSR pattern bit-exact; C, Cf, b, q, u, u* within 1e-10
+relative (max over elements of the Frobenius relative error)."""
+import numpy as np
+import pytest
+import torch
+
+from gpu_util import TOL, gpu_pipeline, np_, oracle_condense, oracle_mesh, submesh
+from oracle import core
+from oracle_util import field, max_slice_relerr, relerr, solve_skeleton, vfield
+from paper_1305_1489_b200.configs import CONFIGS, PAPER_SINE, scaled
+from paper_1305_1489_b200.engine import Engine, HostMesh, dim2, dim3
+
+pytestmark = pytest.mark.gpu
+
+KAP = "2 + sin(x)*sin(y)*sin(z)"
+CC = "1 + 0.5*(x*x + y*y + z*z)"
+FF = "cos(x + 2*y - z)"
+
+
+def perm_cover_host():
+    coords = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1],
+                       [2, 0, 0], [3, 0, 0], [2, 1, 0], [2, 0, 1]], dtype=float)
+    elements = np.array([[0, 1, 2, 3], [4, 5, 6, 7]], dtype=np.int32)
+    sigma = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
+    lf = [(0, 1, 2), (0, 1, 3), (0, 2, 3), (3, 1, 2)]
+    d = np.zeros((8, 3), dtype=np.int32)
+    for e in range(2):
+        for l in range(4):
+            s = sigma[(4 * e + l) % 6]
+            d[4 * e + l] = [elements[e, lf[l][s[i]]] for i in range(3)]
+    return HostMesh.from_raw(coords, elements, d, np.zeros((0, 3), np.int32))
+
+
+# ----------------------------------------------------------------- K1
+@pytest.mark.parametrize("which", ["box", "perturbed", "cover"])
+def test_geometry(which):
+    if which == "box":
+        mesh = HostMesh.box(3, bc="dirichlet_x")
+    elif which == "perturbed":
+        mesh = HostMesh.box(4, bc="dirichlet_top_bottom", perturb=0.15, seed=1305)
+    else:
+        mesh = perm_cover_host()
+    em = oracle_mesh(mesh)
+    eng = Engine(0)
+    eng.set_degree(1)
+    dm = eng.upload(mesh)
+    tau = torch.rand(4, dm.nelt, dtype=torch.float64, device="cuda") + 0.5
+    g = eng.geometry(dm, tau)
+    eng.synchronize()
+    assert np.array_equal(np_(g.perm).T, em.perm)                       # bit-exact
+    assert np.max(np.abs(np_(g.volume) - em.volume) / em.volume) < 1e-14
+    assert np.max(np.abs(np_(g.area) - em.area) / em.area) < 1e-14
+    assert np.max(np.abs(np_(g.normals).T - em.normals)) < 1e-15 * np.max(np.abs(em.normals)) * 10
+    assert np.max(np.abs(np_(g.piola).T - core.piola_coefficients(em))) < 1e-14
+    T = core.Stabilization(np.asfortranarray(np_(tau).T)).scaled(em)
+    assert np.max(np.abs(np_(g.T).T - T)) < 1e-14
+
+
+# ------------------------------------------------ a3-a5: element matrices
+@pytest.mark.parametrize("k,which", [(1, "box"), (2, "cover"), (3, "box")])
+def test_element_matrices(k, which):
+    mesh = HostMesh.box(2) if which == "box" else perm_cover_host()
+    em = oracle_mesh(mesh)
+    eng, dm, g, _ = gpu_pipeline(mesh, k, KAP, CC, FF, tau=1.3)
+    got = eng.element_matrices(g, KAP, CC, FF)
+    _, ms, _, _, _ = oracle_condense(em, k, KAP, CC, FF, 1.3)
+    for name in ("Mkinv", "Mc", "Cx", "Cy", "Cz", "tauPP", "tauDP", "nxDP", "nyDP", "nzDP", "tauDD"):
+        want = ms.get(name)
+        err = max_slice_relerr(np_(got[name]), want)
+        assert err < TOL, (name, err)
+    assert max_slice_relerr(np_(got["fvec"]), ms.get("fvec").T) < TOL
+
+
+# ------------------------------------------------------ a8: condense
+@pytest.mark.parametrize("k,n,bc", [(0, 2, "dirichlet_top_bottom"), (1, 3, "all_dirichlet"),
+                                    (2, 2, "dirichlet_x"), (3, 2, "dirichlet_x"),
+                                    (4, 1, "dirichlet_top_bottom"), (5, 1, "dirichlet_top_bottom")])
+def test_condense(k, n, bc):
+    mesh = HostMesh.box(n, bc=bc)
+    em = oracle_mesh(mesh)
+    eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
+    _, _, _, C, Cf = oracle_condense(em, k, KAP, CC, FF, 1.0)
+    assert max_slice_relerr(np_(cs.C_slices()), C) < TOL
+    assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
+
+
+def test_condense_perm_cover_all_codes():
+    mesh = perm_cover_host()
+    em = oracle_mesh(mesh)
+    assert set(np.unique(em.perm)) == {1, 2, 3, 4, 5, 6}
+    eng, dm, g, cs = gpu_pipeline(mesh, 2, KAP, CC, FF)
+    _, _, _, C, Cf = oracle_condense(em, 2, KAP, CC, FF, 1.0)
+    assert max_slice_relerr(np_(cs.C_slices()), C) < TOL
+    assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
+
+
+def test_condense_sampled_fields():
+    """HDG_FIELD_SAMPLED: caller-evaluated callbacks at the device's nodes."""
+    k = 2
+    mesh = HostMesh.box(2)
+    eng = Engine(0)
+    eng.set_degree(k)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 1.0)
+    X, Y, Z = eng.quad_points(g)
+    kap = 2 + torch.sin(X) * torch.sin(Y) * torch.sin(Z)
+    cc = 1 + 0.5 * (X * X + Y * Y + Z * Z)
+    ff = torch.cos(X + 2 * Y - Z)
+    cs = eng.build_condense(g, kap.contiguous(), cc.contiguous(), ff.contiguous())
+    _, _, _, C, Cf = oracle_condense(oracle_mesh(mesh), k, KAP, CC, FF, 1.0)
+    assert max_slice_relerr(np_(cs.C_slices()), C) < TOL
+    assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
+
+
+def test_singular_element_reported():
+    """local_solver.cpp:89-98 / test_local_solver.cpp:279-290: lowest singular index."""
+    from paper_1305_1489_b200._lib import LocalSolverError
+    k = 1
+    mesh = HostMesh.box(2)
+    eng = Engine(0)
+    eng.set_degree(k)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 1.0)
+    X, _, _ = eng.quad_points(g)
+    kap = torch.ones_like(X)
+    kap[3] = float("inf")   # kappa^-1 = 0 on element 3 -> M = 0 -> singular
+    kap[7] = float("inf")
+    with pytest.raises(LocalSolverError) as ei:
+        eng.build_condense(g, kap.contiguous(), 1.0, 1.0)
+    assert ei.value.element == 3
+
+
+# ------------------------------------------------- a10: gather + recover
+@pytest.mark.parametrize("k", [1, 2, 3, 5])
+def test_recover(k):
+    n = 2 if k < 5 else 1
+    mesh = HostMesh.box(n, bc="dirichlet_x")
+    em = oracle_mesh(mesh)
+    eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
+    d2 = dim2(k)
+    rng = np.random.default_rng(7)
+    uhat = rng.standard_normal(dm.nfc * d2)
+    ls = eng.recover(g, dm, cs, torch.from_numpy(uhat).cuda())
+    _, _, lb, _, _ = oracle_condense(em, k, KAP, CC, FF, 1.0)
+    qx, qy, qz, u = core.local_recover(lb, core.gather_traces(em, d2, uhat), 4)
+    for got, want in ((ls.qx, qx), (ls.qy, qy), (ls.qz, qz), (ls.u, u)):
+        assert max_slice_relerr(np_(got), want.T) < TOL
+
+
+# ------------------------------------------------------ a9: scatter
+@pytest.mark.parametrize("k,bc", [(1, "all_dirichlet"), (2, "dirichlet_x")])
+def test_scatter_pattern_and_values(k, bc):
+    mesh = HostMesh.box(3, bc=bc)
+    em = oracle_mesh(mesh)
+    eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
+    pat = eng.pattern(mesh)
+    sys = eng.assemble(dm, pat, cs)
+    C = np_(cs.C_slices())
+    Cf = np_(cs.Cf_cols()).T
+    colptr, rowidx, vals, b = core.assemble(em, np.ascontiguousarray(C), np.asfortranarray(Cf))
+    # pattern bit-exact (structurally symmetric: CSR(H) pattern == CSC(H) pattern)
+    assert np.array_equal(np_(sys.rowptr), colptr)
+    assert np.array_equal(np_(sys.colidx), rowidx)
+    # values: CSR row r, col c == CSC entry (r, c) of H; compare via scipy
+    import scipy.sparse as sp
+    nd = len(b)
+    Hg = sp.csr_matrix((np_(sys.vals), np_(sys.colidx), np_(sys.rowptr)), shape=(nd, nd))
+    Ho = sp.csc_matrix((vals, rowidx, colptr), shape=(nd, nd))
+    assert abs(Hg - Ho).max() <= 1e-13 * abs(Ho).max()
+    assert np.max(np.abs(np_(sys.b) - b)) <= 1e-13 * np.max(np.abs(b))
+    # two runs bit-identical (fp64 atomics onto zero commute)
+    sys2 = eng.assemble(dm, pat, cs)
+    assert torch.equal(sys.vals, sys2.vals) and torch.equal(sys.b, sys2.b)
+
+
+# ------------------------------------------------ a11: postprocess
+@pytest.mark.parametrize("k", [1, 3])
+def test_postprocess(k):
+    mesh = HostMesh.box(2)
+    em = oracle_mesh(mesh)
+    eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
+    eng.set_postprocess_rule()
+    rng = np.random.default_rng(11)
+    d3 = dim3(k)
+    arrs = [rng.standard_normal((em.n_elements, d3)) for _ in range(4)]
+    from paper_1305_1489_b200.engine import LocalSolution
+    ls = LocalSolution(*(torch.from_numpy(a).cuda() for a in arrs))
+    us = eng.postprocess_star(g, KAP, ls)
+    t1 = core.tables(k + 1, 2 * (k + 1) + 2, 2 * k + 2)
+    want = core.postprocess_star(em, t1, field(KAP), *(np.asfortranarray(a.T) for a in arrs))
+    assert max_slice_relerr(np_(us), want.T) < TOL
+
+
+# ------------------------------------------------ a6: convection block
+def test_convection_block():
+    k = 2
+    mesh = HostMesh.box(2)
+    em = oracle_mesh(mesh)
+    beta = ("x*y", "y*z", "x + z*z")
+    eng = Engine(0)
+    eng.set_degree(k, 2 * k + 4, 2 * k + 4)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 1.0)
+    vol, dp, dd = eng.convection_bilinear_matrices(g, beta)
+    t = core.tables(k, 2 * k + 4, 2 * k + 4)
+    v0, p0, d0 = core.convection_bilinear_matrices(em, t, vfield(beta))
+    assert max_slice_relerr(np_(vol), v0) < TOL
+    assert max_slice_relerr(np_(dp), p0) < TOL
+    assert max_slice_relerr(np_(dd), d0) < TOL
+
+
+# -------------------------------------------- end-to-end (C1 at full size)
+def test_c1_full_pipeline_matches_oracle():
+    """C1 (k=1, 8^3, 3072 tets): GPU condense -> scatter -> scipy solve ->
+    GPU recover -> GPU postprocess reproduces the oracle's errors."""
+    cfg = CONFIGS["C1"]
+    prob = cfg.problem
+    mesh = HostMesh.box(cfg.n, bc=prob.bc)
+    em = oracle_mesh(mesh)
+    k = cfg.k
+    eng, dm, g, cs = gpu_pipeline(mesh, k, prob.kappa, prob.c, prob.f)
+    pat = eng.pattern(mesh)
+    sys = eng.assemble(dm, pat, cs)
+    d2 = dim2(k)
+    qd = 2 * k + 2
+    ub = core.dirichlet_project(em, k, qd, field(prob.u))
+    b = np_(sys.b) - core.neumann_load(em, k, qd, vfield(prob.q))
+    import scipy.sparse as sp
+    nd = len(b)
+    H = sp.csr_matrix((np_(sys.vals), np_(sys.colidx), np_(sys.rowptr)), shape=(nd, nd)).tocsc()
+    uhat = solve_skeleton(em, H.indptr, H.indices, H.data, b, ub, d2)
+    ls = eng.recover(g, dm, cs, torch.from_numpy(uhat).cuda())
+    eng.set_postprocess_rule()
+    us = eng.postprocess_star(g, prob.kappa, ls)
+    # oracle end to end
+    from oracle_util import solve_level
+    raw = (mesh.coordinates, mesh.elements, mesh.dirichlet, mesh.neumann)
+    ref = solve_level(raw, k, prob)
+    assert relerr(uhat, ref["uhat"]) < 1e-10
+    assert max_slice_relerr(np_(ls.u), ref["u"].T) < 1e-9
+    assert max_slice_relerr(np_(us), ref["ustar"].T) < 1e-9
+
+
+# ---------------------------------------- full-size sampled parity (C2, C3)
+@pytest.mark.parametrize("cfg_name", ["C2", "C3"])
+def test_full_size_sampled_elements(cfg_name):
+    """Full BASELINE mesh on the GPU; ~40 scattered elements re-solved by the
+    oracle on a disjoint sub-mesh with the same face parametrisations."""
+    cfg = CONFIGS[cfg_name]
+    prob = cfg.problem
+    mesh = HostMesh.box(cfg.n, bc=prob.bc, perturb=cfg.perturb, seed=cfg.seed)
+    k = cfg.k
+    eng, dm, g, cs = gpu_pipeline(mesh, k, prob.kappa, prob.c, prob.f, tau=cfg.tau)
+    d2 = dim2(k)
+    eng.set_degree(k)
+    # lambda = face projection of u; here any smooth data works
+    uhat = torch.sin(torch.arange(dm.nfc * d2, dtype=torch.float64, device="cuda") * 0.013)
+    ls = eng.recover(g, dm, cs, uhat)
+    nelt = dm.nelt
+    sel = np.unique(np.linspace(0, nelt - 1, 40).astype(int))
+    # keep elements pairwise non-adjacent
+    fb = mesh.facebyele
+    chosen, used = [], set()
+    for K in sel:
+        if used.isdisjoint(fb[K]):
+            chosen.append(K)
+            used.update(fb[K])
+    sub = submesh(mesh, chosen)
+    _, _, lb, C, Cf = oracle_condense(sub, k, prob.kappa, prob.c, prob.f, cfg.tau)
+    Cg = np_(cs.C_slices())[chosen]
+    assert max_slice_relerr(Cg, C) < TOL
+    assert max_slice_relerr(np_(cs.Cf_cols())[chosen], Cf.T) < TOL
+    uh = np_(uhat)
+    lam = np.stack([np.concatenate([uh[f * d2:(f + 1) * d2] for f in fb[K]]) for K in chosen], axis=1)
+    qx, qy, qz, u = core.local_recover(lb, np.asfortranarray(lam), 4)
+    assert max_slice_relerr(np_(ls.u)[chosen], u.T) < TOL
+    assert max_slice_relerr(np_(ls.qz)[chosen], qz.T) < TOL
