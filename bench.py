@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark of the element-local HDG hot path (BASELINE.json metric):
+
+  HDG elements/s (build+condense+recover, fp64) at k=3
+
+One step = K1 geometry + K2 node build + K3 condense + K5 recover (+ K6 u*
+for C5) over the whole mesh, coefficient fields evaluated at the nodes inside
+the step (as the reference evaluates its callbacks inside build). Default
+workload: config C2 (k=3, 32^3 Kuhn box, 196,608 tets) on one GPU. With N
+GPUs (torchrun) rank r owns z-slab r of a 32 x 32 x 32N box: per-GPU work is
+fixed ("weak" scaling) and the element-local step has no data-path collective.
+
+Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
+engine stream; L2 (126 MB) is flushed by a 512 MB write between steps outside
+the timed interval; per-kernel times come from events recorded around each
+kernel on the same stream (hdg_b200_stage_times). Multi-GPU: barrier +
+synchronize around the timed loop and the max over ranks.
+
+`--impl reference` times the reference algorithm's CPU restatement
+(oracle/, the reference itself cannot be compiled here: no Eigen3) on the
+host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "HDG elements/s (build+condense+recover, fp64) at k=3; % of HBM/FP64 roofline"
+FP64_PEAK_TFLOPS = 37.0   # measured DMMA peak on this pool's B200 (profiles/fp64_peaks_r01.jsonl)
+FP64_PEAK_SOURCE = "profiles/fp64_peaks_r01.jsonl (mma.sync f64 microbenchmark; MEASURED_PEAKS.json has no FP64 entry)"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------- flop model
+def k3_flops(k: int) -> float:
+    """Algorithmic fp64 flops per element of the condense kernel as executed
+    (unpadded counts of each contraction)."""
+    d3 = (k + 1) * (k + 2) * (k + 3) // 6
+    m = 2 * (k + 1) * (k + 2)
+    tri = d3 * (d3 + 1) / 2
+    f = 0.0
+    f += 2 * (d3 ** 3 / 3.0) * 2          # two Cholesky + two triangular inverses
+    f += 3 * 2 * tri * d3                 # Q_# = Li Chat_#^T
+    f += 3 * 3 * 2 * d3 * d3              # Y_s = sum a Q
+    f += 2 * tri * m                      # Z = Li W^T
+    f += 3 * 2 * tri * d3                 # S += sum Y^T Y (lower)
+    f += 3 * 2 * d3 * d3 * m              # V = sum_s Y_s^T (Z n_s)
+    f += 2 * tri * m + 2 * tri            # Vt = LSi V, ft
+    f += 2 * 2 * m * m * d3               # Z^T Z and Vt^T Vt
+    f += 2 * m * d3                       # Cf
+    return f
+
+
+def k2_flops(k: int, nq: int) -> float:
+    d3 = (k + 1) * (k + 2) * (k + 3) // 6
+    nsym = d3 * (d3 + 1) // 2
+    return 2.0 * nsym * nq * 2 + 2.0 * nsym * 4 + 2.0 * d3 * nq
+
+
+def k3_bytes(k: int) -> float:
+    d3 = (k + 1) * (k + 2) * (k + 3) // 6
+    m = 2 * (k + 1) * (k + 2)
+    nsym = d3 * (d3 + 1) // 2
+    fac = 2 * nsym + d3 * m + d3
+    return 8.0 * (2 * nsym + d3 + 30 + m * m + m + fac)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and "Active" in r[4 + i]
+                          and "Not" not in r[4 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- reference arm
+def cpu_sample_mesh(cfg, nlayers: int):
+    """The first `nlayers` cell layers of the config's mesh as a stand-alone
+    mesh (same elements, same geometry; sub-mesh boundary faces listed as
+    Dirichlet), for a bounded CPU sample."""
+    from oracle import core
+    from paper_1305_1489_b200.engine import HostMesh
+    mesh = HostMesh.box(cfg.n, bc=cfg.problem.bc, perturb=cfg.perturb, seed=cfg.seed)
+    ne = 6 * cfg.n * cfg.n * nlayers
+    el = mesh.elements[:ne]
+    verts, inv = np.unique(el, return_inverse=True)
+    el_local = inv.reshape(el.shape).astype(np.int32)
+    lf = [(0, 1, 2), (0, 1, 3), (0, 2, 3), (3, 1, 2)]
+    tris = {}
+    for K in range(ne):
+        for l in range(4):
+            t = tuple(el_local[K, list(lf[l])])
+            key = tuple(sorted(t))
+            tris.setdefault(key, []).append(t)
+    bdry = np.array([v[0] for v in tris.values() if len(v) == 1], dtype=np.int32)
+    em = core.expand(np.asfortranarray(mesh.coordinates[verts]), np.asfortranarray(el_local),
+                     np.asfortranarray(bdry), np.zeros((0, 3), np.int32))
+    return em, mesh
+
+
+def oracle_pipeline_time(cfg, nlayers: int, nthreads: int):
+    from oracle import core
+    from paper_1305_1489_b200.fields import compile_field
+    em, _ = cpu_sample_mesh(cfg, nlayers)
+    k = cfg.k
+    qd = 2 * k + 2
+    t = core.tables(k, qd, qd)
+    fld = lambda e: core.Field.program(compile_field(e).ops, compile_field(e).consts)
+    tau = core.Stabilization(np.full((em.n_elements, 4), float(cfg.tau)))
+    d2 = (k + 1) * (k + 2) // 2
+    uhat = np.asfortranarray(np.sin(np.arange(4 * d2 * em.n_elements, dtype=float) * 0.013).reshape(
+        4 * d2, em.n_elements, order="F"))
+    t0 = time.perf_counter()
+    stages = core.time_pipeline(em, t, fld(cfg.problem.kappa), fld(cfg.problem.c), fld(cfg.problem.f), tau,
+                                uhat, nthreads)
+    wall = time.perf_counter() - t0
+    secs = sum(stages[:4])
+    return em.n_elements / secs, secs, em.n_elements, stages[:4], wall
+
+
+def cpu_baseline_line(cfg, nthreads: int, budget_layers: int):
+    eps, secs, ne, stages, wall = oracle_pipeline_time(cfg, budget_layers, nthreads)
+    return {"value": eps, "unit": "elements/s", "cores": nthreads, "kind": "port",
+            "sample": f"{cfg.name}: first {budget_layers} of {cfg.n} cell layers ({ne} tets), "
+                      f"build+local_blocks 1 thread, condense+recover {nthreads} threads "
+                      f"(study.cpp:19-31); stages s={[round(s, 3) for s in stages]}",
+            "seconds": secs}
+
+
+def run_reference(args):
+    from paper_1305_1489_b200.configs import CONFIGS
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    nthreads = os.cpu_count() or 1
+    layers = args.cpu_layers
+    vals = []
+    for i in range(args.warmup + args.steps):
+        eps, secs, ne, stages, wall = oracle_pipeline_time(cfg, layers, nthreads)
+        if i >= args.warmup:
+            vals.append(eps)
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * ne / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} sample", "k": cfg.k, "tets": ne},
+            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": nthreads, "kind": "port",
+                             "sample": f"{cfg.name}: first {layers} of {cfg.n} cell layers ({ne} tets) per step"},
+            "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1305_1489_b200 import partition
+    from paper_1305_1489_b200.configs import CONFIGS
+    from paper_1305_1489_b200.engine import Engine, Field, HostMesh, LocalSolution, dim2, dim3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    prob = cfg.problem
+    k = cfg.k
+    n = cfg.n
+    t_setup = time.perf_counter()
+    mesh = HostMesh.box(n, n, n * world, bc=prob.bc, perturb=cfg.perturb, seed=cfg.seed)
+    sl = partition.slab(mesh, rank, world)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)
+    eng = Engine(local, stream)
+    eng.set_degree(k)
+    if cfg.postprocess:
+        eng.set_postprocess_rule()
+    dims = eng.dims
+    d3, d2, nq = dims["d3"], dims["d2"], dims["nq"]
+    with torch.cuda.stream(stream):
+        dm = partition.upload_slab(sl, dev)
+        nelt = dm.nelt
+        g = eng.geometry(dm, 1.0)
+        if cfg.upwind_beta:
+            tau = eng.upwind_tau(g, cfg.upwind_beta)
+        else:
+            tau = cfg.tau
+        kap, cc, ff = Field.program(prob.kappa), Field.program(prob.c), Field.program(prob.f)
+        cs = eng.alloc_condensed(nelt)
+        work = eng.work_buffer(nelt)
+        ls = LocalSolution(*(torch.empty(nelt, d3, dtype=torch.float64, device=dev) for _ in range(4)))
+        ustar = torch.empty(nelt, dims["d3_post"], dtype=torch.float64, device=dev) if cfg.postprocess else None
+        # lambda: a smooth deterministic skeleton vector (values do not change the cost)
+        uhat = torch.sin(torch.arange(dm.nfc * d2, dtype=torch.float64, device=dev) * 0.013)
+        flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    stream.synchronize()
+    t_setup = time.perf_counter() - t_setup
+
+    def step():
+        eng.geometry(dm, tau, out=g)
+        eng.build_condense(g, kap, cc, ff, out=cs, work=work, check=False)
+        eng.recover(g, dm, cs, uhat, out=ls)
+        if cfg.postprocess:
+            eng.postprocess_star(g, kap, ls, out=ustar)
+
+    launches_per_step = 2 + 1 + 1 + 1 + 1 + (1 if cfg.postprocess else 0)
+    eng.set_timing(True)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        stream.synchronize()
+        eng.stage_times()
+        # singular check once (outside the timed region)
+        eng.build_condense(g, kap, cc, ff, out=cs, work=work, check=True)
+        eng.stage_times()
+        eng.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        stage_acc = {}
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                flush.zero_()
+                ev[i][0].record(stream)
+                step()
+                ev[i][1].record(stream)
+                for kname, v in eng.stage_times().items():   # waits for this step
+                    stage_acc.setdefault(kname, []).append(v)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = world * nelt / (ms_per_step / 1e3)
+    stage_ms = {kname: float(np.mean(v)) for kname, v in stage_acc.items()}
+
+    # sanity: outputs finite
+    assert torch.isfinite(cs.C).all() and torch.isfinite(ls.u).all(), "non-finite outputs"
+
+    # ---------------------------------------------------------------- e2e
+    # Through the public API with HOST buffers: H2D of the step's inputs (mesh
+    # arrays + lambda, pinned), the step, D2H of its results (C, Cf, q, u).
+    host_in = [t.cpu().pin_memory() for t in (dm.coords, dm.elements, dm.faces, dm.facebyele, uhat)]
+    dev_in = [dm.coords, dm.elements, dm.faces, dm.facebyele, uhat]
+    outs = [cs.C, cs.Cf, ls.qx, ls.qy, ls.qz, ls.u] + ([ustar] if cfg.postprocess else [])
+    host_out = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
+    h2d = sum(t.numel() * t.element_size() for t in host_in)
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
+    e2e_steps = max(1, min(args.steps, 5))
+    with torch.cuda.stream(stream):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            for h, d in zip(host_in, dev_in):
+                d.copy_(h, non_blocking=True)
+            step()
+            for h, d in zip(host_out, outs):
+                h.copy_(d, non_blocking=True)
+        e1.record(stream)
+        e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    eng.set_timing(False)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    hbm_peak, hbm_src = load_peaks()
+    k3_ms = stage_ms.get("condense", float("nan"))
+    achieved = k3_flops(k) * nelt / (k3_ms / 1e3) / 1e12
+    roof = {"kernel": "condense_kernel (K3)", "bound": "tensor", "achieved": achieved,
+            "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+            "traffic": None, "peak_source": FP64_PEAK_SOURCE, "flops_per_element": k3_flops(k),
+            "pipe": "fp64 (DMMA mma.sync m8n8k4)"}
+    kern = {}
+    for kname, v in stage_ms.items():
+        kern[kname] = {"ms": v}
+    if "node_build" in stage_ms:
+        kern["node_build"]["tflops"] = k2_flops(k, nq) * nelt / (stage_ms["node_build"] / 1e3) / 1e12
+    if "condense" in stage_ms:
+        kern["condense"]["tflops"] = achieved
+        kern["condense"]["hbm_gbs"] = k3_bytes(k) * nelt / (stage_ms["condense"] / 1e3) / 1e9
+    if "recover" in stage_ms:
+        rb = 8.0 * (dims["factors"] + 4 * d2 + 30 + 4 * d3)
+        kern["recover"]["hbm_gbs"] = rb * nelt / (stage_ms["recover"] / 1e3) / 1e9
+        kern["recover"]["hbm_frac"] = kern["recover"]["hbm_gbs"] / hbm_peak
+    line = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (closed-form fields at the nodes, BASELINE configs)",
+        "config": {"workload": f"{cfg.name}: k={k}, {n}x{n}x{n * world} Kuhn box, {nelt} tets/GPU ({cfg.note})",
+                   "k": k, "tets_per_gpu": nelt, "parallelism": f"z-slabs x{world}",
+                   "l2": "flushed (512 MB write) between timed steps; per-step working set > 1 GB"},
+        "roofline": roof,
+        "kernels_ms": kern,
+        "e2e": {"value": world * nelt / (e2e_ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "path": "pinned host mesh+lambda -> C ABI step -> pinned host C, Cf, q, u"},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+        "setup_s": t_setup,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_line(cfg, os.cpu_count() or 1, args.cpu_layers)
+            line["speedup_vs_cpu_baseline"] = value / line["cpu_baseline"]["value"]
+        except Exception as exc:  # the CPU leg must not sink the GPU line
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)[:200]}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-layers", type=int, default=2, help="cell layers in the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -212,6 +212,15 @@ int hdg_b200_element_matrices(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg
 int hdg_b200_quad_points(hdg_ctx* ctx, int nelt, const hdg_geometry* g, int which, double* d_X,
                          double* d_Y, double* d_Z);
 
+/* Per-kernel timing with CUDA events recorded on the context stream around each
+ * stage. Stages: 0 geometry (K1), 1 node build (K2), 2 condense (K3),
+ * 3 recover (K5), 4 scatter (K4), 5 postprocess (K6). stage_times waits for
+ * the last recorded event of each stage and returns its duration in ms (-1 if
+ * the stage did not run since the previous query).                        */
+#define HDG_NSTAGES 6
+int hdg_b200_set_timing(hdg_ctx* ctx, int enabled);
+int hdg_b200_stage_times(hdg_ctx* ctx, double ms[HDG_NSTAGES]);
+
 /* Block until the context's stream is idle and report any deferred error. */
 int hdg_b200_synchronize(hdg_ctx* ctx);
 

@@ -15,6 +15,7 @@ HDG_OK, HDG_ESINGULAR, HDG_EINVAL, HDG_ECUDA, HDG_ENCCL, HDG_EMESH, HDG_ESTATE =
 FIELD_CONST, FIELD_SAMPLED, FIELD_PROGRAM = 0, 1, 2
 BC = {"all_dirichlet": 0, "dirichlet_top_bottom": 1, "dirichlet_x": 2}
 MESH_COORDS, MESH_ELEMENTS, MESH_DIRICHLET, MESH_NEUMANN, MESH_FACES, MESH_FACETYPE, MESH_FACEBYELE = range(7)
+STAGES = ("geometry", "node_build", "condense", "recover", "scatter", "postprocess")
 TABLES = dict(tet_bary=0, tet_w=1, P=2, Chat=3, Wlm=4, PP=5, DD=6, tri_bary=7, tri_w=8)
 
 P = C.c_void_p
@@ -89,6 +90,8 @@ _SIGS = {
     "hdg_b200_element_matrices": (C.c_int, [P, C.c_int, C.POINTER(hdg_geometry), hdg_field, hdg_field,
                                             hdg_field, C.POINTER(hdg_element_matrices)]),
     "hdg_b200_quad_points": (C.c_int, [P, C.c_int, C.POINTER(hdg_geometry), C.c_int, P, P, P]),
+    "hdg_b200_set_timing": (C.c_int, [P, C.c_int]),
+    "hdg_b200_stage_times": (C.c_int, [P, DP]),
     "hdg_b200_synchronize": (C.c_int, [P]),
 }
 

@@ -214,11 +214,24 @@ struct hdg_ctx {
   long long* h_bad = nullptr;
   int* d_status = nullptr;
   int* h_status = nullptr;
+  bool timing = false;
+  cudaEvent_t ev[2 * HDG_NSTAGES] = {};
+  bool pending[HDG_NSTAGES] = {};
 };
 
 namespace {
 
 void set_device(hdg_ctx* c) { CUDA_OK(cudaSetDevice(c->device)); }
+
+// CUDA events around each stage on the launching stream (hdg_b200_set_timing).
+void stage_begin(hdg_ctx* c, int s) {
+  if (c->timing) CUDA_OK(cudaEventRecord(c->ev[2 * s], c->stream));
+}
+void stage_end(hdg_ctx* c, int s) {
+  if (!c->timing) return;
+  CUDA_OK(cudaEventRecord(c->ev[2 * s + 1], c->stream));
+  c->pending[s] = true;
+}
 
 void* ctx_work(hdg_ctx* c, size_t bytes) {
   if (bytes > c->work_bytes) {
@@ -415,6 +428,8 @@ void hdg_b200_destroy(hdg_ctx* c) {
   if (c->h_bad) cudaFreeHost(c->h_bad);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -507,11 +522,13 @@ int hdg_b200_geometry(hdg_ctx* c, int nver, int nelt, int nfc, const double* d_c
     const int init[2] = {INT_MAX, INT_MAX};
     std::memcpy(c->h_status, init, sizeof(init));
     CUDA_OK(cudaMemcpyAsync(c->d_status, c->h_status, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    stage_begin(c, 0);
     face_area_kernel<<<(nfc + 255) / 256, 256, 0, c->stream>>>(nver, nfc, d_coords, d_faces, g->area);
     geometry_kernel<<<(nelt + 127) / 128, 128, 0, c->stream>>>(
         nver, nelt, nfc, d_coords, d_elements, d_faces, d_facebyele, d_tau, tau_const, g->area,
         g->volume, g->piola, g->normals, g->perm, g->T, g->verts, c->d_status);
     CUDA_OK(cudaGetLastError());
+    stage_end(c, 0);
   });
 }
 
@@ -565,11 +582,15 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     double* fv = Ds + size_t(nelt) * t.nsym;
     const size_t qsmem = size_t(3) * (t.nqp + 4) * kQuadLDB * sizeof(double);
     CUDA_OK(cudaFuncSetAttribute(quad_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
+    stage_begin(c, 1);
     quad_build_kernel<<<(nelt + kQuadEB - 1) / kQuadEB, kQuadThreads, qsmem, c->stream>>>(t, nelt, geo, fk, fc,
                                                                                           ff, Ms, Ds, fv);
     CUDA_OK(cudaGetLastError());
+    stage_end(c, 1);
     set_ll_kernel<<<1, 1, 0, c->stream>>>(c->d_bad, LLONG_MAX);
+    stage_begin(c, 2);
     DISPATCH_K(t.k, launch_condense, c, nelt, geo, Ms, Ds, fv, d_C, d_Cf, d_factors);
+    stage_end(c, 2);
     check_bad(c, bad_element);
   });
 }
@@ -584,8 +605,10 @@ int hdg_b200_recover(hdg_ctx* c, int nelt, const hdg_geometry* g, const int* d_f
     require(c->tab[0].ready, HDG_ESTATE, "set_degree first");
     const GeoDev geo = to_geo(g);
     set_device(c);
+    stage_begin(c, 3);
     DISPATCH_K(c->tab[0].dev.k, launch_recover, c, nelt, geo, d_facebyele, d_factors, d_uhat, d_qx, d_qy,
                d_qz, d_u);
+    stage_end(c, 3);
   });
 }
 
@@ -610,9 +633,11 @@ int hdg_b200_scatter(hdg_ctx* c, int nelt, int d2, const int* d_facebyele, const
     require(c && d_facebyele && d_slot && d_facebase && d_C && d_Cf && d_vals && d_b && nelt > 0 && d2 > 0,
             HDG_EINVAL, "bad argument");
     set_device(c);
+    stage_begin(c, 4);
     scatter_kernel<<<(nelt + 7) / 8, 256, 0, c->stream>>>(nelt, d2, d_facebyele, d_slot, d_facebase, d_C,
                                                          d_Cf, d_vals, d_b);
     CUDA_OK(cudaGetLastError());
+    stage_end(c, 4);
   });
 }
 
@@ -633,9 +658,11 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
     CUDA_OK(cudaFuncSetAttribute(postprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const long need = (long(nelt) + nw - 1) / nw;
     const int grid = int(std::min<long>(need, long(c->sms) * 8));
+    stage_begin(c, 5);
     postprocess_kernel<<<grid, nw * 32, smem, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, qx, qy, qz, u,
                                                           ustar, per_warp);
     CUDA_OK(cudaGetLastError());
+    stage_end(c, 5);
   });
 }
 
@@ -679,6 +706,32 @@ int hdg_b200_element_matrices(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_f
     element_matrices_kernel<<<grid, nw * 32, smem, c->stream>>>(t, nelt, geo, to_dev(kappa, "kappa"),
                                                                to_dev(cf, "c"), to_dev(f, "f"), o, per_warp);
     CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_set_timing(hdg_ctx* c, int enabled) {
+  return guarded([&] {
+    require(c != nullptr, HDG_EINVAL, "ctx is NULL");
+    set_device(c);
+    if (enabled && !c->ev[0])
+      for (auto& e : c->ev) CUDA_OK(cudaEventCreate(&e));
+    c->timing = enabled != 0;
+  });
+}
+
+int hdg_b200_stage_times(hdg_ctx* c, double ms[HDG_NSTAGES]) {
+  return guarded([&] {
+    require(c && ms, HDG_EINVAL, "NULL argument");
+    set_device(c);
+    for (int s = 0; s < HDG_NSTAGES; ++s) {
+      ms[s] = -1.0;
+      if (!c->pending[s]) continue;
+      CUDA_OK(cudaEventSynchronize(c->ev[2 * s + 1]));
+      float t = 0.f;
+      CUDA_OK(cudaEventElapsedTime(&t, c->ev[2 * s], c->ev[2 * s + 1]));
+      ms[s] = t;
+      c->pending[s] = false;
+    }
   });
 }
 

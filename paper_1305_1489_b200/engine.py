@@ -318,6 +318,15 @@ class Engine:
     def synchronize(self) -> None:
         L.check(L.lib().hdg_b200_synchronize(self._ctx))
 
+    def set_timing(self, enabled: bool) -> None:
+        L.check(L.lib().hdg_b200_set_timing(self._ctx, int(enabled)))
+
+    def stage_times(self) -> dict:
+        """ms per stage since the last query (CUDA events on the engine stream)."""
+        ms = (C.c_double * 6)()
+        L.check(L.lib().hdg_b200_stage_times(self._ctx, ms))
+        return {n: ms[i] for i, n in enumerate(L.STAGES) if ms[i] >= 0}
+
     # ---------------------------------------------------------------- K1
     def geometry(self, dm: DeviceMesh, tau: Union[float, torch.Tensor] = 1.0,
                  out: Optional[Geometry] = None) -> Geometry:
