@@ -16,6 +16,7 @@
 #include "kernels_local.cuh"
 #include "kernels_misc.cuh"
 #include "kernels_post.cuh"
+#include "kernels_condense2.cuh"
 
 using namespace hdgb;
 
@@ -250,13 +251,10 @@ int factor_doubles(int k) {
   return d3 * (d3 + 1) + d3 * m + d3;
 }
 
-template <int K_>
-void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, const double* Ds,
-                     const double* fv, double* C, double* Cf, double* F) {
-  using Dm = CondDims<K_>;
-  using Cg = CondCfg<K_>;
+template <class Dm, class Cg, class Kern>
+void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, const double* Ms,
+                          const double* Ds, const double* fv, double* C, double* Cf, double* F) {
   const size_t smem = size_t(Cg::EPB) * Dm::PER_ELT * sizeof(double);
-  auto kern = condense_kernel<K_>;
   CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int occ = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cg::NW * 32 * Cg::EPB, smem));
@@ -268,12 +266,26 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
   CUDA_OK(cudaGetLastError());
 }
 
+// k <= 3: explicit-inverse kernel (kernels_condense2.cuh); k >= 4: triangular-factor kernel.
+template <int K_>
+void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, const double* Ds,
+                     const double* fv, double* C, double* Cf, double* F) {
+  if constexpr (K_ <= 3)
+    launch_condense_impl<C2Dims<K_>, C2Cfg<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+  else
+    launch_condense_impl<CondDims<K_>, CondCfg<K_>>(c, condense_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+}
+
 template <int K_>
 void launch_recover(hdg_ctx* c, int nelt, const GeoDev& geo, const int* fbe, const double* F,
                     const double* uhat, double* qx, double* qy, double* qz, double* u) {
   const int grid = (nelt + kRecWarps - 1) / kRecWarps;
-  recover_kernel<K_><<<grid, kRecWarps * 32, 0, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat, qx,
-                                                              qy, qz, u);
+  if constexpr (K_ <= 3)
+    recover2_kernel<K_><<<grid, kRecWarps * 32, 0, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat, qx,
+                                                                 qy, qz, u);
+  else
+    recover_kernel<K_><<<grid, kRecWarps * 32, 0, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat, qx,
+                                                                qy, qz, u);
   CUDA_OK(cudaGetLastError());
 }
 

@@ -1,0 +1,490 @@
+// K3 v2 (k <= 3): static condensation with explicit inverses.
+//
+// Same block elimination as kernels_local.cuh, written with M^-1 and S^-1
+// instead of triangular factors (only products X M^-1 Y^T appear):
+//   Zp = Mi W^T,                         Gw = W Zp                (face Gram)
+//   Y_s = Mi C_s^T,  S = D + sum_s C_s Y_s,  H = sum_s C_s Zp N_s  (N_s: per-face n_s)
+//   Si = S^-1,  V = H + T^T,  Vs = Si V
+//   C  = tauDD + (n_l1.n_l2) o Gw - V^T Vs,   Cf = Vs^T f
+// The two d3 x d3 inverses are Gauss-Jordan sweeps held in one warp's
+// registers (lane c owns column c; SPD, so no pivoting; the pivots are the
+// Cholesky pivots and feed the reference's 1e-14 singularity test). Every
+// contraction is a DMMA (mma.sync m8n8k4 f64) tile loop over shared memory;
+// a team of NW warps handles one element with 6 named barriers per element.
+// The recovery cache is {Mi, Si (packed lower), V, f}.
+#pragma once
+
+#include "dev_common.cuh"
+#include "kernels_local.cuh"
+
+namespace hdgb {
+
+template <int K_>
+struct C2Dims {
+  static constexpr int D3 = cdim3(K_), D2 = cdim2(K_), M = 4 * cdim2(K_);
+  static constexpr int D3P = round_up(cdim3(K_), 8), MP = round_up(4 * cdim2(K_), 8);
+  static constexpr int LD = D3P + 4;  // 4 or 12 (mod 16): conflict-free fragment loads
+  static constexpr int NSYM = D3 * (D3 + 1) / 2;
+  static constexpr int MT = D3P / 8, NTM = MP / 8, KS = D3P / 4;
+  static constexpr int OFF_MI = 0;
+  static constexpr int OFF_S = OFF_MI + D3P * LD;
+  static constexpr int OFF_Y = OFF_S + D3P * LD;
+  static constexpr int OFF_Z = OFF_Y + 3 * D3P * LD;   // Zp, later Vs
+  static constexpr int OFF_V = OFF_Z + MP * LD;
+  static constexpr int OFF_NSC = OFF_V + MP * LD;      // 3 x MP face normals per column
+  static constexpr int OFF_TC = OFF_NSC + 3 * MP;      // MP: tau|e| per column
+  static constexpr int OFF_WB = OFF_TC + MP;           // MP: W table offset per column (as double)
+  static constexpr int OFF_F = OFF_WB + MP;            // D3P: f
+  static constexpr int OFF_FS = OFF_F + D3P;           // D3P: Si f
+  static constexpr int OFF_STG = OFF_FS + D3P;         // 32: GJ column stage
+  static constexpr int OFF_GEO = OFF_STG + 32;         // 32: geometry record
+  static constexpr int PER_ELT = OFF_GEO + 32;
+  static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
+};
+
+template <int K_> struct C2Cfg;
+template <> struct C2Cfg<0> { static constexpr int NW = 1, EPB = 8; };
+template <> struct C2Cfg<1> { static constexpr int NW = 1, EPB = 16; };
+template <> struct C2Cfg<2> { static constexpr int NW = 2, EPB = 8; };
+template <> struct C2Cfg<3> { static constexpr int NW = 2, EPB = 4; };
+
+// Gauss-Jordan inverse of the SPD N x N matrix whose column c lane c holds in
+// a[]; on return a[] holds column c of the inverse. pmin/pmax: pivot range.
+template <int N>
+__device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, int lane, double& pmin,
+                                                double& pmax) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    if (lane == j) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) stage[i] = a[i];
+    }
+    __syncwarp();
+    double col[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) col[i] = stage[i];
+    __syncwarp();
+    const double p = col[j];
+    pmin = fmin(pmin, p);
+    pmax = fmax(pmax, p);
+    const double ip = 1.0 / p;
+    const bool me = lane == j;
+    const double f = me ? ip : a[j] * ip;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (i == j) continue;
+      const double base = me ? 0.0 : a[i];
+      a[i] = fma(-col[i], f, base);
+    }
+    a[j] = f;
+  }
+}
+
+template <int K_>
+__global__ void __launch_bounds__(C2Cfg<K_>::NW * 32 * C2Cfg<K_>::EPB)
+condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
+                 const double* __restrict__ Dsym, const double* __restrict__ fvec,
+                 double* __restrict__ Cout, double* __restrict__ Cfout, double* __restrict__ factors,
+                 long long* bad_element) {
+  using Dm = C2Dims<K_>;
+  constexpr int NW = C2Cfg<K_>::NW, EPB = C2Cfg<K_>::EPB, NT = NW * 32;
+  constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, D3P = Dm::D3P, MP = Dm::MP, LD = Dm::LD;
+  constexpr int MT = Dm::MT, NTM = Dm::NTM, KS = Dm::KS;
+  extern __shared__ double smem[];
+  for (int i = threadIdx.x; i < EPB * Dm::PER_ELT; i += blockDim.x) smem[i] = 0.0;
+  __syncthreads();
+
+  Team<NW> tm;
+  tm.id = threadIdx.x / NT;
+  tm.tid = threadIdx.x % NT;
+  tm.warp = tm.tid >> 5;
+  tm.lane = tm.tid & 31;
+  const int lane = tm.lane, g = lane >> 2, t = lane & 3;
+  double* base = smem + tm.id * Dm::PER_ELT;
+  double* Mi = base + Dm::OFF_MI;
+  double* Sb = base + Dm::OFF_S;
+  double* Yb = base + Dm::OFF_Y;
+  double* Zb = base + Dm::OFF_Z;
+  double* Vb = base + Dm::OFF_V;
+  double* nsc = base + Dm::OFF_NSC;
+  double* Tc = base + Dm::OFF_TC;
+  int* wb = reinterpret_cast<int*>(base + Dm::OFF_WB);
+  double* fv = base + Dm::OFF_F;
+  double* fs = base + Dm::OFF_FS;
+  double* stg = base + Dm::OFF_STG;
+  double* sg = base + Dm::OFF_GEO;
+  const double* a9 = sg + 1;
+  const double* Wlm = tab.Wlm;
+  const double* Ch = tab.Chat;
+
+  const long stride = long(gridDim.x) * EPB;
+  for (long K = long(blockIdx.x) * EPB + tm.id; K < nelt; K += stride) {
+    double* Ck = Cout + K * M * M;
+    double* F = factors ? factors + K * Dm::FACTORS : nullptr;
+    bool bad = false;
+    // ------------------------------------------------ P0: loads + GJ(M)
+    load_geo(geo, K, nelt, sg, tm.tid, NT);
+    for (int j = 0; j < D3; ++j) {  // D (lower) -> S
+      const int b0 = sym_idx(j, j, D3);
+      for (int i = tm.tid; i < D3 - j; i += NT) Sb[(j + i) + j * LD] = Dsym[K * Dm::NSYM + b0 + i];
+    }
+    for (int i = tm.tid; i < D3; i += NT) fv[i] = fvec[K * D3 + i];
+    if (tm.warp == 0) {
+      double a[D3];
+#pragma unroll
+      for (int i = 0; i < D3; ++i) {
+        const int r = i > lane ? i : lane, c = i > lane ? lane : i;
+        a[i] = lane < D3 ? Msym[K * Dm::NSYM + sym_idx(r, c, D3)] : (i == lane ? 1.0 : 0.0);
+      }
+      double pmin = 1e300, pmax = 0.0;
+      warp_gj_inverse<D3>(a, stg, lane, pmin, pmax);
+      bad |= !(pmin > 0.0) || pmin < 1e-14 * pmax;
+      if (lane < D3) {
+#pragma unroll
+        for (int i = 0; i < D3; ++i) Mi[i + lane * LD] = a[i];
+        if (F) {
+#pragma unroll
+          for (int i = 0; i < D3; ++i)
+            if (i >= lane) F[sym_idx(i, lane, D3)] = a[i];
+        }
+      }
+    }
+    tm.sync();
+    // per-column face data (needs geometry)
+    for (int c = tm.tid; c < MP; c += NT) {
+      if (c < M) {
+        const int l = c / D2, i = c - l * D2;
+        const int mu = int(sg[26 + l]);
+#pragma unroll
+        for (int s = 0; s < 3; ++s) nsc[s * MP + c] = sg[10 + 3 * l + s];
+        Tc[c] = sg[22 + l];
+        wb[c] = (6 * l + mu - 1) * D2 * D3 + i;
+      } else {
+#pragma unroll
+        for (int s = 0; s < 3; ++s) nsc[s * MP + c] = 0.0;
+        Tc[c] = 0.0;
+        wb[c] = -1;
+      }
+    }
+    tm.sync();
+
+    // ------------------------------------- P1: Zp = Mi W^T, Y_s = Mi C_s^T
+    // tasks: NTM column strips of Zp, 3*MT column strips of Y (all MT row tiles per task)
+    for (int task = tm.warp; task < NTM + 3 * MT; task += NW) {
+      double acc[MT][2];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+      if (task < NTM) {
+        const int c = task * 8 + g;
+        const int wbc = wb[c];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          const double b = (wbc >= 0 && k < D3) ? __ldg(Wlm + wbc + k * D2) : 0.0;
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], Mi[(m * 8 + g) + k * LD], b);
+        }
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const int r = m * 8 + g, c0 = task * 8 + 2 * t;
+          Zb[r + c0 * LD] = acc[m][0];
+          Zb[r + (c0 + 1) * LD] = acc[m][1];
+        }
+      } else {
+        const int s = (task - NTM) / MT, nt = (task - NTM) % MT;
+        const int c = nt * 8 + g;
+        const double as0 = a9[3 * s], as1 = a9[3 * s + 1], as2 = a9[3 * s + 2];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          double b = 0.0;  // C_s^T(k, c) = sum_# a(s,#) Chat_#(c, k)
+          if (k < D3 && c < D3) {
+            const int o = c + k * D3;
+            b = as0 * __ldg(Ch + o) + as1 * __ldg(Ch + D3 * D3 + o) + as2 * __ldg(Ch + 2 * D3 * D3 + o);
+          }
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], Mi[(m * 8 + g) + k * LD], b);
+        }
+        double* Y = Yb + s * D3P * LD;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const int r = m * 8 + g, c0 = nt * 8 + 2 * t;
+          Y[r + c0 * LD] = acc[m][0];
+          Y[r + (c0 + 1) * LD] = acc[m][1];
+        }
+      }
+    }
+    tm.sync();
+
+    // ------------------- P2: S += sum_s C_s Y_s (lower), H = sum_s C_s Zp N_s,
+    //                         Gw tiles -> C (tauDD + nn o Gw), mirrored
+    for (int task = tm.warp; task < MT + NTM; task += NW) {
+      if (task < MT) {
+        const int mt = task;
+        double accS[MT][2], accH[NTM][2];
+#pragma unroll
+        for (int j = 0; j < MT; ++j) accS[j][0] = accS[j][1] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NTM; ++j) accH[j][0] = accH[j][1] = 0.0;
+        const int r = mt * 8 + g;
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+          const double as0 = a9[3 * s], as1 = a9[3 * s + 1], as2 = a9[3 * s + 2];
+          const double* Y = Yb + s * D3P * LD;
+          double ns[NTM];
+#pragma unroll
+          for (int j = 0; j < NTM; ++j) ns[j] = nsc[s * MP + j * 8 + g];
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk) {
+            const int k = kk * 4 + t;
+            double a = 0.0;  // C_s(r, k)
+            if (r < D3 && k < D3) {
+              const int o = r + k * D3;
+              a = as0 * __ldg(Ch + o) + as1 * __ldg(Ch + D3 * D3 + o) + as2 * __ldg(Ch + 2 * D3 * D3 + o);
+            }
+#pragma unroll
+            for (int j = 0; j < MT; ++j)
+              if (j <= mt) dmma(accS[j][0], accS[j][1], a, Y[k + (j * 8 + g) * LD]);
+#pragma unroll
+            for (int j = 0; j < NTM; ++j) dmma(accH[j][0], accH[j][1], a, Zb[k + (j * 8 + g) * LD] * ns[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < MT; ++j) {
+          if (j > mt) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = j * 8 + 2 * t + h;
+            if (r < D3 && c <= r) Sb[r + c * LD] += accS[j][h];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NTM; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = j * 8 + 2 * t + h;
+            if (r < D3 && c < M) Vb[r + c * LD] = accH[j][h] + Tc[c] * __ldg(Wlm + wb[c] + r * D2);
+          }
+      } else {
+        // Gw = W Zp, lower tiles of row strip mt; C <- tauDD + nn o Gw (both triangles)
+        const int mt = task - MT;
+        const int r = mt * 8 + g;
+        double acc[NTM][2];
+#pragma unroll
+        for (int j = 0; j < NTM; ++j) acc[j][0] = acc[j][1] = 0.0;
+        const int wbr = wb[r];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          const double a = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
+#pragma unroll
+          for (int j = 0; j < NTM; ++j)
+            if (j <= mt) dmma(acc[j][0], acc[j][1], a, Zb[k + (j * 8 + g) * LD]);
+        }
+        if (r < M) {
+          const int l1 = r / D2;
+          const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
+#pragma unroll
+          for (int j = 0; j < NTM; ++j) {
+            if (j > mt) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = j * 8 + 2 * t + h;
+              if (c > r || c >= M) continue;
+              const int l2 = c / D2;
+              const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
+              double v = nn * acc[j][h];
+              if (l1 == l2) v += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
+              Ck[r + c * M] = v;
+              if (c != r) Ck[c + r * M] = v;
+            }
+          }
+        }
+      }
+    }
+    tm.sync();
+
+    // ----------------------------------------------- P3: Si = S^-1 (warp 0)
+    if (tm.warp == 0) {
+      double a[D3];
+#pragma unroll
+      for (int i = 0; i < D3; ++i) {
+        const int r = i > lane ? i : lane, c = i > lane ? lane : i;
+        a[i] = lane < D3 ? Sb[r + c * LD] : (i == lane ? 1.0 : 0.0);
+      }
+      double pmin = 1e300, pmax = 0.0;
+      warp_gj_inverse<D3>(a, stg, lane, pmin, pmax);
+      bad |= !(pmin > 0.0) || pmin < 1e-14 * pmax;
+      if (lane < D3) {
+#pragma unroll
+        for (int i = 0; i < D3; ++i) Sb[i + lane * LD] = a[i];
+        if (F) {
+#pragma unroll
+          for (int i = 0; i < D3; ++i)
+            if (i >= lane) F[Dm::NSYM + sym_idx(i, lane, D3)] = a[i];
+        }
+      }
+    } else if (F) {
+      for (int idx = tm.tid - 32; idx < D3 * M; idx += NT - 32) {
+        const int r = idx % D3, c = idx / D3;
+        F[2 * Dm::NSYM + idx] = Vb[r + c * LD];
+      }
+    }
+    if (F && tm.warp == NW - 1)
+      for (int i = lane; i < D3; i += 32) F[2 * Dm::NSYM + D3 * M + i] = fv[i];
+    if (F && NW == 1) {
+      for (int idx = lane; idx < D3 * M; idx += 32) {
+        const int r = idx % D3, c = idx / D3;
+        F[2 * Dm::NSYM + idx] = Vb[r + c * LD];
+      }
+    }
+    tm.sync();
+
+    // ----------------------------------------- P4: Vs = Si V (into Zb), fs = Si f
+    for (int task = tm.warp; task < NTM; task += NW) {
+      double acc[MT][2];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+      const int c = task * 8 + g;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const int k = kk * 4 + t;
+        const double b = Vb[k + c * LD];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], Sb[(m * 8 + g) + k * LD], b);
+      }
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int r = m * 8 + g, c0 = task * 8 + 2 * t;
+        Zb[r + c0 * LD] = acc[m][0];
+        Zb[r + (c0 + 1) * LD] = acc[m][1];
+      }
+    }
+    for (int r = tm.tid; r < D3; r += NT) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < D3; ++k) s += Sb[r + k * LD] * fv[k];
+      fs[r] = s;
+    }
+    tm.sync();
+
+    // --------------------------- P5: C -= V^T Vs (lower tiles, mirrored); Cf
+    for (int task = tm.warp; task < NTM; task += NW) {
+      const int mt = task;
+      const int r = mt * 8 + g;
+      double acc[NTM][2];
+#pragma unroll
+      for (int j = 0; j < NTM; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const int k = kk * 4 + t;
+        const double a = Vb[k + r * LD];
+#pragma unroll
+        for (int j = 0; j < NTM; ++j)
+          if (j <= mt) dmma(acc[j][0], acc[j][1], a, Zb[k + (j * 8 + g) * LD]);
+      }
+      if (r < M) {
+#pragma unroll
+        for (int j = 0; j < NTM; ++j) {
+          if (j > mt) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = j * 8 + 2 * t + h;
+            if (c > r || c >= M) continue;
+            const double v = Ck[r + c * M] - acc[j][h];
+            Ck[r + c * M] = v;
+            if (c != r) Ck[c + r * M] = v;
+          }
+        }
+      }
+    }
+    for (int r = tm.tid; r < M; r += NT) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < D3; ++k) s += Vb[k + r * LD] * fs[k];
+      Cfout[K * M + r] = s;
+    }
+    if (bad) flag_bad(bad_element, K);
+    tm.sync();
+  }
+}
+
+// K5 for the v2 cache {Mi, Si, V, f}:
+//   u = Si (f + V lambda),  q_s = Mi (C_s^T u - E_s^T lambda)
+template <int K_>
+__global__ void __launch_bounds__(kRecWarps * 32)
+recover2_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ facebyele,
+                const double* __restrict__ factors, const double* __restrict__ uhat,
+                double* __restrict__ qx, double* __restrict__ qy, double* __restrict__ qz,
+                double* __restrict__ uout) {
+  using Dm = C2Dims<K_>;
+  using Rd = RecDims<K_>;
+  constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, NS = Dm::NSYM;
+  __shared__ double sh[kRecWarps][Rd::PER_WARP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* lam = sh[warp];
+  double* tv = lam + Rd::S1;
+  double* uu = tv + Rd::S3;
+  double* pp = uu + Rd::SD;
+  double* sg = pp + Rd::S3;
+  const long K = long(blockIdx.x) * kRecWarps + warp;
+  if (K >= nelt) return;
+  const double* F = factors + K * Dm::FACTORS;
+  const double* Mi = F;
+  const double* Si = F + NS;
+  const double* V = F + 2 * NS;
+  const double* f = F + 2 * NS + D3 * M;
+  load_geo(geo, K, nelt, sg, lane, 32);
+  for (int i = lane; i < M; i += 32) {
+    const int l = i / D2;
+    lam[i] = uhat[long(facebyele[long(l) * nelt + K]) * D2 + (i - l * D2)];
+  }
+  __syncwarp();
+  for (int r = lane; r < D3; r += 32) {  // t = f + V lambda
+    double s = f[r];
+    for (int c = 0; c < M; ++c) s += V[r + c * D3] * lam[c];
+    tv[r] = s;
+  }
+  __syncwarp();
+  for (int i = lane; i < D3; i += 32) {  // u = Si t (symmetric, packed lower)
+    double s = 0.0;
+    for (int r = 0; r < D3; ++r) s += Si[r >= i ? sym_idx(r, i, D3) : sym_idx(i, r, D3)] * tv[r];
+    uu[i] = s;
+  }
+  __syncwarp();
+  const double* a9 = sg + 1;
+  const double* nrm = sg + 10;
+  const double* pm = sg + 26;
+  for (int j = lane; j < D3; j += 32) {
+    double p[3];
+    for (int s = 0; s < 3; ++s) {
+      const double* C = tab.Chat + s * D3 * D3 + j * D3;
+      double acc = 0.0;
+      for (int i = 0; i < D3; ++i) acc += __ldg(C + i) * uu[i];
+      p[s] = acc;
+    }
+    double w[4];
+    for (int l = 0; l < 4; ++l) {
+      const double* W = tab.Wlm + (6 * l + int(pm[l]) - 1) * D2 * D3 + j * D2;
+      double acc = 0.0;
+      for (int i = 0; i < D2; ++i) acc += __ldg(W + i) * lam[l * D2 + i];
+      w[l] = acc;
+    }
+    for (int s = 0; s < 3; ++s) {
+      double r = a9[3 * s] * p[0] + a9[3 * s + 1] * p[1] + a9[3 * s + 2] * p[2];
+      for (int l = 0; l < 4; ++l) r -= nrm[3 * l + s] * w[l];
+      pp[s * D3 + j] = r;
+    }
+  }
+  __syncwarp();
+  double* outs[3] = {qx, qy, qz};
+  for (int idx = lane; idx < 3 * D3; idx += 32) {  // q_s = Mi r_s
+    const int s = idx / D3, i = idx - s * D3;
+    double acc = 0.0;
+    for (int j = 0; j < D3; ++j) acc += Mi[j >= i ? sym_idx(j, i, D3) : sym_idx(i, j, D3)] * pp[s * D3 + j];
+    outs[s][K * D3 + i] = acc;
+  }
+  for (int i = lane; i < D3; i += 32) uout[K * D3 + i] = uu[i];
+}
+
+}  // namespace hdgb
