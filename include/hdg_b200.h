@@ -221,6 +221,12 @@ int hdg_b200_quad_points(hdg_ctx* ctx, int nelt, const hdg_geometry* g, int whic
 int hdg_b200_set_timing(hdg_ctx* ctx, int enabled);
 int hdg_b200_stage_times(hdg_ctx* ctx, double ms[HDG_NSTAGES]);
 
+/* Program fields are compiled into K2 at run time (NVRTC, cached per field
+ * set); disable to force the in-kernel field interpreter. jit_status returns
+ * the last JIT failure ("" if none; on failure the interpreter runs).      */
+int hdg_b200_set_jit(hdg_ctx* ctx, int enabled);
+const char* hdg_b200_jit_status(const hdg_ctx* ctx);
+
 /* Block until the context's stream is idle and report any deferred error. */
 int hdg_b200_synchronize(hdg_ctx* ctx);
 

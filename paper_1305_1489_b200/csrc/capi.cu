@@ -17,6 +17,7 @@
 #include "kernels_misc.cuh"
 #include "kernels_post.cuh"
 #include "kernels_condense2.cuh"
+#include "jit_quad.hpp"
 
 using namespace hdgb;
 
@@ -216,6 +217,8 @@ struct hdg_ctx {
   int* d_status = nullptr;
   int* h_status = nullptr;
   bool timing = false;
+  bool jit = true;          // NVRTC-specialised K2 for program fields
+  std::string jit_error;    // last JIT failure (kernel then runs interpreted)
   cudaEvent_t ev[2 * HDG_NSTAGES] = {};
   bool pending[HDG_NSTAGES] = {};
 };
@@ -593,10 +596,30 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     double* Ds = Ms + size_t(nelt) * t.nsym;
     double* fv = Ds + size_t(nelt) * t.nsym;
     const size_t qsmem = size_t(3) * (t.nqp + 4) * kQuadLDB * sizeof(double);
-    CUDA_OK(cudaFuncSetAttribute(quad_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
+    const int qgrid = (nelt + kQuadEB - 1) / kQuadEB;
+    const bool any_prog = kappa.kind == HDG_FIELD_PROGRAM || cf.kind == HDG_FIELD_PROGRAM || f.kind == HDG_FIELD_PROGRAM;
+    CUfunction jfn = nullptr;
+    if (c->jit && any_prog) {
+      std::string err;
+      jfn = jit_quad_kernel(kappa, cf, f, &err);
+      if (!jfn) c->jit_error = err;
+    }
     stage_begin(c, 1);
-    quad_build_kernel<<<(nelt + kQuadEB - 1) / kQuadEB, kQuadThreads, qsmem, c->stream>>>(t, nelt, geo, fk, fc,
-                                                                                          ff, Ms, Ds, fv);
+    bool launched = false;
+    if (jfn) {
+      int nel = nelt, nq = t.nq, nqp = t.nqp, nsym = t.nsym, nsymp = t.nsymp, d3 = t.d3, d3p = t.d3p;
+      const double *bary = t.bary, *w = t.w, *As = t.Asym, *Af = t.Af, *vol = geo.volume, *T = geo.T,
+                   *V = geo.verts, *sk = kappa.samples, *sc = cf.samples, *sf = f.samples;
+      void* args[] = {&nel, &nq, &nqp, &nsym, &nsymp, &d3, &d3p, &bary, &w, &As, &Af, &vol, &T, &V,
+                      &sk, &sc, &sf, &Ms, &Ds, &fv};
+      std::string err;
+      launched = launch_quad_jit(jfn, c->stream, qgrid, kQuadThreads, qsmem, args, &err);
+      if (!launched) c->jit_error = err;
+    }
+    if (!launched) {
+      CUDA_OK(cudaFuncSetAttribute(quad_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
+      quad_build_kernel<<<qgrid, kQuadThreads, qsmem, c->stream>>>(t, nelt, geo, fk, fc, ff, Ms, Ds, fv);
+    }
     CUDA_OK(cudaGetLastError());
     stage_end(c, 1);
     set_ll_kernel<<<1, 1, 0, c->stream>>>(c->d_bad, LLONG_MAX);
@@ -746,6 +769,15 @@ int hdg_b200_stage_times(hdg_ctx* c, double ms[HDG_NSTAGES]) {
     }
   });
 }
+
+int hdg_b200_set_jit(hdg_ctx* c, int enabled) {
+  return guarded([&] {
+    require(c != nullptr, HDG_EINVAL, "ctx is NULL");
+    c->jit = enabled != 0;
+  });
+}
+
+const char* hdg_b200_jit_status(const hdg_ctx* c) { return c ? c->jit_error.c_str() : ""; }
 
 int hdg_b200_synchronize(hdg_ctx* c) {
   return guarded([&] {

@@ -1,0 +1,253 @@
+// Runtime specialisation of K2 for coefficient programs (NVRTC, sm_100a).
+//
+// The reference evaluates its coefficient callbacks on the node arrays inside
+// build_element_matrices (element_matrices.cpp:94-109, :84-92). Interpreting a
+// field program per node is dispatch-bound on the GPU, so K2 is compiled at
+// run time with the three field expressions inlined as straight-line device
+// code; compiled kernels are cached per source text. If NVRTC or the driver
+// module loader fails, the caller keeps using the interpreted kernel (same
+// device path, slower) and the failure text is kept for inspection.
+#include <cuda.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/hdg_b200.h"
+#include "jit_quad.hpp"
+
+namespace hdgb {
+
+namespace {
+
+const char* kQuadSource = R"CUDA(
+// JIT: K2 node build with inlined coefficient fields (see kernels_local.cuh quad_build_kernel).
+#define EB 16
+#define LDB (EB + 4)
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+extern "C" __global__ void __launch_bounds__(128)
+quad_build_jit(int nelt, int nq, int nqp, int nsym, int nsymp, int d3, int d3p,
+               const double* __restrict__ bary, const double* __restrict__ wq,
+               const double* __restrict__ Asym, const double* __restrict__ Af,
+               const double* __restrict__ vol, const double* __restrict__ T,
+               const double* __restrict__ V, const double* __restrict__ sk,
+               const double* __restrict__ sc, const double* __restrict__ sf,
+               double* __restrict__ Msym, double* __restrict__ Dsym, double* __restrict__ fvec) {
+  extern __shared__ double smem[];
+  const int rows = nqp + 4;
+  double* Bk = smem;
+  double* Bc = Bk + rows * LDB;
+  double* Bf = Bc + rows * LDB;
+  const long K0 = long(blockIdx.x) * EB;
+  for (int idx = threadIdx.x; idx < rows * EB; idx += blockDim.x) {
+    const int q = idx / EB, e = idx % EB;
+    const long K = K0 + e;
+    double bk = 0.0, bc = 0.0, bf = 0.0;
+    if (K < nelt) {
+      if (q < nq) {
+        const double l0 = __ldg(bary + q), l1 = __ldg(bary + nq + q), l2 = __ldg(bary + 2 * nq + q),
+                     l3 = __ldg(bary + 3 * nq + q);
+        const double x = l0 * V[K] + l1 * V[nelt + K] + l2 * V[2L * nelt + K] + l3 * V[3L * nelt + K];
+        const double y = l0 * V[4L * nelt + K] + l1 * V[5L * nelt + K] + l2 * V[6L * nelt + K] + l3 * V[7L * nelt + K];
+        const double z = l0 * V[8L * nelt + K] + l1 * V[9L * nelt + K] + l2 * V[10L * nelt + K] + l3 * V[11L * nelt + K];
+        const double wv = __ldg(wq + q) * vol[K];
+        bk = wv / (FIELD_KAPPA);
+        bc = wv * (FIELD_C);
+        bf = wv * (FIELD_F);
+      } else if (q >= nqp) {
+        bc = T[long(q - nqp) * nelt + K];
+      }
+    }
+    Bk[q * LDB + e] = bk;
+    Bc[q * LDB + e] = bc;
+    Bf[q * LDB + e] = bf;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mts = nsymp / 8, mtf = d3p / 8;
+  const int ntasks = 2 * mts + mtf;
+  for (int task = warp; task < ntasks; task += nwarp) {
+    int which, mt;
+    if (task < mts) { which = 0; mt = task; }
+    else if (task < 2 * mts) { which = 1; mt = task - mts; }
+    else { which = 2; mt = task - 2 * mts; }
+    const double* A = which == 2 ? Af : Asym;
+    const int acols = which == 2 ? nqp : nqp + 4;
+    const int ksteps = which == 1 ? (nqp + 4) / 4 : nqp / 4;
+    const double* B = which == 0 ? Bk : (which == 1 ? Bc : Bf);
+    const double* Arow = A + (long(mt) * (acols / 4)) * 32 + lane;
+    double c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+#pragma unroll 4
+    for (int kk = 0; kk < ksteps; ++kk) {
+      const double a = __ldg(Arow + kk * 32);
+      const double* brow = B + (kk * 4 + t) * LDB + g;
+      dmma(c00, c01, a, brow[0]);
+      dmma(c10, c11, a, brow[8]);
+    }
+    const int r = mt * 8 + g;
+    const int lim = which == 2 ? d3 : nsym;
+    if (r < lim) {
+      double* out = which == 0 ? Msym : (which == 1 ? Dsym : fvec);
+      const int e0 = 2 * t;
+      const double v[4] = {c00, c01, c10, c11};
+      const int es[4] = {e0, e0 + 1, e0 + 8, e0 + 9};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const long K = K0 + es[i];
+        if (K < nelt) out[K * lim + r] = v[i];
+      }
+    }
+  }
+}
+)CUDA";
+
+std::string lit(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "(%a)", v);  // exact hex-float literal
+  return buf;
+}
+
+// Driver entry points resolved through the runtime (no link-time libcuda
+// dependency, so the library still loads on machines without a driver).
+struct Drv {
+  CUresult (*loadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*getFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*setAttr)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
+                     void**, void**) = nullptr;
+  bool ok = false;
+};
+Drv& drv() {
+  static Drv d = [] {
+    Drv r;
+    cudaDriverEntryPointQueryResult q;
+    auto get = [&](const char* name, void** fn) {
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn;
+    };
+    r.ok = get("cuModuleLoadData", reinterpret_cast<void**>(&r.loadData)) &&
+           get("cuModuleGetFunction", reinterpret_cast<void**>(&r.getFunction)) &&
+           get("cuFuncSetAttribute", reinterpret_cast<void**>(&r.setAttr)) &&
+           get("cuLaunchKernel", reinterpret_cast<void**>(&r.launch));
+    return r;
+  }();
+  return d;
+}
+
+struct Cache {
+  std::mutex mu;
+  std::unordered_map<std::string, CUfunction> fn;
+  std::vector<CUmodule> mods;
+  std::string last_error;
+};
+Cache& cache() {
+  static Cache c;
+  return c;
+}
+
+}  // namespace
+
+// Infix C expression of a field at (x, y, z) for node q of element K.
+std::string field_expr(const hdg_field& f, const char* sample_ptr) {
+  if (f.kind == HDG_FIELD_CONST) return lit(f.value);
+  if (f.kind == HDG_FIELD_SAMPLED) return std::string("__ldg(") + sample_ptr + " + K * nq + q)";
+  std::vector<std::string> st;
+  int ci = 0;
+  for (int i = 0; i < f.nops; ++i) {
+    const int op = f.ops[i];
+    auto pop = [&]() { std::string v = st.back(); st.pop_back(); return v; };
+    switch (op) {
+      case HDG_OP_X: st.push_back("x"); break;
+      case HDG_OP_Y: st.push_back("y"); break;
+      case HDG_OP_Z: st.push_back("z"); break;
+      case HDG_OP_CONST: st.push_back(lit(f.consts[ci++])); break;
+      case HDG_OP_NEG: st.back() = "(-" + st.back() + ")"; break;
+      case HDG_OP_SIN: st.back() = "sin(" + st.back() + ")"; break;
+      case HDG_OP_COS: st.back() = "cos(" + st.back() + ")"; break;
+      case HDG_OP_EXP: st.back() = "exp(" + st.back() + ")"; break;
+      case HDG_OP_SQRT: st.back() = "sqrt(" + st.back() + ")"; break;
+      case HDG_OP_ABS: st.back() = "fabs(" + st.back() + ")"; break;
+      default: {
+        const std::string b = pop(), a = pop();
+        switch (op) {
+          case HDG_OP_ADD: st.push_back("(" + a + " + " + b + ")"); break;
+          case HDG_OP_SUB: st.push_back("(" + a + " - " + b + ")"); break;
+          case HDG_OP_MUL: st.push_back("(" + a + " * " + b + ")"); break;
+          case HDG_OP_DIV: st.push_back("(" + a + " / " + b + ")"); break;
+          case HDG_OP_LT: st.push_back("((" + a + ") < (" + b + ") ? 1.0 : 0.0)"); break;
+          case HDG_OP_POW: st.push_back("pow(" + a + ", " + b + ")"); break;
+          default: st.push_back("0.0");
+        }
+      }
+    }
+  }
+  return st.empty() ? "0.0" : st.back();
+}
+
+CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, std::string* err) {
+  std::string src = "#define FIELD_KAPPA " + field_expr(kap, "sk") + "\n#define FIELD_C " + field_expr(c, "sc") +
+                    "\n#define FIELD_F " + field_expr(f, "sf") + "\n" + kQuadSource;
+  Cache& C = cache();
+  std::lock_guard<std::mutex> lock(C.mu);
+  auto it = C.fn.find(src);
+  if (it != C.fn.end()) return it->second;
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "quad_build_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    if (err) *err = "nvrtcCreateProgram failed";
+    return nullptr;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
+  const nvrtcResult rc = nvrtcCompileProgram(prog, 3, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, log.data());
+    if (err) *err = "nvrtc: " + log;
+    nvrtcDestroyProgram(&prog);
+    return nullptr;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::vector<char> cubin(n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  CUmodule mod;
+  CUfunction fn;
+  if (!drv().ok) {
+    if (err) *err = "driver entry points unavailable";
+    return nullptr;
+  }
+  if (drv().loadData(&mod, cubin.data()) != CUDA_SUCCESS ||
+      drv().getFunction(&fn, mod, "quad_build_jit") != CUDA_SUCCESS) {
+    if (err) *err = "cuModuleLoadData/cuModuleGetFunction failed";
+    return nullptr;
+  }
+  C.mods.push_back(mod);
+  C.fn.emplace(src, fn);
+  return fn;
+}
+
+bool launch_quad_jit(CUfunction fn, cudaStream_t stream, int grid, int block, size_t smem, void** args,
+                     std::string* err) {
+  if (drv().setAttr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, int(smem)) != CUDA_SUCCESS) {
+    if (err) *err = "cuFuncSetAttribute failed";
+    return false;
+  }
+  const CUresult r = drv().launch(fn, grid, 1, 1, block, 1, 1, (unsigned)smem, (CUstream)stream, args, nullptr);
+  if (r != CUDA_SUCCESS) {
+    if (err) *err = "cuLaunchKernel failed: CUresult " + std::to_string(int(r));
+    return false;
+  }
+  return true;
+}
+
+}  // namespace hdgb

@@ -1,0 +1,16 @@
+// NVRTC specialisation of the K2 node-build kernel (jit_quad.cpp).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/hdg_b200.h"
+
+namespace hdgb {
+std::string field_expr(const hdg_field& f, const char* sample_ptr);
+// Compiled (cached) kernel for these fields, or nullptr with *err set.
+CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, std::string* err);
+bool launch_quad_jit(CUfunction fn, cudaStream_t stream, int grid, int block, size_t smem, void** args,
+                     std::string* err);
+}  // namespace hdgb

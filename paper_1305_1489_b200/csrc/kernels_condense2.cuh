@@ -36,7 +36,7 @@ struct C2Dims {
   static constexpr int OFF_WB = OFF_TC + MP;           // MP: W table offset per column (as double)
   static constexpr int OFF_F = OFF_WB + MP;            // D3P: f
   static constexpr int OFF_FS = OFF_F + D3P;           // D3P: Si f
-  static constexpr int OFF_STG = OFF_FS + D3P;         // 32: GJ column stage
+  static constexpr int OFF_STG = round_up(OFF_FS + D3P, 2);  // 32: GJ column stage (16 B aligned)
   static constexpr int OFF_GEO = OFF_STG + 32;         // 32: geometry record
   static constexpr int PER_ELT = OFF_GEO + 32;
   static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
@@ -48,36 +48,44 @@ template <> struct C2Cfg<1> { static constexpr int NW = 1, EPB = 16; };
 template <> struct C2Cfg<2> { static constexpr int NW = 2, EPB = 8; };
 template <> struct C2Cfg<3> { static constexpr int NW = 2, EPB = 4; };
 
-// Gauss-Jordan inverse of the SPD N x N matrix whose column c lane c holds in
-// a[]; on return a[] holds column c of the inverse. pmin/pmax: pivot range.
+// Inverse of the SPD N x N matrix held by a warp (lane c owns column c in
+// a[]) by the symmetric sweep operator: sweeping pivot k keeps the matrix
+// symmetric, so column k is gathered from every lane's own a[k] (one shared
+// store per lane + broadcast loads) instead of being broadcast entry by entry.
+// After N sweeps a = -A^-1; the sign is folded in on return. No pivoting
+// (SPD); the pivots are the Cholesky pivots and feed the 1e-14 test.
 template <int N>
 __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, int lane, double& pmin,
                                                 double& pmax) {
 #pragma unroll
-  for (int j = 0; j < N; ++j) {
-    if (lane == j) {
+  for (int k = 0; k < N; ++k) {
+    if (lane < N) stage[lane] = a[k];
+    __syncwarp();
+    double v[N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) stage[i] = a[i];
+    for (int i = 0; i + 1 < N; i += 2) {
+      const double2 p2 = *reinterpret_cast<const double2*>(stage + i);
+      v[i] = p2.x;
+      v[i + 1] = p2.y;
     }
+    if (N % 2) v[N - 1] = stage[N - 1];
     __syncwarp();
-    double col[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) col[i] = stage[i];
-    __syncwarp();
-    const double p = col[j];
+    const double p = v[k];
     pmin = fmin(pmin, p);
     pmax = fmax(pmax, p);
     const double ip = 1.0 / p;
-    const bool me = lane == j;
-    const double f = me ? ip : a[j] * ip;
+    const bool me = lane == k;
+    const double f = me ? -ip : a[k] * ip;  // new A(k, c)
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      if (i == j) continue;
-      const double base = me ? 0.0 : a[i];
-      a[i] = fma(-col[i], f, base);
+      if (i == k) continue;
+      // lane k: A(i,k)/p ; others: A(i,c) - A(i,k) A(k,c)/p
+      a[i] = me ? v[i] * ip : fma(-v[i], a[k] * ip, a[i]);
     }
-    a[j] = f;
+    a[k] = f;
   }
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = -a[i];
 }
 
 template <int K_>

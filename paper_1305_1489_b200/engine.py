@@ -318,6 +318,14 @@ class Engine:
     def synchronize(self) -> None:
         L.check(L.lib().hdg_b200_synchronize(self._ctx))
 
+    def set_jit(self, enabled: bool) -> None:
+        """NVRTC-specialised node build for program fields (default on)."""
+        L.check(L.lib().hdg_b200_set_jit(self._ctx, int(enabled)))
+
+    @property
+    def jit_status(self) -> str:
+        return L.lib().hdg_b200_jit_status(self._ctx).decode()
+
     def set_timing(self, enabled: bool) -> None:
         L.check(L.lib().hdg_b200_set_timing(self._ctx, int(enabled)))
 

@@ -277,3 +277,20 @@ def test_full_size_sampled_elements(cfg_name):
     qx, qy, qz, u = core.local_recover(lb, np.asfortranarray(lam), 4)
     assert max_slice_relerr(np_(ls.u)[chosen], u.T) < TOL
     assert max_slice_relerr(np_(ls.qz)[chosen], qz.T) < TOL
+
+
+def test_jit_and_interpreter_agree():
+    """NVRTC-specialised node build == interpreted field programs (both GPU paths)."""
+    k = 3
+    mesh = HostMesh.box(2, bc="dirichlet_x")
+    prob = CONFIGS["C2"].problem
+    eng = Engine(0)
+    eng.set_degree(k)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 1.0)
+    cs_jit = eng.build_condense(g, prob.kappa, prob.c, prob.f)
+    assert eng.jit_status == "", eng.jit_status
+    eng.set_jit(False)
+    cs_vm = eng.build_condense(g, prob.kappa, prob.c, prob.f)
+    assert max_slice_relerr(np_(cs_jit.C_slices()), np_(cs_vm.C_slices())) < 1e-13
+    assert max_slice_relerr(np_(cs_jit.Cf_cols()), np_(cs_vm.Cf_cols())) < 1e-13
