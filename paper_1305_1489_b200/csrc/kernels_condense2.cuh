@@ -28,8 +28,8 @@ struct C2Dims {
   static constexpr int MT = D3P / 8, NTM = MP / 8, KS = D3P / 4;
   static constexpr int OFF_MI = 0;
   static constexpr int OFF_S = OFF_MI + D3P * LD;
-  static constexpr int OFF_Y = OFF_S + D3P * LD;
-  static constexpr int OFF_Z = OFF_Y + 3 * D3P * LD;   // Zp, later Vs
+  static constexpr int OFF_Y = OFF_S + D3P * LD;    // Y_s (3), later Vs
+  static constexpr int OFF_Z = OFF_Y + 3 * D3P * LD;   // Zp
   static constexpr int OFF_V = OFF_Z + MP * LD;
   static constexpr int OFF_NSC = OFF_V + MP * LD;      // 3 x MP face normals per column
   static constexpr int OFF_TC = OFF_NSC + 3 * MP;      // MP: tau|e| per column
@@ -46,7 +46,7 @@ template <int K_> struct C2Cfg;
 template <> struct C2Cfg<0> { static constexpr int NW = 1, EPB = 8; };
 template <> struct C2Cfg<1> { static constexpr int NW = 1, EPB = 16; };
 template <> struct C2Cfg<2> { static constexpr int NW = 2, EPB = 8; };
-template <> struct C2Cfg<3> { static constexpr int NW = 2, EPB = 4; };
+template <> struct C2Cfg<3> { static constexpr int NW = 4, EPB = 4; };
 
 // Inverse of the SPD N x N matrix held by a warp (lane c owns column c in
 // a[]) by the symmetric sweep operator: sweeping pivot k keeps the matrix
@@ -61,28 +61,31 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
   for (int k = 0; k < N; ++k) {
     if (lane < N) stage[lane] = a[k];
     __syncwarp();
-    double v[N];
-#pragma unroll
-    for (int i = 0; i + 1 < N; i += 2) {
-      const double2 p2 = *reinterpret_cast<const double2*>(stage + i);
-      v[i] = p2.x;
-      v[i + 1] = p2.y;
-    }
-    if (N % 2) v[N - 1] = stage[N - 1];
-    __syncwarp();
-    const double p = v[k];
+    const double p = stage[k];
     pmin = fmin(pmin, p);
     pmax = fmax(pmax, p);
     const double ip = 1.0 / p;
     const bool me = lane == k;
-    const double f = me ? -ip : a[k] * ip;  // new A(k, c)
+    // lane k holds column k == row k (symmetry), i.e. a[i] == v_i there, so
+    // v_i * ip == a[i] - v_i * (1 - ip): one FMA per entry for every lane.
+    const double t = me ? 1.0 - ip : a[k] * ip;
+    const double nk = me ? -ip : a[k] * ip;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      if (i == k) continue;
-      // lane k: A(i,k)/p ; others: A(i,c) - A(i,k) A(k,c)/p
-      a[i] = me ? v[i] * ip : fma(-v[i], a[k] * ip, a[i]);
+    for (int i0 = 0; i0 < N; i0 += 2) {
+      double v0, v1;
+      if (i0 + 1 < N) {
+        const double2 p2 = *reinterpret_cast<const double2*>(stage + i0);
+        v0 = p2.x;
+        v1 = p2.y;
+      } else {
+        v0 = stage[i0];
+        v1 = 0.0;
+      }
+      if (i0 != k) a[i0] = fma(-v0, t, a[i0]);
+      if (i0 + 1 < N && i0 + 1 != k) a[i0 + 1] = fma(-v1, t, a[i0 + 1]);
     }
-    a[k] = f;
+    a[k] = nk;
+    __syncwarp();
   }
 #pragma unroll
   for (int i = 0; i < N; ++i) a[i] = -a[i];
@@ -98,6 +101,7 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int NW = C2Cfg<K_>::NW, EPB = C2Cfg<K_>::EPB, NT = NW * 32;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, D3P = Dm::D3P, MP = Dm::MP, LD = Dm::LD;
   constexpr int MT = Dm::MT, NTM = Dm::NTM, KS = Dm::KS;
+  constexpr int NLOW = NTM * (NTM + 1) / 2;  // lower tiles of the m x m output
   extern __shared__ double smem[];
   for (int i = threadIdx.x; i < EPB * Dm::PER_ELT; i += blockDim.x) smem[i] = 0.0;
   __syncthreads();
@@ -111,8 +115,8 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   double* base = smem + tm.id * Dm::PER_ELT;
   double* Mi = base + Dm::OFF_MI;
   double* Sb = base + Dm::OFF_S;
-  double* Yb = base + Dm::OFF_Y;
-  double* Zb = base + Dm::OFF_Z;
+  double* Yb = base + Dm::OFF_Y;   // Y_s, later Vs
+  double* Zb = base + Dm::OFF_Z;   // Zp
   double* Vb = base + Dm::OFF_V;
   double* nsc = base + Dm::OFF_NSC;
   double* Tc = base + Dm::OFF_TC;
@@ -130,19 +134,20 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     double* Ck = Cout + K * M * M;
     double* F = factors ? factors + K * Dm::FACTORS : nullptr;
     bool bad = false;
-    // ------------------------------------------------ P0: loads + GJ(M)
+    // ----------------------------------------- P0: loads; GJ(M) || face data
     load_geo(geo, K, nelt, sg, tm.tid, NT);
     for (int j = 0; j < D3; ++j) {  // D (lower) -> S
       const int b0 = sym_idx(j, j, D3);
       for (int i = tm.tid; i < D3 - j; i += NT) Sb[(j + i) + j * LD] = Dsym[K * Dm::NSYM + b0 + i];
     }
     for (int i = tm.tid; i < D3; i += NT) fv[i] = fvec[K * D3 + i];
+    tm.sync();
     if (tm.warp == 0) {
       double a[D3];
 #pragma unroll
       for (int i = 0; i < D3; ++i) {
         const int r = i > lane ? i : lane, c = i > lane ? lane : i;
-        a[i] = lane < D3 ? Msym[K * Dm::NSYM + sym_idx(r, c, D3)] : (i == lane ? 1.0 : 0.0);
+        a[i] = lane < D3 ? Msym[K * Dm::NSYM + sym_idx(r, c, D3)] : 0.0;
       }
       double pmin = 1e300, pmax = 0.0;
       warp_gj_inverse<D3>(a, stg, lane, pmin, pmax);
@@ -157,34 +162,34 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         }
       }
     }
-    tm.sync();
-    // per-column face data (needs geometry)
-    for (int c = tm.tid; c < MP; c += NT) {
-      if (c < M) {
-        const int l = c / D2, i = c - l * D2;
-        const int mu = int(sg[26 + l]);
+    if (tm.warp == NW - 1) {  // per-column face data (NW == 1: after GJ)
+      for (int c = lane; c < MP; c += 32) {
+        if (c < M) {
+          const int l = c / D2, i = c - l * D2;
+          const int mu = int(sg[26 + l]);
 #pragma unroll
-        for (int s = 0; s < 3; ++s) nsc[s * MP + c] = sg[10 + 3 * l + s];
-        Tc[c] = sg[22 + l];
-        wb[c] = (6 * l + mu - 1) * D2 * D3 + i;
-      } else {
+          for (int s = 0; s < 3; ++s) nsc[s * MP + c] = sg[10 + 3 * l + s];
+          Tc[c] = sg[22 + l];
+          wb[c] = (6 * l + mu - 1) * D2 * D3 + i;
+        } else {
 #pragma unroll
-        for (int s = 0; s < 3; ++s) nsc[s * MP + c] = 0.0;
-        Tc[c] = 0.0;
-        wb[c] = -1;
+          for (int s = 0; s < 3; ++s) nsc[s * MP + c] = 0.0;
+          Tc[c] = 0.0;
+          wb[c] = -1;
+        }
       }
     }
     tm.sync();
 
     // ------------------------------------- P1: Zp = Mi W^T, Y_s = Mi C_s^T
-    // tasks: NTM column strips of Zp, 3*MT column strips of Y (all MT row tiles per task)
     for (int task = tm.warp; task < NTM + 3 * MT; task += NW) {
       double acc[MT][2];
 #pragma unroll
       for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+      double* out;
+      int c0;
       if (task < NTM) {
-        const int c = task * 8 + g;
-        const int wbc = wb[c];
+        const int wbc = wb[task * 8 + g];
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
           const int k = kk * 4 + t;
@@ -192,12 +197,8 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
           for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], Mi[(m * 8 + g) + k * LD], b);
         }
-#pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          const int r = m * 8 + g, c0 = task * 8 + 2 * t;
-          Zb[r + c0 * LD] = acc[m][0];
-          Zb[r + (c0 + 1) * LD] = acc[m][1];
-        }
+        out = Zb;
+        c0 = task * 8 + 2 * t;
       } else {
         const int s = (task - NTM) / MT, nt = (task - NTM) % MT;
         const int c = nt * 8 + g;
@@ -213,112 +214,80 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
           for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], Mi[(m * 8 + g) + k * LD], b);
         }
-        double* Y = Yb + s * D3P * LD;
+        out = Yb + s * D3P * LD;
+        c0 = nt * 8 + 2 * t;
+      }
 #pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          const int r = m * 8 + g, c0 = nt * 8 + 2 * t;
-          Y[r + c0 * LD] = acc[m][0];
-          Y[r + (c0 + 1) * LD] = acc[m][1];
-        }
+      for (int m = 0; m < MT; ++m) {
+        const int r = m * 8 + g;
+        out[r + c0 * LD] = acc[m][0];
+        out[r + (c0 + 1) * LD] = acc[m][1];
       }
     }
     tm.sync();
 
-    // ------------------- P2: S += sum_s C_s Y_s (lower), H = sum_s C_s Zp N_s,
-    //                         Gw tiles -> C (tauDD + nn o Gw), mirrored
-    for (int task = tm.warp; task < MT + NTM; task += NW) {
-      if (task < MT) {
-        const int mt = task;
-        double accS[MT][2], accH[NTM][2];
+    // ------------- P2: S += sum_s C_s Y_s (lower) | V = sum_s C_s Zp N_s + T^T
+    for (int task = tm.warp; task < 2 * MT; task += NW) {
+      const bool isS = task < MT;
+      const int mt = isS ? task : task - MT;
+      const int r = mt * 8 + g;
+      double acc[NTM][2];
 #pragma unroll
-        for (int j = 0; j < MT; ++j) accS[j][0] = accS[j][1] = 0.0;
+      for (int j = 0; j < NTM; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
-        for (int j = 0; j < NTM; ++j) accH[j][0] = accH[j][1] = 0.0;
-        const int r = mt * 8 + g;
+      for (int s = 0; s < 3; ++s) {
+        const double as0 = a9[3 * s], as1 = a9[3 * s + 1], as2 = a9[3 * s + 2];
+        const double* Y = Yb + s * D3P * LD;
+        double ns[NTM];
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
-          const double as0 = a9[3 * s], as1 = a9[3 * s + 1], as2 = a9[3 * s + 2];
-          const double* Y = Yb + s * D3P * LD;
-          double ns[NTM];
+        for (int j = 0; j < NTM; ++j) ns[j] = nsc[s * MP + j * 8 + g];
 #pragma unroll
-          for (int j = 0; j < NTM; ++j) ns[j] = nsc[s * MP + j * 8 + g];
-#pragma unroll
-          for (int kk = 0; kk < KS; ++kk) {
-            const int k = kk * 4 + t;
-            double a = 0.0;  // C_s(r, k)
-            if (r < D3 && k < D3) {
-              const int o = r + k * D3;
-              a = as0 * __ldg(Ch + o) + as1 * __ldg(Ch + D3 * D3 + o) + as2 * __ldg(Ch + 2 * D3 * D3 + o);
-            }
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          double a = 0.0;  // C_s(r, k)
+          if (r < D3 && k < D3) {
+            const int o = r + k * D3;
+            a = as0 * __ldg(Ch + o) + as1 * __ldg(Ch + D3 * D3 + o) + as2 * __ldg(Ch + 2 * D3 * D3 + o);
+          }
+          if (isS) {
 #pragma unroll
             for (int j = 0; j < MT; ++j)
-              if (j <= mt) dmma(accS[j][0], accS[j][1], a, Y[k + (j * 8 + g) * LD]);
+              if (j <= mt) dmma(acc[j][0], acc[j][1], a, Y[k + (j * 8 + g) * LD]);
+          } else {
 #pragma unroll
-            for (int j = 0; j < NTM; ++j) dmma(accH[j][0], accH[j][1], a, Zb[k + (j * 8 + g) * LD] * ns[j]);
+            for (int j = 0; j < NTM; ++j) dmma(acc[j][0], acc[j][1], a, Zb[k + (j * 8 + g) * LD] * ns[j]);
           }
         }
+      }
+      if (isS) {
 #pragma unroll
         for (int j = 0; j < MT; ++j) {
           if (j > mt) continue;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int c = j * 8 + 2 * t + h;
-            if (r < D3 && c <= r) Sb[r + c * LD] += accS[j][h];
+            if (r < D3 && c <= r) Sb[r + c * LD] += acc[j][h];
           }
         }
+      } else {
 #pragma unroll
         for (int j = 0; j < NTM; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int c = j * 8 + 2 * t + h;
-            if (r < D3 && c < M) Vb[r + c * LD] = accH[j][h] + Tc[c] * __ldg(Wlm + wb[c] + r * D2);
+            if (r < D3 && c < M) Vb[r + c * LD] = acc[j][h] + Tc[c] * __ldg(Wlm + wb[c] + r * D2);
           }
-      } else {
-        // Gw = W Zp, lower tiles of row strip mt; C <- tauDD + nn o Gw (both triangles)
-        const int mt = task - MT;
-        const int r = mt * 8 + g;
-        double acc[NTM][2];
-#pragma unroll
-        for (int j = 0; j < NTM; ++j) acc[j][0] = acc[j][1] = 0.0;
-        const int wbr = wb[r];
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-          const int k = kk * 4 + t;
-          const double a = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
-#pragma unroll
-          for (int j = 0; j < NTM; ++j)
-            if (j <= mt) dmma(acc[j][0], acc[j][1], a, Zb[k + (j * 8 + g) * LD]);
-        }
-        if (r < M) {
-          const int l1 = r / D2;
-          const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
-#pragma unroll
-          for (int j = 0; j < NTM; ++j) {
-            if (j > mt) continue;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int c = j * 8 + 2 * t + h;
-              if (c > r || c >= M) continue;
-              const int l2 = c / D2;
-              const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
-              double v = nn * acc[j][h];
-              if (l1 == l2) v += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
-              Ck[r + c * M] = v;
-              if (c != r) Ck[c + r * M] = v;
-            }
-          }
-        }
       }
     }
     tm.sync();
 
-    // ----------------------------------------------- P3: Si = S^-1 (warp 0)
+    // ------------------------- P3: Si = S^-1 (warp 0) || V, f -> recovery cache
     if (tm.warp == 0) {
       double a[D3];
 #pragma unroll
       for (int i = 0; i < D3; ++i) {
         const int r = i > lane ? i : lane, c = i > lane ? lane : i;
-        a[i] = lane < D3 ? Sb[r + c * LD] : (i == lane ? 1.0 : 0.0);
+        a[i] = lane < D3 ? Sb[r + c * LD] : 0.0;
       }
       double pmin = 1e300, pmax = 0.0;
       warp_gj_inverse<D3>(a, stg, lane, pmin, pmax);
@@ -332,23 +301,19 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             if (i >= lane) F[Dm::NSYM + sym_idx(i, lane, D3)] = a[i];
         }
       }
-    } else if (F) {
-      for (int idx = tm.tid - 32; idx < D3 * M; idx += NT - 32) {
-        const int r = idx % D3, c = idx / D3;
-        F[2 * Dm::NSYM + idx] = Vb[r + c * LD];
-      }
     }
-    if (F && tm.warp == NW - 1)
-      for (int i = lane; i < D3; i += 32) F[2 * Dm::NSYM + D3 * M + i] = fv[i];
-    if (F && NW == 1) {
-      for (int idx = lane; idx < D3 * M; idx += 32) {
+    if (F && (NW == 1 || tm.warp > 0)) {
+      const int t0 = NW == 1 ? tm.tid : tm.tid - 32, nt0 = NW == 1 ? NT : NT - 32;
+      for (int idx = t0; idx < D3 * M; idx += nt0) {
         const int r = idx % D3, c = idx / D3;
         F[2 * Dm::NSYM + idx] = Vb[r + c * LD];
       }
+      for (int i = t0; i < D3; i += nt0) F[2 * Dm::NSYM + D3 * M + i] = fv[i];
     }
     tm.sync();
 
-    // ----------------------------------------- P4: Vs = Si V (into Zb), fs = Si f
+    // --------------------------------- P4: Vs = Si V (into Yb), fs = Si f
+    double* Vs = Yb;
     for (int task = tm.warp; task < NTM; task += NW) {
       double acc[MT][2];
 #pragma unroll
@@ -364,8 +329,8 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         const int r = m * 8 + g, c0 = task * 8 + 2 * t;
-        Zb[r + c0 * LD] = acc[m][0];
-        Zb[r + (c0 + 1) * LD] = acc[m][1];
+        Vs[r + c0 * LD] = acc[m][0];
+        Vs[r + (c0 + 1) * LD] = acc[m][1];
       }
     }
     for (int r = tm.tid; r < D3; r += NT) {
@@ -376,33 +341,34 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     tm.sync();
 
-    // --------------------------- P5: C -= V^T Vs (lower tiles, mirrored); Cf
-    for (int task = tm.warp; task < NTM; task += NW) {
-      const int mt = task;
+    // ----- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs, lower tiles mirrored; Cf
+    for (int task = tm.warp; task < NLOW; task += NW) {
+      int mt = 0, rem = task;
+      while (rem > mt) { rem -= mt + 1; ++mt; }
+      const int nt = rem;  // nt <= mt
       const int r = mt * 8 + g;
-      double acc[NTM][2];
-#pragma unroll
-      for (int j = 0; j < NTM; ++j) acc[j][0] = acc[j][1] = 0.0;
+      const int wbr = wb[r];
+      double z0 = 0, z1 = 0, v0 = 0, v1 = 0;
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
         const int k = kk * 4 + t;
-        const double a = Vb[k + r * LD];
-#pragma unroll
-        for (int j = 0; j < NTM; ++j)
-          if (j <= mt) dmma(acc[j][0], acc[j][1], a, Zb[k + (j * 8 + g) * LD]);
+        const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
+        dmma(z0, z1, aw, Zb[k + (nt * 8 + g) * LD]);
+        dmma(v0, v1, Vb[k + r * LD], Vs[k + (nt * 8 + g) * LD]);
       }
       if (r < M) {
+        const int l1 = r / D2;
+        const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
 #pragma unroll
-        for (int j = 0; j < NTM; ++j) {
-          if (j > mt) continue;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = j * 8 + 2 * t + h;
-            if (c > r || c >= M) continue;
-            const double v = Ck[r + c * M] - acc[j][h];
-            Ck[r + c * M] = v;
-            if (c != r) Ck[c + r * M] = v;
-          }
+        for (int h = 0; h < 2; ++h) {
+          const int c = nt * 8 + 2 * t + h;
+          if (c > r || c >= M) continue;
+          const int l2 = c / D2;
+          const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
+          double v = nn * (h ? z1 : z0) - (h ? v1 : v0);
+          if (l1 == l2) v += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
+          Ck[r + c * M] = v;
+          if (c != r) Ck[c + r * M] = v;
         }
       }
     }
