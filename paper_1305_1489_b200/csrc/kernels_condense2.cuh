@@ -36,9 +36,11 @@ struct C2Dims {
   static constexpr int OFF_WB = OFF_TC + MP;           // MP: W table offset per column (as double)
   static constexpr int OFF_F = OFF_WB + MP;            // D3P: f
   static constexpr int OFF_FS = OFF_F + D3P;           // D3P: Si f
-  static constexpr int OFF_STG = round_up(OFF_FS + D3P, 2);  // 32: GJ column stage (16 B aligned)
-  static constexpr int OFF_GEO = OFF_STG + 32;         // 32: geometry record
-  static constexpr int PER_ELT = OFF_GEO + 32;
+  static constexpr int OFF_STG = round_up(OFF_FS + D3P, 2);  // 64: GJ column stage (16 B aligned)
+  static constexpr int OFF_STG2 = OFF_STG + 64;        // 64: second GJ stage
+  static constexpr int OFF_GEO = OFF_STG2 + 64;        // 2 x 32: geometry records (cur/next)
+  static constexpr int OFF_COL = OFF_GEO + 64;         // second column-data buffer
+  static constexpr int PER_ELT = OFF_COL + 5 * MP;
   static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
 };
 
@@ -57,8 +59,45 @@ template <> struct C2Cfg<3> { static constexpr int NW = 4, EPB = 4; };
 template <int N>
 __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, int lane, double& pmin,
                                                 double& pmax) {
+  // stage: 2 x 32 doubles (pivot columns k, k+1 gathered from every lane).
 #pragma unroll
-  for (int k = 0; k < N; ++k) {
+  for (int k = 0; k + 1 < N; k += 2) {
+    if (lane < N) {
+      stage[lane] = a[k];
+      stage[32 + lane] = a[k + 1];
+    }
+    __syncwarp();
+    const double p00 = stage[k], p01 = stage[k + 1], p11 = stage[32 + k + 1];
+    const double det = p00 * p11 - p01 * p01;
+    pmin = fmin(pmin, fmin(p00, det / p00));  // Cholesky pivots of the block
+    pmax = fmax(pmax, fmax(p00, det / p00));
+    const double id = 1.0 / det;
+    const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;  // P^-1 (symmetric)
+    const bool m0 = lane == k, m1 = lane == k + 1;
+    // w = P^-1 [a_k; a_k+1] for ordinary lanes; pivot lanes hold their own
+    // block column, for which "a - v w" must produce A(i,block) P^-1.
+    double w0 = i00 * a[k] + i01 * a[k + 1];
+    double w1 = i01 * a[k] + i11 * a[k + 1];
+    if (m0) { w0 = 1.0 - i00; w1 = -i01; }
+    if (m1) { w0 = -i01; w1 = 1.0 - i11; }
+    double nk0 = w0, nk1 = w1;
+    if (m0) { nk0 = -i00; nk1 = -i01; }
+    if (m1) { nk0 = -i01; nk1 = -i11; }
+#pragma unroll
+    for (int i0 = 0; i0 < N; i0 += 2) {
+      const double2 v0 = *reinterpret_cast<const double2*>(stage + i0);
+      const double2 v1 = *reinterpret_cast<const double2*>(stage + 32 + i0);
+      if (i0 != k) {
+        a[i0] = fma(-v0.x, w0, fma(-v1.x, w1, a[i0]));
+        if (i0 + 1 < N) a[i0 + 1] = fma(-v0.y, w0, fma(-v1.y, w1, a[i0 + 1]));
+      }
+    }
+    a[k] = nk0;
+    a[k + 1] = nk1;
+    __syncwarp();
+  }
+  if (N % 2) {  // trailing scalar pivot
+    constexpr int k = N - 1;
     if (lane < N) stage[lane] = a[k];
     __syncwarp();
     const double p = stage[k];
@@ -66,29 +105,50 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
     pmax = fmax(pmax, p);
     const double ip = 1.0 / p;
     const bool me = lane == k;
-    // lane k holds column k == row k (symmetry), i.e. a[i] == v_i there, so
-    // v_i * ip == a[i] - v_i * (1 - ip): one FMA per entry for every lane.
     const double t = me ? 1.0 - ip : a[k] * ip;
     const double nk = me ? -ip : a[k] * ip;
 #pragma unroll
-    for (int i0 = 0; i0 < N; i0 += 2) {
-      double v0, v1;
-      if (i0 + 1 < N) {
-        const double2 p2 = *reinterpret_cast<const double2*>(stage + i0);
-        v0 = p2.x;
-        v1 = p2.y;
-      } else {
-        v0 = stage[i0];
-        v1 = 0.0;
-      }
-      if (i0 != k) a[i0] = fma(-v0, t, a[i0]);
-      if (i0 + 1 < N && i0 + 1 != k) a[i0 + 1] = fma(-v1, t, a[i0 + 1]);
-    }
+    for (int i = 0; i < k; ++i) a[i] = fma(-stage[i], t, a[i]);
     a[k] = nk;
     __syncwarp();
   }
 #pragma unroll
   for (int i = 0; i < N; ++i) a[i] = -a[i];
+}
+
+// Loads column `lane` of a packed-lower SPD matrix and inverts it in place
+// (warp-wide). Returns true if the 1e-14 pivot test fails.
+template <int D3>
+__device__ __forceinline__ bool warp_inverse_packed(const double* __restrict__ P, double (&a)[D3],
+                                                    double* stage, int lane) {
+#pragma unroll
+  for (int i = 0; i < D3; ++i) {
+    const int r = i > lane ? i : lane, c = i > lane ? lane : i;
+    a[i] = lane < D3 ? P[sym_idx(r, c, D3)] : 0.0;
+  }
+  double pmin = 1e300, pmax = 0.0;
+  warp_gj_inverse<D3>(a, stage, lane, pmin, pmax);
+  return !(pmin > 0.0) || pmin < 1e-14 * pmax;
+}
+
+// Column data of element K's faces (per m-column: normals, tau|e|, W offset).
+template <int D2, int D3, int M, int MP>
+__device__ __forceinline__ void build_columns(const double* sg, double* nsc, double* Tc, int* wb, int lane) {
+  for (int c = lane; c < MP; c += 32) {
+    if (c < M) {
+      const int l = c / D2, i = c - l * D2;
+      const int mu = int(sg[26 + l]);
+#pragma unroll
+      for (int s = 0; s < 3; ++s) nsc[s * MP + c] = sg[10 + 3 * l + s];
+      Tc[c] = sg[22 + l];
+      wb[c] = (6 * l + mu - 1) * D2 * D3 + i;
+    } else {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) nsc[s * MP + c] = 0.0;
+      Tc[c] = 0.0;
+      wb[c] = -1;
+    }
+  }
 }
 
 template <int K_>
@@ -101,7 +161,11 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int NW = C2Cfg<K_>::NW, EPB = C2Cfg<K_>::EPB, NT = NW * 32;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, D3P = Dm::D3P, MP = Dm::MP, LD = Dm::LD;
   constexpr int MT = Dm::MT, NTM = Dm::NTM, KS = Dm::KS;
-  constexpr int NLOW = NTM * (NTM + 1) / 2;  // lower tiles of the m x m output
+  constexpr int NLOW = NTM * (NTM + 1) / 2;        // lower tiles of the m x m output
+  constexpr int WM = NW > 1 ? 1 : 0;               // warp inverting the next element's M
+  constexpr int GW0 = NW > 2 ? 2 : (NW > 1 ? 1 : 0);  // first warp owning output tiles
+  constexpr int NGW = NW - GW0;                    // output-tile warps
+  constexpr int TPW = (NLOW + NGW - 1) / NGW;      // tiles per output warp
   extern __shared__ double smem[];
   for (int i = threadIdx.x; i < EPB * Dm::PER_ELT; i += blockDim.x) smem[i] = 0.0;
   __syncthreads();
@@ -118,68 +182,58 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   double* Yb = base + Dm::OFF_Y;   // Y_s, later Vs
   double* Zb = base + Dm::OFF_Z;   // Zp
   double* Vb = base + Dm::OFF_V;
-  double* nsc = base + Dm::OFF_NSC;
-  double* Tc = base + Dm::OFF_TC;
-  int* wb = reinterpret_cast<int*>(base + Dm::OFF_WB);
   double* fv = base + Dm::OFF_F;
   double* fs = base + Dm::OFF_FS;
-  double* stg = base + Dm::OFF_STG;
-  double* sg = base + Dm::OFF_GEO;
-  const double* a9 = sg + 1;
+  double* stgS = base + Dm::OFF_STG;
+  double* stgM = base + Dm::OFF_STG2;
+  // double-buffered per-element records: nsc(3MP) Tc(MP) wb(MP) and geometry
+  auto colbuf = [&](int b) { return base + (b ? Dm::OFF_COL : Dm::OFF_NSC); };
+  auto sgbuf = [&](int b) { return base + Dm::OFF_GEO + 32 * b; };
   const double* Wlm = tab.Wlm;
   const double* Ch = tab.Chat;
-
   const long stride = long(gridDim.x) * EPB;
-  for (long K = long(blockIdx.x) * EPB + tm.id; K < nelt; K += stride) {
-    double* Ck = Cout + K * M * M;
-    double* F = factors ? factors + K * Dm::FACTORS : nullptr;
-    bool bad = false;
-    // ----------------------------------------- P0: loads; GJ(M) || face data
-    load_geo(geo, K, nelt, sg, tm.tid, NT);
-    for (int j = 0; j < D3; ++j) {  // D (lower) -> S
+  int cur = 0;
+
+  // ---- prologue: first element's M^-1, D, f, geometry, column data
+  long K = long(blockIdx.x) * EPB + tm.id;
+  if (K < nelt) {
+    load_geo(geo, K, nelt, sgbuf(0), tm.tid, NT);
+    for (int j = 0; j < D3; ++j) {
       const int b0 = sym_idx(j, j, D3);
       for (int i = tm.tid; i < D3 - j; i += NT) Sb[(j + i) + j * LD] = Dsym[K * Dm::NSYM + b0 + i];
     }
     for (int i = tm.tid; i < D3; i += NT) fv[i] = fvec[K * D3 + i];
-    tm.sync();
     if (tm.warp == 0) {
       double a[D3];
-#pragma unroll
-      for (int i = 0; i < D3; ++i) {
-        const int r = i > lane ? i : lane, c = i > lane ? lane : i;
-        a[i] = lane < D3 ? Msym[K * Dm::NSYM + sym_idx(r, c, D3)] : 0.0;
-      }
-      double pmin = 1e300, pmax = 0.0;
-      warp_gj_inverse<D3>(a, stg, lane, pmin, pmax);
-      bad |= !(pmin > 0.0) || pmin < 1e-14 * pmax;
+      const bool bad = warp_inverse_packed<D3>(Msym + K * Dm::NSYM, a, stgM, lane);
       if (lane < D3) {
 #pragma unroll
         for (int i = 0; i < D3; ++i) Mi[i + lane * LD] = a[i];
-        if (F) {
+        if (factors) {
 #pragma unroll
           for (int i = 0; i < D3; ++i)
-            if (i >= lane) F[sym_idx(i, lane, D3)] = a[i];
+            if (i >= lane) factors[K * Dm::FACTORS + sym_idx(i, lane, D3)] = a[i];
         }
       }
-    }
-    if (tm.warp == NW - 1) {  // per-column face data (NW == 1: after GJ)
-      for (int c = lane; c < MP; c += 32) {
-        if (c < M) {
-          const int l = c / D2, i = c - l * D2;
-          const int mu = int(sg[26 + l]);
-#pragma unroll
-          for (int s = 0; s < 3; ++s) nsc[s * MP + c] = sg[10 + 3 * l + s];
-          Tc[c] = sg[22 + l];
-          wb[c] = (6 * l + mu - 1) * D2 * D3 + i;
-        } else {
-#pragma unroll
-          for (int s = 0; s < 3; ++s) nsc[s * MP + c] = 0.0;
-          Tc[c] = 0.0;
-          wb[c] = -1;
-        }
-      }
+      if (bad && lane == 0) flag_bad(bad_element, K);
     }
     tm.sync();
+    if (tm.warp == NW - 1)
+      build_columns<D2, D3, M, MP>(sgbuf(0), colbuf(0), colbuf(0) + 3 * MP,
+                                   reinterpret_cast<int*>(colbuf(0) + 4 * MP), lane);
+    tm.sync();
+  }
+
+  for (; K < nelt; K += stride) {
+    const long Kn = K + stride;
+    const bool has_next = Kn < nelt;
+    double* Ck = Cout + K * M * M;
+    double* F = factors ? factors + K * Dm::FACTORS : nullptr;
+    const double* sg = sgbuf(cur);
+    const double* a9 = sg + 1;
+    const double* nsc = colbuf(cur);
+    const double* Tc = colbuf(cur) + 3 * MP;
+    const int* wb = reinterpret_cast<const int*>(colbuf(cur) + 4 * MP);
 
     // ------------------------------------- P1: Zp = Mi W^T, Y_s = Mi C_s^T
     for (int task = tm.warp; task < NTM + 3 * MT; task += NW) {
@@ -281,7 +335,11 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     tm.sync();
 
-    // ------------------------- P3: Si = S^-1 (warp 0) || V, f -> recovery cache
+    // --- P3: warp 0 Si = S^-1 | warp WM: M^-1 of the next element | output
+    //         warps: (W Zp) tiles held in registers; V, f -> recovery cache
+    double accz[TPW][2];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) accz[i][0] = accz[i][1] = 0.0;
     if (tm.warp == 0) {
       double a[D3];
 #pragma unroll
@@ -290,8 +348,8 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         a[i] = lane < D3 ? Sb[r + c * LD] : 0.0;
       }
       double pmin = 1e300, pmax = 0.0;
-      warp_gj_inverse<D3>(a, stg, lane, pmin, pmax);
-      bad |= !(pmin > 0.0) || pmin < 1e-14 * pmax;
+      warp_gj_inverse<D3>(a, stgS, lane, pmin, pmax);
+      const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
       if (lane < D3) {
 #pragma unroll
         for (int i = 0; i < D3; ++i) Sb[i + lane * LD] = a[i];
@@ -301,14 +359,46 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             if (i >= lane) F[Dm::NSYM + sym_idx(i, lane, D3)] = a[i];
         }
       }
+      if (bad && lane == 0) flag_bad(bad_element, K);
     }
-    if (F && (NW == 1 || tm.warp > 0)) {
-      const int t0 = NW == 1 ? tm.tid : tm.tid - 32, nt0 = NW == 1 ? NT : NT - 32;
-      for (int idx = t0; idx < D3 * M; idx += nt0) {
-        const int r = idx % D3, c = idx / D3;
-        F[2 * Dm::NSYM + idx] = Vb[r + c * LD];
+    if (tm.warp == WM && has_next) {  // Mi is dead after P1: invert the next M into it
+      double a[D3];
+      const bool bad = warp_inverse_packed<D3>(Msym + Kn * Dm::NSYM, a, stgM, lane);
+      if (lane < D3) {
+#pragma unroll
+        for (int i = 0; i < D3; ++i) Mi[i + lane * LD] = a[i];
+        if (factors) {
+#pragma unroll
+          for (int i = 0; i < D3; ++i)
+            if (i >= lane) factors[Kn * Dm::FACTORS + sym_idx(i, lane, D3)] = a[i];
+        }
       }
-      for (int i = t0; i < D3; i += nt0) F[2 * Dm::NSYM + D3 * M + i] = fv[i];
+      if (bad && lane == 0) flag_bad(bad_element, Kn);
+    }
+    if (tm.warp >= GW0) {
+      const int ow = tm.warp - GW0;
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int tile = ow + i * NGW;
+        if (tile >= NLOW) break;
+        int mt = 0, rem = tile;
+        while (rem > mt) { rem -= mt + 1; ++mt; }
+        const int nt = rem;
+        const int wbr = wb[mt * 8 + g];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
+          dmma(accz[i][0], accz[i][1], aw, Zb[k + (nt * 8 + g) * LD]);
+        }
+      }
+      if (F && tm.warp == NW - 1) {
+        for (int idx = lane; idx < D3 * M; idx += 32) {
+          const int r = idx % D3, c = idx / D3;
+          F[2 * Dm::NSYM + idx] = Vb[r + c * LD];
+        }
+        for (int i = lane; i < D3; i += 32) F[2 * Dm::NSYM + D3 * M + i] = fv[i];
+      }
     }
     tm.sync();
 
@@ -341,45 +431,66 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     tm.sync();
 
-    // ----- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs, lower tiles mirrored; Cf
-    for (int task = tm.warp; task < NLOW; task += NW) {
-      int mt = 0, rem = task;
-      while (rem > mt) { rem -= mt + 1; ++mt; }
-      const int nt = rem;  // nt <= mt
-      const int r = mt * 8 + g;
-      const int wbr = wb[r];
-      double z0 = 0, z1 = 0, v0 = 0, v1 = 0;
+    // ---- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (output warps, lower tiles
+    //      mirrored) | Cf | next element's D, f, geometry, column data
+    if (tm.warp >= GW0) {
+      const int ow = tm.warp - GW0;
 #pragma unroll
-      for (int kk = 0; kk < KS; ++kk) {
-        const int k = kk * 4 + t;
-        const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
-        dmma(z0, z1, aw, Zb[k + (nt * 8 + g) * LD]);
-        dmma(v0, v1, Vb[k + r * LD], Vs[k + (nt * 8 + g) * LD]);
-      }
-      if (r < M) {
-        const int l1 = r / D2;
-        const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
+      for (int i = 0; i < TPW; ++i) {
+        const int tile = ow + i * NGW;
+        if (tile >= NLOW) break;
+        int mt = 0, rem = tile;
+        while (rem > mt) { rem -= mt + 1; ++mt; }
+        const int nt = rem;
+        const int r = mt * 8 + g;
+        double v0 = 0, v1 = 0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = nt * 8 + 2 * t + h;
-          if (c > r || c >= M) continue;
-          const int l2 = c / D2;
-          const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
-          double v = nn * (h ? z1 : z0) - (h ? v1 : v0);
-          if (l1 == l2) v += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
-          Ck[r + c * M] = v;
-          if (c != r) Ck[c + r * M] = v;
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          dmma(v0, v1, Vb[k + r * LD], Vs[k + (nt * 8 + g) * LD]);
+        }
+        if (r < M) {
+          const int l1 = r / D2;
+          const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = nt * 8 + 2 * t + h;
+            if (c > r || c >= M) continue;
+            const int l2 = c / D2;
+            const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
+            double v = nn * accz[i][h] - (h ? v1 : v0);
+            if (l1 == l2) v += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
+            Ck[r + c * M] = v;
+            if (c != r) Ck[c + r * M] = v;
+          }
         }
       }
     }
-    for (int r = tm.tid; r < M; r += NT) {
-      double s = 0.0;
+    if (tm.warp < GW0 || NW == 1) {
+      const int t0 = NW == 1 ? lane : tm.tid, nt0 = NW == 1 ? 32 : GW0 * 32;
+      for (int r = t0; r < M; r += nt0) {
+        double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < D3; ++k) s += Vb[k + r * LD] * fs[k];
-      Cfout[K * M + r] = s;
+        for (int k = 0; k < D3; ++k) s += Vb[k + r * LD] * fs[k];
+        Cfout[K * M + r] = s;
+      }
     }
-    if (bad) flag_bad(bad_element, K);
-    tm.sync();
+    tm.sync();  // Sb, fv, sg[next], colbuf[next] are free below
+    if (has_next) {
+      const int nxt = cur ^ 1;
+      load_geo(geo, Kn, nelt, sgbuf(nxt), tm.tid, NT);
+      for (int j = 0; j < D3; ++j) {
+        const int b0 = sym_idx(j, j, D3);
+        for (int i = tm.tid; i < D3 - j; i += NT) Sb[(j + i) + j * LD] = Dsym[Kn * Dm::NSYM + b0 + i];
+      }
+      for (int i = tm.tid; i < D3; i += NT) fv[i] = fvec[Kn * D3 + i];
+      tm.sync();
+      if (tm.warp == NW - 1)
+        build_columns<D2, D3, M, MP>(sgbuf(nxt), colbuf(nxt), colbuf(nxt) + 3 * MP,
+                                     reinterpret_cast<int*>(colbuf(nxt) + 4 * MP), lane);
+      tm.sync();
+      cur = nxt;
+    }
   }
 }
 
