@@ -53,20 +53,19 @@ def load_peaks():
 # --------------------------------------------------------------- flop model
 def k3_flops(k: int) -> float:
     """Algorithmic fp64 flops per element of the condense kernel as executed
-    (unpadded counts of each contraction)."""
-    d3 = (k + 1) * (k + 2) * (k + 3) // 6
+    (kernels_condense2.cuh; unpadded counts, symmetric products counted once;
+    DESIGN.md §K3)."""
+    n = (k + 1) * (k + 2) * (k + 3) // 6
     m = 2 * (k + 1) * (k + 2)
-    tri = d3 * (d3 + 1) / 2
     f = 0.0
-    f += 2 * (d3 ** 3 / 3.0) * 2          # two Cholesky + two triangular inverses
-    f += 3 * 2 * tri * d3                 # Q_# = Li Chat_#^T
-    f += 3 * 3 * 2 * d3 * d3              # Y_s = sum a Q
-    f += 2 * tri * m                      # Z = Li W^T
-    f += 3 * 2 * tri * d3                 # S += sum Y^T Y (lower)
-    f += 3 * 2 * d3 * d3 * m              # V = sum_s Y_s^T (Z n_s)
-    f += 2 * tri * m + 2 * tri            # Vt = LSi V, ft
-    f += 2 * 2 * m * m * d3               # Z^T Z and Vt^T Vt
-    f += 2 * m * d3                       # Cf
+    f += 2 * 2.0 * n ** 3                 # two Gauss-Jordan inverses (M, S)
+    f += 2.0 * n * n * m                  # Zp = Mi W^T
+    f += 3 * 2.0 * n ** 3 + 3 * 3 * 2.0 * n * n   # Q_# = Mi Chat_#^T, R_# = g Q
+    f += 3 * 2.0 * n * n * (n + 1) / 2    # S += sum_# Chat_# R_# (lower)
+    f += 2.0 * n * n * m + 4 * 3 * 2.0 * n * n    # V: per-face Chat_l Zp_l (+ Chat_l combos)
+    f += 2.0 * n * n * m + 2.0 * n * n    # Vs = Si V, fs
+    f += 2 * 2.0 * n * m * (m + 1) / 2    # W Zp and V^T Vs (lower)
+    f += 2.0 * m * n                      # Cf
     return f
 
 

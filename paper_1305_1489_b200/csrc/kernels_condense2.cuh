@@ -34,13 +34,14 @@ struct C2Dims {
   static constexpr int OFF_NSC = OFF_V + MP * LD;      // 3 x MP face normals per column
   static constexpr int OFF_TC = OFF_NSC + 3 * MP;      // MP: tau|e| per column
   static constexpr int OFF_WB = OFF_TC + MP;           // MP: W table offset per column (as double)
-  static constexpr int OFF_F = OFF_WB + MP;            // D3P: f
+  static constexpr int OFF_BETA = OFF_WB + MP;         // 3 x MP: beta_#(c) = sum_s a(s,#) n_s(face c)
+  static constexpr int OFF_F = OFF_BETA + 3 * MP;      // D3P: f
   static constexpr int OFF_FS = OFF_F + D3P;           // D3P: Si f
   static constexpr int OFF_STG = round_up(OFF_FS + D3P, 2);  // 64: GJ column stage (16 B aligned)
   static constexpr int OFF_STG2 = OFF_STG + 64;        // 64: second GJ stage
   static constexpr int OFF_GEO = OFF_STG2 + 64;        // 2 x 32: geometry records (cur/next)
   static constexpr int OFF_COL = OFF_GEO + 64;         // second column-data buffer
-  static constexpr int PER_ELT = OFF_COL + 5 * MP;
+  static constexpr int PER_ELT = OFF_COL + 8 * MP;
   static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
 };
 
@@ -131,20 +132,29 @@ __device__ __forceinline__ bool warp_inverse_packed(const double* __restrict__ P
   return !(pmin > 0.0) || pmin < 1e-14 * pmax;
 }
 
-// Column data of element K's faces (per m-column: normals, tau|e|, W offset).
+// Column data of element K's faces (per m-column: normals, tau|e|, W offset,
+// beta_#(c) = sum_s a(s,#) n_s(l(c))).
 template <int D2, int D3, int M, int MP>
-__device__ __forceinline__ void build_columns(const double* sg, double* nsc, double* Tc, int* wb, int lane) {
+__device__ __forceinline__ void build_columns(const double* sg, double* col, int lane) {
+  double* nsc = col;
+  double* Tc = col + 3 * MP;
+  int* wb = reinterpret_cast<int*>(col + 4 * MP);
+  double* beta = col + 5 * MP;
   for (int c = lane; c < MP; c += 32) {
     if (c < M) {
       const int l = c / D2, i = c - l * D2;
       const int mu = int(sg[26 + l]);
+      const double n0 = sg[10 + 3 * l], n1 = sg[11 + 3 * l], n2 = sg[12 + 3 * l];
+      nsc[c] = n0;
+      nsc[MP + c] = n1;
+      nsc[2 * MP + c] = n2;
 #pragma unroll
-      for (int s = 0; s < 3; ++s) nsc[s * MP + c] = sg[10 + 3 * l + s];
+      for (int h = 0; h < 3; ++h) beta[h * MP + c] = sg[1 + h] * n0 + sg[4 + h] * n1 + sg[7 + h] * n2;
       Tc[c] = sg[22 + l];
       wb[c] = (6 * l + mu - 1) * D2 * D3 + i;
     } else {
 #pragma unroll
-      for (int s = 0; s < 3; ++s) nsc[s * MP + c] = 0.0;
+      for (int h = 0; h < 3; ++h) nsc[h * MP + c] = beta[h * MP + c] = 0.0;
       Tc[c] = 0.0;
       wb[c] = -1;
     }
@@ -163,9 +173,12 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int MT = Dm::MT, NTM = Dm::NTM, KS = Dm::KS;
   constexpr int NLOW = NTM * (NTM + 1) / 2;        // lower tiles of the m x m output
   constexpr int WM = NW > 1 ? 1 : 0;               // warp inverting the next element's M
-  constexpr int GW0 = NW > 2 ? 2 : (NW > 1 ? 1 : 0);  // first warp owning output tiles
-  constexpr int NGW = NW - GW0;                    // output-tile warps
-  constexpr int TPW = (NLOW + NGW - 1) / NGW;      // tiles per output warp
+  constexpr int GW0 = NW > 2 ? 2 : (NW > 1 ? 1 : 0);  // first warp computing W Zp during GJ
+  constexpr int NGW = NW - GW0;
+  constexpr int TPW = (NLOW + NGW - 1) / NGW;
+  constexpr int HG = 3;                            // H output tiles per task
+  constexpr int NHG = (NTM + HG - 1) / HG;         // H column groups
+  constexpr int NT2 = MT + MT * NHG;               // P2 tasks
   extern __shared__ double smem[];
   for (int i = threadIdx.x; i < EPB * Dm::PER_ELT; i += blockDim.x) smem[i] = 0.0;
   __syncthreads();
@@ -179,14 +192,13 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   double* base = smem + tm.id * Dm::PER_ELT;
   double* Mi = base + Dm::OFF_MI;
   double* Sb = base + Dm::OFF_S;
-  double* Yb = base + Dm::OFF_Y;   // Y_s, later Vs
-  double* Zb = base + Dm::OFF_Z;   // Zp
+  double* Yb = base + Dm::OFF_Y;   // R_#, later Vs
+  double* Zb = base + Dm::OFF_Z;   // Zp, later (W Zp) lower tiles
   double* Vb = base + Dm::OFF_V;
   double* fv = base + Dm::OFF_F;
   double* fs = base + Dm::OFF_FS;
   double* stgS = base + Dm::OFF_STG;
   double* stgM = base + Dm::OFF_STG2;
-  // double-buffered per-element records: nsc(3MP) Tc(MP) wb(MP) and geometry
   auto colbuf = [&](int b) { return base + (b ? Dm::OFF_COL : Dm::OFF_NSC); };
   auto sgbuf = [&](int b) { return base + Dm::OFF_GEO + 32 * b; };
   const double* Wlm = tab.Wlm;
@@ -218,9 +230,7 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       if (bad && lane == 0) flag_bad(bad_element, K);
     }
     tm.sync();
-    if (tm.warp == NW - 1)
-      build_columns<D2, D3, M, MP>(sgbuf(0), colbuf(0), colbuf(0) + 3 * MP,
-                                   reinterpret_cast<int*>(colbuf(0) + 4 * MP), lane);
+    if (tm.warp == NW - 1) build_columns<D2, D3, M, MP>(sgbuf(0), colbuf(0), lane);
     tm.sync();
   }
 
@@ -234,15 +244,14 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     const double* nsc = colbuf(cur);
     const double* Tc = colbuf(cur) + 3 * MP;
     const int* wb = reinterpret_cast<const int*>(colbuf(cur) + 4 * MP);
+    const double* beta = colbuf(cur) + 5 * MP;
 
-    // ------------------------------------- P1: Zp = Mi W^T, Y_s = Mi C_s^T
-    for (int task = tm.warp; task < NTM + 3 * MT; task += NW) {
-      double acc[MT][2];
-#pragma unroll
-      for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
-      double* out;
-      int c0;
+    // -------- P1: Zp = Mi W^T ; R_# = sum_#' g(#,#') Mi Chat_#'^T, g = a^T a
+    for (int task = tm.warp; task < NTM + MT; task += NW) {
       if (task < NTM) {
+        double acc[MT][2];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
         const int wbc = wb[task * 8 + g];
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
@@ -251,92 +260,128 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
           for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], Mi[(m * 8 + g) + k * LD], b);
         }
-        out = Zb;
-        c0 = task * 8 + 2 * t;
+        const int c0 = task * 8 + 2 * t;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          Zb[(m * 8 + g) + c0 * LD] = acc[m][0];
+          Zb[(m * 8 + g) + (c0 + 1) * LD] = acc[m][1];
+        }
       } else {
-        const int s = (task - NTM) / MT, nt = (task - NTM) % MT;
+        const int nt = task - NTM;
         const int c = nt * 8 + g;
-        const double as0 = a9[3 * s], as1 = a9[3 * s + 1], as2 = a9[3 * s + 2];
+        double q[3][MT][2];
+#pragma unroll
+        for (int h = 0; h < 3; ++h)
+#pragma unroll
+          for (int m = 0; m < MT; ++m) q[h][m][0] = q[h][m][1] = 0.0;
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
           const int k = kk * 4 + t;
-          double b = 0.0;  // C_s^T(k, c) = sum_# a(s,#) Chat_#(c, k)
-          if (k < D3 && c < D3) {
-            const int o = c + k * D3;
-            b = as0 * __ldg(Ch + o) + as1 * __ldg(Ch + D3 * D3 + o) + as2 * __ldg(Ch + 2 * D3 * D3 + o);
+          const bool in = k < D3 && c < D3;
+          const int o = c + k * D3;  // Chat_#^T(k, c) = Chat_#(c, k)
+          const double b0 = in ? __ldg(Ch + o) : 0.0, b1 = in ? __ldg(Ch + D3 * D3 + o) : 0.0,
+                       b2 = in ? __ldg(Ch + 2 * D3 * D3 + o) : 0.0;
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const double a = Mi[(m * 8 + g) + k * LD];
+            dmma(q[0][m][0], q[0][m][1], a, b0);
+            dmma(q[1][m][0], q[1][m][1], a, b1);
+            dmma(q[2][m][0], q[2][m][1], a, b2);
           }
-#pragma unroll
-          for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], Mi[(m * 8 + g) + k * LD], b);
         }
-        out = Yb + s * D3P * LD;
-        c0 = nt * 8 + 2 * t;
-      }
+        double gm[3][3];
 #pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        const int r = m * 8 + g;
-        out[r + c0 * LD] = acc[m][0];
-        out[r + (c0 + 1) * LD] = acc[m][1];
+        for (int h = 0; h < 3; ++h)
+#pragma unroll
+          for (int h2 = 0; h2 < 3; ++h2)
+            gm[h][h2] = a9[h] * a9[h2] + a9[3 + h] * a9[3 + h2] + a9[6 + h] * a9[6 + h2];
+        const int c0 = nt * 8 + 2 * t;
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+          double* R = Yb + h * D3P * LD;
+#pragma unroll
+          for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              R[(m * 8 + g) + (c0 + e) * LD] =
+                  gm[h][0] * q[0][m][e] + gm[h][1] * q[1][m][e] + gm[h][2] * q[2][m][e];
+        }
       }
     }
     tm.sync();
 
-    // ------------- P2: S += sum_s C_s Y_s (lower) | V = sum_s C_s Zp N_s + T^T
-    for (int task = tm.warp; task < 2 * MT; task += NW) {
-      const bool isS = task < MT;
-      const int mt = isS ? task : task - MT;
-      const int r = mt * 8 + g;
-      double acc[NTM][2];
+    // ---- P2: S += sum_# Chat_# R_# (lower tiles) | V = sum_# (Chat_# Zp) beta_# + T^T
+    for (int task = tm.warp; task < NT2; task += NW) {
+      if (task < MT) {
+        const int mt = task;
+        const int r = mt * 8 + g;
+        double acc[MT][2];
 #pragma unroll
-      for (int j = 0; j < NTM; ++j) acc[j][0] = acc[j][1] = 0.0;
+        for (int j = 0; j < MT; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        const double as0 = a9[3 * s], as1 = a9[3 * s + 1], as2 = a9[3 * s + 2];
-        const double* Y = Yb + s * D3P * LD;
-        double ns[NTM];
+        for (int h = 0; h < 3; ++h) {
+          const double* R = Yb + h * D3P * LD;
+          const double* C = Ch + h * D3 * D3;
 #pragma unroll
-        for (int j = 0; j < NTM; ++j) ns[j] = nsc[s * MP + j * 8 + g];
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-          const int k = kk * 4 + t;
-          double a = 0.0;  // C_s(r, k)
-          if (r < D3 && k < D3) {
-            const int o = r + k * D3;
-            a = as0 * __ldg(Ch + o) + as1 * __ldg(Ch + D3 * D3 + o) + as2 * __ldg(Ch + 2 * D3 * D3 + o);
-          }
-          if (isS) {
+          for (int kk = 0; kk < KS; ++kk) {
+            const int k = kk * 4 + t;
+            const double a = (r < D3 && k < D3) ? __ldg(C + r + k * D3) : 0.0;
 #pragma unroll
             for (int j = 0; j < MT; ++j)
-              if (j <= mt) dmma(acc[j][0], acc[j][1], a, Y[k + (j * 8 + g) * LD]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < NTM; ++j) dmma(acc[j][0], acc[j][1], a, Zb[k + (j * 8 + g) * LD] * ns[j]);
+              if (j <= mt) dmma(acc[j][0], acc[j][1], a, R[k + (j * 8 + g) * LD]);
           }
         }
-      }
-      if (isS) {
 #pragma unroll
         for (int j = 0; j < MT; ++j) {
           if (j > mt) continue;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = j * 8 + 2 * t + h;
-            if (r < D3 && c <= r) Sb[r + c * LD] += acc[j][h];
+          for (int e = 0; e < 2; ++e) {
+            const int c = j * 8 + 2 * t + e;
+            if (r < D3 && c <= r) Sb[r + c * LD] += acc[j][e];
           }
         }
       } else {
+        const int mt = (task - MT) / NHG, grp = (task - MT) % NHG;
+        const int r = mt * 8 + g;
+        const int n0 = grp * HG;
+        double acc[HG][2], part[HG][2];
 #pragma unroll
-        for (int j = 0; j < NTM; ++j)
+        for (int j = 0; j < HG; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = j * 8 + 2 * t + h;
-            if (r < D3 && c < M) Vb[r + c * LD] = acc[j][h] + Tc[c] * __ldg(Wlm + wb[c] + r * D2);
+        for (int h = 0; h < 3; ++h) {
+          const double* C = Ch + h * D3 * D3;
+#pragma unroll
+          for (int j = 0; j < HG; ++j) part[j][0] = part[j][1] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk) {
+            const int k = kk * 4 + t;
+            const double a = (r < D3 && k < D3) ? __ldg(C + r + k * D3) : 0.0;
+#pragma unroll
+            for (int j = 0; j < HG; ++j)
+              if (n0 + j < NTM) dmma(part[j][0], part[j][1], a, Zb[k + ((n0 + j) * 8 + g) * LD]);
+          }
+#pragma unroll
+          for (int j = 0; j < HG; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = (n0 + j) * 8 + 2 * t + e;
+              if (n0 + j < NTM) acc[j][e] = fma(beta[h * MP + c], part[j][e], acc[j][e]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < HG; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = (n0 + j) * 8 + 2 * t + e;
+            if (n0 + j < NTM && r < D3 && c < M)
+              Vb[r + c * LD] = acc[j][e] + Tc[c] * __ldg(Wlm + wb[c] + r * D2);
           }
       }
     }
     tm.sync();
 
-    // --- P3: warp 0 Si = S^-1 | warp WM: M^-1 of the next element | output
-    //         warps: (W Zp) tiles held in registers; V, f -> recovery cache
+    // --- P3: warp 0 Si = S^-1 | warp WM: M^-1 of the next element | others:
+    //         (W Zp) lower tiles in registers; V, f -> recovery cache
     double accz[TPW][2];
 #pragma unroll
     for (int i = 0; i < TPW; ++i) accz[i][0] = accz[i][1] = 0.0;
@@ -402,26 +447,31 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     tm.sync();
 
-    // --------------------------------- P4: Vs = Si V (into Yb), fs = Si f
-    double* Vs = Yb;
-    for (int task = tm.warp; task < NTM; task += NW) {
-      double acc[MT][2];
+    // -------- P4: (W Zp) tiles -> Zb | Vs = Si V (into Yb) | fs = Si f | next
+    //          element's geometry + column data (double-buffered)
+    if (tm.warp >= GW0) {
+      const int ow = tm.warp - GW0;
 #pragma unroll
-      for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
-      const int c = task * 8 + g;
+      for (int i = 0; i < TPW; ++i) {
+        const int tile = ow + i * NGW;
+        if (tile >= NLOW) break;
+        Zb[tile * 64 + 2 * lane] = accz[i][0];
+        Zb[tile * 64 + 2 * lane + 1] = accz[i][1];
+      }
+    }
+    double* Vs = Yb;
+    for (int task = tm.warp; task < NTM * MT; task += NW) {
+      const int nt = task / MT, m = task % MT;
+      double a0 = 0, a1 = 0;
+      const int c = nt * 8 + g;
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
         const int k = kk * 4 + t;
-        const double b = Vb[k + c * LD];
-#pragma unroll
-        for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], Sb[(m * 8 + g) + k * LD], b);
+        dmma(a0, a1, Sb[(m * 8 + g) + k * LD], Vb[k + c * LD]);
       }
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        const int r = m * 8 + g, c0 = task * 8 + 2 * t;
-        Vs[r + c0 * LD] = acc[m][0];
-        Vs[r + (c0 + 1) * LD] = acc[m][1];
-      }
+      const int r = m * 8 + g, c0 = nt * 8 + 2 * t;
+      Vs[r + c0 * LD] = a0;
+      Vs[r + (c0 + 1) * LD] = a1;
     }
     for (int r = tm.tid; r < D3; r += NT) {
       double s = 0.0;
@@ -429,68 +479,60 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       for (int k = 0; k < D3; ++k) s += Sb[r + k * LD] * fv[k];
       fs[r] = s;
     }
+    if (has_next && tm.warp == NW - 1) {
+      const int nxt = cur ^ 1;
+      load_geo(geo, Kn, nelt, sgbuf(nxt), lane, 32);
+      __syncwarp();
+      build_columns<D2, D3, M, MP>(sgbuf(nxt), colbuf(nxt), lane);
+    }
     tm.sync();
 
-    // ---- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (output warps, lower tiles
-    //      mirrored) | Cf | next element's D, f, geometry, column data
-    if (tm.warp >= GW0) {
-      const int ow = tm.warp - GW0;
+    // ---- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (lower tiles, mirrored);
+    //      Cf; then the next element's D and f (Sb, fv are free)
+    for (int tile = tm.warp; tile < NLOW; tile += NW) {
+      int mt = 0, rem = tile;
+      while (rem > mt) { rem -= mt + 1; ++mt; }
+      const int nt = rem;
+      const int r = mt * 8 + g;
+      double v0 = 0, v1 = 0;
 #pragma unroll
-      for (int i = 0; i < TPW; ++i) {
-        const int tile = ow + i * NGW;
-        if (tile >= NLOW) break;
-        int mt = 0, rem = tile;
-        while (rem > mt) { rem -= mt + 1; ++mt; }
-        const int nt = rem;
-        const int r = mt * 8 + g;
-        double v0 = 0, v1 = 0;
+      for (int kk = 0; kk < KS; ++kk) {
+        const int k = kk * 4 + t;
+        dmma(v0, v1, Vb[k + r * LD], Vs[k + (nt * 8 + g) * LD]);
+      }
+      const double z0 = Zb[tile * 64 + 2 * lane], z1 = Zb[tile * 64 + 2 * lane + 1];
+      if (r < M) {
+        const int l1 = r / D2;
+        const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
 #pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-          const int k = kk * 4 + t;
-          dmma(v0, v1, Vb[k + r * LD], Vs[k + (nt * 8 + g) * LD]);
-        }
-        if (r < M) {
-          const int l1 = r / D2;
-          const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = nt * 8 + 2 * t + h;
-            if (c > r || c >= M) continue;
-            const int l2 = c / D2;
-            const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
-            double v = nn * accz[i][h] - (h ? v1 : v0);
-            if (l1 == l2) v += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
-            Ck[r + c * M] = v;
-            if (c != r) Ck[c + r * M] = v;
-          }
+        for (int e = 0; e < 2; ++e) {
+          const int c = nt * 8 + 2 * t + e;
+          if (c > r || c >= M) continue;
+          const int l2 = c / D2;
+          const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
+          double v = nn * (e ? z1 : z0) - (e ? v1 : v0);
+          if (l1 == l2) v += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
+          Ck[r + c * M] = v;
+          if (c != r) Ck[c + r * M] = v;
         }
       }
     }
-    if (tm.warp < GW0 || NW == 1) {
-      const int t0 = NW == 1 ? lane : tm.tid, nt0 = NW == 1 ? 32 : GW0 * 32;
-      for (int r = t0; r < M; r += nt0) {
-        double s = 0.0;
+    for (int r = tm.tid; r < M; r += NT) {
+      double s = 0.0;
 #pragma unroll
-        for (int k = 0; k < D3; ++k) s += Vb[k + r * LD] * fs[k];
-        Cfout[K * M + r] = s;
-      }
+      for (int k = 0; k < D3; ++k) s += Vb[k + r * LD] * fs[k];
+      Cfout[K * M + r] = s;
     }
-    tm.sync();  // Sb, fv, sg[next], colbuf[next] are free below
-    if (has_next) {
-      const int nxt = cur ^ 1;
-      load_geo(geo, Kn, nelt, sgbuf(nxt), tm.tid, NT);
+    if (has_next) {  // Sb and fv are not read in P5
+
       for (int j = 0; j < D3; ++j) {
         const int b0 = sym_idx(j, j, D3);
         for (int i = tm.tid; i < D3 - j; i += NT) Sb[(j + i) + j * LD] = Dsym[Kn * Dm::NSYM + b0 + i];
       }
       for (int i = tm.tid; i < D3; i += NT) fv[i] = fvec[Kn * D3 + i];
-      tm.sync();
-      if (tm.warp == NW - 1)
-        build_columns<D2, D3, M, MP>(sgbuf(nxt), colbuf(nxt), colbuf(nxt) + 3 * MP,
-                                     reinterpret_cast<int*>(colbuf(nxt) + 4 * MP), lane);
-      tm.sync();
-      cur = nxt;
+      cur ^= 1;
     }
+    tm.sync();
   }
 }
 
