@@ -176,9 +176,8 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int GW0 = NW > 2 ? 2 : (NW > 1 ? 1 : 0);  // first warp computing W Zp during GJ
   constexpr int NGW = NW - GW0;
   constexpr int TPW = (NLOW + NGW - 1) / NGW;
-  constexpr int HG = 3;                            // H output tiles per task
-  constexpr int NHG = (NTM + HG - 1) / HG;         // H column groups
-  constexpr int NT2 = MT + MT * NHG;               // P2 tasks
+  constexpr int NLS = MT * (MT + 1) / 2;           // lower tiles of S
+  constexpr int NTF = (D2 + 7) / 8 + 1;            // N-tiles a face's columns can span
   extern __shared__ double smem[];
   for (int i = threadIdx.x; i < EPB * Dm::PER_ELT; i += blockDim.x) smem[i] = 0.0;
   __syncthreads();
@@ -310,14 +309,16 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     tm.sync();
 
-    // ---- P2: S += sum_# Chat_# R_# (lower tiles) | V = sum_# (Chat_# Zp) beta_# + T^T
-    for (int task = tm.warp; task < NT2; task += NW) {
-      if (task < MT) {
-        const int mt = task;
+    // ---- P2: S += sum_# Chat_# R_# (one task per lower tile, two partial
+    //      chains) | V_l = Chat_l Zp_l + T_l W_l^T per face l, with
+    //      Chat_l = sum_# beta_#(l) Chat_# (H = sum_s C_s Mi E_s^T by faces)
+    for (int task = tm.warp; task < NLS + MT * 4; task += NW) {
+      if (task < NLS) {
+        int mt = 0, rem = task;
+        while (rem > mt) { rem -= mt + 1; ++mt; }
+        const int j = rem;
         const int r = mt * 8 + g;
-        double acc[MT][2];
-#pragma unroll
-        for (int j = 0; j < MT; ++j) acc[j][0] = acc[j][1] = 0.0;
+        double p0 = 0, p1 = 0, q0 = 0, q1 = 0;
 #pragma unroll
         for (int h = 0; h < 3; ++h) {
           const double* R = Yb + h * D3P * LD;
@@ -326,54 +327,45 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           for (int kk = 0; kk < KS; ++kk) {
             const int k = kk * 4 + t;
             const double a = (r < D3 && k < D3) ? __ldg(C + r + k * D3) : 0.0;
-#pragma unroll
-            for (int j = 0; j < MT; ++j)
-              if (j <= mt) dmma(acc[j][0], acc[j][1], a, R[k + (j * 8 + g) * LD]);
+            if (kk & 1) dmma(q0, q1, a, R[k + (j * 8 + g) * LD]);
+            else dmma(p0, p1, a, R[k + (j * 8 + g) * LD]);
           }
         }
 #pragma unroll
-        for (int j = 0; j < MT; ++j) {
-          if (j > mt) continue;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int c = j * 8 + 2 * t + e;
-            if (r < D3 && c <= r) Sb[r + c * LD] += acc[j][e];
-          }
+        for (int e = 0; e < 2; ++e) {
+          const int c = j * 8 + 2 * t + e;
+          if (r < D3 && c <= r) Sb[r + c * LD] += (e ? p1 + q1 : p0 + q0);
         }
       } else {
-        const int mt = (task - MT) / NHG, grp = (task - MT) % NHG;
+        const int mt = (task - NLS) >> 2, l = (task - NLS) & 3;
         const int r = mt * 8 + g;
-        const int n0 = grp * HG;
-        double acc[HG][2], part[HG][2];
+        const int cl0 = l * D2, cl1 = cl0 + D2;     // face-l columns [cl0, cl1)
+        const int nt0 = cl0 / 8;
+        const double b0 = beta[cl0], b1 = beta[MP + cl0], b2 = beta[2 * MP + cl0];
+        double acc[NTF][2];
 #pragma unroll
-        for (int j = 0; j < HG; ++j) acc[j][0] = acc[j][1] = 0.0;
+        for (int j = 0; j < NTF; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
-        for (int h = 0; h < 3; ++h) {
-          const double* C = Ch + h * D3 * D3;
-#pragma unroll
-          for (int j = 0; j < HG; ++j) part[j][0] = part[j][1] = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < KS; ++kk) {
-            const int k = kk * 4 + t;
-            const double a = (r < D3 && k < D3) ? __ldg(C + r + k * D3) : 0.0;
-#pragma unroll
-            for (int j = 0; j < HG; ++j)
-              if (n0 + j < NTM) dmma(part[j][0], part[j][1], a, Zb[k + ((n0 + j) * 8 + g) * LD]);
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          double a = 0.0;
+          if (r < D3 && k < D3) {
+            const int o = r + k * D3;
+            a = b0 * __ldg(Ch + o) + b1 * __ldg(Ch + D3 * D3 + o) + b2 * __ldg(Ch + 2 * D3 * D3 + o);
           }
 #pragma unroll
-          for (int j = 0; j < HG; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int c = (n0 + j) * 8 + 2 * t + e;
-              if (n0 + j < NTM) acc[j][e] = fma(beta[h * MP + c], part[j][e], acc[j][e]);
-            }
+          for (int j = 0; j < NTF; ++j) {
+            const int c = (nt0 + j) * 8 + g;  // B column of this lane
+            const double b = (c >= cl0 && c < cl1) ? Zb[k + c * LD] : 0.0;
+            if ((nt0 + j) * 8 < cl1) dmma(acc[j][0], acc[j][1], a, b);
+          }
         }
 #pragma unroll
-        for (int j = 0; j < HG; ++j)
+        for (int j = 0; j < NTF; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int c = (n0 + j) * 8 + 2 * t + e;
-            if (n0 + j < NTM && r < D3 && c < M)
+            const int c = (nt0 + j) * 8 + 2 * t + e;
+            if (c >= cl0 && c < cl1 && r < D3)
               Vb[r + c * LD] = acc[j][e] + Tc[c] * __ldg(Wlm + wb[c] + r * D2);
           }
       }
