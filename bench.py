@@ -41,6 +41,24 @@ FP64_PEAK_TFLOPS = 37.0   # measured DMMA peak on this pool's B200 (profiles/fp6
 FP64_PEAK_SOURCE = "profiles/fp64_peaks_r01.jsonl (mma.sync f64 microbenchmark; MEASURED_PEAKS.json has no FP64 entry)"
 
 
+def ncu_traffic(kernel_prefix: str):
+    """dram read+write bytes per launch of a kernel from the newest committed
+    ncu launch list (profiles/r*_launches.csv), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_launches.csv")))
+    if not files:
+        return None, None
+    vals = []
+    for line in open(files[-1]):
+        parts = line.strip().split(",")
+        if len(parts) >= 5 and kernel_prefix in parts[1]:
+            try:
+                vals.append(float(parts[3]) + float(parts[4]))
+            except ValueError:
+                pass
+    return (min(vals) if vals else None), os.path.relpath(files[-1], ROOT)
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -344,9 +362,12 @@ def run_ours(args):
     hbm_peak, hbm_src = load_peaks()
     k3_ms = stage_ms.get("condense", float("nan"))
     achieved = k3_flops(k) * nelt / (k3_ms / 1e3) / 1e12
+    traffic, traffic_src = ncu_traffic(f"condense2_kernel<{k}>" if k <= 3 else f"condense_kernel<{k}>")
     roof = {"kernel": "condense_kernel (K3)", "bound": "tensor", "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-            "traffic": None, "peak_source": FP64_PEAK_SOURCE, "flops_per_element": k3_flops(k),
+            "traffic": traffic if cfg.name == "C2" and world == 1 else None,
+            "traffic_source": traffic_src, "algorithmic_bytes": k3_bytes(k) * nelt,
+            "peak_source": FP64_PEAK_SOURCE, "flops_per_element": k3_flops(k),
             "pipe": "fp64 (DMMA mma.sync m8n8k4)"}
     kern = {}
     for kname, v in stage_ms.items():

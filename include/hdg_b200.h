@@ -102,6 +102,10 @@ int hdg_b200_pattern_dims(const hdg_mesh* m, int64_t* nnbr_total);
 int hdg_b200_pattern_build(const hdg_mesh* m, int64_t* h_facebase /* nfc+1 */,
                            int* h_nbr /* nfc x 8 row-major, -1 padded */,
                            uint8_t* h_slot /* nelt x 16 */);
+/* Same from a bare facebyele (nelt x 4, faces numbered 0..nfc-1), e.g. a
+ * slab's locally renumbered faces in multi-GPU runs. Any output may be NULL. */
+int hdg_b200_pattern_build_raw(int nelt, int nfc, const int* h_facebyele, int64_t* nnbr_total,
+                               int64_t* h_facebase, int* h_nbr, uint8_t* h_slot);
 
 /* ------------------------------------------------------------- context */
 int hdg_b200_create(int device, void* cuda_stream, hdg_ctx** out);

@@ -67,6 +67,7 @@ _SIGS = {
     "hdg_b200_mesh_free": (None, [P]),
     "hdg_b200_pattern_dims": (C.c_int, [P, I64P]),
     "hdg_b200_pattern_build": (C.c_int, [P, P, P, P]),
+    "hdg_b200_pattern_build_raw": (C.c_int, [C.c_int, C.c_int, P, I64P, P, P, P]),
     "hdg_b200_create": (C.c_int, [C.c_int, P, C.POINTER(P)]),
     "hdg_b200_destroy": (None, [P]),
     "hdg_b200_set_stream": (C.c_int, [P, P]),

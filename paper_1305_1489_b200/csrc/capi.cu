@@ -414,6 +414,19 @@ int hdg_b200_pattern_build(const hdg_mesh* mc, int64_t* h_facebase, int* h_nbr, 
   });
 }
 
+int hdg_b200_pattern_build_raw(int nelt, int nfc, const int* h_facebyele, int64_t* nnbr_total,
+                               int64_t* h_facebase, int* h_nbr, uint8_t* h_slot) {
+  return guarded([&] {
+    require(nelt > 0 && nfc > 0 && h_facebyele, HDG_EINVAL, "bad argument");
+    SkeletonPattern p;
+    build_pattern_raw(nelt, nfc, h_facebyele, p);
+    if (nnbr_total) *nnbr_total = p.facebase.back();
+    if (h_facebase) std::memcpy(h_facebase, p.facebase.data(), p.facebase.size() * 8);
+    if (h_nbr) std::memcpy(h_nbr, p.nbr.data(), p.nbr.size() * 4);
+    if (h_slot) std::memcpy(h_slot, p.slot.data(), p.slot.size());
+  });
+}
+
 // --------------------------------------------------------------- context
 int hdg_b200_create(int device, void* stream, hdg_ctx** out) {
   return guarded([&] {

@@ -79,5 +79,6 @@ struct SkeletonPattern {
   std::vector<uint8_t> slot;    // nelt x 16
 };
 void build_pattern(const HostMesh& m, SkeletonPattern& p);
+void build_pattern_raw(int nelt, int nfc, const int* facebyele, SkeletonPattern& p);
 
 }  // namespace hdgb

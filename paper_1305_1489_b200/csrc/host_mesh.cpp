@@ -255,17 +255,27 @@ void expand_mesh(HostMesh& m) {
 // and f2 are faces of a common element; structurally symmetric, so the CSR
 // pattern equals Eigen's CSC pattern (rows sorted, duplicates summed).
 void build_pattern(const HostMesh& m, SkeletonPattern& p) {
-  const int nfc = m.nfc, nelt = m.nelt;
+  build_pattern_raw(m.nelt, m.nfc, m.facebyele.data(), p);
+}
+
+// Same from a bare facebyele (nelt x 4, column-major): used for slab-local
+// patterns in multi-GPU runs, where a slab's faces are renumbered locally.
+void build_pattern_raw(int nelt, int nfc, const int* facebyele, SkeletonPattern& p) {
+  struct {
+    const int* fbe;
+    int fb(size_t i) const { return fbe[i]; }
+  } m{facebyele};
   p.nfc = nfc;
   p.nbr.assign(size_t(nfc) * 8, -1);
   p.nnbr.assign(nfc, 0);
   std::vector<int> cand(size_t(nfc) * 8, -1), ncand(nfc, 0);
   for (int K = 0; K < nelt; ++K)
     for (int l1 = 0; l1 < 4; ++l1) {
-      const int f1 = m.facebyele[K + size_t(l1) * nelt];
+      const int f1 = m.fb(K + size_t(l1) * nelt);
+      if (f1 < 0 || f1 >= nfc) throw MeshError("facebyele entry out of range");
       for (int l2 = 0; l2 < 4; ++l2) {
         if (ncand[f1] >= 8) throw MeshError("face belongs to more than two elements");
-        cand[size_t(f1) * 8 + ncand[f1]++] = m.facebyele[K + size_t(l2) * nelt];
+        cand[size_t(f1) * 8 + ncand[f1]++] = m.fb(K + size_t(l2) * nelt);
       }
     }
   p.maxnbr = 0;
@@ -282,10 +292,10 @@ void build_pattern(const HostMesh& m, SkeletonPattern& p) {
   p.slot.assign(size_t(nelt) * 16, 0);
   for (int K = 0; K < nelt; ++K)
     for (int l1 = 0; l1 < 4; ++l1) {
-      const int f1 = m.facebyele[K + size_t(l1) * nelt];
+      const int f1 = m.fb(K + size_t(l1) * nelt);
       const int* nb = &p.nbr[size_t(f1) * 8];
       for (int l2 = 0; l2 < 4; ++l2) {
-        const int f2 = m.facebyele[K + size_t(l2) * nelt];
+        const int f2 = m.fb(K + size_t(l2) * nelt);
         const int pos = int(std::lower_bound(nb, nb + p.nnbr[f1], f2) - nb);
         p.slot[size_t(K) * 16 + l1 * 4 + l2] = uint8_t(pos);
       }

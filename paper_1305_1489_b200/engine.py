@@ -407,7 +407,10 @@ class Engine:
 
     # ---------------------------------------------------------------- K4
     def pattern(self, mesh: HostMesh, csr: bool = True) -> DevicePattern:
-        fb, nb, sl = mesh.pattern()
+        return self.pattern_from_arrays(*mesh.pattern(), csr=csr)
+
+    def pattern_from_arrays(self, fb: np.ndarray, nb: np.ndarray, sl: np.ndarray, csr: bool = True) -> DevicePattern:
+        """Device pattern from (facebase, nbr, slot), e.g. partition.slab_pattern."""
         dev = self.device
         p = DevicePattern(torch.from_numpy(fb).to(dev), torch.from_numpy(nb).to(dev), torch.from_numpy(sl).to(dev))
         if csr:

@@ -25,6 +25,7 @@ class Slab:
     vert_global: np.ndarray   # local vertex -> global vertex
     face_global: np.ndarray   # local face -> global face (ascending)
     interface: np.ndarray     # local ids of faces shared with another slab
+    interface_rank: np.ndarray  # rank owning the other side of each interface face
     coords: np.ndarray        # (nver_local, 3)
     elements: np.ndarray      # (nelt_local, 4) local vertex ids
     faces: np.ndarray         # (nfc_local, 3) local vertex ids, global parametrisation
@@ -48,7 +49,16 @@ def slab(mesh: HostMesh, rank: int, nranks: int) -> Slab:
     counts_in = np.bincount(fbe_local.reshape(-1), minlength=len(fg))
     ftype = mesh.facetype[fg]
     interface = np.flatnonzero((ftype == 0) & (counts_in == 1))
-    return Slab(rank, nranks, e0, e1, vg, fg, interface, mesh.coordinates[vg],
+    # the rank on the other side: the face's element outside [e0, e1)
+    all_f = mesh.facebyele.reshape(-1)
+    all_e = np.repeat(np.arange(nelt), 4)
+    order = np.argsort(all_f, kind="stable")
+    fs, es = all_f[order], all_e[order]
+    pos = np.searchsorted(fs, fg[interface])
+    ea, eb = es[pos], es[np.minimum(pos + 1, len(es) - 1)]
+    other = np.where((ea >= e0) & (ea < e1), eb, ea)
+    irank = (other // (nelt // nranks)).astype(np.int32)
+    return Slab(rank, nranks, e0, e1, vg, fg, interface, irank, mesh.coordinates[vg],
                 el_local.reshape(el.shape).astype(np.int32), faces.astype(np.int32),
                 fbe_local.reshape(fbe.shape).astype(np.int32), ftype)
 
@@ -58,3 +68,17 @@ def upload_slab(s: Slab, device: torch.device) -> DeviceMesh:
     return DeviceMesh(len(s.vert_global), s.elements.shape[0], len(s.face_global),
                       t(s.coords, torch.float64), t(s.elements, torch.int32), t(s.faces, torch.int32),
                       t(s.facebyele, torch.int32), torch.from_numpy(s.facetype).to(device))
+
+
+def slab_pattern(s: Slab):
+    """Skeleton sparsity of the slab's local faces (hdg_b200_pattern_build_raw)."""
+    import ctypes as C
+    from . import _lib as L
+    nelt, nfc = s.facebyele.shape[0], len(s.face_global)
+    fbe = np.asfortranarray(s.facebyele, dtype=np.int32)
+    fb = np.zeros(nfc + 1, np.int64)
+    nb = np.zeros((nfc, 8), np.int32)
+    sl = np.zeros((nelt, 16), np.uint8)
+    L.check(L.lib().hdg_b200_pattern_build_raw(nelt, nfc, fbe.ctypes.data, None, fb.ctypes.data,
+                                               nb.ctypes.data, sl.ctypes.data))
+    return fb, nb, sl

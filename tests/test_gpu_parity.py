@@ -295,3 +295,47 @@ def test_jit_and_interpreter_agree():
     # fields differ only by FMA contraction in the compiled expressions
     assert max_slice_relerr(np_(cs_jit.C_slices()), np_(cs_vm.C_slices())) < 1e-11
     assert max_slice_relerr(np_(cs_jit.Cf_cols()), np_(cs_vm.Cf_cols())) < 1e-11
+
+
+def test_two_slab_scatter_exchange_matches_global():
+    """z-slab scatter on the GPU (K4 into slab-local CSR) + interface exchange
+    == the single-mesh GPU assembly, bit for bit."""
+    from paper_1305_1489_b200.distributed import SlabExchange, exchange_local
+    from paper_1305_1489_b200.partition import slab, slab_pattern, upload_slab
+    k = 2
+    mesh = HostMesh.box(3, 3, 6, bc="dirichlet_x")
+    eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
+    pat = eng.pattern(mesh)
+    full = eng.assemble(dm, pat, cs)
+    d2 = dim2(k)
+    m = 4 * d2
+    exs, systems, slabs = [], [], []
+    for r in range(2):
+        s = slab(mesh, r, 2)
+        fb, nb, sl = slab_pattern(s)
+        sdm = upload_slab(s, torch.device("cuda"))
+        sp_ = eng.pattern_from_arrays(fb, nb, sl)
+        from paper_1305_1489_b200.engine import CondensedSystem
+        n = s.elem_end - s.elem_begin
+        scs = CondensedSystem(cs.C[s.elem_begin * m * m:s.elem_end * m * m], cs.Cf[s.elem_begin * m:s.elem_end * m],
+                              None, m)
+        ssys = eng.assemble(sdm, sp_, scs)
+        exs.append(SlabExchange(s, fb, nb, d2, torch.device("cuda")))
+        systems.append((ssys.vals, ssys.b))
+        slabs.append((s, fb, nb, ssys))
+    exchange_local(exs, systems)
+    import scipy.sparse as sp
+    nd = dm.nfc * d2
+    H = sp.csr_matrix((np_(full.vals), np_(full.colidx), np_(full.rowptr)), shape=(nd, nd))
+    bg = np_(full.b)
+    for s, fb, nb, ssys in slabs:
+        fg = s.face_global
+        vals, b = np_(ssys.vals), np_(ssys.b)
+        rows = (fg[:, None] * d2 + np.arange(d2)).reshape(-1)
+        assert np.array_equal(b, bg[rows])
+        rp, ci = np_(ssys.rowptr), np_(ssys.colidx)
+        gcols = (fg[ci // d2] * d2 + ci % d2)
+        for lr in range(len(rows)):
+            seg = slice(rp[lr], rp[lr + 1])
+            want = np.asarray(H[rows[lr], gcols[seg]].todense()).ravel()
+            assert np.array_equal(vals[seg], want)
