@@ -324,6 +324,40 @@ def run_ours(args):
     # sanity: outputs finite
     assert torch.isfinite(cs.C).all() and torch.isfinite(ls.u).all(), "non-finite outputs"
 
+    # ------------------------------------------- K4 scatter + slab exchange
+    # Reported beside the step ("K4 and the NCCL exchange are
+    # reported separately"): slab-local CSR values + b, then the interface
+    # faces' diagonal blocks and b summed with the neighbour slabs.
+    scatter_info = None
+    if not args.no_scatter:
+        from paper_1305_1489_b200.distributed import SlabExchange
+        fb, nb, slt = partition.slab_pattern(sl)
+        with torch.cuda.stream(stream):
+            pat = eng.pattern_from_arrays(fb, nb, slt)
+            sysH = eng.assemble(dm, pat, cs)
+            ex = SlabExchange(sl, fb, nb, d2, dev)
+            stream.synchronize()
+            if world > 1:
+                dist.barrier()
+            sc_ms, ex_ms = [], []
+            for _ in range(max(1, min(args.steps, 5))):
+                a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                a0.record(stream)
+                eng.assemble(dm, pat, cs, out=sysH)
+                a1.record(stream)
+                if world > 1:
+                    ex.exchange(sysH.vals, sysH.b)
+                a2.record(stream)
+                a2.synchronize()
+                sc_ms.append(a0.elapsed_time(a1))
+                ex_ms.append(a1.elapsed_time(a2))
+        eng.stage_times()
+        scatter_info = {"scatter_ms": float(np.median(sc_ms)), "exchange_ms": float(np.median(ex_ms)),
+                        "nnz": int(sysH.vals.numel()), "interface_faces": int(len(sl.interface)),
+                        "exchange_bytes": int(sum(v[0].numel() + v[1].numel() for v in ex.peers.values()) * 8),
+                        "scatter_hbm_gbs": 2 * 8.0 * (4 * d2) * (4 * d2 + 1) * nelt / (np.median(sc_ms) / 1e3) / 1e9}
+        del sysH, pat
+
     # ---------------------------------------------------------------- e2e
     # Through the public API with HOST buffers: H2D of the step's inputs (mesh
     # arrays + lambda, pinned), the step, D2H of its results (C, Cf, q, u).
@@ -393,6 +427,7 @@ def run_ours(args):
         "e2e": {"value": world * nelt / (e2e_ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                 "path": "pinned host mesh+lambda -> C ABI step -> pinned host C, Cf, q, u"},
+        "scatter": scatter_info,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "setup_s": t_setup,
@@ -418,6 +453,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-layers", type=int, default=2, help="cell layers in the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scatter", action="store_true",
+                    help="skip the separately reported K4 scatter + interface exchange timing")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
