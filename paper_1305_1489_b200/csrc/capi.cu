@@ -17,6 +17,7 @@
 #include "kernels_misc.cuh"
 #include "kernels_post.cuh"
 #include "kernels_condense2.cuh"
+#include "kernels_condense3.cuh"
 #include "jit_quad.hpp"
 
 using namespace hdgb;
@@ -218,6 +219,7 @@ struct hdg_ctx {
   int* h_status = nullptr;
   bool timing = false;
   bool jit = true;          // NVRTC-specialised K2 for program fields
+  int condense_variant = 3; // k = 2, 3: 3 = CTA-batched kernel, 2 = per-element teams
   std::string jit_error;    // last JIT failure (kernel then runs interpreted)
   cudaEvent_t ev[2 * HDG_NSTAGES] = {};
   bool pending[HDG_NSTAGES] = {};
@@ -254,6 +256,12 @@ int factor_doubles(int k) {
   return d3 * (d3 + 1) + d3 * m + d3;
 }
 
+// launch shape of the CTA-batched kernel in the (NW, EPB) vocabulary
+template <int K_>
+struct C3Launch {
+  static constexpr int EPB = C3Cfg<K_>::EPB, NW = C3Cfg<K_>::NWT / C3Cfg<K_>::EPB;
+};
+
 template <class Dm, class Cg, class Kern>
 void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, const double* Ms,
                           const double* Ds, const double* fv, double* C, double* Cf, double* F) {
@@ -273,7 +281,12 @@ void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, co
 template <int K_>
 void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, const double* Ds,
                      const double* fv, double* C, double* Cf, double* F) {
-  if constexpr (K_ <= 3)
+  if constexpr (K_ == 2 || K_ == 3) {
+    if (c->condense_variant == 2)
+      launch_condense_impl<C2Dims<K_>, C2Cfg<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+    else
+      launch_condense_impl<C2Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+  } else if constexpr (K_ <= 3)
     launch_condense_impl<C2Dims<K_>, C2Cfg<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
   else
     launch_condense_impl<CondDims<K_>, CondCfg<K_>>(c, condense_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
@@ -791,6 +804,13 @@ int hdg_b200_set_jit(hdg_ctx* c, int enabled) {
 }
 
 const char* hdg_b200_jit_status(const hdg_ctx* c) { return c ? c->jit_error.c_str() : ""; }
+
+int hdg_b200_set_variant(hdg_ctx* c, int variant) {
+  return guarded([&] {
+    require(c != nullptr && (variant == 2 || variant == 3), HDG_EINVAL, "variant must be 2 or 3");
+    c->condense_variant = variant;
+  });
+}
 
 int hdg_b200_synchronize(hdg_ctx* c) {
   return guarded([&] {

@@ -1,0 +1,399 @@
+// K3 v3 (k = 2, 3): CTA-batched static condensation.
+//
+// Same algebra as kernels_condense2.cuh (explicit M^-1, S^-1 by warp-register
+// sweep Gauss-Jordan; every contraction a DMMA tile loop over shared memory),
+// but the CTA advances EPB elements phase by phase: every phase pools the
+// tasks of all EPB elements over all warps (better balance, 5 CTA barriers
+// per EPB elements instead of 5 team barriers per element), and in P3 the
+// S^-1 sweeps of the batch run concurrently with the M^-1 sweeps of the next
+// batch and the W Zp tiles.
+#pragma once
+
+#include "kernels_condense2.cuh"
+
+namespace hdgb {
+
+template <int K_> struct C3Cfg;
+template <> struct C3Cfg<2> { static constexpr int EPB = 8, NWT = 16; };
+template <> struct C3Cfg<3> { static constexpr int EPB = 4, NWT = 16; };
+
+template <int K_>
+__global__ void __launch_bounds__(C3Cfg<K_>::NWT * 32)
+condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
+                 const double* __restrict__ Dsym, const double* __restrict__ fvec,
+                 double* __restrict__ Cout, double* __restrict__ Cfout, double* __restrict__ factors,
+                 long long* bad_element) {
+  using Dm = C2Dims<K_>;
+  constexpr int EPB = C3Cfg<K_>::EPB, NWT = C3Cfg<K_>::NWT, NT = NWT * 32;
+  constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, D3P = Dm::D3P, MP = Dm::MP, LD = Dm::LD;
+  constexpr int MT = Dm::MT, NTM = Dm::NTM, KS = Dm::KS;
+  constexpr int NLOW = NTM * (NTM + 1) / 2;  // lower tiles of the m x m output
+  constexpr int NLS = MT * (MT + 1) / 2;     // lower tiles of S
+  constexpr int NTF = (D2 + 7) / 8 + 1;      // N-tiles one face's columns can span
+  constexpr int NGJ = 2 * EPB;               // GJ tasks in P3
+  constexpr bool GJ_SEP = NWT > NGJ;         // GJ warps do nothing else in P3
+  static_assert(NLOW * 64 <= 3 * D3P * LD, "W Zp tiles must fit in the R buffer");
+  extern __shared__ double smem[];
+  for (int i = threadIdx.x; i < EPB * Dm::PER_ELT; i += blockDim.x) smem[i] = 0.0;
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const double* Wlm = tab.Wlm;
+  const double* Ch = tab.Chat;
+  auto B = [&](int e) { return smem + e * Dm::PER_ELT; };
+  auto Mi = [&](int e) { return B(e) + Dm::OFF_MI; };
+  auto Sb = [&](int e) { return B(e) + Dm::OFF_S; };
+  auto Yb = [&](int e) { return B(e) + Dm::OFF_Y; };  // R_#, then W Zp tiles
+  auto Zb = [&](int e) { return B(e) + Dm::OFF_Z; };  // Zp, then Vs
+  auto Vb = [&](int e) { return B(e) + Dm::OFF_V; };
+  auto fv = [&](int e) { return B(e) + Dm::OFF_F; };
+  auto fs = [&](int e) { return B(e) + Dm::OFF_FS; };
+  auto stS = [&](int e) { return B(e) + Dm::OFF_STG; };
+  auto stM = [&](int e) { return B(e) + Dm::OFF_STG2; };
+  auto colb = [&](int e, int b) { return B(e) + (b ? Dm::OFF_COL : Dm::OFF_NSC); };
+  auto sgb = [&](int e, int b) { return B(e) + Dm::OFF_GEO + 32 * b; };
+
+  const long stride = long(gridDim.x) * EPB;
+  long K0 = long(blockIdx.x) * EPB;
+  int cur = 0;
+
+  auto load_inputs = [&](long Kb, int which) {  // D, f, geometry of batch Kb (all threads)
+    for (int idx = threadIdx.x; idx < EPB * Dm::NSYM; idx += NT) {
+      const int e = idx / Dm::NSYM, p = idx - e * Dm::NSYM;
+      const long K = Kb + e;
+      if (K >= nelt) continue;
+      int j = 0, rem = p;  // packed lower (column-major) -> (i, j)
+      while (rem >= D3 - j) { rem -= D3 - j; ++j; }
+      Sb(e)[(j + rem) + j * LD] = Dsym[K * Dm::NSYM + p];
+    }
+    for (int idx = threadIdx.x; idx < EPB * D3; idx += NT) {
+      const int e = idx / D3, i = idx - e * D3;
+      if (Kb + e < nelt) fv(e)[i] = fvec[(Kb + e) * D3 + i];
+    }
+    for (int idx = threadIdx.x; which >= 0 && idx < EPB * 32; idx += NT) {
+      const int e = idx >> 5, i = idx & 31;
+      if (Kb + e < nelt && i < 30) {
+        const long K = Kb + e;
+        double v;
+        if (i == 0) v = geo.volume[K];
+        else if (i < 10) v = geo.piola[long(i - 1) * nelt + K];
+        else if (i < 22) v = geo.normals[long(i - 10) * nelt + K];
+        else if (i < 26) v = geo.T[long(i - 22) * nelt + K];
+        else v = double(geo.perm[long(i - 26) * nelt + K]);
+        sgb(e, which)[i] = v;
+      }
+    }
+  };
+  auto invert_M = [&](int e, long K) {  // warp-wide
+    double a[D3];
+    const bool bad = warp_inverse_packed<D3>(Msym + K * Dm::NSYM, a, stM(e), lane);
+    if (lane < D3) {
+#pragma unroll
+      for (int i = 0; i < D3; ++i) Mi(e)[i + lane * LD] = a[i];
+      if (factors) {
+#pragma unroll
+        for (int i = 0; i < D3; ++i)
+          if (i >= lane) factors[K * Dm::FACTORS + sym_idx(i, lane, D3)] = a[i];
+      }
+    }
+    if (bad && lane == 0) flag_bad(bad_element, K);
+  };
+
+  // ---- prologue: first batch
+  if (K0 < nelt) {
+    load_inputs(K0, 0);
+    for (int e = warp; e < EPB; e += NWT)
+      if (K0 + e < nelt) invert_M(e, K0 + e);
+    __syncthreads();
+    for (int e = warp; e < EPB; e += NWT) build_columns<D2, D3, M, MP>(sgb(e, 0), colb(e, 0), lane);
+    __syncthreads();
+  }
+
+  for (; K0 < nelt; K0 += stride) {
+    const long Kn0 = K0 + stride;
+    const bool has_next = Kn0 < nelt;
+    const int nb = int(nelt - K0 < EPB ? nelt - K0 : EPB);  // live elements in this batch
+
+    // -------- P1: Zp = Mi W^T (strips) ; R_# = sum_#' g(#,#') Mi Chat_#'^T (tiles)
+    for (int task = warp; task < nb * (MT * MT + NTM); task += NWT) {
+      const int e = task / (MT * MT + NTM), sub = task % (MT * MT + NTM);
+      const double* sg = sgb(e, cur);
+      const double* mi = Mi(e);
+      if (sub < MT * MT) {
+        const int m = sub / MT, nt = sub % MT;
+        const int c = nt * 8 + g;
+        double q[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          const bool in = k < D3 && c < D3;
+          const int o = c + k * D3;
+          const double a = mi[(m * 8 + g) + k * LD];
+          dmma(q[0][0], q[0][1], a, in ? __ldg(Ch + o) : 0.0);
+          dmma(q[1][0], q[1][1], a, in ? __ldg(Ch + D3 * D3 + o) : 0.0);
+          dmma(q[2][0], q[2][1], a, in ? __ldg(Ch + 2 * D3 * D3 + o) : 0.0);
+        }
+        const double* a9 = sg + 1;
+        const int c0 = nt * 8 + 2 * t, r = m * 8 + g;
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+          const double g0 = a9[h] * a9[0] + a9[3 + h] * a9[3] + a9[6 + h] * a9[6];
+          const double g1 = a9[h] * a9[1] + a9[3 + h] * a9[4] + a9[6 + h] * a9[7];
+          const double g2 = a9[h] * a9[2] + a9[3 + h] * a9[5] + a9[6 + h] * a9[8];
+          double* R = Yb(e) + h * D3P * LD;
+          R[r + c0 * LD] = g0 * q[0][0] + g1 * q[1][0] + g2 * q[2][0];
+          R[r + (c0 + 1) * LD] = g0 * q[0][1] + g1 * q[1][1] + g2 * q[2][1];
+        }
+      } else {
+        const int nt = sub - MT * MT;
+        const int* wb = reinterpret_cast<const int*>(colb(e, cur) + 4 * MP);
+        const int wbc = wb[nt * 8 + g];
+        double acc[MT][2];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          const double b = (wbc >= 0 && k < D3) ? __ldg(Wlm + wbc + k * D2) : 0.0;
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], mi[(m * 8 + g) + k * LD], b);
+        }
+        const int c0 = nt * 8 + 2 * t;
+        double* Z = Zb(e);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          Z[(m * 8 + g) + c0 * LD] = acc[m][0];
+          Z[(m * 8 + g) + (c0 + 1) * LD] = acc[m][1];
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- P2: S += sum_# Chat_# R_# (lower tiles) | V_l = Chat_l Zp_l + T_l W_l^T
+    for (int task = warp; task < nb * (NLS + 4 * MT); task += NWT) {
+      const int e = task / (NLS + 4 * MT), sub = task % (NLS + 4 * MT);
+      if (sub < NLS) {
+        int mt = 0, rem = sub;
+        while (rem > mt) { rem -= mt + 1; ++mt; }
+        const int j = rem, r = mt * 8 + g;
+        double p0 = 0, p1 = 0, q0 = 0, q1 = 0;
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+          const double* R = Yb(e) + h * D3P * LD;
+          const double* C = Ch + h * D3 * D3;
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk) {
+            const int k = kk * 4 + t;
+            const double a = (r < D3 && k < D3) ? __ldg(C + r + k * D3) : 0.0;
+            if (kk & 1) dmma(q0, q1, a, R[k + (j * 8 + g) * LD]);
+            else dmma(p0, p1, a, R[k + (j * 8 + g) * LD]);
+          }
+        }
+        double* S = Sb(e);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = j * 8 + 2 * t + h;
+          if (r < D3 && c <= r) S[r + c * LD] += (h ? p1 + q1 : p0 + q0);
+        }
+      } else {
+        const int mt = (sub - NLS) >> 2, l = (sub - NLS) & 3;
+        const int r = mt * 8 + g;
+        const int cl0 = l * D2, cl1 = cl0 + D2, nt0 = cl0 / 8;
+        const double* col = colb(e, cur);
+        const double* Tc = col + 3 * MP;
+        const int* wb = reinterpret_cast<const int*>(col + 4 * MP);
+        const double* beta = col + 5 * MP;
+        const double b0 = beta[cl0], b1 = beta[MP + cl0], b2 = beta[2 * MP + cl0];
+        const double* Z = Zb(e);
+        double acc[NTF][2];
+#pragma unroll
+        for (int j = 0; j < NTF; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          double a = 0.0;
+          if (r < D3 && k < D3) {
+            const int o = r + k * D3;
+            a = b0 * __ldg(Ch + o) + b1 * __ldg(Ch + D3 * D3 + o) + b2 * __ldg(Ch + 2 * D3 * D3 + o);
+          }
+#pragma unroll
+          for (int j = 0; j < NTF; ++j) {
+            const int c = (nt0 + j) * 8 + g;
+            const double b = (c >= cl0 && c < cl1) ? Z[k + c * LD] : 0.0;
+            if ((nt0 + j) * 8 < cl1) dmma(acc[j][0], acc[j][1], a, b);
+          }
+        }
+        double* V = Vb(e);
+#pragma unroll
+        for (int j = 0; j < NTF; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = (nt0 + j) * 8 + 2 * t + h;
+            if (c >= cl0 && c < cl1 && r < D3) V[r + c * LD] = acc[j][h] + Tc[c] * __ldg(Wlm + wb[c] + r * D2);
+          }
+      }
+    }
+    __syncthreads();
+
+    // ---- P3: S^-1 of the batch || M^-1 of the next batch || (W Zp) tiles -> Yb
+    //      || V, f -> recovery cache
+    {
+      const bool gj_warp = warp < NGJ;
+      if (gj_warp || !GJ_SEP) {
+        for (int task = warp; task < NGJ; task += (GJ_SEP ? NGJ : NWT)) {
+          const int e = task % EPB;
+          if (task < EPB) {
+            if (e >= nb) continue;
+            const long K = K0 + e;
+            double a[D3];
+#pragma unroll
+            for (int i = 0; i < D3; ++i) {
+              const int r = i > lane ? i : lane, c = i > lane ? lane : i;
+              a[i] = lane < D3 ? Sb(e)[r + c * LD] : 0.0;
+            }
+            double pmin = 1e300, pmax = 0.0;
+            warp_gj_inverse<D3>(a, stS(e), lane, pmin, pmax);
+            const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
+            if (lane < D3) {
+#pragma unroll
+              for (int i = 0; i < D3; ++i) Sb(e)[i + lane * LD] = a[i];
+              if (factors) {
+#pragma unroll
+                for (int i = 0; i < D3; ++i)
+                  if (i >= lane) factors[K * Dm::FACTORS + Dm::NSYM + sym_idx(i, lane, D3)] = a[i];
+              }
+            }
+            if (bad && lane == 0) flag_bad(bad_element, K);
+          } else if (has_next && Kn0 + e < nelt) {
+            invert_M(e, Kn0 + e);  // Mi(e) is dead after P1
+          }
+        }
+      }
+      if (!gj_warp || !GJ_SEP) {
+        const int w0 = GJ_SEP ? warp - NGJ : warp, nw = GJ_SEP ? NWT - NGJ : NWT;
+        for (int task = w0; task < nb * NLOW; task += nw) {
+          const int e = task / NLOW, tile = task % NLOW;
+          int mt = 0, rem = tile;
+          while (rem > mt) { rem -= mt + 1; ++mt; }
+          const int nt = rem;
+          const int* wb = reinterpret_cast<const int*>(colb(e, cur) + 4 * MP);
+          const int wbr = wb[mt * 8 + g];
+          const double* Z = Zb(e);
+          double z0 = 0, z1 = 0;
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk) {
+            const int k = kk * 4 + t;
+            const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
+            dmma(z0, z1, aw, Z[k + (nt * 8 + g) * LD]);
+          }
+          Yb(e)[tile * 64 + 2 * lane] = z0;
+          Yb(e)[tile * 64 + 2 * lane + 1] = z1;
+        }
+        if (factors) {
+          const int tid0 = w0 * 32 + lane, nth = nw * 32;
+          for (int idx = tid0; idx < nb * (D3 * M + D3); idx += nth) {
+            const int e = idx / (D3 * M + D3), p = idx % (D3 * M + D3);
+            double* F = factors + (K0 + e) * Dm::FACTORS + 2 * Dm::NSYM;
+            F[p] = p < D3 * M ? Vb(e)[(p % D3) + (p / D3) * LD] : fv(e)[p - D3 * M];
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- P4: Vs = Si V (into Zb) | fs = Si f | next batch's geometry + columns
+    for (int task = warp; task < nb * NTM * MT; task += NWT) {
+      const int e = task / (NTM * MT), sub = task % (NTM * MT);
+      const int nt = sub / MT, m = sub % MT;
+      const double* S = Sb(e);
+      const double* V = Vb(e);
+      double a0 = 0, a1 = 0;
+      const int c = nt * 8 + g;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const int k = kk * 4 + t;
+        dmma(a0, a1, S[(m * 8 + g) + k * LD], V[k + c * LD]);
+      }
+      const int r = m * 8 + g, c0 = nt * 8 + 2 * t;
+      Zb(e)[r + c0 * LD] = a0;
+      Zb(e)[r + (c0 + 1) * LD] = a1;
+    }
+    for (int idx = threadIdx.x; idx < nb * D3; idx += NT) {
+      const int e = idx / D3, r = idx % D3;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < D3; ++k) s += Sb(e)[r + k * LD] * fv(e)[k];
+      fs(e)[r] = s;
+    }
+    if (has_next) {
+      for (int idx = threadIdx.x; idx < EPB * 32; idx += NT) {
+        const int e = idx >> 5, i = idx & 31;
+        const long K = Kn0 + e;
+        if (K < nelt && i < 30) {
+          double v;
+          if (i == 0) v = geo.volume[K];
+          else if (i < 10) v = geo.piola[long(i - 1) * nelt + K];
+          else if (i < 22) v = geo.normals[long(i - 10) * nelt + K];
+          else if (i < 26) v = geo.T[long(i - 22) * nelt + K];
+          else v = double(geo.perm[long(i - 26) * nelt + K]);
+          sgb(e, cur ^ 1)[i] = v;
+        }
+      }
+    }
+    __syncthreads();
+    if (has_next)
+      for (int e = warp; e < EPB; e += NWT)
+        if (Kn0 + e < nelt) build_columns<D2, D3, M, MP>(sgb(e, cur ^ 1), colb(e, cur ^ 1), lane);
+
+    // ---- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (lower tiles, mirrored) | Cf
+    for (int task = warp; task < nb * NLOW; task += NWT) {
+      const int e = task / NLOW, tile = task % NLOW;
+      int mt = 0, rem = tile;
+      while (rem > mt) { rem -= mt + 1; ++mt; }
+      const int nt = rem, r = mt * 8 + g;
+      const double* V = Vb(e);
+      const double* Vs = Zb(e);
+      double v0 = 0, v1 = 0;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const int k = kk * 4 + t;
+        dmma(v0, v1, V[k + r * LD], Vs[k + (nt * 8 + g) * LD]);
+      }
+      const double z0 = Yb(e)[tile * 64 + 2 * lane], z1 = Yb(e)[tile * 64 + 2 * lane + 1];
+      if (r < M) {
+        const double* sg = sgb(e, cur);
+        const double* nsc = colb(e, cur);
+        const double* Tc = nsc + 3 * MP;
+        const int l1 = r / D2;
+        const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
+        double* Ck = Cout + (K0 + e) * M * M;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = nt * 8 + 2 * t + h;
+          if (c > r || c >= M) continue;
+          const int l2 = c / D2;
+          const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
+          double v = nn * (h ? z1 : z0) - (h ? v1 : v0);
+          if (l1 == l2) v += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
+          Ck[r + c * M] = v;
+          if (c != r) Ck[c + r * M] = v;
+        }
+      }
+    }
+    for (int idx = threadIdx.x; idx < nb * M; idx += NT) {
+      const int e = idx / M, r = idx % M;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < D3; ++k) s += Vb(e)[k + r * LD] * fs(e)[k];
+      Cfout[(K0 + e) * M + r] = s;
+    }
+    __syncthreads();
+    if (has_next) {
+      load_inputs(Kn0, -1);  // D and f only (geometry already staged)
+      cur ^= 1;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace hdgb

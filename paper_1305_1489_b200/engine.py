@@ -322,6 +322,10 @@ class Engine:
         """NVRTC-specialised node build for program fields (default on)."""
         L.check(L.lib().hdg_b200_set_jit(self._ctx, int(enabled)))
 
+    def set_variant(self, variant: int) -> None:
+        """k = 2, 3 condensation kernel: 3 = CTA-batched (default), 2 = per-element teams."""
+        L.check(L.lib().hdg_b200_set_variant(self._ctx, int(variant)))
+
     @property
     def jit_status(self) -> str:
         return L.lib().hdg_b200_jit_status(self._ctx).decode()
