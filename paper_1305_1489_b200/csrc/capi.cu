@@ -812,6 +812,12 @@ int hdg_b200_set_variant(hdg_ctx* c, int variant) {
   });
 }
 
+#ifdef HDG_PHASE_TIMING
+extern "C" int hdg_b200_debug_phase_clocks(long long* out) {
+  return guarded([&] { CUDA_OK(cudaMemcpyFromSymbol(out, g_phase_clk, sizeof(g_phase_clk))); });
+}
+#endif
+
 int hdg_b200_synchronize(hdg_ctx* c) {
   return guarded([&] {
     require(c != nullptr, HDG_EINVAL, "ctx is NULL");

@@ -37,9 +37,9 @@ struct C2Dims {
   static constexpr int OFF_BETA = OFF_WB + MP;         // 3 x MP: beta_#(c) = sum_s a(s,#) n_s(face c)
   static constexpr int OFF_F = OFF_BETA + 3 * MP;      // D3P: f
   static constexpr int OFF_FS = OFF_F + D3P;           // D3P: Si f
-  static constexpr int OFF_STG = round_up(OFF_FS + D3P, 2);  // 64: GJ column stage (16 B aligned)
-  static constexpr int OFF_STG2 = OFF_STG + 64;        // 64: second GJ stage
-  static constexpr int OFF_GEO = OFF_STG2 + 64;        // 2 x 32: geometry records (cur/next)
+  static constexpr int OFF_STG = round_up(OFF_FS + D3P, 2);  // 128: GJ column stage (2 buffers, 16 B aligned)
+  static constexpr int OFF_STG2 = OFF_STG + 128;       // 128: second GJ stage
+  static constexpr int OFF_GEO = OFF_STG2 + 128;        // 2 x 32: geometry records (cur/next)
   static constexpr int OFF_COL = OFF_GEO + 64;         // second column-data buffer
   static constexpr int PER_ELT = OFF_COL + 8 * MP;
   static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
@@ -57,64 +57,92 @@ template <> struct C2Cfg<3> { static constexpr int NW = 4, EPB = 4; };
 // store per lane + broadcast loads) instead of being broadcast entry by entry.
 // After N sweeps a = -A^-1; the sign is folded in on return. No pivoting
 // (SPD); the pivots are the Cholesky pivots and feed the 1e-14 test.
+// 1/x to full double precision: MUFU reciprocal seed + two Newton steps
+// (shorter dependency chain than IEEE division; last-bit rounding may differ).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 template <int N>
 __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, int lane, double& pmin,
                                                 double& pmax) {
-  // stage: 2 x 32 doubles (pivot columns k, k+1 gathered from every lane).
+  // stage: 2 buffers x (2 x 32) doubles: the two pivot columns gathered from
+  // every lane (column k of a symmetric matrix == every lane's a[k]).
+  double piv0[N / 2 + 1], pdet[N / 2 + 1];
 #pragma unroll
   for (int k = 0; k + 1 < N; k += 2) {
+    double* st = stage + ((k >> 1) & 1) * 64;
     if (lane < N) {
-      stage[lane] = a[k];
-      stage[32 + lane] = a[k + 1];
+      st[lane] = a[k];
+      st[32 + lane] = a[k + 1];
     }
-    __syncwarp();
-    const double p00 = stage[k], p01 = stage[k + 1], p11 = stage[32 + k + 1];
-    const double det = p00 * p11 - p01 * p01;
-    pmin = fmin(pmin, fmin(p00, det / p00));  // Cholesky pivots of the block
-    pmax = fmax(pmax, fmax(p00, det / p00));
-    const double id = 1.0 / det;
+    // pivot block straight from the pivot lanes (off the shared-memory path)
+    const double p00 = __shfl_sync(0xffffffffu, a[k], k);
+    const double p01 = __shfl_sync(0xffffffffu, a[k + 1], k);
+    const double p11 = __shfl_sync(0xffffffffu, a[k + 1], k + 1);
+    const double det = fma(p00, p11, -p01 * p01);
+    piv0[k >> 1] = p00;
+    pdet[k >> 1] = det;
+    const double id = fast_rcp(det);
     const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;  // P^-1 (symmetric)
     const bool m0 = lane == k, m1 = lane == k + 1;
     // w = P^-1 [a_k; a_k+1] for ordinary lanes; pivot lanes hold their own
     // block column, for which "a - v w" must produce A(i,block) P^-1.
-    double w0 = i00 * a[k] + i01 * a[k + 1];
-    double w1 = i01 * a[k] + i11 * a[k + 1];
+    double w0 = fma(i00, a[k], i01 * a[k + 1]);
+    double w1 = fma(i01, a[k], i11 * a[k + 1]);
     if (m0) { w0 = 1.0 - i00; w1 = -i01; }
     if (m1) { w0 = -i01; w1 = 1.0 - i11; }
     double nk0 = w0, nk1 = w1;
     if (m0) { nk0 = -i00; nk1 = -i01; }
     if (m1) { nk0 = -i01; nk1 = -i11; }
+    __syncwarp();
+    // next pivot pair first: it heads the next step's dependency chain
 #pragma unroll
-    for (int i0 = 0; i0 < N; i0 += 2) {
-      const double2 v0 = *reinterpret_cast<const double2*>(stage + i0);
-      const double2 v1 = *reinterpret_cast<const double2*>(stage + 32 + i0);
-      if (i0 != k) {
+    for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+      for (int i0 = 0; i0 < N; i0 += 2) {
+        if (i0 == k) continue;
+        if ((pass == 0) != (i0 == k + 2)) continue;
+        const double2 v0 = *reinterpret_cast<const double2*>(st + i0);
+        const double2 v1 = *reinterpret_cast<const double2*>(st + 32 + i0);
         a[i0] = fma(-v0.x, w0, fma(-v1.x, w1, a[i0]));
         if (i0 + 1 < N) a[i0 + 1] = fma(-v0.y, w0, fma(-v1.y, w1, a[i0 + 1]));
       }
     }
     a[k] = nk0;
     a[k + 1] = nk1;
-    __syncwarp();
   }
   if (N % 2) {  // trailing scalar pivot
     constexpr int k = N - 1;
-    if (lane < N) stage[lane] = a[k];
-    __syncwarp();
-    const double p = stage[k];
-    pmin = fmin(pmin, p);
-    pmax = fmax(pmax, p);
-    const double ip = 1.0 / p;
+    double* st = stage + (((k >> 1)) & 1) * 64;
+    if (lane < N) st[lane] = a[k];
+    const double p = __shfl_sync(0xffffffffu, a[k], k);
+    piv0[k >> 1] = p;
+    pdet[k >> 1] = p * p;
+    const double ip = fast_rcp(p);
     const bool me = lane == k;
     const double t = me ? 1.0 - ip : a[k] * ip;
     const double nk = me ? -ip : a[k] * ip;
-#pragma unroll
-    for (int i = 0; i < k; ++i) a[i] = fma(-stage[i], t, a[i]);
-    a[k] = nk;
     __syncwarp();
+#pragma unroll
+    for (int i = 0; i < k; ++i) a[i] = fma(-st[i], t, a[i]);
+    a[k] = nk;
   }
+  __syncwarp();
 #pragma unroll
   for (int i = 0; i < N; ++i) a[i] = -a[i];
+  // Cholesky pivots of each block: p00 and det / p00 (scalar tail: p, p)
+#pragma unroll
+  for (int j = 0; j < (N + 1) / 2; ++j) {
+    const double d1 = pdet[j] / piv0[j];
+    pmin = fmin(pmin, fmin(piv0[j], d1));
+    pmax = fmax(pmax, fmax(piv0[j], d1));
+  }
 }
 
 // Loads column `lane` of a packed-lower SPD matrix and inverts it in place

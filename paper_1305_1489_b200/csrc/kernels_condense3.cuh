@@ -13,6 +13,15 @@
 
 namespace hdgb {
 
+#ifdef HDG_PHASE_TIMING
+// Diagnostics build only: clock64() at each CTA barrier of the first batches.
+__device__ long long g_phase_clk[148][8][8];
+#define PHASE_MARK(b, p) \
+  if (threadIdx.x == 0 && blockIdx.x < 148 && (b) < 8) g_phase_clk[blockIdx.x][(b)][(p)] = clock64();
+#else
+#define PHASE_MARK(b, p)
+#endif
+
 template <int K_> struct C3Cfg;
 template <> struct C3Cfg<2> { static constexpr int EPB = 8, NWT = 16; };
 template <> struct C3Cfg<3> { static constexpr int EPB = 4, NWT = 16; };
@@ -56,6 +65,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   const long stride = long(gridDim.x) * EPB;
   long K0 = long(blockIdx.x) * EPB;
   int cur = 0;
+  int batch = 0;
 
   auto load_inputs = [&](long Kb, int which) {  // D, f, geometry of batch Kb (all threads)
     for (int idx = threadIdx.x; idx < EPB * Dm::NSYM; idx += NT) {
@@ -109,7 +119,8 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     __syncthreads();
   }
 
-  for (; K0 < nelt; K0 += stride) {
+  for (; K0 < nelt; K0 += stride, ++batch) {
+    PHASE_MARK(batch, 0);
     const long Kn0 = K0 + stride;
     const bool has_next = Kn0 < nelt;
     const int nb = int(nelt - K0 < EPB ? nelt - K0 : EPB);  // live elements in this batch
@@ -169,6 +180,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     __syncthreads();
 
+    PHASE_MARK(batch, 1);
     // ---- P2: S += sum_# Chat_# R_# (lower tiles) | V_l = Chat_l Zp_l + T_l W_l^T
     for (int task = warp; task < nb * (NLS + 4 * MT); task += NWT) {
       const int e = task / (NLS + 4 * MT), sub = task % (NLS + 4 * MT);
@@ -235,6 +247,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     __syncthreads();
 
+    PHASE_MARK(batch, 2);
     // ---- P3: S^-1 of the batch || M^-1 of the next batch || (W Zp) tiles -> Yb
     //      || V, f -> recovery cache
     {
@@ -301,6 +314,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     __syncthreads();
 
+    PHASE_MARK(batch, 3);
     // ---- P4: Vs = Si V (into Zb) | fs = Si f | next batch's geometry + columns
     for (int task = warp; task < nb * NTM * MT; task += NWT) {
       const int e = task / (NTM * MT), sub = task % (NTM * MT);
@@ -345,6 +359,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       for (int e = warp; e < EPB; e += NWT)
         if (Kn0 + e < nelt) build_columns<D2, D3, M, MP>(sgb(e, cur ^ 1), colb(e, cur ^ 1), lane);
 
+    PHASE_MARK(batch, 4);
     // ---- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (lower tiles, mirrored) | Cf
     for (int task = warp; task < nb * NLOW; task += NWT) {
       const int e = task / NLOW, tile = task % NLOW;
@@ -388,6 +403,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       Cfout[(K0 + e) * M + r] = s;
     }
     __syncthreads();
+    PHASE_MARK(batch, 5);
     if (has_next) {
       load_inputs(Kn0, -1);  // D and f only (geometry already staged)
       cur ^= 1;

@@ -1,0 +1,39 @@
+// Latency of the warp-register sweep Gauss-Jordan inverse (kernels_condense2.cuh).
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../../paper_1305_1489_b200/csrc/kernels_condense2.cuh"
+using namespace hdgb;
+
+template <int N>
+__global__ void gj_kernel(double* out, long long* cyc, int reps) {
+  __shared__ __align__(16) double stage[128 * 8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double a[N];
+  for (int i = 0; i < N; ++i) a[i] = (i == lane ? 4.0 * N : 0.0) + 1.0 / (1.0 + i + lane);
+  double pmin = 1e300, pmax = 0;
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    warp_gj_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
+  }
+  long long t1 = clock64();
+  if (lane == 0) cyc[blockIdx.x * 8 + warp] = (t1 - t0) / reps;
+  double s = 0;
+  for (int i = 0; i < N; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s + pmin + pmax;
+}
+
+int main() {
+  double* out; long long* cyc;
+  cudaMalloc(&out, 148 * 256 * 8); cudaMalloc(&cyc, 148 * 8 * 8);
+  long long h[148 * 8];
+  for (int warps : {1, 4, 8}) {
+    gj_kernel<20><<<148, 32 * warps>>>(out, cyc, 4);
+    gj_kernel<20><<<148, 32 * warps>>>(out, cyc, 32);
+    cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("N=20 warps/SM=%d: %lld cycles per inverse\n", warps, h[0]);
+  }
+  gj_kernel<10><<<148, 32>>>(out, cyc, 32);
+  cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("N=10 warps/SM=1: %lld cycles per inverse\n", h[0]);
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+}
