@@ -229,7 +229,8 @@ int hdg_b200_stage_times(hdg_ctx* ctx, double ms[HDG_NSTAGES]);
  * set); disable to force the in-kernel field interpreter. jit_status returns
  * the last JIT failure ("" if none; on failure the interpreter runs).      */
 int hdg_b200_set_jit(hdg_ctx* ctx, int enabled);
-/* k = 2, 3 condensation kernel: 3 = CTA-batched (default), 2 = per-element teams. */
+/* k = 2, 3 condensation kernel: 4 = element-batched tasks (default), 3 = CTA-batched
+ * phases, 2 = per-element warp teams (all equivalent; kept for comparison). */
 int hdg_b200_set_variant(hdg_ctx* ctx, int variant);
 const char* hdg_b200_jit_status(const hdg_ctx* ctx);
 

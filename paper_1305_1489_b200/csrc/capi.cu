@@ -18,6 +18,7 @@
 #include "kernels_post.cuh"
 #include "kernels_condense2.cuh"
 #include "kernels_condense3.cuh"
+#include "kernels_condense4.cuh"
 #include "jit_quad.hpp"
 
 using namespace hdgb;
@@ -219,7 +220,7 @@ struct hdg_ctx {
   int* h_status = nullptr;
   bool timing = false;
   bool jit = true;          // NVRTC-specialised K2 for program fields
-  int condense_variant = 3; // k = 2, 3: 3 = CTA-batched kernel, 2 = per-element teams
+  int condense_variant = 3; // k = 2, 3: 4 = element-batched tasks, 3 = CTA-batched, 2 = per-element teams
   std::string jit_error;    // last JIT failure (kernel then runs interpreted)
   cudaEvent_t ev[2 * HDG_NSTAGES] = {};
   bool pending[HDG_NSTAGES] = {};
@@ -262,6 +263,12 @@ struct C3Launch {
   static constexpr int EPB = C3Cfg<K_>::EPB, NW = C3Cfg<K_>::NWT / C3Cfg<K_>::EPB;
 };
 
+template <int K_>
+struct C4Launch {
+  static constexpr int EPB = C4Cfg<K_>::EPB, NW = C4Cfg<K_>::NWT / C4Cfg<K_>::EPB > 0 ? C4Cfg<K_>::NWT / C4Cfg<K_>::EPB : 1;
+  static_assert(C4Cfg<K_>::NWT % C4Cfg<K_>::EPB == 0 || C4Cfg<K_>::EPB % C4Cfg<K_>::NWT == 0, "");
+};
+
 template <class Dm, class Cg, class Kern>
 void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, const double* Ms,
                           const double* Ds, const double* fv, double* C, double* Cf, double* F) {
@@ -284,8 +291,10 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
   if constexpr (K_ == 2 || K_ == 3) {
     if (c->condense_variant == 2)
       launch_condense_impl<C2Dims<K_>, C2Cfg<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-    else
+    else if (c->condense_variant == 3)
       launch_condense_impl<C2Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+    else
+      launch_condense_impl<C2Dims<K_>, C4Launch<K_>>(c, condense4_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
   } else if constexpr (K_ <= 3)
     launch_condense_impl<C2Dims<K_>, C2Cfg<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
   else
@@ -807,7 +816,7 @@ const char* hdg_b200_jit_status(const hdg_ctx* c) { return c ? c->jit_error.c_st
 
 int hdg_b200_set_variant(hdg_ctx* c, int variant) {
   return guarded([&] {
-    require(c != nullptr && (variant == 2 || variant == 3), HDG_EINVAL, "variant must be 2 or 3");
+    require(c != nullptr && variant >= 2 && variant <= 4, HDG_EINVAL, "variant must be 2, 3 or 4");
     c->condense_variant = variant;
   });
 }

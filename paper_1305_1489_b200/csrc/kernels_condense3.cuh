@@ -22,6 +22,12 @@ __device__ long long g_phase_clk[148][8][8];
 #define PHASE_MARK(b, p)
 #endif
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 template <int K_> struct C3Cfg;
 template <> struct C3Cfg<2> { static constexpr int EPB = 8, NWT = 16; };
 template <> struct C3Cfg<3> { static constexpr int EPB = 4, NWT = 16; };
@@ -93,6 +99,29 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         sgb(e, which)[i] = v;
       }
     }
+  };
+  auto invert_M_staged = [&](int e, long K) {  // packed M staged in Mi(e) by cp.async (warp-wide)
+    double a[D3];
+    const double* P = Mi(e);
+#pragma unroll
+    for (int i = 0; i < D3; ++i) {
+      const int r = i > lane ? i : lane, c = i > lane ? lane : i;
+      a[i] = lane < D3 ? P[sym_idx(r, c, D3)] : 0.0;
+    }
+    __syncwarp();
+    double pmin = 1e300, pmax = 0.0;
+    warp_gj_inverse<D3>(a, stM(e), lane, pmin, pmax);
+    const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
+    if (lane < D3) {
+#pragma unroll
+      for (int i = 0; i < D3; ++i) Mi(e)[i + lane * LD] = a[i];
+      if (factors) {
+#pragma unroll
+        for (int i = 0; i < D3; ++i)
+          if (i >= lane) factors[K * Dm::FACTORS + sym_idx(i, lane, D3)] = a[i];
+      }
+    }
+    if (bad && lane == 0) flag_bad(bad_element, K);
   };
   auto invert_M = [&](int e, long K) {  // warp-wide
     double a[D3];
@@ -181,6 +210,14 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     __syncthreads();
 
     PHASE_MARK(batch, 1);
+    // next batch's packed M -> Mi(e) (dead after P1), asynchronously under P2
+    if (has_next) {
+      for (int idx = threadIdx.x; idx < EPB * Dm::NSYM; idx += NT) {
+        const int e = idx / Dm::NSYM, p = idx - e * Dm::NSYM;
+        if (Kn0 + e < nelt) cp_async8(Mi(e) + p, Msym + (Kn0 + e) * Dm::NSYM + p);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
     // ---- P2: S += sum_# Chat_# R_# (lower tiles) | V_l = Chat_l Zp_l + T_l W_l^T
     for (int task = warp; task < nb * (NLS + 4 * MT); task += NWT) {
       const int e = task / (NLS + 4 * MT), sub = task % (NLS + 4 * MT);
@@ -245,6 +282,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           }
       }
     }
+    cp_async_wait_all();
     __syncthreads();
 
     PHASE_MARK(batch, 2);
@@ -278,36 +316,35 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             }
             if (bad && lane == 0) flag_bad(bad_element, K);
           } else if (has_next && Kn0 + e < nelt) {
-            invert_M(e, Kn0 + e);  // Mi(e) is dead after P1
+            invert_M_staged(e, Kn0 + e);  // packed M copied into the dead Mi(e) during P2
           }
         }
       }
       if (!gj_warp || !GJ_SEP) {
+        // No FP64 here: the sweeps' dependent DFMA chains stall badly behind
+        // DMMA traffic on the same pipe, so this phase only moves data.
         const int w0 = GJ_SEP ? warp - NGJ : warp, nw = GJ_SEP ? NWT - NGJ : NWT;
-        for (int task = w0; task < nb * NLOW; task += nw) {
-          const int e = task / NLOW, tile = task % NLOW;
-          int mt = 0, rem = tile;
-          while (rem > mt) { rem -= mt + 1; ++mt; }
-          const int nt = rem;
-          const int* wb = reinterpret_cast<const int*>(colb(e, cur) + 4 * MP);
-          const int wbr = wb[mt * 8 + g];
-          const double* Z = Zb(e);
-          double z0 = 0, z1 = 0;
-#pragma unroll
-          for (int kk = 0; kk < KS; ++kk) {
-            const int k = kk * 4 + t;
-            const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
-            dmma(z0, z1, aw, Z[k + (nt * 8 + g) * LD]);
-          }
-          Yb(e)[tile * 64 + 2 * lane] = z0;
-          Yb(e)[tile * 64 + 2 * lane + 1] = z1;
-        }
         if (factors) {
-          const int tid0 = w0 * 32 + lane, nth = nw * 32;
-          for (int idx = tid0; idx < nb * (D3 * M + D3); idx += nth) {
-            const int e = idx / (D3 * M + D3), p = idx % (D3 * M + D3);
+          for (int e = w0; e < nb; e += nw) {  // one warp per element: V columns, then f
             double* F = factors + (K0 + e) * Dm::FACTORS + 2 * Dm::NSYM;
-            F[p] = p < D3 * M ? Vb(e)[(p % D3) + (p / D3) * LD] : fv(e)[p - D3 * M];
+            for (int c = 0; c < M; ++c)
+              for (int r = lane; r < D3; r += 32) F[r + c * D3] = Vb(e)[r + c * LD];
+            for (int i = lane; i < D3; i += 32) F[D3 * M + i] = fv(e)[i];
+          }
+        }
+        if (has_next) {
+          for (int idx = w0 * 32 + lane; idx < EPB * 32; idx += nw * 32) {
+            const int e = idx >> 5, i = idx & 31;
+            const long K = Kn0 + e;
+            if (K < nelt && i < 30) {
+              double v;
+              if (i == 0) v = geo.volume[K];
+              else if (i < 10) v = geo.piola[long(i - 1) * nelt + K];
+              else if (i < 22) v = geo.normals[long(i - 10) * nelt + K];
+              else if (i < 26) v = geo.T[long(i - 22) * nelt + K];
+              else v = double(geo.perm[long(i - 26) * nelt + K]);
+              sgb(e, cur ^ 1)[i] = v;
+            }
           }
         }
       }
@@ -329,8 +366,8 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         dmma(a0, a1, S[(m * 8 + g) + k * LD], V[k + c * LD]);
       }
       const int r = m * 8 + g, c0 = nt * 8 + 2 * t;
-      Zb(e)[r + c0 * LD] = a0;
-      Zb(e)[r + (c0 + 1) * LD] = a1;
+      Yb(e)[r + c0 * LD] = a0;      // Vs (R_# is dead)
+      Yb(e)[r + (c0 + 1) * LD] = a1;
     }
     for (int idx = threadIdx.x; idx < nb * D3; idx += NT) {
       const int e = idx / D3, r = idx % D3;
@@ -338,21 +375,6 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int k = 0; k < D3; ++k) s += Sb(e)[r + k * LD] * fv(e)[k];
       fs(e)[r] = s;
-    }
-    if (has_next) {
-      for (int idx = threadIdx.x; idx < EPB * 32; idx += NT) {
-        const int e = idx >> 5, i = idx & 31;
-        const long K = Kn0 + e;
-        if (K < nelt && i < 30) {
-          double v;
-          if (i == 0) v = geo.volume[K];
-          else if (i < 10) v = geo.piola[long(i - 1) * nelt + K];
-          else if (i < 22) v = geo.normals[long(i - 10) * nelt + K];
-          else if (i < 26) v = geo.T[long(i - 22) * nelt + K];
-          else v = double(geo.perm[long(i - 26) * nelt + K]);
-          sgb(e, cur ^ 1)[i] = v;
-        }
-      }
     }
     __syncthreads();
     if (has_next)
@@ -367,14 +389,17 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       while (rem > mt) { rem -= mt + 1; ++mt; }
       const int nt = rem, r = mt * 8 + g;
       const double* V = Vb(e);
-      const double* Vs = Zb(e);
-      double v0 = 0, v1 = 0;
+      const double* Vs = Yb(e);
+      const double* Z = Zb(e);
+      const int wbr = reinterpret_cast<const int*>(colb(e, cur) + 4 * MP)[r];
+      double v0 = 0, v1 = 0, z0 = 0, z1 = 0;
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
         const int k = kk * 4 + t;
+        const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
+        dmma(z0, z1, aw, Z[k + (nt * 8 + g) * LD]);
         dmma(v0, v1, V[k + r * LD], Vs[k + (nt * 8 + g) * LD]);
       }
-      const double z0 = Yb(e)[tile * 64 + 2 * lane], z1 = Yb(e)[tile * 64 + 2 * lane + 1];
       if (r < M) {
         const double* sg = sgb(e, cur);
         const double* nsc = colb(e, cur);

@@ -5,9 +5,20 @@
 using namespace hdgb;
 
 template <int N>
-__global__ void gj_kernel(double* out, long long* cyc, int reps) {
+__global__ void gj_kernel(double* out, long long* cyc, int reps, int dmma_warps) {
   __shared__ __align__(16) double stage[128 * 8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp >= int(blockDim.x / 32) - dmma_warps) {  // background DMMA load
+    double c[8][2] = {};
+    const double a = 1.0 + lane * 1e-3, b = 0.5;
+    for (int r = 0; r < reps * 400; ++r)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dmma(c[u][0], c[u][1], a, b);
+    double s = 0;
+    for (int u = 0; u < 8; ++u) s += c[u][0] + c[u][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    return;
+  }
   double a[N];
   for (int i = 0; i < N; ++i) a[i] = (i == lane ? 4.0 * N : 0.0) + 1.0 / (1.0 + i + lane);
   double pmin = 1e300, pmax = 0;
@@ -27,12 +38,17 @@ int main() {
   cudaMalloc(&out, 148 * 256 * 8); cudaMalloc(&cyc, 148 * 8 * 8);
   long long h[148 * 8];
   for (int warps : {1, 4, 8}) {
-    gj_kernel<20><<<148, 32 * warps>>>(out, cyc, 4);
-    gj_kernel<20><<<148, 32 * warps>>>(out, cyc, 32);
+    gj_kernel<20><<<148, 32 * warps>>>(out, cyc, 4, 0);
+    gj_kernel<20><<<148, 32 * warps>>>(out, cyc, 32, 0);
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
     printf("N=20 warps/SM=%d: %lld cycles per inverse\n", warps, h[0]);
   }
-  gj_kernel<10><<<148, 32>>>(out, cyc, 32);
+  for (int dw : {4, 8, 12}) {
+    gj_kernel<20><<<148, 32 * (4 + dw)>>>(out, cyc, 32, dw);
+    cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("N=20 4 GJ warps + %d DMMA warps: %lld cycles per inverse\n", dw, h[0]);
+  }
+  gj_kernel<10><<<148, 32>>>(out, cyc, 32, 0);
   cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
   printf("N=10 warps/SM=1: %lld cycles per inverse\n", h[0]);
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
