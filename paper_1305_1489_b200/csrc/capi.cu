@@ -292,7 +292,7 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
     if (c->condense_variant == 2)
       launch_condense_impl<C2Dims<K_>, C2Cfg<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
     else if (c->condense_variant == 3)
-      launch_condense_impl<C2Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+      launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
     else
       launch_condense_impl<C2Dims<K_>, C4Launch<K_>>(c, condense4_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
   } else if constexpr (K_ <= 3)

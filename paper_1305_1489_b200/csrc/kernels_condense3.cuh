@@ -28,17 +28,34 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) 
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// C2Dims plus a packed copy of D (filled by cp.async one batch ahead).
+template <int K_>
+struct C3Dims : C2Dims<K_> {
+  static constexpr int OFF_DP = C2Dims<K_>::PER_ELT;
+  static constexpr int PER_ELT = OFF_DP + round_up(C2Dims<K_>::NSYM, 2);
+};
+
 template <int K_> struct C3Cfg;
-template <> struct C3Cfg<2> { static constexpr int EPB = 8, NWT = 16; };
-template <> struct C3Cfg<3> { static constexpr int EPB = 4, NWT = 16; };
+#ifndef HDG_C3_EPB2
+#define HDG_C3_EPB2 8
+#define HDG_C3_NWT2 16
+#define HDG_C3_MINB2 1
+#endif
+#ifndef HDG_C3_EPB3
+#define HDG_C3_EPB3 4
+#define HDG_C3_NWT3 16
+#define HDG_C3_MINB3 1
+#endif
+template <> struct C3Cfg<2> { static constexpr int EPB = HDG_C3_EPB2, NWT = HDG_C3_NWT2, MINB = HDG_C3_MINB2; };
+template <> struct C3Cfg<3> { static constexpr int EPB = HDG_C3_EPB3, NWT = HDG_C3_NWT3, MINB = HDG_C3_MINB3; };
 
 template <int K_>
-__global__ void __launch_bounds__(C3Cfg<K_>::NWT * 32)
+__global__ void __launch_bounds__(C3Cfg<K_>::NWT * 32, C3Cfg<K_>::MINB)
 condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
                  const double* __restrict__ Dsym, const double* __restrict__ fvec,
                  double* __restrict__ Cout, double* __restrict__ Cfout, double* __restrict__ factors,
                  long long* bad_element) {
-  using Dm = C2Dims<K_>;
+  using Dm = C3Dims<K_>;
   constexpr int EPB = C3Cfg<K_>::EPB, NWT = C3Cfg<K_>::NWT, NT = NWT * 32;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, D3P = Dm::D3P, MP = Dm::MP, LD = Dm::LD;
   constexpr int MT = Dm::MT, NTM = Dm::NTM, KS = Dm::KS;
@@ -49,7 +66,10 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr bool GJ_SEP = NWT > NGJ;         // GJ warps do nothing else in P3
   static_assert(NLOW * 64 <= 3 * D3P * LD, "W Zp tiles must fit in the R buffer");
   extern __shared__ double smem[];
+  __shared__ unsigned short pk_rc[Dm::NSYM];  // packed lower index -> row | col << 8
   for (int i = threadIdx.x; i < EPB * Dm::PER_ELT; i += blockDim.x) smem[i] = 0.0;
+  for (int j = threadIdx.x; j < D3; j += blockDim.x)
+    for (int i = j; i < D3; ++i) pk_rc[sym_idx(i, j, D3)] = static_cast<unsigned short>(i | (j << 8));
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -63,6 +83,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   auto Vb = [&](int e) { return B(e) + Dm::OFF_V; };
   auto fv = [&](int e) { return B(e) + Dm::OFF_F; };
   auto fs = [&](int e) { return B(e) + Dm::OFF_FS; };
+  auto Dp = [&](int e) { return B(e) + Dm::OFF_DP; };  // packed D
   auto stS = [&](int e) { return B(e) + Dm::OFF_STG; };
   auto stM = [&](int e) { return B(e) + Dm::OFF_STG2; };
   auto colb = [&](int e, int b) { return B(e) + (b ? Dm::OFF_COL : Dm::OFF_NSC); };
@@ -73,20 +94,19 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   int cur = 0;
   int batch = 0;
 
-  auto load_inputs = [&](long Kb, int which) {  // D, f, geometry of batch Kb (all threads)
+  auto load_Df_async = [&](long Kb) {  // packed D and f of batch Kb -> smem (cp.async group)
     for (int idx = threadIdx.x; idx < EPB * Dm::NSYM; idx += NT) {
       const int e = idx / Dm::NSYM, p = idx - e * Dm::NSYM;
-      const long K = Kb + e;
-      if (K >= nelt) continue;
-      int j = 0, rem = p;  // packed lower (column-major) -> (i, j)
-      while (rem >= D3 - j) { rem -= D3 - j; ++j; }
-      Sb(e)[(j + rem) + j * LD] = Dsym[K * Dm::NSYM + p];
+      if (Kb + e < nelt) cp_async8(Dp(e) + p, Dsym + (Kb + e) * Dm::NSYM + p);
     }
     for (int idx = threadIdx.x; idx < EPB * D3; idx += NT) {
       const int e = idx / D3, i = idx - e * D3;
-      if (Kb + e < nelt) fv(e)[i] = fvec[(Kb + e) * D3 + i];
+      if (Kb + e < nelt) cp_async8(fv(e) + i, fvec + (Kb + e) * D3 + i);
     }
-    for (int idx = threadIdx.x; which >= 0 && idx < EPB * 32; idx += NT) {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto load_geometry = [&](long Kb, int which) {
+    for (int idx = threadIdx.x; idx < EPB * 32; idx += NT) {
       const int e = idx >> 5, i = idx & 31;
       if (Kb + e < nelt && i < 30) {
         const long K = Kb + e;
@@ -115,11 +135,6 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     if (lane < D3) {
 #pragma unroll
       for (int i = 0; i < D3; ++i) Mi(e)[i + lane * LD] = a[i];
-      if (factors) {
-#pragma unroll
-        for (int i = 0; i < D3; ++i)
-          if (i >= lane) factors[K * Dm::FACTORS + sym_idx(i, lane, D3)] = a[i];
-      }
     }
     if (bad && lane == 0) flag_bad(bad_element, K);
   };
@@ -129,21 +144,28 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     if (lane < D3) {
 #pragma unroll
       for (int i = 0; i < D3; ++i) Mi(e)[i + lane * LD] = a[i];
-      if (factors) {
-#pragma unroll
-        for (int i = 0; i < D3; ++i)
-          if (i >= lane) factors[K * Dm::FACTORS + sym_idx(i, lane, D3)] = a[i];
-      }
     }
     if (bad && lane == 0) flag_bad(bad_element, K);
+  };
+  // packed lower triangle of an LD-strided symmetric smem matrix -> recovery cache (all threads)
+  auto write_factor = [&](long Kb, int off, bool si) {
+    for (int idx = threadIdx.x; idx < EPB * Dm::NSYM; idx += NT) {
+      const int e = idx / Dm::NSYM, p = idx - e * Dm::NSYM;
+      const int rc = pk_rc[p];
+      if (Kb + e < nelt)
+        factors[(Kb + e) * Dm::FACTORS + off + p] = (si ? Sb(e) : Mi(e))[(rc & 255) + (rc >> 8) * LD];
+    }
   };
 
   // ---- prologue: first batch
   if (K0 < nelt) {
-    load_inputs(K0, 0);
+    load_Df_async(K0);
+    load_geometry(K0, 0);
     for (int e = warp; e < EPB; e += NWT)
       if (K0 + e < nelt) invert_M(e, K0 + e);
+    cp_async_wait_all();
     __syncthreads();
+    if (factors) write_factor(K0, 0, false);
     for (int e = warp; e < EPB; e += NWT) build_columns<D2, D3, M, MP>(sgb(e, 0), colb(e, 0), lane);
     __syncthreads();
   }
@@ -207,6 +229,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         }
       }
     }
+    cp_async_wait_all();  // D, f of this batch (issued during the previous P5)
     __syncthreads();
 
     PHASE_MARK(batch, 1);
@@ -242,7 +265,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = j * 8 + 2 * t + h;
-          if (r < D3 && c <= r) S[r + c * LD] += (h ? p1 + q1 : p0 + q0);
+          if (r < D3 && c <= r) S[r + c * LD] = Dp(e)[sym_idx(r, c, D3)] + (h ? p1 + q1 : p0 + q0);
         }
       } else {
         const int mt = (sub - NLS) >> 2, l = (sub - NLS) & 3;
@@ -308,11 +331,6 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             if (lane < D3) {
 #pragma unroll
               for (int i = 0; i < D3; ++i) Sb(e)[i + lane * LD] = a[i];
-              if (factors) {
-#pragma unroll
-                for (int i = 0; i < D3; ++i)
-                  if (i >= lane) factors[K * Dm::FACTORS + Dm::NSYM + sym_idx(i, lane, D3)] = a[i];
-              }
             }
             if (bad && lane == 0) flag_bad(bad_element, K);
           } else if (has_next && Kn0 + e < nelt) {
@@ -324,12 +342,11 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         // No FP64 here: the sweeps' dependent DFMA chains stall badly behind
         // DMMA traffic on the same pipe, so this phase only moves data.
         const int w0 = GJ_SEP ? warp - NGJ : warp, nw = GJ_SEP ? NWT - NGJ : NWT;
-        if (factors) {
-          for (int e = w0; e < nb; e += nw) {  // one warp per element: V columns, then f
-            double* F = factors + (K0 + e) * Dm::FACTORS + 2 * Dm::NSYM;
-            for (int c = 0; c < M; ++c)
-              for (int r = lane; r < D3; r += 32) F[r + c * D3] = Vb(e)[r + c * LD];
-            for (int i = lane; i < D3; i += 32) F[D3 * M + i] = fv(e)[i];
+        if (factors) {  // V (D3 x M) and f of each element, contiguous in the cache record
+          constexpr int NVF = D3 * M + D3;
+          for (int q = w0 * 32 + lane; q < nb * NVF; q += nw * 32) {
+            const int e = q / NVF, rem = q - e * NVF, c = rem / D3, r = rem - c * D3;
+            factors[(K0 + e) * Dm::FACTORS + 2 * Dm::NSYM + rem] = c < M ? Vb(e)[r + c * LD] : fv(e)[r];
           }
         }
         if (has_next) {
@@ -376,12 +393,17 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       for (int k = 0; k < D3; ++k) s += Sb(e)[r + k * LD] * fv(e)[k];
       fs(e)[r] = s;
     }
+    if (factors) {
+      write_factor(K0, Dm::NSYM, true);       // S^-1 of this batch
+      if (has_next) write_factor(Kn0, 0, false);  // M^-1 of the next batch
+    }
     __syncthreads();
     if (has_next)
       for (int e = warp; e < EPB; e += NWT)
         if (Kn0 + e < nelt) build_columns<D2, D3, M, MP>(sgb(e, cur ^ 1), colb(e, cur ^ 1), lane);
 
     PHASE_MARK(batch, 4);
+    if (has_next) load_Df_async(Kn0);  // D, f of this batch are dead after P4
     // ---- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (lower tiles, mirrored) | Cf
     for (int task = warp; task < nb * NLOW; task += NWT) {
       const int e = task / NLOW, tile = task % NLOW;
@@ -429,11 +451,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     __syncthreads();
     PHASE_MARK(batch, 5);
-    if (has_next) {
-      load_inputs(Kn0, -1);  // D and f only (geometry already staged)
-      cur ^= 1;
-    }
-    __syncthreads();
+    cur ^= 1;
   }
 }
 

@@ -1,0 +1,30 @@
+"""Time build_condense (K3 only) of a libhdg_b200 variant: sweep_time.py LIB CONFIG [variant]."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from paper_1305_1489_b200 import _lib as L  # noqa: E402
+
+L.LIB_PATH = os.path.abspath(sys.argv[1])
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from paper_1305_1489_b200.configs import CONFIGS  # noqa: E402
+from paper_1305_1489_b200.engine import Engine, HostMesh  # noqa: E402
+
+cfg = CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "C2"]
+mesh = HostMesh.box(cfg.n, bc=cfg.problem.bc, perturb=cfg.perturb, seed=cfg.seed)
+eng = Engine(0)
+eng.set_degree(cfg.k)
+if len(sys.argv) > 3:
+    eng.set_variant(int(sys.argv[3]))
+dm = eng.upload(mesh)
+g = eng.geometry(dm, cfg.tau)
+eng.set_timing(True)
+ts = []
+for i in range(8):
+    cs = eng.build_condense(g, cfg.problem.kappa, cfg.problem.c, cfg.problem.f)
+    torch.cuda.synchronize()
+    if i >= 2:
+        ts.append(eng.stage_times()["condense"])
+print(f"{os.path.basename(sys.argv[1])} {cfg.name}: condense median {np.median(ts):.3f} ms  min {min(ts):.3f}")
