@@ -229,9 +229,12 @@ int hdg_b200_stage_times(hdg_ctx* ctx, double ms[HDG_NSTAGES]);
  * set); disable to force the in-kernel field interpreter. jit_status returns
  * the last JIT failure ("" if none; on failure the interpreter runs).      */
 int hdg_b200_set_jit(hdg_ctx* ctx, int enabled);
-/* k = 2, 3 condensation kernel: 4 = element-batched tasks (default), 3 = CTA-batched
- * phases, 2 = per-element warp teams (all equivalent; kept for comparison). */
+/* k = 2, 3 condensation kernel: 3 = CTA-batched phases (default), 4 = element-batched
+ * tasks, 2 = per-element warp teams (all equivalent; kept for comparison). */
 int hdg_b200_set_variant(hdg_ctx* ctx, int variant);
+/* k = 1..3 recovery kernel: 3 = TMA-streamed cache records (default), 2 = one warp
+ * per element with direct loads (equivalent; kept for comparison). */
+int hdg_b200_set_recover_variant(hdg_ctx* ctx, int variant);
 const char* hdg_b200_jit_status(const hdg_ctx* ctx);
 
 /* Block until the context's stream is idle and report any deferred error. */

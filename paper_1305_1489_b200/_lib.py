@@ -95,6 +95,7 @@ _SIGS = {
     "hdg_b200_stage_times": (C.c_int, [P, DP]),
     "hdg_b200_set_jit": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_variant": (C.c_int, [P, C.c_int]),
+    "hdg_b200_set_recover_variant": (C.c_int, [P, C.c_int]),
     "hdg_b200_jit_status": (C.c_char_p, [P]),
     "hdg_b200_synchronize": (C.c_int, [P]),
 }

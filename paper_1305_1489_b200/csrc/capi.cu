@@ -19,6 +19,7 @@
 #include "kernels_condense2.cuh"
 #include "kernels_condense3.cuh"
 #include "kernels_condense4.cuh"
+#include "kernels_recover3.cuh"
 #include "jit_quad.hpp"
 
 using namespace hdgb;
@@ -144,6 +145,17 @@ void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
   }
   push(Asym_f);                                                  // 13
   push(Af_f);                                                    // 14
+  {  // lane-contiguous transposes for row-per-lane contractions (K5)
+    std::vector<double> s(size_t(3) * d3 * d3), w(size_t(24) * d2 * d3);
+    for (int h3 = 0; h3 < 3; ++h3)
+      for (int j = 0; j < d3; ++j)
+        for (int i = 0; i < d3; ++i) s[size_t(h3) * d3 * d3 + j + size_t(i) * d3] = h.Chat[h3][i + size_t(j) * d3];
+    for (int lm = 0; lm < 24; ++lm)
+      for (int j = 0; j < d3; ++j)
+        for (int i = 0; i < d2; ++i) w[size_t(lm) * d2 * d3 + j + size_t(i) * d3] = h.Wlm[lm][i + size_t(j) * d2];
+    push(s);                                                     // 15
+    push(w);                                                     // 16
+  }
   CUDA_OK(cudaMalloc(&ts.buf, all.size() * sizeof(double)));
   CUDA_OK(cudaMemcpy(ts.buf, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice));
   ts.doubles = all.size();
@@ -154,7 +166,7 @@ void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
   t.bary = b + off[0]; t.w = b + off[1]; t.P = b + off[2]; t.Pd = b + off[3]; t.Chat = b + off[4];
   t.Shat = b + off[5]; t.Wlm = b + off[6]; t.PP = b + off[7]; t.DD = b + off[8];
   t.tri_bary = b + off[9]; t.tri_w = b + off[10]; t.Pface = b + off[11]; t.Dperm = b + off[12];
-  t.Asym = b + off[13]; t.Af = b + off[14];
+  t.Asym = b + off[13]; t.Af = b + off[14]; t.ChatT = b + off[15]; t.WlmT = b + off[16];
   ts.ready = true;
 }
 
@@ -220,6 +232,7 @@ struct hdg_ctx {
   int* h_status = nullptr;
   bool timing = false;
   bool jit = true;          // NVRTC-specialised K2 for program fields
+  int recover_variant = 3;  // k = 1..3: 3 = TMA-streamed cache, 2 = warp per element
   int condense_variant = 3; // k = 2, 3: 4 = element-batched tasks, 3 = CTA-batched, 2 = per-element teams
   std::string jit_error;    // last JIT failure (kernel then runs interpreted)
   cudaEvent_t ev[2 * HDG_NSTAGES] = {};
@@ -304,6 +317,20 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
 template <int K_>
 void launch_recover(hdg_ctx* c, int nelt, const GeoDev& geo, const int* fbe, const double* F,
                     const double* uhat, double* qx, double* qy, double* qz, double* u) {
+  if constexpr (K_ >= 1 && K_ <= 3) {
+    if (c->recover_variant == 3) {  // TMA-streamed cache, persistent warps
+      using Rd = Rec3Dims<K_>;
+      constexpr int kRec3Warps = Rec3Cfg<K_>::WARPS;
+      const size_t smem = (size_t(kRec3Warps) * Rd::PER_WARP + Rd::TABLES) * sizeof(double);
+      CUDA_OK(cudaFuncSetAttribute(recover3_kernel<K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      const long need = (long(nelt) + kRec3Warps - 1) / kRec3Warps;
+      const int grid3 = int(std::min<long>(need, c->sms));
+      recover3_kernel<K_><<<grid3, kRec3Warps * 32, smem, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat,
+                                                                       qx, qy, qz, u);
+      CUDA_OK(cudaGetLastError());
+      return;
+    }
+  }
   const int grid = (nelt + kRecWarps - 1) / kRecWarps;
   if constexpr (K_ <= 3)
     recover2_kernel<K_><<<grid, kRecWarps * 32, 0, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat, qx,
@@ -818,6 +845,13 @@ int hdg_b200_set_variant(hdg_ctx* c, int variant) {
   return guarded([&] {
     require(c != nullptr && variant >= 2 && variant <= 4, HDG_EINVAL, "variant must be 2, 3 or 4");
     c->condense_variant = variant;
+  });
+}
+
+int hdg_b200_set_recover_variant(hdg_ctx* c, int variant) {
+  return guarded([&] {
+    require(c != nullptr && (variant == 2 || variant == 3), HDG_EINVAL, "recover variant must be 2 or 3");
+    c->recover_variant = variant;
   });
 }
 

@@ -36,6 +36,8 @@ struct DevTab {
   const double* Dperm;     // 6 x (nqd x d2)
   const double* Asym;   // fragment-ordered [Wsym | PPsym]: nsymp x (nqp + 4)
   const double* Af;     // fragment-ordered P^T: d3p x nqp
+  const double* ChatT;  // 3 x (d3 x d3), Chat transposed
+  const double* WlmT;   // 24 x (d3 x d2), Wlm transposed
 };
 
 // ------------------------------------------------------------------ fields

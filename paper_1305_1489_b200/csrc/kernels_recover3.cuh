@@ -1,0 +1,228 @@
+// K5 v3 (k = 1..3): gather + local recovery from the condensation cache,
+// HBM-streaming form.
+//
+// Per element the cache record {M^-1, S^-1 (packed lower), V (d3 x m), f} is
+// read exactly once (k=3: 9,920 B), so the kernel is a stream over the cache.
+// Each warp owns a chain of elements (persistent grid) and double-buffers the
+// records in shared memory with 1-D TMA bulk copies (cp.async.bulk, completion
+// on a per-buffer mbarrier): the copies of the next kRec3Bufs-1 elements of the
+// chain are in flight while element K is recovered. The skeleton gather (lambda) and the geometry record
+// of the next element are prefetched into registers one iteration ahead.
+//
+// Algebra as recover2_kernel (local_solver.cpp:102-135 restated on the
+// condensed factors): u = S^-1 (f + V lambda), q_s = M^-1 (r_s) with
+// r_s = sum_# a(s,#) Chat_#^T-contraction of u - sum_l n_l,s W_l lambda_l.
+#pragma once
+
+#include "kernels_condense2.cuh"
+
+namespace hdgb {
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+
+// Arm the barrier for `bytes` of async-proxy data and start the bulk copy.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "fence.proxy.async.shared::cta;\n"
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n"
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %3, [%2];\n" ::"r"(d),
+      "l"(src), "r"(b), "r"(bytes)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+
+// warps per CTA (one CTA per SM) and cache records in flight per warp
+template <int K_> struct Rec3Cfg { static constexpr int WARPS = 16, BUFS = 2; };
+template <> struct Rec3Cfg<3> { static constexpr int WARPS = 8, BUFS = 2; };
+
+template <int K_>
+struct Rec3Dims {
+  static constexpr int D3 = cdim3(K_), D2 = cdim2(K_), M = 4 * cdim2(K_), NS = D3 * (D3 + 1) / 2;
+  static constexpr int FACTORS = 2 * NS + D3 * M + D3;  // doubles per cache record
+  static constexpr int REC = round_up(FACTORS, 2);       // 16-byte multiple
+  static constexpr int SCR = round_up(M, 2) + 2 * 32 + 3 * D3 + 32;  // lambda, t, u, r_s, geometry
+  static constexpr int PER_WARP = Rec3Cfg<K_>::BUFS * REC + SCR;
+  static constexpr int TABLES = 3 * D3 * D3 + 24 * D2 * D3;  // per CTA
+  static_assert((FACTORS * 8) % 16 == 0, "cache record must be a 16-byte multiple for cp.async.bulk");
+};
+
+template <int K_>
+__global__ void __launch_bounds__(Rec3Cfg<K_>::WARPS * 32, 1)
+recover3_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ facebyele,
+                const double* __restrict__ factors, const double* __restrict__ uhat,
+                double* __restrict__ qx, double* __restrict__ qy, double* __restrict__ qz,
+                double* __restrict__ uout) {
+  using Rd = Rec3Dims<K_>;
+  constexpr int kRec3Warps = Rec3Cfg<K_>::WARPS, kRec3Bufs = Rec3Cfg<K_>::BUFS;
+  constexpr int D3 = Rd::D3, D2 = Rd::D2, M = Rd::M, NS = Rd::NS, F = Rd::FACTORS;
+  static_assert(M <= 64 && D3 <= 32, "one warp per element: lambda in 2 registers, u in 1");
+  extern __shared__ __align__(16) double rsm[];
+  __shared__ unsigned long long bars[kRec3Warps][kRec3Bufs];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* buf = rsm + warp * Rd::PER_WARP;
+  double* lam = buf + kRec3Bufs * Rd::REC;
+  double* tv = lam + round_up(M, 2);
+  double* uu = tv + 32;
+  double* rs = uu + 32;
+  double* sg = rs + 3 * D3;
+  double* ChT = rsm + kRec3Warps * Rd::PER_WARP;  // CTA copies of Chat^T, Wlm^T
+  double* WT = ChT + 3 * D3 * D3;
+  for (int i = threadIdx.x; i < 3 * D3 * D3; i += blockDim.x) ChT[i] = tab.ChatT[i];
+  for (int i = threadIdx.x; i < 24 * D2 * D3; i += blockDim.x) WT[i] = tab.WlmT[i];
+  __syncthreads();
+  if (lane == 0) {
+    for (int i = 0; i < kRec3Bufs; ++i) mbar_init(&bars[warp][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+
+  const long stride = long(gridDim.x) * kRec3Warps;
+  long K = long(blockIdx.x) * kRec3Warps + warp;
+  // Register prefetch, software-pipelined so no load is consumed in the
+  // iteration that issues it: face ids two elements ahead, lambda and the
+  // geometry record one element ahead. Lane i < m owns lambda entry i (and
+  // i + 32), lane i < 30 geometry entry i.
+  auto face_ids = [&](long Ke, int& f0, int& f1) {
+    f0 = f1 = -1;
+    if (Ke >= nelt) return;
+    if (lane < M) f0 = facebyele[long(lane / D2) * nelt + Ke];
+    if (lane + 32 < M) f1 = facebyele[long((lane + 32) / D2) * nelt + Ke];
+  };
+  auto traces = [&](int f0, int f1, double& l0, double& l1) {
+    l0 = f0 >= 0 ? uhat[long(f0) * D2 + lane % D2] : 0.0;
+    l1 = f1 >= 0 ? uhat[long(f1) * D2 + (lane + 32) % D2] : 0.0;
+  };
+  auto geometry = [&](long Ke, double& gv, int& gp) {
+    gv = 0.0;
+    gp = 0;
+    if (Ke >= nelt || lane >= 30) return;
+    if (lane == 0) gv = geo.volume[Ke];
+    else if (lane < 10) gv = geo.piola[long(lane - 1) * nelt + Ke];
+    else if (lane < 22) gv = geo.normals[long(lane - 10) * nelt + Ke];
+    else if (lane < 26) gv = geo.T[long(lane - 22) * nelt + Ke];
+    else gp = geo.perm[long(lane - 26) * nelt + Ke];
+  };
+  int f0, f1, fn0, fn1, gp;
+  double l0, l1, gv;
+  face_ids(K, f0, f1);
+  traces(f0, f1, l0, l1);
+  geometry(K, gv, gp);
+  face_ids(K + stride, fn0, fn1);
+  for (int i = 0; i + 1 < kRec3Bufs; ++i) {
+    const long Ki = K + i * stride;
+    if (Ki < nelt && lane == 0) bulk_load(buf + i * Rd::REC, factors + Ki * F, F * 8, &bars[warp][i]);
+  }
+  unsigned phase = 0u;  // parity bits, one per buffer
+  int b = 0;
+  for (; K < nelt; K += stride, b = b + 1 == kRec3Bufs ? 0 : b + 1) {
+    const long Kn = K + stride;
+    {
+      const long Kp = K + (kRec3Bufs - 1) * stride;  // refill the buffer freed last iteration
+      const int bp = (b + kRec3Bufs - 1) % kRec3Bufs;
+      if (Kp < nelt && lane == 0) bulk_load(buf + bp * Rd::REC, factors + Kp * F, F * 8, &bars[warp][bp]);
+    }
+    if (lane < M) lam[lane] = l0;
+    if (lane + 32 < M) lam[lane + 32] = l1;
+    if (lane < 30) sg[lane] = lane < 26 ? gv : double(gp);
+    traces(fn0, fn1, l0, l1);  // element Kn
+    geometry(Kn, gv, gp);
+    face_ids(Kn + stride, fn0, fn1);
+    __syncwarp();
+    mbar_wait(&bars[warp][b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+    const double* Mi = buf + b * Rd::REC;
+    const double* Si = Mi + NS;
+    const double* V = Mi + 2 * NS;
+    const double* f = V + D3 * M;
+
+    if (lane < D3) {  // t = f + V lambda
+      double s0 = f[lane], s1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < M; c += 2) {
+        s0 = fma(V[lane + c * D3], lam[c], s0);
+        if (c + 1 < M) s1 = fma(V[lane + (c + 1) * D3], lam[c + 1], s1);
+      }
+      tv[lane] = s0 + s1;
+    }
+    __syncwarp();
+    double u = 0.0;
+    if (lane < D3) {  // u = S^-1 t (packed lower)
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int r = 0; r < D3; ++r) {
+        const double v = Si[r >= lane ? sym_idx(r, lane, D3) : sym_idx(lane, r, D3)] * tv[r];
+        if (r & 1) s1 += v; else s0 += v;
+      }
+      u = s0 + s1;
+      uu[lane] = u;
+      uout[K * D3 + lane] = u;
+    }
+    __syncwarp();
+    if (lane < D3) {  // r_s(j) = sum_# a(s,#) (Chat_# u)(j) - sum_l n_l,s (W_l lambda_l)(j)
+      const int j = lane;
+      double p[3];
+#pragma unroll
+      for (int h = 0; h < 3; ++h) {
+        const double* C = ChT + h * D3 * D3 + j;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < D3; ++i) {
+          if (i & 1) a1 = fma(C[i * D3], uu[i], a1);
+          else a0 = fma(C[i * D3], uu[i], a0);
+        }
+        p[h] = a0 + a1;
+      }
+      double w[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const double* W = WT + (6 * l + int(sg[26 + l]) - 1) * D2 * D3 + j;
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < D2; ++i) acc = fma(W[i * D3], lam[l * D2 + i], acc);
+        w[l] = acc;
+      }
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        double r = sg[1 + 3 * s] * p[0] + sg[2 + 3 * s] * p[1] + sg[3 + 3 * s] * p[2];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) r -= sg[10 + 3 * l + s] * w[l];
+        rs[s * D3 + j] = r;
+      }
+    }
+    __syncwarp();
+    if (lane < D3) {  // q_s = M^-1 r_s, s = x, y, z (one pass over row `lane` of M^-1)
+      const int i = lane;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < D3; ++j) {
+        const double m = Mi[j >= i ? sym_idx(j, i, D3) : sym_idx(i, j, D3)];
+        a0 = fma(m, rs[j], a0);
+        a1 = fma(m, rs[D3 + j], a1);
+        a2 = fma(m, rs[2 * D3 + j], a2);
+      }
+      qx[K * D3 + i] = a0;
+      qy[K * D3 + i] = a1;
+      qz[K * D3 + i] = a2;
+    }
+    __syncwarp();  // buffer b and the scratch are reused next
+  }
+}
+
+}  // namespace hdgb

@@ -323,8 +323,13 @@ class Engine:
         L.check(L.lib().hdg_b200_set_jit(self._ctx, int(enabled)))
 
     def set_variant(self, variant: int) -> None:
-        """k = 2, 3 condensation kernel: 3 = CTA-batched (default), 2 = per-element teams."""
+        """k = 2, 3 condensation kernel: 3 = CTA-batched (default), 4 = element-batched
+        tasks, 2 = per-element teams."""
         L.check(L.lib().hdg_b200_set_variant(self._ctx, int(variant)))
+
+    def set_recover_variant(self, variant: int) -> None:
+        """k = 1..3 recovery kernel: 3 = TMA-streamed cache (default), 2 = direct loads."""
+        L.check(L.lib().hdg_b200_set_recover_variant(self._ctx, int(variant)))
 
     @property
     def jit_status(self) -> str:

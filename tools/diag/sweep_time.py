@@ -1,4 +1,5 @@
-"""Time build_condense (K3 only) of a libhdg_b200 variant: sweep_time.py LIB CONFIG [variant]."""
+"""Time K3 (build_condense) and K5 (recover) of a libhdg_b200 variant:
+sweep_time.py LIB CONFIG [condense variant]."""
 import os
 import sys
 
@@ -21,10 +22,16 @@ if len(sys.argv) > 3:
 dm = eng.upload(mesh)
 g = eng.geometry(dm, cfg.tau)
 eng.set_timing(True)
-ts = []
+ts, tr = [], []
+d2 = (cfg.k + 1) * (cfg.k + 2) // 2
+uhat = torch.sin(torch.arange(dm.nfc * d2, dtype=torch.float64, device="cuda") * 0.37)
 for i in range(8):
     cs = eng.build_condense(g, cfg.problem.kappa, cfg.problem.c, cfg.problem.f)
+    ls = eng.recover(g, dm, cs, uhat)
     torch.cuda.synchronize()
+    st = eng.stage_times()
     if i >= 2:
-        ts.append(eng.stage_times()["condense"])
-print(f"{os.path.basename(sys.argv[1])} {cfg.name}: condense median {np.median(ts):.3f} ms  min {min(ts):.3f}")
+        ts.append(st["condense"])
+        tr.append(st["recover"])
+print(f"{os.path.basename(sys.argv[1])} {cfg.name}: condense median {np.median(ts):.3f} ms  "
+      f"recover median {np.median(tr):.3f} ms")
