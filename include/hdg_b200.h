@@ -190,6 +190,30 @@ int hdg_b200_postprocess(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_fiel
                          const double* d_qx, const double* d_qy, const double* d_qz,
                          const double* d_u, double* d_ustar);
 
+/* ------------------------------------------- K8: skeleton boundary data
+ * Face moments of a field against the trace basis, over the face's global
+ * vertex triple (face_quad_points, global_system.cpp:9-29). Boundary faces
+ * are numbered first (Dirichlet [0, ndir), then Neumann [ndir, ndir+nneu)),
+ * mesh.cpp:99-116. A SAMPLED field holds nqd x (faces in the set) samples.
+ *  dirichlet_project  replaces dirichlet_project (global_system.cpp:58-70):
+ *                     d_out (ndir x d2) = 1/2 sum_r w_r D_i g.
+ *  skeleton_project   replaces l2_project_skeleton (postprocess.cpp:84-93):
+ *                     d_out (nfc x d2), same moments on every face.
+ *  neumann_load       replaces neumann_load (global_system.cpp:72-104):
+ *                     d_b[f d2 + i] += alpha sum_r w_r D_i (g . n) on the
+ *                     Neumann faces only, n = area-scaled normal of the face's
+ *                     element (g->normals). alpha = -1 on the assembled b is
+ *                     study.cpp:25 "b -= neumann_load(...)"; alpha = 1 on a
+ *                     zeroed vector reproduces the reference's return value. */
+int hdg_b200_dirichlet_project(hdg_ctx* ctx, int nver, const double* d_coords, int nfc,
+                               const int* d_faces, int ndir, hdg_field g, double* d_out);
+int hdg_b200_skeleton_project(hdg_ctx* ctx, int nver, const double* d_coords, int nfc,
+                              const int* d_faces, hdg_field g, double* d_out);
+int hdg_b200_neumann_load(hdg_ctx* ctx, int nver, const double* d_coords, int nfc,
+                          const int* d_faces, int nelt, const int* d_facebyele,
+                          const hdg_geometry* g, int ndir, int nneu, hdg_field gx,
+                          hdg_field gy, hdg_field gz, double alpha, double* d_b);
+
 /* --------------------------------------------- K7: convection block
  * Replaces convection_bilinear_matrices (convdiff.cpp:5-28): vol d3 x d3,
  * dp 4d2 x d3, dd 4d2 x 4d2 per element (Batch3 layout).                   */

@@ -96,6 +96,10 @@ _SIGS = {
     "hdg_b200_set_jit": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_variant": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_recover_variant": (C.c_int, [P, C.c_int]),
+    "hdg_b200_dirichlet_project": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, hdg_field, P]),
+    "hdg_b200_skeleton_project": (C.c_int, [P, C.c_int, P, C.c_int, P, hdg_field, P]),
+    "hdg_b200_neumann_load": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, P, C.POINTER(hdg_geometry),
+                                        C.c_int, C.c_int, hdg_field, hdg_field, hdg_field, C.c_double, P]),
     "hdg_b200_jit_status": (C.c_char_p, [P]),
     "hdg_b200_synchronize": (C.c_int, [P]),
 }

@@ -20,6 +20,7 @@
 #include "kernels_condense3.cuh"
 #include "kernels_condense4.cuh"
 #include "kernels_recover3.cuh"
+#include "kernels_boundary.cuh"
 #include "jit_quad.hpp"
 
 using namespace hdgb;
@@ -235,6 +236,8 @@ struct hdg_ctx {
   int recover_variant = 3;  // k = 1..3: 3 = TMA-streamed cache, 2 = warp per element
   int condense_variant = 3; // k = 2, 3: 4 = element-batched tasks, 3 = CTA-batched, 2 = per-element teams
   std::string jit_error;    // last JIT failure (kernel then runs interpreted)
+  int* d_adj = nullptr;     // boundary face -> 4 K + l (neumann_load)
+  int adj_len = 0;
   cudaEvent_t ev[2 * HDG_NSTAGES] = {};
   bool pending[HDG_NSTAGES] = {};
 };
@@ -256,6 +259,7 @@ void stage_end(hdg_ctx* c, int s) {
 void* ctx_work(hdg_ctx* c, size_t bytes) {
   if (bytes > c->work_bytes) {
     if (c->work) cudaFree(c->work);
+  if (c->d_adj) cudaFree(c->d_adj);
     c->work = nullptr;
     CUDA_OK(cudaMalloc(&c->work, bytes));
     c->work_bytes = bytes;
@@ -501,6 +505,7 @@ void hdg_b200_destroy(hdg_ctx* c) {
   for (auto& t : c->tab)
     if (t.buf) cudaFree(t.buf);
   if (c->work) cudaFree(c->work);
+  if (c->d_adj) cudaFree(c->d_adj);
   if (c->d_bad) cudaFree(c->d_bad);
   if (c->h_bad) cudaFreeHost(c->h_bad);
   if (c->d_status) cudaFree(c->d_status);
@@ -760,6 +765,72 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
                                                           ustar, per_warp);
     CUDA_OK(cudaGetLastError());
     stage_end(c, 5);
+  });
+}
+
+// ----------------------------------------------------------- boundary data
+namespace {
+void launch_face_moments(hdg_ctx* c, int mode, int f0, int f1, int nver, const double* coords, int nfc,
+                         const int* faces, const int* adj, const double* normals, int nelt, const FieldDev& g0,
+                         const FieldDev& g1, const FieldDev& g2, double scale, double* out) {
+  const DevTab& t = c->tab[0].dev;
+  require(t.nqd <= kFaceMaxNodes, HDG_EINVAL, "face rule too large for the face-moment kernel");
+  if (f1 <= f0) return;
+  const long need = (long(f1 - f0) + kFaceWarps - 1) / kFaceWarps;
+  const int grid = int(std::min<long>(need, long(c->sms) * 8));
+  face_moments_kernel<<<grid, kFaceWarps * 32, 0, c->stream>>>(t, mode, f0, f1, coords, nver, faces, nfc, adj,
+                                                               normals, nelt, g0, g1, g2, scale, out);
+  CUDA_OK(cudaGetLastError());
+}
+}  // namespace
+
+int hdg_b200_dirichlet_project(hdg_ctx* c, int nver, const double* d_coords, int nfc, const int* d_faces,
+                               int ndir, hdg_field g, double* d_out) {
+  return guarded([&] {
+    require(c && d_coords && d_faces && d_out && nver > 0 && nfc > 0 && ndir >= 0 && ndir <= nfc, HDG_EINVAL,
+            "bad argument");
+    require(c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    const FieldDev fg = to_dev(g, "g");
+    set_device(c);
+    launch_face_moments(c, 0, 0, ndir, nver, d_coords, nfc, d_faces, nullptr, nullptr, 0, fg, fg, fg, 0.5, d_out);
+  });
+}
+
+int hdg_b200_skeleton_project(hdg_ctx* c, int nver, const double* d_coords, int nfc, const int* d_faces,
+                              hdg_field g, double* d_out) {
+  return guarded([&] {
+    require(c && d_coords && d_faces && d_out && nver > 0 && nfc > 0, HDG_EINVAL, "bad argument");
+    require(c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    const FieldDev fg = to_dev(g, "g");
+    set_device(c);
+    launch_face_moments(c, 0, 0, nfc, nver, d_coords, nfc, d_faces, nullptr, nullptr, 0, fg, fg, fg, 0.5, d_out);
+  });
+}
+
+int hdg_b200_neumann_load(hdg_ctx* c, int nver, const double* d_coords, int nfc, const int* d_faces, int nelt,
+                          const int* d_facebyele, const hdg_geometry* g, int ndir, int nneu, hdg_field gx,
+                          hdg_field gy, hdg_field gz, double alpha, double* d_b) {
+  return guarded([&] {
+    require(c && d_coords && d_faces && d_facebyele && d_b && nver > 0 && nfc > 0 && nelt > 0 && ndir >= 0 &&
+                nneu >= 0 && ndir + nneu <= nfc,
+            HDG_EINVAL, "bad argument");
+    require(c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    require(g && g->normals, HDG_EINVAL, "neumann_load needs the element normals");
+    const FieldDev fx = to_dev(gx, "gx"), fy = to_dev(gy, "gy"), fz = to_dev(gz, "gz");
+    set_device(c);
+    if (nneu == 0) return;
+    const int nbdy = ndir + nneu;
+    if (c->adj_len < nbdy) {
+      if (c->d_adj) cudaFree(c->d_adj);
+      c->d_adj = nullptr;
+      CUDA_OK(cudaMalloc(&c->d_adj, size_t(nbdy) * sizeof(int)));
+      c->adj_len = nbdy;
+    }
+    boundary_adjacency_kernel<<<int((4L * nelt + 255) / 256), 256, 0, c->stream>>>(nelt, d_facebyele, nbdy,
+                                                                                   c->d_adj);
+    CUDA_OK(cudaGetLastError());
+    launch_face_moments(c, 1, ndir, nbdy, nver, d_coords, nfc, d_faces, c->d_adj, g->normals, nelt, fx, fy, fz,
+                        alpha, d_b);
   });
 }
 

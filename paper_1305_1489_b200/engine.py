@@ -197,6 +197,8 @@ class DeviceMesh:
     faces: torch.Tensor      # (3, nfc) int32
     facebyele: torch.Tensor  # (4, nelt) int32
     facetype: torch.Tensor   # (nfc,) uint8
+    ndir: int = 0            # Dirichlet faces are [0, ndir) (mesh.cpp:99-116)
+    nneu: int = 0            # Neumann faces are [ndir, ndir + nneu)
 
 
 @dataclass
@@ -313,7 +315,7 @@ class Engine:
         return DeviceMesh(d["nver"], d["nelt"], d["nfc"], t(mesh.coordinates, torch.float64),
                           t(mesh.elements, torch.int32), t(mesh.faces, torch.int32),
                           t(mesh.facebyele, torch.int32),
-                          torch.from_numpy(mesh.facetype).to(dev))
+                          torch.from_numpy(mesh.facetype).to(dev), d["ndir"], d["nneu"])
 
     def synchronize(self) -> None:
         L.check(L.lib().hdg_b200_synchronize(self._ctx))
@@ -458,6 +460,44 @@ class Engine:
         L.check(L.lib().hdg_b200_postprocess(self._ctx, g.nelt, C.byref(gs), fk.c_struct(), _ptr(ls.qx),
                                              _ptr(ls.qy), _ptr(ls.qz), _ptr(ls.u), _ptr(out)))
         return out
+
+    # ---------------------------------------------------------------- K8
+    def dirichlet_project(self, dm: DeviceMesh, g, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """dirichlet_project (global_system.cpp:58-70): (ndir, d2), row j = Dirichlet face j."""
+        d2 = self.dims["d2"]
+        if out is None:
+            out = torch.empty(dm.ndir, d2, dtype=torch.float64, device=self.device)
+        fg = as_field(g)
+        L.check(L.lib().hdg_b200_dirichlet_project(self._ctx, dm.nver, _ptr(dm.coords), dm.nfc, _ptr(dm.faces),
+                                                   dm.ndir, fg.c_struct(), _ptr(out)))
+        return out
+
+    def skeleton_project(self, dm: DeviceMesh, g, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """l2_project_skeleton (postprocess.cpp:84-93): (nfc, d2), dof f*d2 + i."""
+        d2 = self.dims["d2"]
+        if out is None:
+            out = torch.empty(dm.nfc, d2, dtype=torch.float64, device=self.device)
+        fg = as_field(g)
+        L.check(L.lib().hdg_b200_skeleton_project(self._ctx, dm.nver, _ptr(dm.coords), dm.nfc, _ptr(dm.faces),
+                                                  fg.c_struct(), _ptr(out)))
+        return out
+
+    def neumann_load(self, dm: DeviceMesh, g: Geometry, q: Sequence, b: Optional[torch.Tensor] = None,
+                     alpha: float = 1.0) -> torch.Tensor:
+        """neumann_load (global_system.cpp:72-104) of the vector field q = (qx, qy, qz):
+        b[f*d2 + i] += alpha * <q . n, D_i>_f on the Neumann faces. With b None a zeroed
+        vector is returned (the reference's value); alpha=-1 on the assembled b is
+        study.cpp:25."""
+        d2 = self.dims["d2"]
+        if b is None:
+            b = torch.zeros(dm.nfc * d2, dtype=torch.float64, device=self.device)
+        fs = [as_field(x) for x in q]
+        gs = g.c_struct()
+        L.check(L.lib().hdg_b200_neumann_load(self._ctx, dm.nver, _ptr(dm.coords), dm.nfc, _ptr(dm.faces),
+                                              dm.nelt, _ptr(dm.facebyele), C.byref(gs), dm.ndir, dm.nneu,
+                                              fs[0].c_struct(), fs[1].c_struct(), fs[2].c_struct(),
+                                              float(alpha), _ptr(b)))
+        return b
 
     # ---------------------------------------------------------------- K7
     def convection_bilinear_matrices(self, g: Geometry, beta: Sequence):

@@ -211,6 +211,35 @@ def test_convection_block():
     assert max_slice_relerr(np_(dd), d0) < TOL
 
 
+# --------------------------------------------- K8: skeleton boundary data
+@pytest.mark.parametrize("k", [0, 1, 3, 5])
+def test_boundary_data(k):
+    """dirichlet_project / neumann_load / l2_project_skeleton against the
+    oracle on a perturbed box with Dirichlet and Neumann faces."""
+    mesh = HostMesh.box(3, bc="dirichlet_x", perturb=0.1)
+    em = oracle_mesh(mesh)
+    eng = Engine(0)
+    eng.set_degree(k)
+    dm = eng.upload(mesh)
+    assert dm.ndir > 0 and dm.nneu > 0
+    g = eng.geometry(dm, 1.0)
+    qd, d2 = 2 * k + 2, dim2(k)
+    u, q = "exp(x + y)*sin(3*z)", ("x*y - z", "cos(x*z)", "y + x*x")
+    ub = np_(eng.dirichlet_project(dm, u))
+    want = core.dirichlet_project(em, k, qd, field(u)).reshape(-1, d2)
+    assert ub.shape == (dm.ndir, d2) and relerr(ub, want) < 1e-13
+    nl = np_(eng.neumann_load(dm, g, q))
+    want = core.neumann_load(em, k, qd, vfield(q))
+    assert relerr(nl, want) < 1e-13
+    assert not nl[:dm.ndir * d2].any() and not nl[(dm.ndir + dm.nneu) * d2:].any()
+    b0 = torch.randn(dm.nfc * d2, dtype=torch.float64, device="cuda")
+    b1 = np_(eng.neumann_load(dm, g, q, b=b0.clone(), alpha=-1.0))
+    assert np.allclose(b1, np_(b0) - want, rtol=0, atol=1e-13)
+    sk = np_(eng.skeleton_project(dm, u))
+    want = core.l2_project_skeleton(em, k, qd, field(u)).T
+    assert sk.shape == (dm.nfc, d2) and relerr(sk, want) < 1e-13
+
+
 # -------------------------------------------- end-to-end (C1 at full size)
 def test_c1_full_pipeline_matches_oracle():
     """C1 (k=1, 8^3, 3072 tets): GPU condense -> scatter -> scipy solve ->
@@ -224,9 +253,9 @@ def test_c1_full_pipeline_matches_oracle():
     pat = eng.pattern(mesh)
     sys = eng.assemble(dm, pat, cs)
     d2 = dim2(k)
-    qd = 2 * k + 2
-    ub = core.dirichlet_project(em, k, qd, field(prob.u))
-    b = np_(sys.b) - core.neumann_load(em, k, qd, vfield(prob.q))
+    # boundary data on the GPU (study.cpp:25-26)
+    ub = np_(eng.dirichlet_project(dm, prob.u)).ravel()
+    b = np_(eng.neumann_load(dm, g, prob.q, b=sys.b, alpha=-1.0))
     import scipy.sparse as sp
     nd = len(b)
     H = sp.csr_matrix((np_(sys.vals), np_(sys.colidx), np_(sys.rowptr)), shape=(nd, nd)).tocsc()
