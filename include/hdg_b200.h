@@ -190,6 +190,24 @@ int hdg_b200_postprocess(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_fiel
                          const double* d_qx, const double* d_qy, const double* d_qz,
                          const double* d_u, double* d_ustar);
 
+/* ------------------------------------------------ device mesh setup
+ * expand_device: mesh.cpp:74-171 on the GPU, bit-exact with
+ * hdg_b200_mesh_expand (face numbering, parametrisation, facetype,
+ * facebyele; same MeshError conditions and messages). Inputs and outputs are
+ * device arrays in the host-mesh layouts (column-major: coords nver x 3,
+ * elements nelt x 4, dirichlet/neumann rows x 3, faces nfc x 3, facebyele
+ * nelt x 4). d_faces/d_facetype hold nfc = (4 nelt + ndir + nneu) / 2 rows,
+ * returned in *nfc_out. Vertex ids must fit 21 bits (nver < 2^21).
+ * pattern_device: hdg_b200_pattern_build_raw on the GPU from a device
+ * facebyele (facebase nfc + 1, nbr nfc x 8, slot nelt x 16).
+ * Both synchronise the context stream once to report errors.           */
+int hdg_b200_expand_device(hdg_ctx* ctx, int nver, const double* d_coords, int nelt,
+                           const int* d_elements, int ndir, const int* d_dirichlet, int nneu,
+                           const int* d_neumann, int* d_faces, uint8_t* d_facetype,
+                           int* d_facebyele, int* nfc_out);
+int hdg_b200_pattern_device(hdg_ctx* ctx, int nelt, int nfc, const int* d_facebyele,
+                            int64_t* d_facebase, int* d_nbr, uint8_t* d_slot, int* maxnbr);
+
 /* ------------------------------------------- K8: skeleton boundary data
  * Face moments of a field against the trace basis, over the face's global
  * vertex triple (face_quad_points, global_system.cpp:9-29). Boundary faces

@@ -96,6 +96,9 @@ _SIGS = {
     "hdg_b200_set_jit": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_variant": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_recover_variant": (C.c_int, [P, C.c_int]),
+    "hdg_b200_expand_device": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, P, C.c_int, P, P, P, P,
+                                         C.POINTER(C.c_int)]),
+    "hdg_b200_pattern_device": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P, C.POINTER(C.c_int)]),
     "hdg_b200_dirichlet_project": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, hdg_field, P]),
     "hdg_b200_skeleton_project": (C.c_int, [P, C.c_int, P, C.c_int, P, hdg_field, P]),
     "hdg_b200_neumann_load": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, P, C.POINTER(hdg_geometry),

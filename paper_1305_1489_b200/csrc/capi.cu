@@ -22,6 +22,7 @@
 #include "kernels_recover3.cuh"
 #include "kernels_boundary.cuh"
 #include "jit_quad.hpp"
+#include "mesh_dev.hpp"
 
 using namespace hdgb;
 
@@ -52,6 +53,9 @@ int guarded(F&& fn) {
   } catch (const MeshError& e) {
     g_err = e.what();
     return HDG_EMESH;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return HDG_ECUDA;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return HDG_EINVAL;
@@ -765,6 +769,32 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
                                                           ustar, per_warp);
     CUDA_OK(cudaGetLastError());
     stage_end(c, 5);
+  });
+}
+
+// ------------------------------------------------- device mesh expansion
+int hdg_b200_expand_device(hdg_ctx* c, int nver, const double* d_coords, int nelt, const int* d_elements,
+                           int ndir, const int* d_dirichlet, int nneu, const int* d_neumann, int* d_faces,
+                           uint8_t* d_facetype, int* d_facebyele, int* nfc_out) {
+  return guarded([&] {
+    require(c && d_coords && d_elements && d_faces && d_facetype && d_facebyele && nver > 0 && nelt > 0 &&
+                ndir >= 0 && nneu >= 0 && (ndir == 0 || d_dirichlet) && (nneu == 0 || d_neumann),
+            HDG_EINVAL, "bad argument");
+    set_device(c);
+    expand_device(c->stream, nver, d_coords, nelt, d_elements, ndir, d_dirichlet, nneu, d_neumann, d_faces,
+                  d_facetype, d_facebyele);
+    if (nfc_out) *nfc_out = expanded_face_count(nelt, ndir, nneu);
+  });
+}
+
+int hdg_b200_pattern_device(hdg_ctx* c, int nelt, int nfc, const int* d_facebyele, int64_t* d_facebase,
+                            int* d_nbr, uint8_t* d_slot, int* maxnbr) {
+  return guarded([&] {
+    require(c && d_facebyele && d_facebase && d_nbr && d_slot && nelt > 0 && nfc > 0, HDG_EINVAL,
+            "bad argument");
+    set_device(c);
+    const int mx = pattern_device(c->stream, nelt, nfc, d_facebyele, d_facebase, d_nbr, d_slot);
+    if (maxnbr) *maxnbr = mx;
   });
 }
 

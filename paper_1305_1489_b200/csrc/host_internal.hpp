@@ -15,6 +15,7 @@ inline int pdim3(int k) { return (k + 1) * (k + 2) * (k + 3) / 6; }
 inline int pdim2(int k) { return (k + 1) * (k + 2) / 2; }
 
 struct MeshError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 // ---------------------------------------------------------------- tables
 struct HostTables {

@@ -102,7 +102,7 @@ class HostMesh:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and L is not None and L.lib is not None:  # module teardown at exit
             L.lib().hdg_b200_mesh_free(h)
             self._h = None
 
@@ -276,7 +276,7 @@ class Engine:
 
     def __del__(self):
         ctx = getattr(self, "_ctx", None)
-        if ctx:
+        if ctx and L is not None and L.lib is not None:  # module teardown at exit
             L.lib().hdg_b200_destroy(ctx)
             self._ctx = None
 
@@ -419,6 +419,48 @@ class Engine:
     # ---------------------------------------------------------------- K4
     def pattern(self, mesh: HostMesh, csr: bool = True) -> DevicePattern:
         return self.pattern_from_arrays(*mesh.pattern(), csr=csr)
+
+    def expand(self, coords, elements, dirichlet, neumann) -> DeviceMesh:
+        """mesh.cpp:74-171 on the GPU (bit-exact with HostMesh.expand): the raw mesh
+        (reference shapes: coords nver x 3, elements nelt x 4, dirichlet/neumann
+        rows x 3; numpy or torch) -> DeviceMesh with faces, facetype, facebyele."""
+        dev = self.device
+
+        def soa(a, dt):
+            t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a))
+            return t.to(dev, dt).reshape(-1, t.shape[-1] if t.dim() == 2 else 3).t().contiguous()
+
+        X, E = soa(coords, torch.float64), soa(elements, torch.int32)
+        Dr, Nr = soa(dirichlet, torch.int32), soa(neumann, torch.int32)
+        nver, nelt, ndir, nneu = X.shape[1], E.shape[1], Dr.shape[1], Nr.shape[1]
+        nfc = (4 * nelt + ndir + nneu) // 2
+        faces = torch.empty(3, nfc, dtype=torch.int32, device=dev)
+        ftype = torch.empty(nfc, dtype=torch.uint8, device=dev)
+        fbe = torch.empty(4, nelt, dtype=torch.int32, device=dev)
+        out = C.c_int()
+        L.check(L.lib().hdg_b200_expand_device(self._ctx, nver, _ptr(X), nelt, _ptr(E), ndir, _ptr(Dr) if ndir else None,
+                                               nneu, _ptr(Nr) if nneu else None, _ptr(faces), _ptr(ftype), _ptr(fbe),
+                                               C.byref(out)))
+        return DeviceMesh(nver, nelt, out.value, X, E, faces, fbe, ftype, ndir, nneu)
+
+    def pattern_device(self, dm: DeviceMesh, csr: bool = True) -> DevicePattern:
+        """Skeleton sparsity built on the GPU from dm.facebyele (== HostMesh.pattern())."""
+        dev = self.device
+        fb = torch.empty(dm.nfc + 1, dtype=torch.int64, device=dev)
+        nb = torch.empty(dm.nfc, 8, dtype=torch.int32, device=dev)
+        sl = torch.empty(dm.nelt, 16, dtype=torch.uint8, device=dev)
+        mx = C.c_int()
+        L.check(L.lib().hdg_b200_pattern_device(self._ctx, dm.nelt, dm.nfc, _ptr(dm.facebyele), _ptr(fb), _ptr(nb),
+                                                _ptr(sl), C.byref(mx)))
+        p = DevicePattern(fb, nb, sl)
+        if csr:
+            d2 = self.dims["d2"]
+            nnz = int(fb[-1].item()) * d2 * d2
+            p.rowptr = torch.empty(dm.nfc * d2 + 1, dtype=torch.int64, device=dev)
+            p.colidx = torch.empty(nnz, dtype=torch.int32, device=dev)
+            L.check(L.lib().hdg_b200_pattern_fill(self._ctx, dm.nfc, d2, _ptr(fb), _ptr(nb), _ptr(p.rowptr),
+                                                  _ptr(p.colidx)))
+        return p
 
     def pattern_from_arrays(self, fb: np.ndarray, nb: np.ndarray, sl: np.ndarray, csr: bool = True) -> DevicePattern:
         """Device pattern from (facebase, nbr, slot), e.g. partition.slab_pattern."""
