@@ -34,6 +34,7 @@ extern "C" {
 #define HDG_ENCCL 4     /* NCCL failure */
 #define HDG_EMESH 5     /* MeshError (mesh.hpp:75-78) */
 #define HDG_ESTATE 6    /* call order (e.g. no degree set) */
+#define HDG_ESOLVE 7    /* GlobalSolverError (global_system.hpp:44-46) */
 
 /* boundary classifiers for generated box meshes (mesh.cpp:173-183) */
 #define HDG_BC_ALL_DIRICHLET 0
@@ -231,6 +232,27 @@ int hdg_b200_neumann_load(hdg_ctx* ctx, int nver, const double* d_coords, int nf
                           const int* d_faces, int nelt, const int* d_facebyele,
                           const hdg_geometry* g, int ndir, int nneu, hdg_field gx,
                           hdg_field gy, hdg_field gz, double alpha, double* d_b);
+
+/* ------------------------------------------------- K9: skeleton solve
+ * Replaces solve_skeleton (global_system.cpp:106-165), SPD branch: Dirichlet
+ * dofs (faces [0, ndir)) fixed to d_ub (ndir x d2, hdg_b200_dirichlet_project),
+ * the free dofs from H_ff x = b_f - H_fD u_D by block-Jacobi preconditioned CG
+ * (d2 x d2 face blocks) on the block CSR of hdg_b200_scatter, iterated until
+ * ||r|| <= rtol ||r_0|| or maxit. A system failing the reference's symmetry
+ * test (sum|H - H^T| >= 1e-12 sum|H| over the free block) returns HDG_EINVAL
+ * (the reference's SparseLU branch is not implemented); a non-SPD diagonal
+ * block or no convergence returns HDG_ESOLVE. d_uhat: nfc x d2.            */
+typedef struct {
+  int iterations;
+  int converged;
+  double relres;  /* ||r|| / ||r_0|| at exit */
+  double asym;    /* sum |H_ij - H_ji| over the free block */
+  double scale;   /* sum |H_ij| over the free block */
+} hdg_solve_info;
+int hdg_b200_solve_skeleton(hdg_ctx* ctx, int nfc, int d2, const int64_t* d_facebase,
+                            const int* d_nbr, const double* d_vals, const double* d_b, int ndir,
+                            const double* d_ub, double rtol, int maxit, double* d_uhat,
+                            hdg_solve_info* info);
 
 /* --------------------------------------------- K7: convection block
  * Replaces convection_bilinear_matrices (convdiff.cpp:5-28): vol d3 x d3,

@@ -11,7 +11,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhdg_b200.so")
 
-HDG_OK, HDG_ESINGULAR, HDG_EINVAL, HDG_ECUDA, HDG_ENCCL, HDG_EMESH, HDG_ESTATE = range(7)
+HDG_OK, HDG_ESINGULAR, HDG_EINVAL, HDG_ECUDA, HDG_ENCCL, HDG_EMESH, HDG_ESTATE, HDG_ESOLVE = range(8)
 FIELD_CONST, FIELD_SAMPLED, FIELD_PROGRAM = 0, 1, 2
 BC = {"all_dirichlet": 0, "dirichlet_top_bottom": 1, "dirichlet_x": 2}
 MESH_COORDS, MESH_ELEMENTS, MESH_DIRICHLET, MESH_NEUMANN, MESH_FACES, MESH_FACETYPE, MESH_FACEBYELE = range(7)
@@ -53,6 +53,15 @@ class LocalSolverError(HdgError):
 
 class MeshError(HdgError):
     """Reference MeshError (mesh.hpp:75-78)."""
+
+
+class GlobalSolverError(HdgError):
+    """Reference GlobalSolverError (global_system.hpp:44-46)."""
+
+
+class hdg_solve_info(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("relres", C.c_double), ("asym", C.c_double),
+                ("scale", C.c_double)]
 
 
 _SIGS = {
@@ -99,6 +108,8 @@ _SIGS = {
     "hdg_b200_expand_device": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, P, C.c_int, P, P, P, P,
                                          C.POINTER(C.c_int)]),
     "hdg_b200_pattern_device": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P, C.POINTER(C.c_int)]),
+    "hdg_b200_solve_skeleton": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P, C.c_int, P, C.c_double, C.c_int, P,
+                                          C.POINTER(hdg_solve_info)]),
     "hdg_b200_dirichlet_project": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, hdg_field, P]),
     "hdg_b200_skeleton_project": (C.c_int, [P, C.c_int, P, C.c_int, P, hdg_field, P]),
     "hdg_b200_neumann_load": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, P, C.POINTER(hdg_geometry),
@@ -134,6 +145,8 @@ def check(status: int, bad_element: int = -1) -> None:
         raise LocalSolverError(status, msg, bad_element)
     if status == HDG_EMESH:
         raise MeshError(status, msg)
+    if status == HDG_ESOLVE:
+        raise GlobalSolverError(status, msg)
     raise HdgError(status, msg)
 
 

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -21,6 +22,7 @@
 #include "kernels_condense4.cuh"
 #include "kernels_recover3.cuh"
 #include "kernels_boundary.cuh"
+#include "kernels_solve.cuh"
 #include "jit_quad.hpp"
 #include "mesh_dev.hpp"
 
@@ -375,6 +377,116 @@ int warps_for(size_t per_warp_bytes) {
   return std::max(1, w);
 }
 
+}  // namespace
+
+// K9 driver (template: outside the extern "C" block)
+namespace {
+template <int D2>
+void solve_cg(hdg_ctx* c, int nfc, const int64_t* fb, const int* nbr, const double* vals, const double* b, int ndir,
+              const double* ub, double rtol, int maxit, double* x, hdg_solve_info* info) {
+  cudaStream_t s = c->stream;
+  const long n = long(nfc) * D2;
+  const int nblk = c->sms * 4;
+  auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+  const size_t vb = al(size_t(n) * 8), pb = al(size_t(nblk) * 8);
+  const size_t total = 4 * vb + al(size_t(nfc) * D2 * D2 * 8) + 3 * pb + 256 + 256;
+  void* mem = nullptr;
+  CUDA_OK(cudaMallocAsync(&mem, total, s));
+  struct Free {
+    void* p; cudaStream_t s;
+    ~Free() { cudaFreeAsync(p, s); }
+  } guard{mem, s};
+  char* base = static_cast<char*>(mem);
+  double* r = reinterpret_cast<double*>(base);
+  double* z = reinterpret_cast<double*>(base + vb);
+  double* p = reinterpret_cast<double*>(base + 2 * vb);
+  double* y = reinterpret_cast<double*>(base + 3 * vb);
+  double* binv = reinterpret_cast<double*>(base + 4 * vb);
+  double* p0 = reinterpret_cast<double*>(base + 4 * vb + al(size_t(nfc) * D2 * D2 * 8));
+  double* p1 = p0 + pb / 8;
+  double* p2 = p1 + pb / 8;
+  auto* sc = reinterpret_cast<SolveScalars*>(reinterpret_cast<char*>(p2) + pb);
+  auto* bad = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sc) + 256);
+
+  // reference symmetry test over the free block (global_system.cpp:144-147)
+  asym_kernel<D2><<<nblk, kSolveThreads, 0, s>>>(nfc, ndir, fb, nbr, vals, p0, p1);
+  CUDA_OK(cudaGetLastError());
+  std::vector<double> ha(nblk), hs(nblk);
+  CUDA_OK(cudaMemcpyAsync(ha.data(), p0, nblk * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaMemcpyAsync(hs.data(), p1, nblk * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  double asym = 0.0, scale = 0.0;
+  for (int i = 0; i < nblk; ++i) { asym += ha[i]; scale += hs[i]; }
+  info->asym = asym;
+  info->scale = scale;
+  require(scale == 0.0 || asym < 1e-12 * scale, HDG_EINVAL,
+          "skeleton system is not symmetric: only the SPD (SimplicialLDLT) branch runs on the GPU");
+
+  CUDA_OK(cudaMemsetAsync(bad, 0xff, 8, s));
+  block_jacobi_kernel<D2><<<nblk, kSolveThreads, 0, s>>>(nfc, ndir, fb, nbr, vals, binv, bad);
+  CUDA_OK(cudaGetLastError());
+  // x0: u_D on the Dirichlet dofs, 0 on the free ones
+  if (ndir > 0) CUDA_OK(cudaMemcpyAsync(x, ub, size_t(ndir) * D2 * 8, cudaMemcpyDeviceToDevice, s));
+  CUDA_OK(cudaMemsetAsync(x + long(ndir) * D2, 0, size_t(n - long(ndir) * D2) * 8, s));
+  spmv_kernel<D2><<<nblk, kSolveThreads, 0, s>>>(nfc, fb, nbr, vals, x, y, ndir, nullptr);
+  update_kernel<D2><<<nblk, kSolveThreads, 0, s>>>(0, nfc, ndir, binv, b, y, p, x, r, z, sc, p1, p2);
+  finalize_kernel<<<1, kSolveThreads, 0, s>>>(0, nblk, p1, p2, sc);
+  direction_kernel<<<nblk, kSolveThreads, 0, s>>>(n, z, p, sc, 1);
+  CUDA_OK(cudaGetLastError());
+  unsigned long long hbad = 0;
+  CUDA_OK(cudaMemcpyAsync(&hbad, bad, 8, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  if (hbad != ~0ull)
+    throw HdgError{HDG_ESOLVE, "symmetric factorization of the condensed system failed (face " +
+                                   std::to_string(hbad) + " diagonal block not SPD)"};
+
+  // one CG iteration = 5 launches; captured once into a graph of kChunk iterations
+  constexpr int kChunk = 16;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  // capture on a private stream (the context stream may be the legacy default
+  // stream, which cannot be captured); the graph is then launched on s
+  cudaStream_t cs = nullptr;
+  CUDA_OK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  struct StreamFree {
+    cudaStream_t s;
+    ~StreamFree() { cudaStreamDestroy(s); }
+  } sguard{cs};
+  CUDA_OK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  for (int it = 0; it < kChunk; ++it) {
+    spmv_kernel<D2><<<nblk, kSolveThreads, 0, cs>>>(nfc, fb, nbr, vals, p, y, ndir, p0);
+    finalize_kernel<<<1, kSolveThreads, 0, cs>>>(1, nblk, p0, nullptr, sc);
+    update_kernel<D2><<<nblk, kSolveThreads, 0, cs>>>(1, nfc, ndir, binv, b, y, p, x, r, z, sc, p1, p2);
+    finalize_kernel<<<1, kSolveThreads, 0, cs>>>(2, nblk, p1, p2, sc);
+    direction_kernel<<<nblk, kSolveThreads, 0, cs>>>(n, z, p, sc, 0);
+  }
+  CUDA_OK(cudaStreamEndCapture(cs, &graph));
+  struct GraphFree {
+    cudaGraph_t g; cudaGraphExec_t* e;
+    ~GraphFree() { if (*e) cudaGraphExecDestroy(*e); if (g) cudaGraphDestroy(g); }
+  } gguard{graph, &exec};
+  CUDA_OK(cudaGraphInstantiate(&exec, graph, 0));
+  SolveScalars h{};
+  CUDA_OK(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  int iters = 0;
+  double rel = 0.0;
+  bool done = !(h.rr0 > 0.0);  // zero right-hand side: x0 is the solution
+  while (!done && iters < maxit) {
+    CUDA_OK(cudaGraphLaunch(exec, s));
+    iters += kChunk;
+    CUDA_OK(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    rel = std::sqrt(std::max(h.rr, 0.0) / h.rr0);
+    done = rel <= rtol || !(h.pap > 0.0);
+  }
+  info->iterations = iters;
+  info->relres = rel;
+  info->converged = rel <= rtol ? 1 : 0;
+  if (!info->converged)
+    throw HdgError{HDG_ESOLVE, "skeleton CG did not converge: relative residual " + std::to_string(rel) +
+                                   " after " + std::to_string(iters) + " iterations"};
+}
 }  // namespace
 
 extern "C" {
@@ -795,6 +907,31 @@ int hdg_b200_pattern_device(hdg_ctx* c, int nelt, int nfc, const int* d_facebyel
     set_device(c);
     const int mx = pattern_device(c->stream, nelt, nfc, d_facebyele, d_facebase, d_nbr, d_slot);
     if (maxnbr) *maxnbr = mx;
+  });
+}
+
+// ------------------------------------------------------------ K9: solve
+
+int hdg_b200_solve_skeleton(hdg_ctx* c, int nfc, int d2, const int64_t* d_facebase, const int* d_nbr,
+                            const double* d_vals, const double* d_b, int ndir, const double* d_ub, double rtol,
+                            int maxit, double* d_uhat, hdg_solve_info* info) {
+  hdg_solve_info local{};
+  hdg_solve_info* inf = info ? info : &local;
+  *inf = hdg_solve_info{};
+  return guarded([&] {
+    require(c && d_facebase && d_nbr && d_vals && d_b && d_uhat && nfc > 0 && ndir >= 0 && ndir <= nfc &&
+                (ndir == 0 || d_ub) && rtol > 0.0 && maxit > 0,
+            HDG_EINVAL, "bad argument");
+    set_device(c);
+    switch (d2) {
+      case 1: solve_cg<1>(c, nfc, d_facebase, d_nbr, d_vals, d_b, ndir, d_ub, rtol, maxit, d_uhat, inf); break;
+      case 3: solve_cg<3>(c, nfc, d_facebase, d_nbr, d_vals, d_b, ndir, d_ub, rtol, maxit, d_uhat, inf); break;
+      case 6: solve_cg<6>(c, nfc, d_facebase, d_nbr, d_vals, d_b, ndir, d_ub, rtol, maxit, d_uhat, inf); break;
+      case 10: solve_cg<10>(c, nfc, d_facebase, d_nbr, d_vals, d_b, ndir, d_ub, rtol, maxit, d_uhat, inf); break;
+      case 15: solve_cg<15>(c, nfc, d_facebase, d_nbr, d_vals, d_b, ndir, d_ub, rtol, maxit, d_uhat, inf); break;
+      case 21: solve_cg<21>(c, nfc, d_facebase, d_nbr, d_vals, d_b, ndir, d_ub, rtol, maxit, d_uhat, inf); break;
+      default: throw HdgError{HDG_EINVAL, "d2 must be dim2(k) for k <= 5"};
+    }
   });
 }
 

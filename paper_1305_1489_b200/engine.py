@@ -491,6 +491,21 @@ class Engine:
                                          _ptr(pat.facebase), _ptr(cs.C), _ptr(cs.Cf), _ptr(out.vals), _ptr(out.b)))
         return out
 
+    # ---------------------------------------------------------------- K9
+    def solve_skeleton(self, dm: DeviceMesh, pat: DevicePattern, sys: SkeletonSystem, ub: torch.Tensor,
+                       rtol: float = 1e-13, maxit: int = 200000, out: Optional[torch.Tensor] = None):
+        """solve_skeleton (global_system.cpp:106-165), SPD branch, on the GPU: Dirichlet dofs
+        = ub, free dofs by block-Jacobi CG to ||r|| <= rtol ||r0||. Returns (uhat, info)."""
+        d2 = sys.d2
+        if out is None:
+            out = torch.empty(dm.nfc * d2, dtype=torch.float64, device=self.device)
+        info = L.hdg_solve_info()
+        ubc = ub.contiguous() if dm.ndir else None
+        L.check(L.lib().hdg_b200_solve_skeleton(self._ctx, dm.nfc, d2, _ptr(pat.facebase), _ptr(pat.nbr),
+                                                _ptr(sys.vals), _ptr(sys.b), dm.ndir, _ptr(ubc), float(rtol),
+                                                int(maxit), _ptr(out), C.byref(info)))
+        return out, {f: getattr(info, f) for f, _ in info._fields_}
+
     # ---------------------------------------------------------------- K6
     def postprocess_star(self, g: Geometry, kappa, ls: LocalSolution,
                          out: Optional[torch.Tensor] = None) -> torch.Tensor:

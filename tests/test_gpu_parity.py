@@ -240,6 +240,41 @@ def test_boundary_data(k):
     assert sk.shape == (dm.nfc, d2) and relerr(sk, want) < 1e-13
 
 
+# ------------------------------------------------------ K9: skeleton solve
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_solve_skeleton(k):
+    """GPU block-Jacobi CG against the reference's direct solve of the same
+    assembled system (global_system.cpp:106-165) on a perturbed mixed-BC mesh."""
+    prob = CONFIGS["C2"].problem
+    mesh = HostMesh.box(4, bc=prob.bc, perturb=0.1)
+    em = oracle_mesh(mesh)
+    eng, dm, g, cs = gpu_pipeline(mesh, k, prob.kappa, prob.c, prob.f)
+    pat = eng.pattern_device(dm)
+    sys = eng.assemble(dm, pat, cs)
+    ub = eng.dirichlet_project(dm, prob.u)
+    eng.neumann_load(dm, g, prob.q, b=sys.b, alpha=-1.0)
+    uhat, info = eng.solve_skeleton(dm, pat, sys, ub)
+    assert info["converged"] and info["relres"] <= 1e-13
+    import scipy.sparse as sp
+    nd = sys.b.numel()
+    H = sp.csr_matrix((np_(sys.vals), np_(sys.colidx), np_(sys.rowptr)), shape=(nd, nd)).tocsc()
+    want = solve_skeleton(em, H.indptr, H.indices, H.data, np_(sys.b), np_(ub).ravel(), dim2(k))
+    assert relerr(np_(uhat), want) < 1e-10
+    # Dirichlet dofs are the projected data, bit for bit
+    assert np.array_equal(np_(uhat)[:ub.numel()], np_(ub).ravel())
+
+
+def test_solve_skeleton_rejects_nonsymmetric():
+    from paper_1305_1489_b200._lib import HdgError
+    mesh = HostMesh.box(2, bc="dirichlet_x")
+    eng, dm, g, cs = gpu_pipeline(mesh, 1, KAP, CC, FF)
+    pat = eng.pattern_device(dm)
+    sys = eng.assemble(dm, pat, cs)
+    sys.vals[-2] += 1.0  # off-diagonal entry of the last (interior) face: breaks H = H^T
+    with pytest.raises(HdgError, match="not symmetric"):
+        eng.solve_skeleton(dm, pat, sys, eng.dirichlet_project(dm, "x"))
+
+
 # -------------------------------------------- end-to-end (C1 at full size)
 def test_c1_full_pipeline_matches_oracle():
     """C1 (k=1, 8^3, 3072 tets): GPU condense -> scatter -> scipy solve ->
@@ -250,17 +285,15 @@ def test_c1_full_pipeline_matches_oracle():
     em = oracle_mesh(mesh)
     k = cfg.k
     eng, dm, g, cs = gpu_pipeline(mesh, k, prob.kappa, prob.c, prob.f)
-    pat = eng.pattern(mesh)
+    pat = eng.pattern_device(dm)
     sys = eng.assemble(dm, pat, cs)
-    d2 = dim2(k)
-    # boundary data on the GPU (study.cpp:25-26)
-    ub = np_(eng.dirichlet_project(dm, prob.u)).ravel()
-    b = np_(eng.neumann_load(dm, g, prob.q, b=sys.b, alpha=-1.0))
-    import scipy.sparse as sp
-    nd = len(b)
-    H = sp.csr_matrix((np_(sys.vals), np_(sys.colidx), np_(sys.rowptr)), shape=(nd, nd)).tocsc()
-    uhat = solve_skeleton(em, H.indptr, H.indices, H.data, b, ub, d2)
-    ls = eng.recover(g, dm, cs, torch.from_numpy(uhat).cuda())
+    # boundary data and the skeleton solve on the GPU (study.cpp:25-28)
+    ub = eng.dirichlet_project(dm, prob.u)
+    eng.neumann_load(dm, g, prob.q, b=sys.b, alpha=-1.0)
+    uhat_d, info = eng.solve_skeleton(dm, pat, sys, ub)
+    assert info["converged"] and info["asym"] < 1e-12 * info["scale"]
+    uhat = np_(uhat_d)
+    ls = eng.recover(g, dm, cs, uhat_d)
     eng.set_postprocess_rule()
     us = eng.postprocess_star(g, prob.kappa, ls)
     # oracle end to end
