@@ -389,7 +389,7 @@ void solve_cg(hdg_ctx* c, int nfc, const int64_t* fb, const int* nbr, const doub
   const int nblk = c->sms * 4;
   auto al = [](size_t v) { return (v + 255) / 256 * 256; };
   const size_t vb = al(size_t(n) * 8), pb = al(size_t(nblk) * 8);
-  const size_t total = 4 * vb + al(size_t(nfc) * D2 * D2 * 8) + 3 * pb + 256 + 256;
+  const size_t total = 5 * vb + al(size_t(nfc) * D2 * D2 * 8) + 3 * pb + 256 + 256;
   void* mem = nullptr;
   CUDA_OK(cudaMallocAsync(&mem, total, s));
   struct Free {
@@ -401,13 +401,15 @@ void solve_cg(hdg_ctx* c, int nfc, const int64_t* fb, const int* nbr, const doub
   double* z = reinterpret_cast<double*>(base + vb);
   double* p = reinterpret_cast<double*>(base + 2 * vb);
   double* y = reinterpret_cast<double*>(base + 3 * vb);
-  double* binv = reinterpret_cast<double*>(base + 4 * vb);
-  double* p0 = reinterpret_cast<double*>(base + 4 * vb + al(size_t(nfc) * D2 * D2 * 8));
+  double* r2 = reinterpret_cast<double*>(base + 4 * vb);  // ping-pong partner of r
+  float* binv = reinterpret_cast<float*>(base + 5 * vb);
+  double* p0 = reinterpret_cast<double*>(base + 5 * vb + al(size_t(nfc) * D2 * D2 * 8));
   double* p1 = p0 + pb / 8;
   double* p2 = p1 + pb / 8;
   auto* sc = reinterpret_cast<SolveScalars*>(reinterpret_cast<char*>(p2) + pb);
   auto* bad = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sc) + 256);
 
+  CUDA_OK(cudaFuncSetAttribute(spmv_kernel<D2>, cudaFuncAttributeMaxDynamicSharedMemorySize, spmv_smem_bytes<D2>()));
   // reference symmetry test over the free block (global_system.cpp:144-147)
   asym_kernel<D2><<<nblk, kSolveThreads, 0, s>>>(nfc, ndir, fb, nbr, vals, p0, p1);
   CUDA_OK(cudaGetLastError());
@@ -428,8 +430,9 @@ void solve_cg(hdg_ctx* c, int nfc, const int64_t* fb, const int* nbr, const doub
   // x0: u_D on the Dirichlet dofs, 0 on the free ones
   if (ndir > 0) CUDA_OK(cudaMemcpyAsync(x, ub, size_t(ndir) * D2 * 8, cudaMemcpyDeviceToDevice, s));
   CUDA_OK(cudaMemsetAsync(x + long(ndir) * D2, 0, size_t(n - long(ndir) * D2) * 8, s));
-  spmv_kernel<D2><<<nblk, kSolveThreads, 0, s>>>(nfc, fb, nbr, vals, x, y, ndir, nullptr);
-  update_kernel<D2><<<nblk, kSolveThreads, 0, s>>>(0, nfc, ndir, binv, b, y, p, x, r, z, sc, p1, p2);
+  spmv_kernel<D2><<<nblk, kSolveThreads, spmv_smem_bytes<D2>(), s>>>(nfc, fb, nbr, vals, x, y, ndir, nullptr);
+  update_kernel<D2><<<nblk, kSolveThreads, 0, s>>>(0, nfc, ndir, binv, b, y, p, x, r, r, z, sc, p1, p2);
+  CUDA_OK(cudaMemcpyAsync(r2, r, size_t(n) * 8, cudaMemcpyDeviceToDevice, s));  // zero Dirichlet rows in both
   finalize_kernel<<<1, kSolveThreads, 0, s>>>(0, nblk, p1, p2, sc);
   direction_kernel<<<nblk, kSolveThreads, 0, s>>>(n, z, p, sc, 1);
   CUDA_OK(cudaGetLastError());
@@ -441,7 +444,7 @@ void solve_cg(hdg_ctx* c, int nfc, const int64_t* fb, const int* nbr, const doub
                                    std::to_string(hbad) + " diagonal block not SPD)"};
 
   // one CG iteration = 5 launches; captured once into a graph of kChunk iterations
-  constexpr int kChunk = 16;
+  constexpr int kChunk = 16;  // even: r is current again after every chunk
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   // capture on a private stream (the context stream may be the legacy default
@@ -454,9 +457,11 @@ void solve_cg(hdg_ctx* c, int nfc, const int64_t* fb, const int* nbr, const doub
   } sguard{cs};
   CUDA_OK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   for (int it = 0; it < kChunk; ++it) {
-    spmv_kernel<D2><<<nblk, kSolveThreads, 0, cs>>>(nfc, fb, nbr, vals, p, y, ndir, p0);
+    spmv_kernel<D2><<<nblk, kSolveThreads, spmv_smem_bytes<D2>(), cs>>>(nfc, fb, nbr, vals, p, y, ndir, p0);
     finalize_kernel<<<1, kSolveThreads, 0, cs>>>(1, nblk, p0, nullptr, sc);
-    update_kernel<D2><<<nblk, kSolveThreads, 0, cs>>>(1, nfc, ndir, binv, b, y, p, x, r, z, sc, p1, p2);
+    const double* rin = (it & 1) ? r2 : r;
+    double* rout = (it & 1) ? r : r2;
+    update_kernel<D2><<<nblk, kSolveThreads, 0, cs>>>(1, nfc, ndir, binv, b, y, p, x, rin, rout, z, sc, p1, p2);
     finalize_kernel<<<1, kSolveThreads, 0, cs>>>(2, nblk, p1, p2, sc);
     direction_kernel<<<nblk, kSolveThreads, 0, cs>>>(n, z, p, sc, 0);
   }

@@ -35,42 +35,55 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;  // valid in thread 0
 }
 
-// y = mask(H x); partial[b] = sum over the block's rows of x . y (if partial)
+template <int D2>
+constexpr int spmv_smem_bytes() { return (kSolveThreads / 32) * (8 * D2 + D2 * 33) * 8; }
+
+// y = mask(H x); partial[b] = sum over the block's rows of x . y (if partial).
+// One warp per face: the face's n1 * d2 neighbour values of x are gathered
+// once into shared memory (instead of once per row), then every lane walks
+// its column positions of all d2 rows (independent loads, all in flight) and
+// the per-row partials are reduced through shared memory.
 template <int D2>
 __global__ void __launch_bounds__(kSolveThreads)
 spmv_kernel(int nfc, const int64_t* __restrict__ fb, const int* __restrict__ nbr, const double* __restrict__ vals,
             const double* __restrict__ x, double* __restrict__ y, int ndir, double* __restrict__ partial) {
-  __shared__ double red[kSolveThreads / 32];
-  const int lane = threadIdx.x & 31, hl = lane & 15;  // half-warp per row, two rows per warp
-  const long nrows = long(nfc) * D2;
-  const long w0 = (long(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const long nw = (long(gridDim.x) * blockDim.x) >> 5;
+  constexpr int NW = kSolveThreads / 32;
+  __shared__ double red[NW];
+  extern __shared__ double spmv_smem[];  // spmv_smem_bytes<D2>()
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* xs = spmv_smem + warp * (8 * D2 + D2 * 33);
+  double* part = xs + 8 * D2;  // [D2][33]
   double dot = 0.0;
-  for (long w = w0; 2 * w < nrows; w += nw) {  // warp-uniform trip count
-    const long row = 2 * w + (lane >> 4);
-    double acc = 0.0;
-    const bool live = row < nrows;
-    long f = 0;
-    int i = 0;
-    if (live) {
-      f = row / D2;
-      i = int(row - f * D2);
-      const int64_t b0 = fb[f];
-      const int n1 = int(fb[f + 1] - b0);
-      const double* v = vals + b0 * D2 * D2 + long(i) * n1 * D2;
-      const int* nb = nbr + 8 * f;
-      for (int k = hl; k < n1 * D2; k += 16) {
-        const int s = k / D2, j = k - s * D2;
-        acc = fma(__ldg(v + k), __ldg(x + long(__ldg(nb + s)) * D2 + j), acc);
-      }
+  for (long f = long(blockIdx.x) * NW + warp; f < nfc; f += long(gridDim.x) * NW) {
+    const int64_t b0 = fb[f];
+    const int n1 = int(fb[f + 1] - b0), w = n1 * D2;
+    for (int k = lane; k < w; k += 32) {
+      const int s = k / D2;
+      xs[k] = __ldg(x + long(__ldg(nbr + 8 * f + s)) * D2 + (k - s * D2));
+    }
+    __syncwarp();
+    const double* v = vals + b0 * D2 * D2;
+    double acc[D2];
+#pragma unroll
+    for (int i = 0; i < D2; ++i) acc[i] = 0.0;
+    for (int k = lane; k < w; k += 32) {
+      const double xk = xs[k];
+#pragma unroll
+      for (int i = 0; i < D2; ++i) acc[i] = fma(__ldg(v + long(i) * w + k), xk, acc[i]);
     }
 #pragma unroll
-    for (int o = 8; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (live && hl == 0) {
-      const double yv = f < ndir ? 0.0 : acc;
+    for (int i = 0; i < D2; ++i) part[i * 33 + lane] = acc[i];
+    __syncwarp();
+    if (lane < D2) {
+      double s = 0.0;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) s += part[lane * 33 + l];
+      const long row = f * D2 + lane;
+      const double yv = f < ndir ? 0.0 : s;
       y[row] = yv;
       dot += x[row] * yv;
     }
+    __syncwarp();
   }
   if (partial) {
     const double s = block_sum(dot, red);
@@ -78,11 +91,14 @@ spmv_kernel(int nfc, const int64_t* __restrict__ fb, const int* __restrict__ nbr
   }
 }
 
-// Inverse of each free face's diagonal block (SPD): one warp per face.
+// Inverse of each free face's diagonal block (SPD): one warp per face, stored
+// packed lower in fp32 (a preconditioner only steers the iteration; the
+// residual test is fp64), 4 d2(d2+1)/2 bytes per face instead of 8 d2^2.
 template <int D2>
 __global__ void block_jacobi_kernel(int nfc, int ndir, const int64_t* __restrict__ fb, const int* __restrict__ nbr,
-                                    const double* __restrict__ vals, double* __restrict__ binv,
+                                    const double* __restrict__ vals, float* __restrict__ binv,
                                     unsigned long long* __restrict__ bad) {
+  constexpr int NS = D2 * (D2 + 1) / 2;
   __shared__ __align__(16) double stage[kSolveThreads / 32][128];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (long f = long(blockIdx.x) * (blockDim.x >> 5) + warp; f < nfc; f += long(gridDim.x) * (blockDim.x >> 5)) {
@@ -104,7 +120,8 @@ __global__ void block_jacobi_kernel(int nfc, int ndir, const int64_t* __restrict
     }
     if (lane < D2) {
 #pragma unroll
-      for (int i = 0; i < D2; ++i) binv[f * D2 * D2 + long(lane) * D2 + i] = a[i];
+      for (int i = 0; i < D2; ++i)
+        if (i >= lane) binv[f * NS + sym_idx(i, lane, D2)] = float(a[i]);
     }
   }
 }
@@ -134,48 +151,46 @@ __global__ void finalize_kernel(int mode, int nblk, const double* __restrict__ p
   }
 }
 
-// r = mask(b - y) on entry (mode 0, y = H x0) or r -= alpha Ap, x += alpha p
-// (mode 1); then z = Binv r per face; partials: r.z and r.r. One warp per face.
+// r_out = mask(b - y) (mode 0, y = H x0) or r_out = r_in - alpha Ap and
+// x += alpha p (mode 1); z = Binv r_out per face; partials r.z and r.r.
+// One thread per row; a row's z needs its whole face's r, which each thread
+// recomputes from r_in (ping-pong buffers, so no thread reads a value another
+// has overwritten).
 template <int D2>
 __global__ void __launch_bounds__(kSolveThreads)
-update_kernel(int mode, int nfc, int ndir, const double* __restrict__ binv, const double* __restrict__ b,
+update_kernel(int mode, int nfc, int ndir, const float* __restrict__ binv, const double* __restrict__ b,
               const double* __restrict__ y, const double* __restrict__ p, double* __restrict__ x,
-              double* __restrict__ r, double* __restrict__ z, const SolveScalars* __restrict__ sc,
-              double* __restrict__ prz, double* __restrict__ prr) {
+              const double* __restrict__ rin, double* __restrict__ rout, double* __restrict__ z,
+              const SolveScalars* __restrict__ sc, double* __restrict__ prz, double* __restrict__ prr) {
+  constexpr int NS = D2 * (D2 + 1) / 2;
   __shared__ double red[kSolveThreads / 32];
-  __shared__ double rs[kSolveThreads / 32][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double alpha = mode == 1 ? sc->alpha : 0.0;
   double dz = 0.0, dr = 0.0;
-  const long nwarps = long(gridDim.x) * (blockDim.x >> 5);
-  for (long f = long(blockIdx.x) * (blockDim.x >> 5) + warp; f < nfc; f += nwarps) {  // warp per face
-    const bool live = f >= ndir;
-    double ri = 0.0;
-    if (live && lane < D2) {
-      const long row = f * D2 + lane;
+  const long rows = long(nfc) * D2;
+  for (long row = long(blockIdx.x) * blockDim.x + threadIdx.x; row < rows; row += long(gridDim.x) * blockDim.x) {
+    const long f = row / D2;
+    const int i = int(row - f * D2);
+    if (f < ndir) {
       if (mode == 0) {
-        ri = b[row] - y[row];
-      } else {
-        x[row] += alpha * p[row];
-        ri = r[row] - alpha * y[row];
+        rout[row] = 0.0;
+        z[row] = 0.0;
       }
-      r[row] = ri;
-    } else if (lane < D2 && mode == 0) {
-      r[f * D2 + lane] = 0.0;
-      z[f * D2 + lane] = 0.0;
+      continue;
     }
-    rs[warp][lane] = ri;
-    __syncwarp();
-    if (live && lane < D2) {
-      const double* B = binv + f * D2 * D2;
-      double zi = 0.0;
+    const long base = f * D2;
+    const float* B = binv + f * NS;
+    double zi = 0.0, ri = 0.0;
 #pragma unroll
-      for (int j = 0; j < D2; ++j) zi = fma(B[long(j) * D2 + lane], rs[warp][j], zi);
-      z[f * D2 + lane] = zi;
-      dz += ri * zi;
-      dr += ri * ri;
+    for (int j = 0; j < D2; ++j) {
+      const double rj = mode == 0 ? b[base + j] - y[base + j] : rin[base + j] - alpha * y[base + j];
+      if (j == i) ri = rj;
+      zi = fma(double(B[j >= i ? sym_idx(j, i, D2) : sym_idx(i, j, D2)]), rj, zi);
     }
-    __syncwarp();
+    rout[row] = ri;
+    if (mode == 1) x[row] += alpha * p[row];
+    z[row] = zi;
+    dz += ri * zi;
+    dr += ri * ri;
   }
   const double s0 = block_sum(dz, red);
   const double s1 = block_sum(dr, red);
