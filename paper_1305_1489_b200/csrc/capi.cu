@@ -295,7 +295,7 @@ struct C4Launch {
 template <class Dm, class Cg, class Kern>
 void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, const double* Ms,
                           const double* Ds, const double* fv, double* C, double* Cf, double* F) {
-  const size_t smem = size_t(Cg::EPB) * Dm::PER_ELT * sizeof(double);
+  const size_t smem = (size_t(Cg::EPB) * Dm::PER_ELT + Dm::CTA_EXTRA) * sizeof(double);
   CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int occ = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cg::NW * 32 * Cg::EPB, smem));

@@ -43,6 +43,7 @@ struct C2Dims {
   static constexpr int OFF_COL = OFF_GEO + 64;         // second column-data buffer
   static constexpr int PER_ELT = OFF_COL + 8 * MP;
   static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
+  static constexpr int CTA_EXTRA = 0;  // per-CTA shared doubles beyond EPB * PER_ELT
 };
 
 template <int K_> struct C2Cfg;

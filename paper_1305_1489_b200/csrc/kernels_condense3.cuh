@@ -33,6 +33,7 @@ template <int K_>
 struct C3Dims : C2Dims<K_> {
   static constexpr int OFF_DP = C2Dims<K_>::PER_ELT;
   static constexpr int PER_ELT = OFF_DP + round_up(C2Dims<K_>::NSYM, 2);
+  static constexpr int CTA_EXTRA = 3 * C2Dims<K_>::D3 * C2Dims<K_>::D3;  // Chat copy
 };
 
 template <int K_> struct C3Cfg;
@@ -74,7 +75,12 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const double* Wlm = tab.Wlm;
-  const double* Ch = tab.Chat;
+  // CTA copy of Chat (3 d3^2): its fragments are re-read every phase, and the
+  // L1 left beside ~218 KB of shared memory does not hold the tables
+  double* Ch = smem + EPB * Dm::PER_ELT;
+  for (int i = threadIdx.x; i < 3 * D3 * D3; i += NT) Ch[i] = tab.Chat[i];
+  __syncthreads();
+#define CH_LD(p) (*(p))
   auto B = [&](int e) { return smem + e * Dm::PER_ELT; };
   auto Mi = [&](int e) { return B(e) + Dm::OFF_MI; };
   auto Sb = [&](int e) { return B(e) + Dm::OFF_S; };
@@ -191,9 +197,9 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           const bool in = k < D3 && c < D3;
           const int o = c + k * D3;
           const double a = mi[(m * 8 + g) + k * LD];
-          dmma(q[0][0], q[0][1], a, in ? __ldg(Ch + o) : 0.0);
-          dmma(q[1][0], q[1][1], a, in ? __ldg(Ch + D3 * D3 + o) : 0.0);
-          dmma(q[2][0], q[2][1], a, in ? __ldg(Ch + 2 * D3 * D3 + o) : 0.0);
+          dmma(q[0][0], q[0][1], a, in ? CH_LD(Ch + o) : 0.0);
+          dmma(q[1][0], q[1][1], a, in ? CH_LD(Ch + D3 * D3 + o) : 0.0);
+          dmma(q[2][0], q[2][1], a, in ? CH_LD(Ch + 2 * D3 * D3 + o) : 0.0);
         }
         const double* a9 = sg + 1;
         const int c0 = nt * 8 + 2 * t, r = m * 8 + g;
@@ -256,7 +262,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
           for (int kk = 0; kk < KS; ++kk) {
             const int k = kk * 4 + t;
-            const double a = (r < D3 && k < D3) ? __ldg(C + r + k * D3) : 0.0;
+            const double a = (r < D3 && k < D3) ? CH_LD(C + r + k * D3) : 0.0;
             if (kk & 1) dmma(q0, q1, a, R[k + (j * 8 + g) * LD]);
             else dmma(p0, p1, a, R[k + (j * 8 + g) * LD]);
           }
@@ -286,7 +292,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           double a = 0.0;
           if (r < D3 && k < D3) {
             const int o = r + k * D3;
-            a = b0 * __ldg(Ch + o) + b1 * __ldg(Ch + D3 * D3 + o) + b2 * __ldg(Ch + 2 * D3 * D3 + o);
+            a = b0 * CH_LD(Ch + o) + b1 * CH_LD(Ch + D3 * D3 + o) + b2 * CH_LD(Ch + 2 * D3 * D3 + o);
           }
 #pragma unroll
           for (int j = 0; j < NTF; ++j) {
@@ -454,5 +460,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     cur ^= 1;
   }
 }
+
+#undef CH_LD
 
 }  // namespace hdgb

@@ -226,6 +226,7 @@ struct CondDims {
   static constexpr int PER_ELT = OFF_GEO + 32;          // vol a[9] n[12] T[4] perm[4]
   // recovery cache per element: Li (packed), LSi (packed), Vt (D3 x M), ft (D3)
   static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
+  static constexpr int CTA_EXTRA = 0;
 };
 
 template <int K_>
