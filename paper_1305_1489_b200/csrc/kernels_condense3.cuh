@@ -33,8 +33,18 @@ template <int K_>
 struct C3Dims : C2Dims<K_> {
   static constexpr int OFF_DP = C2Dims<K_>::PER_ELT;
   static constexpr int PER_ELT = OFF_DP + round_up(C2Dims<K_>::NSYM, 2);
-  static constexpr int CTA_EXTRA = 3 * C2Dims<K_>::D3 * C2Dims<K_>::D3;  // Chat copy
+  static constexpr int CTA_EXTRA = 3 * C2Dims<K_>::D3 * C2Dims<K_>::D3 + C2Dims<K_>::D2 * C2Dims<K_>::D2;  // Chat, DD
 };
+
+// Most 8-column tiles one face's d2 columns (starting at l d2) touch.
+constexpr int face_tiles(int d2) {
+  int n = 0;
+  for (int l = 0; l < 4; ++l) {
+    const int t = (l * d2 + d2 - 1) / 8 - (l * d2) / 8 + 1;
+    n = t > n ? t : n;
+  }
+  return n;
+}
 
 template <int K_> struct C3Cfg;
 #ifndef HDG_C3_EPB2
@@ -62,7 +72,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int MT = Dm::MT, NTM = Dm::NTM, KS = Dm::KS;
   constexpr int NLOW = NTM * (NTM + 1) / 2;  // lower tiles of the m x m output
   constexpr int NLS = MT * (MT + 1) / 2;     // lower tiles of S
-  constexpr int NTF = (D2 + 7) / 8 + 1;      // N-tiles one face's columns can span
+  constexpr int NTF = face_tiles(D2);        // N-tiles one face's columns span
   constexpr int NGJ = 2 * EPB;               // GJ tasks in P3
   constexpr bool GJ_SEP = NWT > NGJ;         // GJ warps do nothing else in P3
   static_assert(NLOW * 64 <= 3 * D3P * LD, "W Zp tiles must fit in the R buffer");
@@ -78,7 +88,9 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   // CTA copy of Chat (3 d3^2): its fragments are re-read every phase, and the
   // L1 left beside ~218 KB of shared memory does not hold the tables
   double* Ch = smem + EPB * Dm::PER_ELT;
+  double* DDs = Ch + 3 * D3 * D3;  // tauDD reference block (d2 x d2)
   for (int i = threadIdx.x; i < 3 * D3 * D3; i += NT) Ch[i] = tab.Chat[i];
+  for (int i = threadIdx.x; i < D2 * D2; i += NT) DDs[i] = tab.DD[i];
   __syncthreads();
 #define CH_LD(p) (*(p))
   auto B = [&](int e) { return smem + e * Dm::PER_ELT; };
@@ -283,9 +295,14 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         const double* beta = col + 5 * MP;
         const double b0 = beta[cl0], b1 = beta[MP + cl0], b2 = beta[2 * MP + cl0];
         const double* Z = Zb(e);
-        double acc[NTF][2];
+        double acc[NTF][2];  // starts at T_l W_l^T (its loads overlap the DMMA chain)
 #pragma unroll
-        for (int j = 0; j < NTF; ++j) acc[j][0] = acc[j][1] = 0.0;
+        for (int j = 0; j < NTF; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = (nt0 + j) * 8 + 2 * t + h;
+            acc[j][h] = (c >= cl0 && c < cl1 && r < D3) ? Tc[c] * __ldg(Wlm + wb[c] + r * D2) : 0.0;
+          }
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
           const int k = kk * 4 + t;
@@ -307,7 +324,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int c = (nt0 + j) * 8 + 2 * t + h;
-            if (c >= cl0 && c < cl1 && r < D3) V[r + c * LD] = acc[j][h] + Tc[c] * __ldg(Wlm + wb[c] + r * D2);
+            if (c >= cl0 && c < cl1 && r < D3) V[r + c * LD] = acc[j][h];
           }
       }
     }
@@ -442,7 +459,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           const int l2 = c / D2;
           const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
           double v = nn * (h ? z1 : z0) - (h ? v1 : v0);
-          if (l1 == l2) v += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
+          if (l1 == l2) v += Tc[c] * DDs[(r - l1 * D2) + (c - l2 * D2) * D2];
           Ck[r + c * M] = v;
           if (c != r) Ck[c + r * M] = v;
         }
