@@ -74,7 +74,9 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
                                                 double& pmax) {
   // stage: 2 buffers x (2 x 32) doubles: the two pivot columns gathered from
   // every lane (column k of a symmetric matrix == every lane's a[k]).
-  double piv0[N / 2 + 1], pdet[N / 2 + 1];
+  // Cholesky pivots of each 2x2 block: p00 and det / p00 = 1 / i11, tracked as
+  // running extremes (p00, i11, det) instead of stored, to save registers.
+  double p00min = 1e300, p00max = 0.0, i11min = 1e300, i11max = 0.0, detmin = 1e300;
 #pragma unroll
   for (int k = 0; k + 1 < N; k += 2) {
     double* st = stage + ((k >> 1) & 1) * 64;
@@ -87,10 +89,13 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
     const double p01 = __shfl_sync(0xffffffffu, a[k + 1], k);
     const double p11 = __shfl_sync(0xffffffffu, a[k + 1], k + 1);
     const double det = fma(p00, p11, -p01 * p01);
-    piv0[k >> 1] = p00;
-    pdet[k >> 1] = det;
     const double id = fast_rcp(det);
     const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;  // P^-1 (symmetric)
+    p00min = fmin(p00min, p00);
+    p00max = fmax(p00max, p00);
+    i11min = fmin(i11min, i11);
+    i11max = fmax(i11max, i11);
+    detmin = fmin(detmin, det);
     const bool m0 = lane == k, m1 = lane == k + 1;
     // w = P^-1 [a_k; a_k+1] for ordinary lanes; pivot lanes hold their own
     // block column, for which "a - v w" must produce A(i,block) P^-1.
@@ -123,8 +128,9 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
     double* st = stage + (((k >> 1)) & 1) * 64;
     if (lane < N) st[lane] = a[k];
     const double p = __shfl_sync(0xffffffffu, a[k], k);
-    piv0[k >> 1] = p;
-    pdet[k >> 1] = p * p;
+    p00min = fmin(p00min, p);
+    p00max = fmax(p00max, p);
+    detmin = fmin(detmin, p);
     const double ip = fast_rcp(p);
     const bool me = lane == k;
     const double t = me ? 1.0 - ip : a[k] * ip;
@@ -137,12 +143,13 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < N; ++i) a[i] = -a[i];
-  // Cholesky pivots of each block: p00 and det / p00 (scalar tail: p, p)
-#pragma unroll
-  for (int j = 0; j < (N + 1) / 2; ++j) {
-    const double d1 = pdet[j] / piv0[j];
-    pmin = fmin(pmin, fmin(piv0[j], d1));
-    pmax = fmax(pmax, fmax(piv0[j], d1));
+  if (!(p00min > 0.0) || !(detmin > 0.0)) {
+    pmin = fmin(pmin, fmin(p00min, detmin));  // not SPD: fails the pivot test
+    pmax = fmax(pmax, p00max);
+  } else {
+    const double dmin = N >= 2 ? 1.0 / i11max : 1e300, dmax = N >= 2 ? 1.0 / i11min : 0.0;
+    pmin = fmin(pmin, fmin(p00min, dmin));
+    pmax = fmax(pmax, fmax(p00max, dmax));
   }
 }
 
