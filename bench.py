@@ -396,8 +396,10 @@ def run_ours(args):
     hbm_peak, hbm_src = load_peaks()
     k3_ms = stage_ms.get("condense", float("nan"))
     achieved = k3_flops(k) * nelt / (k3_ms / 1e3) / 1e12
-    traffic, traffic_src = ncu_traffic(f"condense2_kernel<{k}>" if k <= 3 else f"condense_kernel<{k}>")
-    roof = {"kernel": "condense_kernel (K3)", "bound": "tensor", "achieved": achieved,
+    kname3 = f"condense3_kernel<{k}>" if k in (2, 3) else (f"condense2_kernel<{k}>" if k <= 1 else
+                                                           f"condense_kernel<{k}>")
+    traffic, traffic_src = ncu_traffic(kname3)
+    roof = {"kernel": f"{kname3} (K3)", "bound": "tensor", "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
             "traffic": traffic if cfg.name == "C2" and world == 1 else None,
             "traffic_source": traffic_src, "algorithmic_bytes": k3_bytes(k) * nelt,

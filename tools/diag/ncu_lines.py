@@ -1,5 +1,5 @@
 """Summarise an ncu report: headline metrics, stall mix, and the hottest source
-lines (warp-stall samples). Usage: ncu_lines.py REPORT.ncu-rep [N]."""
+lines (warp-stall samples). Usage: ncu_lines.py REPORT.ncu-rep [N] [kernel-regex]."""
 import collections
 import csv
 import io
@@ -8,7 +8,8 @@ import sys
 
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 16
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+filt = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"] + filt, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, units, v = rows[0], rows[1], rows[2]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -30,7 +31,7 @@ for i, n in enumerate(h):
             pass
 s = sum(tot.values()) or 1
 print("stalls:", ", ".join(f"{k} {x / s * 100:.1f}%" for k, x in sorted(tot.items(), key=lambda a: -a[1])[:8]))
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + filt,
                      capture_output=True, text=True).stdout
 agg = collections.defaultdict(lambda: [0.0, 0.0, collections.Counter()])
 hdr = f = None

@@ -14,7 +14,7 @@ lines = [ln for ln in open(src) if ln.startswith('"')]
 for r in csv.DictReader(lines):
     key = r["ID"]
     if key not in rows:
-        name = r["Kernel Name"].split("(")[0].replace("void ", "").strip()
+        name = r["Kernel Name"].split("(")[0].replace("void ", "").strip().replace(",", ";")
         rows[key] = {"kernel": name}
         order.append(key)
     v = float(r["Metric Value"].replace(",", "")) * scale.get(r["Metric Unit"], 1.0)
