@@ -254,6 +254,29 @@ int hdg_b200_solve_skeleton(hdg_ctx* ctx, int nfc, int d2, const int64_t* d_face
                             const double* d_ub, double rtol, int maxit, double* d_uhat,
                             hdg_solve_info* info);
 
+/* ------------------------------------------ error functionals (§8(f)4)
+ * set_error_rule: tables of degree k and k+1 on tet/tri_rule(deg) (deg < 0:
+ * 2k+4, postprocess.cpp:182-183); call after set_degree.
+ * hdg_project replaces hdg_project (postprocess.cpp:95-176): the HDG
+ * projection of (q, u) into P_k, d3 x nelt each; element matrices from the
+ * level's tables, data moments on the error rule; HDG_ESINGULAR + element.
+ * compute_errors replaces compute_errors (postprocess.cpp:178-250): relative
+ * L2 errors of q, u, u* (d_ustar may be NULL), the skeleton error of uhat,
+ * and the superconvergence measures against the HDG (or, tau == 0, L2)
+ * projection and l2_project_skeleton. Fields must be CONST or PROGRAM.     */
+typedef struct {
+  double e_q, e_u, e_uhat, eps_u, eps_uhat, e_star;
+} hdg_error_report;
+int hdg_b200_set_error_rule(hdg_ctx* ctx, int deg);
+int hdg_b200_hdg_project(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_field qx, hdg_field qy,
+                         hdg_field qz, hdg_field u, double* d_qx, double* d_qy, double* d_qz,
+                         double* d_u, int64_t* bad_element);
+int hdg_b200_compute_errors(hdg_ctx* ctx, int nelt, const hdg_geometry* g, int nver,
+                            const double* d_coords, int nfc, const int* d_faces, hdg_field qx,
+                            hdg_field qy, hdg_field qz, hdg_field u, const double* d_uhat,
+                            const double* d_qx, const double* d_qy, const double* d_qz,
+                            const double* d_u, const double* d_ustar, hdg_error_report* out);
+
 /* --------------------------------------------- K7: convection block
  * Replaces convection_bilinear_matrices (convdiff.cpp:5-28): vol d3 x d3,
  * dp 4d2 x d3, dd 4d2 x 4d2 per element (Batch3 layout).                   */

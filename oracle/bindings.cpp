@@ -337,6 +337,11 @@ PYBIND11_MODULE(_hdg_oracle, m) {
   m.def("l2_project_skeleton", [](const ExpandedMesh& em, int k, int tri_deg, const Field& f) {
     return np_mat(l2_project_skeleton(em, k, tri_rule(tri_deg), f.f));
   });
+  m.def("hdg_project", [](const ExpandedMesh& em, const ElementMatrixSet& ms, const Tables& t,
+                          const StabilizationField& tau, const VField& q, const Field& u) {
+    const LocalSolution ls = hdg_project(em, ms, t.tb, t.tet, t.tri, tau, q.f, u.f, 1);
+    return py::make_tuple(np_mat(ls.qx), np_mat(ls.qy), np_mat(ls.qz), np_mat(ls.u));
+  });
   m.def("compute_errors",
         [](const ExpandedMesh& em, const ElementMatrixSet& ms, const StabilizationField& tau,
            const Field& u, const VField& q, int k, const py::array_t<double>& uhat,

@@ -59,6 +59,10 @@ class GlobalSolverError(HdgError):
     """Reference GlobalSolverError (global_system.hpp:44-46)."""
 
 
+class hdg_error_report(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("e_q", "e_u", "e_uhat", "eps_u", "eps_uhat", "e_star")]
+
+
 class hdg_solve_info(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("relres", C.c_double), ("asym", C.c_double),
                 ("scale", C.c_double)]
@@ -110,6 +114,12 @@ _SIGS = {
     "hdg_b200_pattern_device": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P, C.POINTER(C.c_int)]),
     "hdg_b200_solve_skeleton": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P, C.c_int, P, C.c_double, C.c_int, P,
                                           C.POINTER(hdg_solve_info)]),
+    "hdg_b200_set_error_rule": (C.c_int, [P, C.c_int]),
+    "hdg_b200_hdg_project": (C.c_int, [P, C.c_int, C.POINTER(hdg_geometry), hdg_field, hdg_field, hdg_field,
+                                       hdg_field, P, P, P, P, I64P]),
+    "hdg_b200_compute_errors": (C.c_int, [P, C.c_int, C.POINTER(hdg_geometry), C.c_int, P, C.c_int, P, hdg_field,
+                                          hdg_field, hdg_field, hdg_field, P, P, P, P, P, P,
+                                          C.POINTER(hdg_error_report)]),
     "hdg_b200_dirichlet_project": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, hdg_field, P]),
     "hdg_b200_skeleton_project": (C.c_int, [P, C.c_int, P, C.c_int, P, hdg_field, P]),
     "hdg_b200_neumann_load": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, P, C.POINTER(hdg_geometry),

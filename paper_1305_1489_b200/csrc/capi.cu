@@ -23,6 +23,7 @@
 #include "kernels_recover3.cuh"
 #include "kernels_boundary.cuh"
 #include "kernels_solve.cuh"
+#include "kernels_errors.cuh"
 #include "jit_quad.hpp"
 #include "mesh_dev.hpp"
 
@@ -228,7 +229,7 @@ struct hdg_ctx {
   int device = 0;
   int sms = 148;
   cudaStream_t stream = nullptr;
-  TabSet tab[2];  // [0] degree k, [1] postprocess degree k+1
+  TabSet tab[4];  // [0] degree k, [1] postprocess degree k+1, [2]/[3] degree k / k+1 on the error rule
   int post_tet_deg = -1;
   int tri_deg = 0;
   void* work = nullptr;
@@ -494,6 +495,87 @@ void solve_cg(hdg_ctx* c, int nfc, const int64_t* fb, const int* nbr, const doub
 }
 }  // namespace
 
+// error-functional helpers (outside the extern "C" block: member templates)
+namespace {
+// inverses of W_{l,mu}[:, t:] (d2 x d2, column-major) for the 24 (l, mu):
+// Gauss-Jordan with partial pivoting on the host (level tables)
+std::vector<double> face_block_inverses(const HostTables& h) {
+  const int d2 = h.d2, d3 = h.d3, t = d3 - d2;
+  std::vector<double> out(size_t(24) * d2 * d2);
+  for (int lm = 0; lm < 24; ++lm) {
+    std::vector<double> a(size_t(d2) * d2), inv(size_t(d2) * d2, 0.0);
+    for (int j = 0; j < d2; ++j)
+      for (int i = 0; i < d2; ++i) a[i + size_t(j) * d2] = h.Wlm[lm][i + size_t(t + j) * d2];
+    for (int i = 0; i < d2; ++i) inv[i + size_t(i) * d2] = 1.0;
+    double pmax = 0.0, pmin = 1e300;
+    for (int c = 0; c < d2; ++c) {
+      int p = c;
+      for (int r = c + 1; r < d2; ++r)
+        if (std::fabs(a[r + size_t(c) * d2]) > std::fabs(a[p + size_t(c) * d2])) p = r;
+      for (int j = 0; j < d2; ++j) {
+        std::swap(a[c + size_t(j) * d2], a[p + size_t(j) * d2]);
+        std::swap(inv[c + size_t(j) * d2], inv[p + size_t(j) * d2]);
+      }
+      const double piv = a[c + size_t(c) * d2];
+      pmax = std::max(pmax, std::fabs(piv));
+      pmin = std::min(pmin, std::fabs(piv));
+      require(piv != 0.0, HDG_EINVAL, "singular face block in hdg_project tables");
+      for (int j = 0; j < d2; ++j) {
+        a[c + size_t(j) * d2] /= piv;
+        inv[c + size_t(j) * d2] /= piv;
+      }
+      for (int r = 0; r < d2; ++r) {
+        if (r == c) continue;
+        const double m = a[r + size_t(c) * d2];
+        if (m == 0.0) continue;
+        for (int j = 0; j < d2; ++j) {
+          a[r + size_t(j) * d2] -= m * a[c + size_t(j) * d2];
+          inv[r + size_t(j) * d2] -= m * inv[c + size_t(j) * d2];
+        }
+      }
+    }
+    require(pmin >= 1e-14 * pmax, HDG_EINVAL, "ill-conditioned face block in hdg_project tables");
+    std::copy(inv.begin(), inv.end(), out.begin() + size_t(lm) * d2 * d2);
+  }
+  return out;
+}
+
+FieldDev program_field(const hdg_field& f, const char* name) {
+  require(f.kind != HDG_FIELD_SAMPLED, HDG_EINVAL,
+          std::string("error functionals need CONST or PROGRAM fields (no node samples): ") + name);
+  return to_dev(f, name);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  DevBuf(cudaStream_t st, size_t bytes) : s(st) { CUDA_OK(cudaMallocAsync(&p, bytes ? bytes : 8, s)); }
+  ~DevBuf() { cudaFreeAsync(p, s); }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+void launch_hdg_project(hdg_ctx* c, int nelt, const GeoDev& geo, const FieldDev* F, double* qx, double* qy,
+                        double* qz, double* u) {
+  const DevTab& tE = c->tab[2].dev;
+  const std::vector<double> wi = face_block_inverses(c->tab[0].host);
+  DevBuf dw(c->stream, wi.size() * 8);
+  CUDA_OK(cudaMemcpyAsync(dw.p, wi.data(), wi.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  set_ll_kernel<<<1, 1, 0, c->stream>>>(c->d_bad, LLONG_MAX);
+  const int per_warp = 4 * tE.nq + 4 * tE.nqd + 4 * tE.d3 + 4 * tE.d2 + 32;
+  const size_t smem = size_t(kErrWarps) * per_warp * 8;
+  CUDA_OK(cudaFuncSetAttribute(hdg_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int grid = int(std::min<long>((long(nelt) + kErrWarps - 1) / kErrWarps, long(c->sms) * 16));
+  hdg_project_kernel<<<grid, kErrWarps * 32, smem, c->stream>>>(tE, c->tab[0].dev, nelt, geo, F[0], F[1], F[2],
+                                                                F[3], dw.as<double>(), qx, qy, qz, u, c->d_bad,
+                                                                per_warp);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  if (*c->h_bad != LLONG_MAX)
+    throw HdgError{HDG_ESINGULAR, "singular projection system on element " + std::to_string(*c->h_bad)};
+}
+}  // namespace
+
 extern "C" {
 
 const char* hdg_b200_version(void) { return "hdg_b200 1.0 (sm_100a)"; }
@@ -652,6 +734,7 @@ int hdg_b200_set_degree(hdg_ctx* c, int k, int tet_deg, int tri_deg) {
     c->tri_deg = tri_deg;
     c->tab[1].ready = false;
     if (c->post_tet_deg >= 0) upload_tables(c->tab[1], k + 1, c->post_tet_deg, tri_deg);
+    c->tab[2].ready = c->tab[3].ready = false;
   });
 }
 
@@ -937,6 +1020,106 @@ int hdg_b200_solve_skeleton(hdg_ctx* c, int nfc, int d2, const int64_t* d_faceba
       case 21: solve_cg<21>(c, nfc, d_facebase, d_nbr, d_vals, d_b, ndir, d_ub, rtol, maxit, d_uhat, inf); break;
       default: throw HdgError{HDG_EINVAL, "d2 must be dim2(k) for k <= 5"};
     }
+  });
+}
+
+// --------------------------------------------- error functionals (§8(f)4)
+
+int hdg_b200_set_error_rule(hdg_ctx* c, int deg) {
+  return guarded([&] {
+    require(c && c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    set_device(c);
+    const int k = c->tab[0].host.k;
+    const int d = deg >= 0 ? deg : 2 * k + 4;  // postprocess.cpp:182-183
+    upload_tables(c->tab[2], k, d, d);
+    upload_tables(c->tab[3], k + 1, d, d);
+  });
+}
+
+int hdg_b200_hdg_project(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field qx, hdg_field qy, hdg_field qz,
+                         hdg_field u, double* d_qx, double* d_qy, double* d_qz, double* d_u, int64_t* bad_element) {
+  if (bad_element) *bad_element = -1;
+  return guarded([&] {
+    require(c && d_qx && d_qy && d_qz && d_u && nelt > 0, HDG_EINVAL, "bad argument");
+    require(c->tab[0].ready && c->tab[2].ready, HDG_ESTATE, "set_error_rule first");
+    const GeoDev geo = to_geo(g);
+    const FieldDev F[4] = {program_field(qx, "qx"), program_field(qy, "qy"), program_field(qz, "qz"),
+                           program_field(u, "u")};
+    set_device(c);
+    try {
+      launch_hdg_project(c, nelt, geo, F, d_qx, d_qy, d_qz, d_u);
+    } catch (const HdgError& e) {
+      if (e.code == HDG_ESINGULAR && bad_element) *bad_element = *c->h_bad;
+      throw;
+    }
+  });
+}
+
+int hdg_b200_compute_errors(hdg_ctx* c, int nelt, const hdg_geometry* g, int nver, const double* d_coords, int nfc,
+                            const int* d_faces, hdg_field qx, hdg_field qy, hdg_field qz, hdg_field u,
+                            const double* d_uhat, const double* d_qx, const double* d_qy, const double* d_qz,
+                            const double* d_u, const double* d_ustar, hdg_error_report* out) {
+  return guarded([&] {
+    require(c && out && d_coords && d_faces && d_uhat && d_qx && d_qy && d_qz && d_u && nelt > 0 && nfc > 0 &&
+                nver > 0,
+            HDG_EINVAL, "bad argument");
+    require(c->tab[0].ready && c->tab[2].ready && c->tab[3].ready, HDG_ESTATE, "set_error_rule first");
+    require(g && g->area, HDG_EINVAL, "compute_errors needs the face areas (hdg_geometry.area)");
+    const GeoDev geo = to_geo(g);
+    const FieldDev F[4] = {program_field(qx, "qx"), program_field(qy, "qy"), program_field(qz, "qz"),
+                           program_field(u, "u")};
+    set_device(c);
+    cudaStream_t s = c->stream;
+    const DevTab& tE = c->tab[2].dev;
+    const DevTab& tE1 = c->tab[3].dev;
+    require(tE.nqd <= 64, HDG_EINVAL, "error tri rule too large (nqd <= 64)");
+    const int d3 = tE.d3;
+    // superconvergence reference (postprocess.cpp:226-232): HDG projection,
+    // or the L2 projection when tau == 0 everywhere (BDM)
+    double tmax = 0.0;
+    {
+      std::vector<double> T(size_t(4) * nelt);
+      CUDA_OK(cudaMemcpyAsync(T.data(), g->T, T.size() * 8, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(cudaStreamSynchronize(s));
+      for (double v : T) tmax = std::max(tmax, std::fabs(v));
+    }
+    DevBuf proj(s, size_t(4) * d3 * nelt * 8);
+    double* pq = proj.as<double>();
+    double* pu = pq + size_t(3) * d3 * nelt;
+    if (tmax == 0.0) {
+      const size_t smem = size_t(kErrWarps) * tE.nq * 8;
+      CUDA_OK(cudaFuncSetAttribute(l2_project_volume_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+      const int grid = int(std::min<long>((long(nelt) + kErrWarps - 1) / kErrWarps, long(c->sms) * 16));
+      l2_project_volume_kernel<<<grid, kErrWarps * 32, smem, s>>>(tE, nelt, geo, F[3], pu, tE.nq);
+      CUDA_OK(cudaGetLastError());
+    } else {
+      launch_hdg_project(c, nelt, geo, F, pq, pq + size_t(d3) * nelt, pq + size_t(2) * d3 * nelt, pu);
+    }
+    const int nblk = c->sms * 4;
+    DevBuf part(s, size_t(nblk) * sizeof(ErrSums));
+    CUDA_OK(cudaMemsetAsync(part.p, 0, size_t(nblk) * sizeof(ErrSums), s));
+    const int per_warp = 4 * d3 + tE1.d3;
+    const size_t smem = size_t(kErrWarps) * per_warp * 8;
+    CUDA_OK(cudaFuncSetAttribute(volume_errors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    volume_errors_kernel<<<nblk, kErrWarps * 32, smem, s>>>(tE, tE1, nelt, geo, F[0], F[1], F[2], F[3], d_qx, d_qy,
+                                                          d_qz, d_u, d_ustar, pu, part.as<ErrSums>(), per_warp);
+    face_errors_kernel<<<nblk, kErrWarps * 32, 0, s>>>(tE, nfc, d_coords, nver, d_faces, g->area, F[3], d_uhat,
+                                                       part.as<ErrSums>());
+    CUDA_OK(cudaGetLastError());
+    std::vector<ErrSums> h(nblk);
+    CUDA_OK(cudaMemcpyAsync(h.data(), part.p, size_t(nblk) * sizeof(ErrSums), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    double S[9] = {0};
+    for (const auto& b : h)
+      for (int j = 0; j < 9; ++j) S[j] += b.v[j];
+    auto rel = [](double e2, double n2) { return std::sqrt(n2 > 0 ? e2 / n2 : e2); };
+    out->e_q = rel(S[1], S[0]);
+    out->e_u = rel(S[3], S[2]);
+    out->e_star = d_ustar ? rel(S[4], S[2]) : 0.0;
+    out->eps_u = rel(S[5], S[2]);
+    out->e_uhat = rel(S[7], S[6]);
+    out->eps_uhat = rel(S[8], S[6]);
   });
 }
 

@@ -518,6 +518,36 @@ class Engine:
                                              _ptr(ls.qy), _ptr(ls.qz), _ptr(ls.u), _ptr(out)))
         return out
 
+    # ------------------------------------------------- error functionals
+    def set_error_rule(self, deg: int = -1) -> None:
+        """Tables of degree k and k+1 on tet/tri_rule(deg) (default 2k+4, postprocess.cpp:182-183)."""
+        L.check(L.lib().hdg_b200_set_error_rule(self._ctx, int(deg)))
+
+    def hdg_project(self, g: Geometry, q: Sequence, u) -> LocalSolution:
+        """hdg_project (postprocess.cpp:95-176): HDG projection of (q, u) into P_k."""
+        d3 = self.dims["d3"]
+        out = LocalSolution(*(torch.empty(g.nelt, d3, dtype=torch.float64, device=self.device) for _ in range(4)))
+        fs = [as_field(x) for x in q] + [as_field(u)]
+        gs = g.c_struct()
+        bad = C.c_int64(-1)
+        st = L.lib().hdg_b200_hdg_project(self._ctx, g.nelt, C.byref(gs), fs[0].c_struct(), fs[1].c_struct(),
+                                          fs[2].c_struct(), fs[3].c_struct(), _ptr(out.qx), _ptr(out.qy),
+                                          _ptr(out.qz), _ptr(out.u), C.byref(bad))
+        L.check(st, bad.value)
+        return out
+
+    def compute_errors(self, dm: DeviceMesh, g: Geometry, q: Sequence, u, uhat: torch.Tensor, ls: LocalSolution,
+                       ustar: Optional[torch.Tensor] = None) -> dict:
+        """compute_errors (postprocess.cpp:178-250) on the GPU: e_q, e_u, e_uhat, eps_u, eps_uhat, e_star."""
+        fs = [as_field(x) for x in q] + [as_field(u)]
+        gs = g.c_struct()
+        rep = L.hdg_error_report()
+        L.check(L.lib().hdg_b200_compute_errors(self._ctx, g.nelt, C.byref(gs), dm.nver, _ptr(dm.coords), dm.nfc,
+                                                _ptr(dm.faces), fs[0].c_struct(), fs[1].c_struct(),
+                                                fs[2].c_struct(), fs[3].c_struct(), _ptr(uhat), _ptr(ls.qx),
+                                                _ptr(ls.qy), _ptr(ls.qz), _ptr(ls.u), _ptr(ustar), C.byref(rep)))
+        return {f: getattr(rep, f) for f, _ in rep._fields_}
+
     # ---------------------------------------------------------------- K8
     def dirichlet_project(self, dm: DeviceMesh, g, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """dirichlet_project (global_system.cpp:58-70): (ndir, d2), row j = Dirichlet face j."""
