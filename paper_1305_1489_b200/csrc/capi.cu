@@ -866,13 +866,14 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     double* Ms = work;
     double* Ds = Ms + size_t(nelt) * t.nsym;
     double* fv = Ds + size_t(nelt) * t.nsym;
-    const size_t qsmem = size_t(3) * (t.nqp + 4) * kQuadLDB * sizeof(double);
-    const int qgrid = (nelt + kQuadEB - 1) / kQuadEB;
+    const int eb = quad_eb(t.nqp);
+    const size_t qsmem = quad_smem_bytes(eb, t.nqp);
+    const int qgrid = (nelt + eb - 1) / eb;
     const bool any_prog = kappa.kind == HDG_FIELD_PROGRAM || cf.kind == HDG_FIELD_PROGRAM || f.kind == HDG_FIELD_PROGRAM;
     CUfunction jfn = nullptr;
     if (c->jit && any_prog) {
       std::string err;
-      jfn = jit_quad_kernel(kappa, cf, f, &err);
+      jfn = jit_quad_kernel(kappa, cf, f, eb, &err);
       if (!jfn) c->jit_error = err;
     }
     stage_begin(c, 1);
@@ -884,12 +885,17 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
       void* args[] = {&nel, &nq, &nqp, &nsym, &nsymp, &d3, &d3p, &bary, &w, &As, &Af, &vol, &T, &V,
                       &sk, &sc, &sf, &Ms, &Ds, &fv};
       std::string err;
-      launched = launch_quad_jit(jfn, c->stream, qgrid, kQuadThreads, qsmem, args, &err);
+      launched = launch_quad_jit(jfn, c->stream, qgrid, eb * 8, qsmem, args, &err);
       if (!launched) c->jit_error = err;
     }
     if (!launched) {
-      CUDA_OK(cudaFuncSetAttribute(quad_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
-      quad_build_kernel<<<qgrid, kQuadThreads, qsmem, c->stream>>>(t, nelt, geo, fk, fc, ff, Ms, Ds, fv);
+      if (eb == 32) {
+        CUDA_OK(cudaFuncSetAttribute(quad_build_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
+        quad_build_kernel<32><<<qgrid, 256, qsmem, c->stream>>>(t, nelt, geo, fk, fc, ff, Ms, Ds, fv);
+      } else {
+        CUDA_OK(cudaFuncSetAttribute(quad_build_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
+        quad_build_kernel<16><<<qgrid, 128, qsmem, c->stream>>>(t, nelt, geo, fk, fc, ff, Ms, Ds, fv);
+      }
     }
     CUDA_OK(cudaGetLastError());
     stage_end(c, 1);

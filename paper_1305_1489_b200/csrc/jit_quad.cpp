@@ -26,13 +26,14 @@ namespace {
 
 const char* kQuadSource = R"CUDA(
 // JIT: K2 node build with inlined coefficient fields (see kernels_local.cuh quad_build_kernel).
-#define EB 16
+// EB (elements per CTA, a multiple of 8) is defined by the host before this text
 #define LDB (EB + 4)
+#define NTI (EB / 8)
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
-extern "C" __global__ void __launch_bounds__(128)
+extern "C" __global__ void __launch_bounds__(EB * 8)
 quad_build_jit(int nelt, int nq, int nqp, int nsym, int nsymp, int d3, int d3p,
                const double* __restrict__ bary, const double* __restrict__ wq,
                const double* __restrict__ Asym, const double* __restrict__ Af,
@@ -70,40 +71,54 @@ quad_build_jit(int nelt, int nq, int nqp, int nsym, int nsymp, int d3, int d3p,
     Bf[q * LDB + e] = bf;
   }
   __syncthreads();
+  // M and D share the table rows (Wsym): one task loads each A fragment once
+  // for both (2 NTI DMMA per load); D's 4 tau PP columns are one extra k-step.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int mts = nsymp / 8, mtf = d3p / 8;
-  const int ntasks = 2 * mts + mtf;
+  const int ntasks = mts + mtf;
   for (int task = warp; task < ntasks; task += nwarp) {
-    int which, mt;
-    if (task < mts) { which = 0; mt = task; }
-    else if (task < 2 * mts) { which = 1; mt = task - mts; }
-    else { which = 2; mt = task - 2 * mts; }
-    const double* A = which == 2 ? Af : Asym;
-    const int acols = which == 2 ? nqp : nqp + 4;
-    const int ksteps = which == 1 ? (nqp + 4) / 4 : nqp / 4;
-    const double* B = which == 0 ? Bk : (which == 1 ? Bc : Bf);
-    const double* Arow = A + (long(mt) * (acols / 4)) * 32 + lane;
-    double c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+    double cm[NTI][2], cd[NTI][2];
+#pragma unroll
+    for (int j = 0; j < NTI; ++j) cm[j][0] = cm[j][1] = cd[j][0] = cd[j][1] = 0.0;
+    const bool sym = task < mts;
+    const int mt = sym ? task : task - mts;
+    const double* Arow = sym ? Asym + (long(mt) * ((nqp + 4) / 4)) * 32 + lane
+                             : Af + (long(mt) * (nqp / 4)) * 32 + lane;
+    const double* B0 = sym ? Bk : Bf;
 #pragma unroll 4
-    for (int kk = 0; kk < ksteps; ++kk) {
+    for (int kk = 0; kk < nqp / 4; ++kk) {
       const double a = __ldg(Arow + kk * 32);
-      const double* brow = B + (kk * 4 + t) * LDB + g;
-      dmma(c00, c01, a, brow[0]);
-      dmma(c10, c11, a, brow[8]);
+      const int o = (kk * 4 + t) * LDB + g;
+#pragma unroll
+      for (int j = 0; j < NTI; ++j) dmma(cm[j][0], cm[j][1], a, B0[o + 8 * j]);
+      if (sym) {
+#pragma unroll
+        for (int j = 0; j < NTI; ++j) dmma(cd[j][0], cd[j][1], a, Bc[o + 8 * j]);
+      }
+    }
+    if (sym) {  // tau PP rows (k = nqp .. nqp+3): D only
+      const double a = __ldg(Arow + (nqp / 4) * 32);
+      const int o = (nqp + t) * LDB + g;
+#pragma unroll
+      for (int j = 0; j < NTI; ++j) dmma(cd[j][0], cd[j][1], a, Bc[o + 8 * j]);
     }
     const int r = mt * 8 + g;
-    const int lim = which == 2 ? d3 : nsym;
+    const int lim = sym ? nsym : d3;
     if (r < lim) {
-      double* out = which == 0 ? Msym : (which == 1 ? Dsym : fvec);
-      const int e0 = 2 * t;
-      const double v[4] = {c00, c01, c10, c11};
-      const int es[4] = {e0, e0 + 1, e0 + 8, e0 + 9};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const long K = K0 + es[i];
-        if (K < nelt) out[K * lim + r] = v[i];
-      }
+      for (int j = 0; j < NTI; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const long K = K0 + 8 * j + 2 * t + h;
+          if (K >= nelt) continue;
+          if (sym) {
+            Msym[K * lim + r] = cm[j][h];
+            Dsym[K * lim + r] = cd[j][h];
+          } else {
+            fvec[K * lim + r] = cm[j][h];
+          }
+        }
     }
   }
 }
@@ -192,8 +207,8 @@ std::string field_expr(const hdg_field& f, const char* sample_ptr) {
   return st.empty() ? "0.0" : st.back();
 }
 
-CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, std::string* err) {
-  std::string src = "#define FIELD_KAPPA " + field_expr(kap, "sk") + "\n#define FIELD_C " + field_expr(c, "sc") +
+CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, std::string* err) {
+  std::string src = "#define EB " + std::to_string(eb) + "\n#define FIELD_KAPPA " + field_expr(kap, "sk") + "\n#define FIELD_C " + field_expr(c, "sc") +
                     "\n#define FIELD_F " + field_expr(f, "sf") + "\n" + kQuadSource;
   Cache& C = cache();
   std::lock_guard<std::mutex> lock(C.mu);

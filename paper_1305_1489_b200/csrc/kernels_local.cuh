@@ -38,13 +38,18 @@ struct GeoDev {
 // (streamed from L2) as A:
 //   Msym = Wsym Bk,  Dsym = [Wsym | PPsym] [Bc; T],  fv = P^T Bf
 // (element_matrices.cpp:94-109 mass_matrices x2, :155-167 type_a, :84-92).
-constexpr int kQuadEB = 16;                 // elements per CTA (2 N-tiles)
-constexpr int kQuadLDB = kQuadEB + 4;       // conflict-free [q][e] stride
-constexpr int kQuadThreads = 128;
+// EB elements per CTA (EB / 8 N-tiles), EB * 8 threads; EB = 32 where the
+// three right-hand sides fit two CTAs per SM (each A fragment then feeds 8
+// DMMAs), else 16.
+constexpr int quad_ldb(int eb) { return eb + 4; }  // conflict-free [q][e] stride
+inline size_t quad_smem_bytes(int eb, int nqp) { return size_t(3) * (nqp + 4) * quad_ldb(eb) * sizeof(double); }
+inline int quad_eb(int nqp) { return quad_smem_bytes(32, nqp) <= 116 * 1024 ? 32 : 16; }
 
-__global__ void __launch_bounds__(kQuadThreads)
+template <int EB>
+__global__ void __launch_bounds__(EB * 8)
 quad_build_kernel(DevTab tab, int nelt, GeoDev geo, FieldDev kap, FieldDev cc, FieldDev ff,
                   double* __restrict__ Msym, double* __restrict__ Dsym, double* __restrict__ fvec) {
+  constexpr int kQuadEB = EB, kQuadLDB = quad_ldb(EB), NTI = EB / 8;
   extern __shared__ double smem[];
   const int nqp = tab.nqp, nq = tab.nq;
   const int rows = nqp + 4;
@@ -83,40 +88,54 @@ quad_build_kernel(DevTab tab, int nelt, GeoDev geo, FieldDev kap, FieldDev cc, F
   __syncthreads();
 
   // ---- phase 2: DMMA contraction over nodes
+  // M and D share the table rows (Wsym): one task loads each A fragment once
+  // for both (2 NTI DMMA per load); D's 4 tau PP columns are one extra k-step.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int mts = tab.nsymp / 8, mtf = tab.d3p / 8;
-  const int ntasks = 2 * mts + mtf;
+  const int ntasks = mts + mtf;
   for (int task = warp; task < ntasks; task += nwarp) {
-    int which, mt;
-    if (task < mts) { which = 0; mt = task; }
-    else if (task < 2 * mts) { which = 1; mt = task - mts; }
-    else { which = 2; mt = task - 2 * mts; }
-    const double* A = which == 2 ? tab.Af : tab.Asym;
-    const int acols = which == 2 ? nqp : nqp + 4;   // fragment table width
-    const int ksteps = which == 1 ? (nqp + 4) / 4 : nqp / 4;
-    const double* B = which == 0 ? Bk : (which == 1 ? Bc : Bf);
-    const double* Arow = A + (long(mt) * (acols / 4)) * 32 + lane;
-    double c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+    double cm[NTI][2], cd[NTI][2];
+#pragma unroll
+    for (int j = 0; j < NTI; ++j) cm[j][0] = cm[j][1] = cd[j][0] = cd[j][1] = 0.0;
+    const bool sym = task < mts;
+    const int mt = sym ? task : task - mts;
+    const double* Arow = sym ? tab.Asym + (long(mt) * ((nqp + 4) / 4)) * 32 + lane
+                             : tab.Af + (long(mt) * (nqp / 4)) * 32 + lane;
+    const double* B0 = sym ? Bk : Bf;
 #pragma unroll 4
-    for (int kk = 0; kk < ksteps; ++kk) {
+    for (int kk = 0; kk < nqp / 4; ++kk) {
       const double a = __ldg(Arow + kk * 32);
-      const double* brow = B + (kk * 4 + t) * kQuadLDB + g;
-      dmma(c00, c01, a, brow[0]);
-      dmma(c10, c11, a, brow[8]);
+      const int o = (kk * 4 + t) * kQuadLDB + g;
+#pragma unroll
+      for (int j = 0; j < NTI; ++j) dmma(cm[j][0], cm[j][1], a, B0[o + 8 * j]);
+      if (sym) {
+#pragma unroll
+        for (int j = 0; j < NTI; ++j) dmma(cd[j][0], cd[j][1], a, Bc[o + 8 * j]);
+      }
+    }
+    if (sym) {  // tau PP rows (k = nqp .. nqp+3): D only
+      const double a = __ldg(Arow + (nqp / 4) * 32);
+      const int o = (nqp + t) * kQuadLDB + g;
+#pragma unroll
+      for (int j = 0; j < NTI; ++j) dmma(cd[j][0], cd[j][1], a, Bc[o + 8 * j]);
     }
     const int r = mt * 8 + g;
-    const int lim = which == 2 ? tab.d3 : tab.nsym;
+    const int lim = sym ? tab.nsym : tab.d3;
     if (r < lim) {
-      double* out = which == 0 ? Msym : (which == 1 ? Dsym : fvec);
-      const int e0 = 2 * t;
-      const double v[4] = {c00, c01, c10, c11};
-      const int es[4] = {e0, e0 + 1, e0 + 8, e0 + 9};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const long K = K0 + es[i];
-        if (K < nelt) out[K * lim + r] = v[i];
-      }
+      for (int j = 0; j < NTI; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const long K = K0 + 8 * j + 2 * t + h;
+          if (K >= nelt) continue;
+          if (sym) {
+            Msym[K * lim + r] = cm[j][h];
+            Dsym[K * lim + r] = cd[j][h];
+          } else {
+            fvec[K * lim + r] = cm[j][h];
+          }
+        }
     }
   }
 }
