@@ -24,6 +24,7 @@
 #include "kernels_boundary.cuh"
 #include "kernels_solve.cuh"
 #include "kernels_errors.cuh"
+#include "kernels_post2.cuh"
 #include "jit_quad.hpp"
 #include "mesh_dev.hpp"
 
@@ -164,6 +165,16 @@ void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
     push(s);                                                     // 15
     push(w);                                                     // 16
   }
+  {  // Shat packed lower (column-major), 9 x d3(d3+1)/2: A operand of the postprocess S GEMM
+    const int ns = d3 * (d3 + 1) / 2;
+    std::vector<double> sp(size_t(9) * ns);
+    for (int hh = 0; hh < 9; ++hh) {
+      int p = 0;
+      for (int j = 0; j < d3; ++j)
+        for (int i = j; i < d3; ++i) sp[size_t(hh) * ns + p++] = h.Shat[hh][i + size_t(j) * d3];
+    }
+    push(sp);                                                    // 17
+  }
   CUDA_OK(cudaMalloc(&ts.buf, all.size() * sizeof(double)));
   CUDA_OK(cudaMemcpy(ts.buf, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice));
   ts.doubles = all.size();
@@ -175,6 +186,7 @@ void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
   t.Shat = b + off[5]; t.Wlm = b + off[6]; t.PP = b + off[7]; t.DD = b + off[8];
   t.tri_bary = b + off[9]; t.tri_w = b + off[10]; t.Pface = b + off[11]; t.Dperm = b + off[12];
   t.Asym = b + off[13]; t.Af = b + off[14]; t.ChatT = b + off[15]; t.WlmT = b + off[16];
+  t.ShatP = b + off[17];
   ts.ready = true;
 }
 
@@ -964,15 +976,28 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
     set_device(c);
     const DevTab& tp = c->tab[1].dev;
     const int n = tp.d3;
-    const int per_warp = n * (n + 1) + round_up(n, 8) + 3 * tp.nq + 32 + round_up(n, 8);
-    const int nw = warps_for(size_t(per_warp) * 8);
-    const size_t smem = size_t(nw) * per_warp * sizeof(double);
+    require(n - 1 <= 96, HDG_EINVAL, "postprocess degree too high (d3(k+1) <= 97)");
+    if (n <= 40) {  // k <= 3: CTA-batched DMMA version (kernels_post2.cuh)
+      const Post2Dims pd(n, tp.nq, c->tab[0].dev.d3);
+      const size_t smem2 = size_t(pd.total) * sizeof(double);
+      CUDA_OK(cudaFuncSetAttribute(postprocess2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+      const long need2 = (long(nelt) + kPost2EB - 1) / kPost2EB;
+      const int grid2 = int(std::min<long>(need2, long(c->sms) * 2));
+      stage_begin(c, 5);
+      postprocess2_kernel<<<grid2, kPost2Warps * 32, smem2, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, qx,
+                                                                        qy, qz, u, ustar);
+      CUDA_OK(cudaGetLastError());
+      stage_end(c, 5);
+      return;
+    }
+    const int per_warp = post_per_warp(n, tp.nq, c->tab[0].dev.d3);
+    const size_t smem = size_t(kPostWarps) * per_warp * sizeof(double);
     CUDA_OK(cudaFuncSetAttribute(postprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const long need = (long(nelt) + nw - 1) / nw;
-    const int grid = int(std::min<long>(need, long(c->sms) * 8));
+    const long need = (long(nelt) + kPostWarps - 1) / kPostWarps;
+    const int grid = int(std::min<long>(need, long(c->sms) * 16));
     stage_begin(c, 5);
-    postprocess_kernel<<<grid, nw * 32, smem, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, qx, qy, qz, u,
-                                                          ustar, per_warp);
+    postprocess_kernel<<<grid, kPostWarps * 32, smem, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, qx, qy, qz,
+                                                                  u, ustar, per_warp);
     CUDA_OK(cudaGetLastError());
     stage_end(c, 5);
   });

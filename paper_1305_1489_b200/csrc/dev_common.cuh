@@ -38,6 +38,7 @@ struct DevTab {
   const double* Af;     // fragment-ordered P^T: d3p x nqp
   const double* ChatT;  // 3 x (d3 x d3), Chat transposed
   const double* WlmT;   // 24 x (d3 x d2), Wlm transposed
+  const double* ShatP;  // 9 x d3(d3+1)/2, Shat packed lower (column-major)
 };
 
 // ------------------------------------------------------------------ fields

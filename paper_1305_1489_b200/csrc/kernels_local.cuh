@@ -161,9 +161,16 @@ __device__ bool team_cholesky(const Team<NW>& tm, double* A, int ld, int n, doub
   for (int j = 0; j < n; ++j) {
     // s_i = A(i,j) - sum_{k<j} L(i,k) L(j,k), i >= j
     for (int i = j + tm.tid; i < n; i += NT) {
-      double s = A[i + j * ld];
-      for (int k = 0; k < j; ++k) s -= A[i + k * ld] * A[j + k * ld];
-      scratch[i] = s;
+      double s0 = A[i + j * ld], s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 short chains
+      int k = 0;
+      for (; k + 3 < j; k += 4) {
+        s0 = fma(-A[i + k * ld], A[j + k * ld], s0);
+        s1 = fma(-A[i + (k + 1) * ld], A[j + (k + 1) * ld], s1);
+        s2 = fma(-A[i + (k + 2) * ld], A[j + (k + 2) * ld], s2);
+        s3 = fma(-A[i + (k + 3) * ld], A[j + (k + 3) * ld], s3);
+      }
+      for (; k < j; ++k) s0 = fma(-A[i + k * ld], A[j + k * ld], s0);
+      scratch[i] = (s0 + s1) + (s2 + s3);
     }
     tm.sync();
     const double d = scratch[j];

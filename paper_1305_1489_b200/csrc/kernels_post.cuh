@@ -23,90 +23,159 @@ __device__ __forceinline__ void elem_point(const GeoDev& geo, long K, int nelt, 
 //   row 0 <- [detB/sqrt6, 0, ...], rhs 0 <- detB/sqrt6 u_0   (mean constraint)
 // Because S's constant row/column vanish, the system splits into u*_0 = u_0 and
 // an SPD solve on the trailing block, done here by Cholesky.
-// Shared memory per warp: S (d31 x (d31+1)), R, G (3 nq), Q (3 nq), scratch.
-__global__ void postprocess_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap,
-                                   const double* __restrict__ qx, const double* __restrict__ qy,
-                                   const double* __restrict__ qz, const double* __restrict__ u,
-                                   double* __restrict__ ustar, int per_warp) {
+// One warp per element. Shared memory per warp: S lower (n x ldS, ldS odd so
+// row walks are conflict-free), G (3 nq), q/u coefficients, geometry. R is
+// accumulated lane-per-row with four independent chains; the triangular
+// solves keep the right-hand side in registers (lane owns rows lane, lane+32,
+// lane+64) and broadcast each solved entry by shuffle.
+constexpr int kPostWarps = 4;
+__host__ __device__ constexpr int post_ld(int n) { return n | 1; }
+__host__ __device__ constexpr int post_per_warp(int n, int nq, int d3k) {
+  return n * post_ld(n) + 3 * nq + 3 * d3k + 32 + 8;
+}
+
+__global__ void __launch_bounds__(kPostWarps * 32)
+postprocess_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, const double* __restrict__ qx,
+                   const double* __restrict__ qy, const double* __restrict__ qz, const double* __restrict__ u,
+                   double* __restrict__ ustar, int per_warp) {
   extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int n = tp.d3, nq = tp.nq, ld = n + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = tp.d3, nq = tp.nq, ld = post_ld(n);
   double* S = smem + long(warp) * per_warp;
-  double* R = S + n * ld;
-  double* G = R + round_up(n, 8);  // 3 x nq
-  double* sg = G + 3 * nq;         // geometry (32)
-  double* scr = sg + 32;           // n
+  double* G = S + n * ld;       // 3 x nq
+  double* qc = G + 3 * nq;      // 3 x d3k
+  double* sg = qc + 3 * d3k;    // geometry (32)
   const double* qs[3] = {qx, qy, qz};
-  Team<1> tm;
-  tm.id = 0;
-  tm.tid = lane;
-  tm.warp = 0;
-  tm.lane = lane;
-  for (long K = long(blockIdx.x) * nw + warp; K < nelt; K += long(gridDim.x) * nw) {
+  for (long K = long(blockIdx.x) * kPostWarps + warp; K < nelt; K += long(gridDim.x) * kPostWarps) {
     load_geo(geo, K, nelt, sg, lane, 32);
+    for (int idx = lane; idx < 3 * d3k; idx += 32) {
+      const int s = idx / d3k, i = idx - s * d3k;
+      qc[idx] = qs[s][K * d3k + i];
+    }
     __syncwarp();
     const double* a9 = sg + 1;
     const double detB = 6.0 * sg[0];
-    // S
+    // G_# at the nodes
+    for (int q = lane; q < nq; q += 32) {
+      double x, y, z;
+      elem_point(geo, K, nelt, __ldg(tp.bary + q), __ldg(tp.bary + nq + q), __ldg(tp.bary + 2 * nq + q),
+                 __ldg(tp.bary + 3 * nq + q), x, y, z);
+      const double kinv = 1.0 / eval_field(kap, x, y, z, q, K, nq);
+      double Qv[3] = {0.0, 0.0, 0.0};
+      for (int i = 0; i < d3k; ++i) {
+        const double p = __ldg(tp.P + long(i) * nq + q);
+        Qv[0] = fma(p, qc[i], Qv[0]);
+        Qv[1] = fma(p, qc[d3k + i], Qv[1]);
+        Qv[2] = fma(p, qc[2 * d3k + i], Qv[2]);
+      }
+      const double wk = kinv * __ldg(tp.w + q);
+#pragma unroll
+      for (int h = 0; h < 3; ++h) G[h * nq + q] = (Qv[0] * a9[h] + Qv[1] * a9[3 + h] + Qv[2] * a9[6 + h]) * wk;
+    }
+    __syncwarp();
+    // R(i), i >= 1 (row 0 is the mean constraint): full rounds lane per row
+    // (4 chains); the < 8 rows of a ragged last round are split over the
+    // lanes along the nodes and warp-reduced instead.
+    const double u0 = u[K * d3k];
+    double rr[3] = {0.0, 0.0, 0.0};  // rows 1 + lane + 32 j of the trailing system
+    const int m = n - 1;
+    const int rag = m & 31;                       // rows in the last round
+    const int lane_rounds = (m >> 5) + (rag >= 8 ? 1 : 0);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int i = 1 + lane + 32 * j;
+      if (j >= lane_rounds || i >= n) continue;
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+      for (int h = 0; h < 3; ++h) {
+        const double* Pd = tp.Pd + long(h) * nq * n + long(i) * nq;
+        const double* Gh = G + h * nq;
+        int q = 0;
+        for (; q + 3 < nq; q += 4) {
+          c0 = fma(__ldg(Pd + q), Gh[q], c0);
+          c1 = fma(__ldg(Pd + q + 1), Gh[q + 1], c1);
+          c2 = fma(__ldg(Pd + q + 2), Gh[q + 2], c2);
+          c3 = fma(__ldg(Pd + q + 3), Gh[q + 3], c3);
+        }
+        for (; q < nq; ++q) c0 = fma(__ldg(Pd + q), Gh[q], c0);
+      }
+      rr[j] = -(1.0 / 6.0) * ((c0 + c1) + (c2 + c3));
+    }
+    if (rag > 0 && rag < 8) {
+      const int jr = m >> 5;
+      for (int rr_i = 0; rr_i < rag; ++rr_i) {
+        const int i = 1 + 32 * jr + rr_i;
+        double c = 0.0;
+        for (int h = 0; h < 3; ++h) {
+          const double* Pd = tp.Pd + long(h) * nq * n + long(i) * nq;
+          for (int q = lane; q < nq; q += 32) c = fma(__ldg(Pd + q), G[h * nq + q], c);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == rr_i) rr[jr] = -(1.0 / 6.0) * c;
+      }
+    }
+    // S, lower triangle (stiffness_matrices, element_matrices.cpp:258-280)
     double gm[9];
 #pragma unroll
     for (int p = 0; p < 3; ++p)
 #pragma unroll
       for (int r = 0; r < 3; ++r)
         gm[3 * p + r] = (a9[p] * a9[r] + a9[3 + p] * a9[3 + r] + a9[6 + p] * a9[6 + r]) / detB;
-    for (int idx = lane; idx < n * n; idx += 32) {
-      const int i = idx % n, j = idx / n;
-      double s = 0.0;
+    for (int j = 0; j < n; ++j)
+      for (int i = j + lane; i < n; i += 32) {
+        const long idx = i + long(j) * n;
+        double v = 0.0;
 #pragma unroll
-      for (int h = 0; h < 9; ++h) s += __ldg(tp.Shat + long(h) * n * n + idx) * gm[h];
-      S[i + j * ld] = s;
-    }
-    // G_# at nodes
-    for (int q = lane; q < nq; q += 32) {
-      double x, y, z;
-      elem_point(geo, K, nelt, __ldg(tp.bary + q), __ldg(tp.bary + nq + q), __ldg(tp.bary + 2 * nq + q),
-                 __ldg(tp.bary + 3 * nq + q), x, y, z);
-      const double kinv = 1.0 / eval_field(kap, x, y, z, q, K, nq);
-      double Qv[3];
-      for (int s = 0; s < 3; ++s) {
-        double acc = 0.0;
-        for (int i = 0; i < d3k; ++i) acc += __ldg(tp.P + long(i) * nq + q) * qs[s][K * d3k + i];
-        Qv[s] = acc * kinv;
+        for (int h = 0; h < 9; ++h) v = fma(__ldg(tp.Shat + long(h) * n * n + idx), gm[h], v);
+        S[i + j * ld] = v;
       }
-      for (int h = 0; h < 3; ++h) G[h * nq + q] = (Qv[0] * a9[h] + Qv[1] * a9[3 + h] + Qv[2] * a9[6 + h]) * __ldg(tp.w + q);
-    }
     __syncwarp();
-    for (int i = lane; i < n; i += 32) {
-      double acc = 0.0;
-      for (int h = 0; h < 3; ++h) {
-        const double* Pd = tp.Pd + long(h) * nq * n + long(i) * nq;
-        for (int q = 0; q < nq; ++q) acc += __ldg(Pd + q) * G[h * nq + q];
-      }
-      R[i] = -(1.0 / 6.0) * acc;
-    }
-    __syncwarp();
-    const double u0 = u[K * d3k];
     // trailing SPD block: S[1:,1:] x = R[1:] - S[1:,0] u0
-    for (int i = 1 + lane; i < n; i += 32) R[i] -= S[i] * u0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int i = 1 + lane + 32 * j;
+      if (i < n) rr[j] -= S[i] * u0;
+    }
+    Team<1> tm;
+    tm.id = 0;
+    tm.tid = lane;
+    tm.warp = 0;
+    tm.lane = lane;
+    double* L = S + 1 + ld;  // trailing block, (n-1) x (n-1), stride ld
+    team_cholesky(tm, L, ld, m, G);  // scratch: G is dead after R
     __syncwarp();
-    team_cholesky(tm, S + 1 + ld, ld, n - 1, scr);
-    // forward: L y = R[1:]
-    for (int i = 1; i < n; ++i) {
-      double part = 0.0;
-      for (int k = 1 + lane; k < i; k += 32) part += S[i + k * ld] * R[k];
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0) R[i] = (R[i] - part) / S[i + i * ld];
-      __syncwarp();
+    // forward L y = r: column sweep, y_k broadcast from its owner lane
+    for (int k = 0; k < m; ++k) {
+      const int owner = k & 31, slot = k >> 5;
+      double rk = slot == 0 ? rr[0] : (slot == 1 ? rr[1] : rr[2]);
+      rk = __shfl_sync(0xffffffffu, rk, owner);
+      const double yk = rk / L[k + k * ld];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int i = lane + 32 * j;
+        if (i == k) rr[j] = yk;
+        else if (i > k && i < m) rr[j] = fma(-L[i + k * ld], yk, rr[j]);
+      }
     }
-    // backward: L^T x = y
-    for (int i = n - 1; i >= 1; --i) {
-      double part = 0.0;
-      for (int k = i + 1 + lane; k < n; k += 32) part += S[k + i * ld] * R[k];
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0) R[i] = (R[i] - part) / S[i + i * ld];
-      __syncwarp();
+    // backward L^T x = y: row k of L^T is column k of L
+    for (int k = m - 1; k >= 0; --k) {
+      const int owner = k & 31, slot = k >> 5;
+      double yk = slot == 0 ? rr[0] : (slot == 1 ? rr[1] : rr[2]);
+      yk = __shfl_sync(0xffffffffu, yk, owner);
+      const double xk = yk / L[k + k * ld];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int i = lane + 32 * j;
+        if (i == k) rr[j] = xk;
+        else if (i < k) rr[j] = fma(-L[k + i * ld], xk, rr[j]);
+      }
     }
-    for (int i = lane; i < n; i += 32) ustar[K * n + i] = i == 0 ? u0 : R[i];
+    if (lane == 0) ustar[K * n] = u0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int i = lane + 32 * j;
+      if (i < m) ustar[K * n + 1 + i] = rr[j];
+    }
     __syncwarp();
   }
 }

@@ -176,9 +176,9 @@ def test_scatter_pattern_and_values(k, bc):
 
 
 # ------------------------------------------------ a11: postprocess
-@pytest.mark.parametrize("k", [1, 3])
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 4])
 def test_postprocess(k):
-    mesh = HostMesh.box(2)
+    mesh = HostMesh.box(2, 1, 3) if k % 2 else HostMesh.box(2)  # 36 tets: a partial 8-element batch
     em = oracle_mesh(mesh)
     eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
     eng.set_postprocess_rule()
