@@ -23,7 +23,8 @@ namespace hdgb {
 
 constexpr int kPost2EB = 8;     // elements per CTA (one DMMA N-tile)
 constexpr int kPost2Warps = 8;  // one warp per element in the solve phase
-constexpr int kPost2LDG = kPost2EB + 4;
+constexpr int kPost2LDG = kPost2EB;  // G rows [q][e]: B-fragment reads are conflict-free at 8
+constexpr int kPost2MaxNS = 40 * 41 / 2;
 
 struct Post2Dims {
   int n, nq, nq4, d3k, npad, ns, nsp;
@@ -52,7 +53,15 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
                     const double* __restrict__ qy, const double* __restrict__ qz, const double* __restrict__ u,
                     double* __restrict__ ustar) {
   extern __shared__ double psm[];
+  __shared__ unsigned char pk_i[kPost2MaxNS], pk_j[kPost2MaxNS];  // packed index -> (row, col)
+  __shared__ double invd[kPost2Warps][40];                         // 1 / L(k,k) per warp
   const Post2Dims dm(tp.d3, tp.nq, d3k);
+  for (int j = threadIdx.x; j < tp.d3; j += blockDim.x)
+    for (int i = j; i < tp.d3; ++i) {
+      const int p = pk_lower(i, j, tp.d3);
+      pk_i[p] = static_cast<unsigned char>(i);
+      pk_j[p] = static_cast<unsigned char>(j);
+    }
   const int n = dm.n, nq = dm.nq, nq4 = dm.nq4, npad = dm.npad, ns = dm.ns;
   double* verts = psm + dm.off_verts;
   double* sg = psm + dm.off_sg;
@@ -198,22 +207,23 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
           const int i = 1 + lane + 32 * j;
           if (i < n) rr[j] = R[i * kPost2EB + e] - S[pk_lower(i, 0, n)] * u0;
         }
-        // right-looking Cholesky on packed storage (full indices i, j >= 1)
+        // right-looking Cholesky on packed storage (full indices i, j >= 1):
+        // the trailing triangle of columns > k is one contiguous packed range,
+        // so its rank-1 update runs entry-parallel over all 32 lanes
         for (int k = 1; k < n; ++k) {
           const int ck = pk_lower(k, k, n);
           const double lkk = sqrt(S[ck]);
           const double inv = 1.0 / lkk;
           __syncwarp();
-          if (lane == 0) S[ck] = lkk;
+          if (lane == 0) {
+            S[ck] = lkk;
+            invd[warp][k - 1] = inv;
+          }
           for (int i = k + 1 + lane; i < n; i += 32) S[ck + (i - k)] *= inv;
           __syncwarp();
-          for (int i = k + 1 + lane; i < n; i += 32) {
-            const double lik = S[ck + (i - k)];
-            int cj = pk_lower(k + 1, k + 1, n);
-            for (int j = k + 1; j <= i; ++j) {
-              S[cj + (i - j)] = fma(-lik, S[ck + (j - k)], S[cj + (i - j)]);
-              cj += n - j;
-            }
+          for (int p = ck + (n - k) + lane; p < ns; p += 32) {
+            const int i = pk_i[p], j = pk_j[p];
+            S[p] = fma(-S[ck + (i - k)], S[ck + (j - k)], S[p]);
           }
           __syncwarp();
         }
@@ -223,7 +233,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
           double rk = slot == 0 ? rr[0] : rr[1];
           rk = __shfl_sync(0xffffffffu, rk, owner);
           const int ck = pk_lower(k + 1, k + 1, n);
-          const double yk = rk / S[ck];
+          const double yk = rk * invd[warp][k];
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int i = lane + 32 * j;
@@ -235,7 +245,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
           const int owner = k & 31, slot = k >> 5;
           double yk = slot == 0 ? rr[0] : rr[1];
           yk = __shfl_sync(0xffffffffu, yk, owner);
-          const double xk = yk / S[pk_lower(k + 1, k + 1, n)];
+          const double xk = yk * invd[warp][k];
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int i = lane + 32 * j;
