@@ -361,23 +361,68 @@ def run_ours(args):
     # ---------------------------------------------------------------- e2e
     # Through the public API with HOST buffers: H2D of the step's inputs (mesh
     # arrays + lambda, pinned), the step, D2H of its results (C, Cf, q, u).
-    host_in = [t.cpu().pin_memory() for t in (dm.coords, dm.elements, dm.faces, dm.facebyele, uhat)]
-    dev_in = [dm.coords, dm.elements, dm.faces, dm.facebyele, uhat]
-    outs = [cs.C, cs.Cf, ls.qx, ls.qy, ls.qz, ls.u] + ([ustar] if cfg.postprocess else [])
-    host_out = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
-    h2d = sum(t.numel() * t.element_size() for t in host_in)
-    d2h = sum(t.numel() * t.element_size() for t in host_out)
+    # The element range is processed in E2E_CHUNKS contiguous chunks (each its
+    # own DeviceMesh/Geometry; the outputs are contiguous slices of the global
+    # Batch3/column-major arrays), and the D2H of chunk i runs on a copy stream
+    # while chunk i+1 computes: the step is PCIe-bound (2.7 GB of C at C2), so
+    # this overlap is the end-to-end schedule a user of the API would run.
+    from paper_1305_1489_b200.engine import CondensedSystem, DeviceMesh, Geometry
+    E2E_CHUNKS = 4
+    bounds = [round(i * nelt / E2E_CHUNKS) for i in range(E2E_CHUNKS + 1)]
+    m = 4 * d2
+    nf = dims["factors"]
+    host_shared = [t.cpu().pin_memory() for t in (dm.coords, dm.faces, uhat)]
+    dev_shared = [dm.coords, dm.faces, uhat]
+    host_el = dm.elements.cpu()
+    host_fb = dm.facebyele.cpu()
+    chunks = []
+    for i in range(E2E_CHUNKS):
+        k0, k1 = bounds[i], bounds[i + 1]
+        nc = k1 - k0
+        h_el = host_el[:, k0:k1].contiguous().pin_memory()
+        h_fb = host_fb[:, k0:k1].contiguous().pin_memory()
+        dmc = DeviceMesh(dm.nver, nc, dm.nfc, dm.coords, torch.empty_like(h_el, device=dev), dm.faces,
+                         torch.empty_like(h_fb, device=dev), dm.facetype, dm.ndir, dm.nneu)
+        gc = eng.geometry(dmc, 1.0)
+        csc = CondensedSystem(cs.C[k0 * m * m:k1 * m * m], cs.Cf[k0 * m:k1 * m], cs.factors[k0 * nf:k1 * nf], m)
+        lsc = LocalSolution(ls.qx[k0:k1], ls.qy[k0:k1], ls.qz[k0:k1], ls.u[k0:k1])
+        usc = ustar[k0:k1] if cfg.postprocess else None
+        outs_c = [csc.C, csc.Cf, lsc.qx, lsc.qy, lsc.qz, lsc.u] + ([usc] if cfg.postprocess else [])
+        host_c = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs_c]
+        chunks.append(dict(h_in=[h_el, h_fb], d_in=[dmc.elements, dmc.facebyele], dm=dmc, g=gc, cs=csc,
+                           ls=lsc, us=usc, outs=outs_c, host=host_c, work=eng.work_buffer(nc),
+                           ev=torch.cuda.Event()))
+    h2d = sum(t.numel() * t.element_size() for t in host_shared) + \
+        sum(t.numel() * t.element_size() for c in chunks for t in c["h_in"])
+    d2h = sum(t.numel() * t.element_size() for c in chunks for t in c["host"])
+    copy_stream = torch.cuda.Stream(dev)
     e2e_steps = max(1, min(args.steps, 5))
+
+    def e2e_step():
+        for h, d in zip(host_shared, dev_shared):
+            d.copy_(h, non_blocking=True)
+        for c in chunks:
+            for h, d in zip(c["h_in"], c["d_in"]):
+                d.copy_(h, non_blocking=True)
+            eng.geometry(c["dm"], tau, out=c["g"])
+            eng.build_condense(c["g"], kap, cc, ff, out=c["cs"], work=c["work"], check=False)
+            eng.recover(c["g"], c["dm"], c["cs"], uhat, out=c["ls"])
+            if cfg.postprocess:
+                eng.postprocess_star(c["g"], kap, c["ls"], out=c["us"])
+            c["ev"].record(stream)
+            copy_stream.wait_event(c["ev"])
+            with torch.cuda.stream(copy_stream):
+                for h, d in zip(c["host"], c["outs"]):
+                    h.copy_(d, non_blocking=True)
+        stream.wait_stream(copy_stream)
+
     with torch.cuda.stream(stream):
+        e2e_step()  # warm-up (chunk-sized work buffers, JIT cache)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(e2e_steps):
-            for h, d in zip(host_in, dev_in):
-                d.copy_(h, non_blocking=True)
-            step()
-            for h, d in zip(host_out, outs):
-                h.copy_(d, non_blocking=True)
+            e2e_step()
         e1.record(stream)
         e1.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
@@ -427,8 +472,8 @@ def run_ours(args):
         "roofline": roof,
         "kernels_ms": kern,
         "e2e": {"value": world * nelt / (e2e_ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                "path": "pinned host mesh+lambda -> C ABI step -> pinned host C, Cf, q, u"},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "chunks": E2E_CHUNKS,
+                "path": "pinned host mesh+lambda -> C ABI step in 4 element chunks, D2H of chunk i overlapped with chunk i+1 -> pinned host C, Cf, q, u"},
         "scatter": scatter_info,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
