@@ -393,21 +393,28 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 
     PHASE_MARK(batch, 3);
     // ---- P4: Vs = Si V (into Zb) | fs = Si f | next batch's geometry + columns
-    for (int task = warp; task < nb * NTM * MT; task += NWT) {
-      const int e = task / (NTM * MT), sub = task % (NTM * MT);
-      const int nt = sub / MT, m = sub % MT;
+    for (int task = warp; task < nb * NTM; task += NWT) {  // one column strip per task:
+      const int e = task / NTM, nt = task % NTM;           // the V fragment feeds MT chains
       const double* S = Sb(e);
       const double* V = Vb(e);
-      double a0 = 0, a1 = 0;
+      double acc[MT][2];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
       const int c = nt * 8 + g;
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
         const int k = kk * 4 + t;
-        dmma(a0, a1, S[(m * 8 + g) + k * LD], V[k + c * LD]);
+        const double b = V[k + c * LD];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], S[(m * 8 + g) + k * LD], b);
       }
-      const int r = m * 8 + g, c0 = nt * 8 + 2 * t;
-      Yb(e)[r + c0 * LD] = a0;      // Vs (R_# is dead)
-      Yb(e)[r + (c0 + 1) * LD] = a1;
+      const int c0 = nt * 8 + 2 * t;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int r = m * 8 + g;
+        Yb(e)[r + c0 * LD] = acc[m][0];  // Vs (R_# is dead)
+        Yb(e)[r + (c0 + 1) * LD] = acc[m][1];
+      }
     }
     for (int idx = threadIdx.x; idx < nb * D3; idx += NT) {
       const int e = idx / D3, r = idx % D3;
