@@ -381,8 +381,8 @@ def run_ours(args):
         nc = k1 - k0
         h_el = host_el[:, k0:k1].contiguous().pin_memory()
         h_fb = host_fb[:, k0:k1].contiguous().pin_memory()
-        dmc = DeviceMesh(dm.nver, nc, dm.nfc, dm.coords, torch.empty_like(h_el, device=dev), dm.faces,
-                         torch.empty_like(h_fb, device=dev), dm.facetype, dm.ndir, dm.nneu)
+        dmc = DeviceMesh(dm.nver, nc, dm.nfc, dm.coords, dm.elements[:, k0:k1].contiguous(), dm.faces,
+                         dm.facebyele[:, k0:k1].contiguous(), dm.facetype, dm.ndir, dm.nneu)
         gc = eng.geometry(dmc, 1.0)
         csc = CondensedSystem(cs.C[k0 * m * m:k1 * m * m], cs.Cf[k0 * m:k1 * m], cs.factors[k0 * nf:k1 * nf], m)
         lsc = LocalSolution(ls.qx[k0:k1], ls.qy[k0:k1], ls.qz[k0:k1], ls.u[k0:k1])

@@ -897,7 +897,7 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
       void* args[] = {&nel, &nq, &nqp, &nsym, &nsymp, &d3, &d3p, &bary, &w, &As, &Af, &vol, &T, &V,
                       &sk, &sc, &sf, &Ms, &Ds, &fv};
       std::string err;
-      launched = launch_quad_jit(jfn, c->stream, qgrid, eb * 8, qsmem, args, &err);
+      launched = launch_quad_jit(jfn, c->stream, qgrid, 256, qsmem, args, &err);
       if (!launched) c->jit_error = err;
     }
     if (!launched) {
@@ -906,7 +906,7 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
         quad_build_kernel<32><<<qgrid, 256, qsmem, c->stream>>>(t, nelt, geo, fk, fc, ff, Ms, Ds, fv);
       } else {
         CUDA_OK(cudaFuncSetAttribute(quad_build_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
-        quad_build_kernel<16><<<qgrid, 128, qsmem, c->stream>>>(t, nelt, geo, fk, fc, ff, Ms, Ds, fv);
+        quad_build_kernel<16><<<qgrid, 256, qsmem, c->stream>>>(t, nelt, geo, fk, fc, ff, Ms, Ds, fv);
       }
     }
     CUDA_OK(cudaGetLastError());

@@ -33,7 +33,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
-extern "C" __global__ void __launch_bounds__(EB * 8)
+extern "C" __global__ void __launch_bounds__(256)
 quad_build_jit(int nelt, int nq, int nqp, int nsym, int nsymp, int d3, int d3p,
                const double* __restrict__ bary, const double* __restrict__ wq,
                const double* __restrict__ Asym, const double* __restrict__ Af,

@@ -38,7 +38,7 @@ struct GeoDev {
 // (streamed from L2) as A:
 //   Msym = Wsym Bk,  Dsym = [Wsym | PPsym] [Bc; T],  fv = P^T Bf
 // (element_matrices.cpp:94-109 mass_matrices x2, :155-167 type_a, :84-92).
-// EB elements per CTA (EB / 8 N-tiles), EB * 8 threads; EB = 32 where the
+// EB elements per CTA (EB / 8 N-tiles), 256 threads; EB = 32 where the
 // three right-hand sides fit two CTAs per SM (each A fragment then feeds 8
 // DMMAs), else 16.
 constexpr int quad_ldb(int eb) { return eb + 4; }  // conflict-free [q][e] stride
@@ -46,7 +46,7 @@ inline size_t quad_smem_bytes(int eb, int nqp) { return size_t(3) * (nqp + 4) * 
 inline int quad_eb(int nqp) { return quad_smem_bytes(32, nqp) <= 116 * 1024 ? 32 : 16; }
 
 template <int EB>
-__global__ void __launch_bounds__(EB * 8)
+__global__ void __launch_bounds__(256)
 quad_build_kernel(DevTab tab, int nelt, GeoDev geo, FieldDev kap, FieldDev cc, FieldDev ff,
                   double* __restrict__ Msym, double* __restrict__ Dsym, double* __restrict__ fvec) {
   constexpr int kQuadEB = EB, kQuadLDB = quad_ldb(EB), NTI = EB / 8;
