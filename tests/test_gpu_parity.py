@@ -306,17 +306,23 @@ def test_c1_full_pipeline_matches_oracle():
 
 
 # ---------------------------------------- full-size sampled parity (C2, C3)
-@pytest.mark.parametrize("cfg_name", ["C2", "C3"])
+@pytest.mark.parametrize("cfg_name", ["C2", "C3", "C4", "C5"])
 def test_full_size_sampled_elements(cfg_name):
     """Full BASELINE mesh on the GPU; ~40 scattered elements re-solved by the
-    oracle on a disjoint sub-mesh with the same face parametrisations."""
+    oracle on a disjoint sub-mesh with the same face parametrisations (C4 with
+    its upwind tau, C5 including the P_{k+1} postprocess)."""
     cfg = CONFIGS[cfg_name]
     prob = cfg.problem
     mesh = HostMesh.box(cfg.n, bc=prob.bc, perturb=cfg.perturb, seed=cfg.seed)
     k = cfg.k
-    eng, dm, g, cs = gpu_pipeline(mesh, k, prob.kappa, prob.c, prob.f, tau=cfg.tau)
-    d2 = dim2(k)
+    eng = Engine(0)
     eng.set_degree(k)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 1.0)
+    tau = eng.upwind_tau(g, cfg.upwind_beta) if cfg.upwind_beta else cfg.tau
+    g = eng.geometry(dm, tau)
+    cs = eng.build_condense(g, prob.kappa, prob.c, prob.f)
+    d2 = dim2(k)
     # lambda = face projection of u (SURVEY §8(d)); here any smooth data works
     uhat = torch.sin(torch.arange(dm.nfc * d2, dtype=torch.float64, device="cuda") * 0.013)
     ls = eng.recover(g, dm, cs, uhat)
@@ -330,15 +336,23 @@ def test_full_size_sampled_elements(cfg_name):
             chosen.append(K)
             used.update(fb[K])
     sub = submesh(mesh, chosen)
-    _, _, lb, C, Cf = oracle_condense(sub, k, prob.kappa, prob.c, prob.f, cfg.tau)
-    Cg = np_(cs.C_slices())[chosen]
-    assert max_slice_relerr(Cg, C) < TOL
-    assert max_slice_relerr(np_(cs.Cf_cols())[chosen], Cf.T) < TOL
+    idx = torch.tensor(chosen, device="cuda")
+    tau_sub = np_(tau)[:, chosen].T.copy() if isinstance(tau, torch.Tensor) else cfg.tau
+    _, _, lb, C, Cf = oracle_condense(sub, k, prob.kappa, prob.c, prob.f, tau_sub)
+    assert max_slice_relerr(np_(cs.C_slices()[idx]), C) < TOL
+    assert max_slice_relerr(np_(cs.Cf_cols()[idx]), Cf.T) < TOL
     uh = np_(uhat)
     lam = np.stack([np.concatenate([uh[f * d2:(f + 1) * d2] for f in fb[K]]) for K in chosen], axis=1)
     qx, qy, qz, u = core.local_recover(lb, np.asfortranarray(lam), 4)
-    assert max_slice_relerr(np_(ls.u)[chosen], u.T) < TOL
-    assert max_slice_relerr(np_(ls.qz)[chosen], qz.T) < TOL
+    assert max_slice_relerr(np_(ls.u[idx]), u.T) < TOL
+    assert max_slice_relerr(np_(ls.qz[idx]), qz.T) < TOL
+    if cfg.postprocess:
+        eng.set_postprocess_rule()
+        us = eng.postprocess_star(g, prob.kappa, ls)
+        t1 = core.tables(k + 1, 2 * (k + 1) + 2, 2 * k + 2)
+        want = core.postprocess_star(sub, t1, field(prob.kappa),
+                                     *(np.asfortranarray(np_(x[idx]).T) for x in (ls.qx, ls.qy, ls.qz, ls.u)))
+        assert max_slice_relerr(np_(us[idx]), want.T) < TOL
 
 
 def test_jit_and_interpreter_agree():
