@@ -322,6 +322,12 @@ int hdg_b200_set_variant(hdg_ctx* ctx, int variant);
 /* k = 1..3 recovery kernel: 3 = TMA-streamed cache records (default), 2 = one warp
  * per element with direct loads (equivalent; kept for comparison). */
 int hdg_b200_set_recover_variant(hdg_ctx* ctx, int variant);
+/* BDM variant (bdm_blocks, local_solver.cpp:65-69): the scalar space of the
+ * local solve is truncated to its first d3 - d2 modes (P_{k-1}) and tau is
+ * ignored (tauPP, tauDP and tauDD dropped); build_condense then returns the
+ * condensed system of the BDM blocks and recover returns u zero-padded to
+ * d3, as the reference. k = 1..3 (k = 0 is rejected as in the reference). */
+int hdg_b200_set_bdm(hdg_ctx* ctx, int enabled);
 const char* hdg_b200_jit_status(const hdg_ctx* ctx);
 
 /* Block until the context's stream is idle and report any deferred error. */

@@ -109,6 +109,7 @@ _SIGS = {
     "hdg_b200_set_jit": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_variant": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_recover_variant": (C.c_int, [P, C.c_int]),
+    "hdg_b200_set_bdm": (C.c_int, [P, C.c_int]),
     "hdg_b200_expand_device": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, P, C.c_int, P, P, P, P,
                                          C.POINTER(C.c_int)]),
     "hdg_b200_pattern_device": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P, C.POINTER(C.c_int)]),

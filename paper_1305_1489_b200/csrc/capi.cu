@@ -180,7 +180,7 @@ void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
   ts.doubles = all.size();
   DevTab& t = ts.dev;
   t.k = k; t.d3 = d3; t.d2 = d2; t.nq = nq; t.nqd = nqd; t.nqp = nqp;
-  t.nsym = nsym; t.nsymp = nsymp; t.d3p = d3p;
+  t.nsym = nsym; t.nsymp = nsymp; t.d3p = d3p; t.nu = d3;
   const double* b = ts.buf;
   t.bary = b + off[0]; t.w = b + off[1]; t.P = b + off[2]; t.Pd = b + off[3]; t.Chat = b + off[4];
   t.Shat = b + off[5]; t.Wlm = b + off[6]; t.PP = b + off[7]; t.DD = b + off[8];
@@ -252,6 +252,9 @@ struct hdg_ctx {
   int* h_status = nullptr;
   bool timing = false;
   bool jit = true;          // NVRTC-specialised K2 for program fields
+  bool bdm = false;         // bdm_blocks variant (hdg_b200_set_bdm)
+  double* d_zero_T = nullptr;  // tau = 0 for the BDM variant
+  long zero_T_len = 0;
   int recover_variant = 3;  // k = 1..3: 3 = TMA-streamed cache, 2 = warp per element
   int condense_variant = 3; // k = 2, 3: 4 = element-batched tasks, 3 = CTA-batched, 2 = per-element teams
   std::string jit_error;    // last JIT failure (kernel then runs interpreted)
@@ -278,7 +281,6 @@ void stage_end(hdg_ctx* c, int s) {
 void* ctx_work(hdg_ctx* c, size_t bytes) {
   if (bytes > c->work_bytes) {
     if (c->work) cudaFree(c->work);
-  if (c->d_adj) cudaFree(c->d_adj);
     c->work = nullptr;
     CUDA_OK(cudaMalloc(&c->work, bytes));
     c->work_bytes = bytes;
@@ -315,8 +317,9 @@ void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, co
   require(occ > 0, HDG_ECUDA, "condense kernel does not fit on an SM");
   const long need = (long(nelt) + Cg::EPB - 1) / Cg::EPB;
   const int grid = int(std::min<long>(need, long(c->sms) * occ));
-  kern<<<grid, Cg::NW * 32 * Cg::EPB, smem, c->stream>>>(c->tab[0].dev, nelt, geo, Ms, Ds, fv, C, Cf, F,
-                                                          c->d_bad);
+  DevTab td = c->tab[0].dev;
+  if (c->bdm) td.nu = td.d3 - td.d2;  // bdm_blocks (local_solver.cpp:65-69): u truncated to P_{k-1}
+  kern<<<grid, Cg::NW * 32 * Cg::EPB, smem, c->stream>>>(td, nelt, geo, Ms, Ds, fv, C, Cf, F, c->d_bad);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -325,6 +328,10 @@ template <int K_>
 void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, const double* Ds,
                      const double* fv, double* C, double* Cf, double* F) {
   if constexpr (K_ == 2 || K_ == 3) {
+    if (c->bdm) {  // the u-space truncation is implemented in the v3 kernel
+      launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+      return;
+    }
     if (c->condense_variant == 2)
       launch_condense_impl<C2Dims<K_>, C2Cfg<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
     else if (c->condense_variant == 3)
@@ -721,6 +728,7 @@ void hdg_b200_destroy(hdg_ctx* c) {
     if (t.buf) cudaFree(t.buf);
   if (c->work) cudaFree(c->work);
   if (c->d_adj) cudaFree(c->d_adj);
+  if (c->d_zero_T) cudaFree(c->d_zero_T);
   if (c->d_bad) cudaFree(c->d_bad);
   if (c->h_bad) cudaFreeHost(c->h_bad);
   if (c->d_status) cudaFree(c->d_status);
@@ -874,6 +882,19 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     const FieldDev fk = to_dev(kappa, "kappa"), fc = to_dev(cf, "c"), ff = to_dev(f, "f");
     set_device(c);
     const DevTab& t = c->tab[0].dev;
+    GeoDev geo_b = geo;
+    if (c->bdm) {  // bdm_blocks ignores tau entirely (local_solver.cpp:36-43): run with T = 0
+      require(t.k >= 1, HDG_EINVAL, "the BDM variant needs degree k >= 1");
+      require(t.k <= 3, HDG_EINVAL, "the BDM variant is built for k = 1..3");
+      if (c->zero_T_len < 4L * nelt) {
+        if (c->d_zero_T) cudaFree(c->d_zero_T);
+        c->d_zero_T = nullptr;
+        CUDA_OK(cudaMalloc(&c->d_zero_T, sizeof(double) * 4 * size_t(nelt)));
+        c->zero_T_len = 4L * nelt;
+      }
+      CUDA_OK(cudaMemsetAsync(c->d_zero_T, 0, sizeof(double) * 4 * size_t(nelt), c->stream));
+      geo_b.T = c->d_zero_T;
+    }
     double* work = static_cast<double*>(d_work ? d_work : ctx_work(c, work_doubles(t, nelt) * sizeof(double)));
     double* Ms = work;
     double* Ds = Ms + size_t(nelt) * t.nsym;
@@ -892,8 +913,8 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     bool launched = false;
     if (jfn) {
       int nel = nelt, nq = t.nq, nqp = t.nqp, nsym = t.nsym, nsymp = t.nsymp, d3 = t.d3, d3p = t.d3p;
-      const double *bary = t.bary, *w = t.w, *As = t.Asym, *Af = t.Af, *vol = geo.volume, *T = geo.T,
-                   *V = geo.verts, *sk = kappa.samples, *sc = cf.samples, *sf = f.samples;
+      const double *bary = t.bary, *w = t.w, *As = t.Asym, *Af = t.Af, *vol = geo_b.volume, *T = geo_b.T,
+                   *V = geo_b.verts, *sk = kappa.samples, *sc = cf.samples, *sf = f.samples;
       void* args[] = {&nel, &nq, &nqp, &nsym, &nsymp, &d3, &d3p, &bary, &w, &As, &Af, &vol, &T, &V,
                       &sk, &sc, &sf, &Ms, &Ds, &fv};
       std::string err;
@@ -903,17 +924,17 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     if (!launched) {
       if (eb == 32) {
         CUDA_OK(cudaFuncSetAttribute(quad_build_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
-        quad_build_kernel<32><<<qgrid, 256, qsmem, c->stream>>>(t, nelt, geo, fk, fc, ff, Ms, Ds, fv);
+        quad_build_kernel<32><<<qgrid, 256, qsmem, c->stream>>>(t, nelt, geo_b, fk, fc, ff, Ms, Ds, fv);
       } else {
         CUDA_OK(cudaFuncSetAttribute(quad_build_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qsmem)));
-        quad_build_kernel<16><<<qgrid, 256, qsmem, c->stream>>>(t, nelt, geo, fk, fc, ff, Ms, Ds, fv);
+        quad_build_kernel<16><<<qgrid, 256, qsmem, c->stream>>>(t, nelt, geo_b, fk, fc, ff, Ms, Ds, fv);
       }
     }
     CUDA_OK(cudaGetLastError());
     stage_end(c, 1);
     set_ll_kernel<<<1, 1, 0, c->stream>>>(c->d_bad, LLONG_MAX);
     stage_begin(c, 2);
-    DISPATCH_K(t.k, launch_condense, c, nelt, geo, Ms, Ds, fv, d_C, d_Cf, d_factors);
+    DISPATCH_K(t.k, launch_condense, c, nelt, geo_b, Ms, Ds, fv, d_C, d_Cf, d_factors);
     stage_end(c, 2);
     check_bad(c, bad_element);
   });
@@ -1302,6 +1323,13 @@ int hdg_b200_set_variant(hdg_ctx* c, int variant) {
   return guarded([&] {
     require(c != nullptr && variant >= 2 && variant <= 4, HDG_EINVAL, "variant must be 2, 3 or 4");
     c->condense_variant = variant;
+  });
+}
+
+int hdg_b200_set_bdm(hdg_ctx* c, int enabled) {
+  return guarded([&] {
+    require(c != nullptr, HDG_EINVAL, "ctx is NULL");
+    c->bdm = enabled != 0;
   });
 }
 

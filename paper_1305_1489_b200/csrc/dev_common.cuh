@@ -21,6 +21,7 @@ __host__ __device__ constexpr int sym_idx(int i, int j, int n) { return j * (2 *
 // One degree's reference-element tables in device memory (host_tables.cpp).
 struct DevTab {
   int k, d3, d2, nq, nqd, nqp, nsym, nsymp, d3p;
+  int nu;  // scalar-space dimension of the local solve: d3, or d3 - d2 for the BDM variant
   const double* bary;   // nq x 4
   const double* w;      // nq
   const double* P;      // nq x d3

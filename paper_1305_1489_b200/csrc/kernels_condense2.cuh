@@ -370,7 +370,9 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = j * 8 + 2 * t + e;
-          if (r < D3 && c <= r) Sb[r + c * LD] += (e ? p1 + q1 : p0 + q0);
+          if (r < D3 && c <= r)  // BDM (tab.nu < D3): decoupled diagonal outside the P_{k-1} block
+            Sb[r + c * LD] = (r >= tab.nu || c >= tab.nu) ? (r == c ? 6.0 * sg[0] : 0.0)
+                                                          : Sb[r + c * LD] + (e ? p1 + q1 : p0 + q0);
         }
       } else {
         const int mt = (task - NLS) >> 2, l = (task - NLS) & 3;
@@ -402,7 +404,7 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           for (int e = 0; e < 2; ++e) {
             const int c = (nt0 + j) * 8 + 2 * t + e;
             if (c >= cl0 && c < cl1 && r < D3)
-              Vb[r + c * LD] = acc[j][e] + Tc[c] * __ldg(Wlm + wb[c] + r * D2);
+              Vb[r + c * LD] = r < tab.nu ? acc[j][e] + Tc[c] * __ldg(Wlm + wb[c] + r * D2) : 0.0;
           }
       }
     }
@@ -470,7 +472,7 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           const int r = idx % D3, c = idx / D3;
           F[2 * Dm::NSYM + idx] = Vb[r + c * LD];
         }
-        for (int i = lane; i < D3; i += 32) F[2 * Dm::NSYM + D3 * M + i] = fv[i];
+        for (int i = lane; i < D3; i += 32) F[2 * Dm::NSYM + D3 * M + i] = i < tab.nu ? fv[i] : 0.0;
       }
     }
     tm.sync();

@@ -283,7 +283,10 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = j * 8 + 2 * t + h;
-          if (r < D3 && c <= r) S[r + c * LD] = Dp(e)[sym_idx(r, c, D3)] + (h ? p1 + q1 : p0 + q0);
+          if (r < D3 && c <= r)  // BDM (tab.nu < D3): decoupled diagonal outside the P_{k-1} block
+            S[r + c * LD] = (r >= tab.nu || c >= tab.nu)
+                                ? (r == c ? 6.0 * sgb(e, cur)[0] : 0.0)
+                                : Dp(e)[sym_idx(r, c, D3)] + (h ? p1 + q1 : p0 + q0);
         }
       } else {
         const int mt = (sub - NLS) >> 2, l = (sub - NLS) & 3;
@@ -324,7 +327,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int c = (nt0 + j) * 8 + 2 * t + h;
-            if (c >= cl0 && c < cl1 && r < D3) V[r + c * LD] = acc[j][h];
+            if (c >= cl0 && c < cl1 && r < D3) V[r + c * LD] = r < tab.nu ? acc[j][h] : 0.0;
           }
       }
     }
@@ -369,7 +372,8 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           constexpr int NVF = D3 * M + D3;
           for (int q = w0 * 32 + lane; q < nb * NVF; q += nw * 32) {
             const int e = q / NVF, rem = q - e * NVF, c = rem / D3, r = rem - c * D3;
-            factors[(K0 + e) * Dm::FACTORS + 2 * Dm::NSYM + rem] = c < M ? Vb(e)[r + c * LD] : fv(e)[r];
+            factors[(K0 + e) * Dm::FACTORS + 2 * Dm::NSYM + rem] =
+                c < M ? Vb(e)[r + c * LD] : (r < tab.nu ? fv(e)[r] : 0.0);
           }
         }
         if (has_next) {

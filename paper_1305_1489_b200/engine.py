@@ -329,6 +329,10 @@ class Engine:
         tasks, 2 = per-element teams."""
         L.check(L.lib().hdg_b200_set_variant(self._ctx, int(variant)))
 
+    def set_bdm(self, enabled: bool) -> None:
+        """BDM variant (bdm_blocks, local_solver.cpp:65-69): u truncated to P_{k-1}, tau ignored."""
+        L.check(L.lib().hdg_b200_set_bdm(self._ctx, int(enabled)))
+
     def set_recover_variant(self, variant: int) -> None:
         """k = 1..3 recovery kernel: 3 = TMA-streamed cache (default), 2 = direct loads."""
         L.check(L.lib().hdg_b200_set_recover_variant(self._ctx, int(variant)))

@@ -451,3 +451,45 @@ def test_recover_variants_agree(k):
     ls2 = eng.recover(g, dm, cs, uhat)
     for a, b in ((ls3.qx, ls2.qx), (ls3.qy, ls2.qy), (ls3.qz, ls2.qz), (ls3.u, ls2.u)):
         assert max_slice_relerr(np_(a), np_(b)) < 1e-12
+
+
+# -------------------------------------------- a7: BDM variant (bdm_blocks)
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_bdm_variant(k):
+    """bdm_blocks (local_solver.cpp:65-69): u truncated to P_{k-1}, tau ignored;
+    C, Cf and the recovered (q, u) (u zero-padded) match the oracle."""
+    mesh = HostMesh.box(2, bc="dirichlet_top_bottom", perturb=0.1)
+    em = oracle_mesh(mesh)
+    eng = Engine(0)
+    eng.set_degree(k)
+    eng.set_bdm(True)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 1.0)  # tau = 1 is ignored by the variant
+    cs = eng.build_condense(g, KAP, CC, FF)
+    t = core.tables(k, 2 * k + 2, 2 * k + 2)
+    tauf = core.Stabilization(np.ones((em.n_elements, 4)))
+    ms = core.build_element_matrices(em, t, field(KAP), field(CC), field(FF), tauf)
+    lb = core.bdm_blocks(ms)
+    C, Cf = core.condense(lb, 4)
+    assert max_slice_relerr(np_(cs.C_slices()), C) < TOL
+    assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
+    d2 = dim2(k)
+    uhat = np.sin(np.arange(dm.nfc * d2) * 0.37)
+    ls = eng.recover(g, dm, cs, torch.from_numpy(uhat).cuda())
+    qx, qy, qz, u = core.local_recover(lb, core.gather_traces(em, d2, uhat), 4)
+    for got, want in ((ls.qx, qx), (ls.qy, qy), (ls.qz, qz), (ls.u, u)):
+        assert max_slice_relerr(np_(got), want.T) < TOL
+    nu = dim3(k) - d2
+    assert not np_(ls.u)[:, nu:].any()  # zero padding beyond P_{k-1}
+
+
+def test_bdm_rejects_degree_zero():
+    from paper_1305_1489_b200._lib import HdgError
+    mesh = HostMesh.box(1)
+    eng = Engine(0)
+    eng.set_degree(0)
+    eng.set_bdm(True)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 0.0)
+    with pytest.raises(HdgError, match="k >= 1"):
+        eng.build_condense(g, KAP, CC, FF)
