@@ -175,7 +175,7 @@ def cpu_sample_mesh(cfg, nlayers: int):
     return em, mesh
 
 
-def oracle_pipeline_time(cfg, nlayers: int, nthreads: int):
+def oracle_pipeline_time(cfg, nlayers: int, nthreads: int, all_cores: bool = False):
     from oracle import core
     from paper_1305_1489_b200.fields import compile_field
     em, _ = cpu_sample_mesh(cfg, nlayers)
@@ -192,16 +192,23 @@ def oracle_pipeline_time(cfg, nlayers: int, nthreads: int):
                                 uhat, nthreads)
     wall = time.perf_counter() - t0
     secs = sum(stages[:4])
+    if all_cores:
+        ac = core.time_pipeline_all_cores(em, t, fld(cfg.problem.kappa), fld(cfg.problem.c), fld(cfg.problem.f),
+                                          tau, uhat, nthreads)
+        return em.n_elements / secs, secs, em.n_elements, stages[:4], wall, em.n_elements / ac[0]
     return em.n_elements / secs, secs, em.n_elements, stages[:4], wall
 
 
 def cpu_baseline_line(cfg, nthreads: int, budget_layers: int):
-    eps, secs, ne, stages, wall = oracle_pipeline_time(cfg, budget_layers, nthreads)
+    eps, secs, ne, stages, wall, eps_all = oracle_pipeline_time(cfg, budget_layers, nthreads, all_cores=True)
     return {"value": eps, "unit": "elements/s", "cores": nthreads, "kind": "port",
             "sample": f"{cfg.name}: first {budget_layers} of {cfg.n} cell layers ({ne} tets), "
                       f"build+local_blocks 1 thread, condense+recover {nthreads} threads "
                       f"(study.cpp:19-31); stages s={[round(s, 3) for s in stages]}",
-            "seconds": secs}
+            "seconds": secs,
+            "all_cores_value": eps_all,
+            "all_cores_sample": f"same sample, every stage over {nthreads} contiguous element chunks "
+                                f"(SURVEY §8(d) 'all-cores' mode)"}
 
 
 def run_reference(args):

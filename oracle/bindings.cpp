@@ -376,6 +376,56 @@ PYBIND11_MODULE(_hdg_oracle, m) {
   // Times the reference-faithful path on an element range: build (1 thread),
   // local_blocks (1 thread), condense + recover (nthreads). Returns seconds per
   // stage; uhat is the per-element stacked trace (4 d2 x nelt).
+  // "all-cores" CPU baseline: every stage of the path parallel
+  // over contiguous element chunks (same per-element math and summation order).
+  m.def("time_pipeline_all_cores",
+        [](const ExpandedMesh& em, const Tables& t, const Field& kappa, const Field& c,
+           const Field& f, const StabilizationField& tau, const DArr& uhat, int nthreads) {
+          const Mat U = mat_from(uhat);
+          py::gil_scoped_release r;
+          const int nelt = em.n_elements();
+          auto rows = [](const auto& src, int k0, int k1, auto& dst) {
+            dst.r = k1 - k0;
+            dst.c = src.c;
+            dst.a.assign(size_t(dst.r) * dst.c, {});
+            for (int j = 0; j < src.c; ++j)
+              for (int i = k0; i < k1; ++i) dst.a[size_t(i - k0) + size_t(j) * dst.r] = src.a[size_t(i) + size_t(j) * src.r];
+          };
+          std::vector<ExpandedMesh> sub(nthreads, em);
+          std::vector<StabilizationField> stau(nthreads, tau);
+          std::vector<Mat> su(nthreads);
+          std::vector<int> k0s(nthreads + 1);
+          for (int i = 0; i <= nthreads; ++i) k0s[i] = int(long(nelt) * i / nthreads);
+          for (int i = 0; i < nthreads; ++i) {  // chunk views (setup, not timed)
+            const int k0 = k0s[i], k1 = k0s[i + 1];
+            rows(em.raw.elements, k0, k1, sub[i].raw.elements);
+            rows(em.facebyele, k0, k1, sub[i].facebyele);
+            rows(em.perm, k0, k1, sub[i].perm);
+            rows(em.normals, k0, k1, sub[i].normals);
+            sub[i].volume.assign(em.volume.begin() + k0, em.volume.begin() + k1);
+            rows(tau.tau, k0, k1, stau[i].tau);
+            su[i] = Mat(U.r, k1 - k0);
+            for (int K = k0; K < k1; ++K)
+              for (int j = 0; j < U.r; ++j) su[i](j, K - k0) = U(j, K);
+          }
+          std::vector<double> chk(nthreads, 0.0);
+          using clk = std::chrono::steady_clock;
+          auto t0 = clk::now();
+          parallel_for(nthreads, nthreads, [&](int b, int e) {
+            for (int i = b; i < e; ++i) {
+              if (k0s[i + 1] == k0s[i]) continue;
+              ElementMatrixSet ms = build_element_matrices(sub[i], t.tb, t.tet, t.tri, kappa.f, c.f, f.f, stau[i]);
+              LocalBlocks lb = local_blocks(ms);
+              CondensedSystem cs = condense(lb, 1);
+              LocalSolution ls = local_recover(lb, su[i], 1);
+              chk[i] = cs.C.data[0] + ls.u.a[0];
+            }
+          });
+          auto t1 = clk::now();
+          double sum = 0.0;
+          for (double v : chk) sum += v;
+          return std::vector<double>{std::chrono::duration<double>(t1 - t0).count(), sum};
+        });
   m.def("time_pipeline",
         [](const ExpandedMesh& em, const Tables& t, const Field& kappa, const Field& c,
            const Field& f, const StabilizationField& tau, const DArr& uhat, int nthreads) {
