@@ -1001,12 +1001,21 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
     if (n <= 40) {  // k <= 3: CTA-batched DMMA version (kernels_post2.cuh)
       const Post2Dims pd(n, tp.nq, c->tab[0].dev.d3);
       const size_t smem2 = size_t(pd.total) * sizeof(double);
-      CUDA_OK(cudaFuncSetAttribute(postprocess2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
       const long need2 = (long(nelt) + kPost2EB - 1) / kPost2EB;
       const int grid2 = int(std::min<long>(need2, long(c->sms) * 2));
+      auto go = [&](auto kern) {
+        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+        kern<<<grid2, kPost2Warps * 32, smem2, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, qx, qy, qz, u,
+                                                            ustar);
+      };
       stage_begin(c, 5);
-      postprocess2_kernel<<<grid2, kPost2Warps * 32, smem2, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, qx,
-                                                                        qy, qz, u, ustar);
+      switch (n - 1) {  // trailing system size for k + 1 = 1..4
+        case 3: go(postprocess2_kernel<3>); break;
+        case 9: go(postprocess2_kernel<9>); break;
+        case 19: go(postprocess2_kernel<19>); break;
+        case 34: go(postprocess2_kernel<34>); break;
+        default: throw HdgError{HDG_EINVAL, "postprocess: unexpected P_{k+1} dimension"};
+      }
       CUDA_OK(cudaGetLastError());
       stage_end(c, 5);
       return;

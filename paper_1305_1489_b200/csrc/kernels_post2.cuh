@@ -10,9 +10,9 @@
 //   S (packed lower, n(n+1)/2 x 8) = Shat_packed (. x 9) . gm (9 x 8),
 //                gm_e = (a_e^T a_e) / detB_e        (stiffness_matrices)
 // The K dimension of R is split over the 8 warps (partials reduced in shared
-// memory). Then each warp owns one element: mean constraint row, right-looking
-// Cholesky of the trailing SPD block in packed storage, register-resident
-// triangular solves (as the v1 kernel, kernels_post.cuh).
+// memory). Then each warp owns one element: mean constraint row, and the
+// trailing SPD system by the register sweep inverse of kernels_condense2.cuh
+// (lane c owns column c) for m <= 32, plus a Schur-complement border beyond.
 #pragma once
 
 #include "dev_common.cuh"
@@ -24,7 +24,6 @@ namespace hdgb {
 constexpr int kPost2EB = 8;     // elements per CTA (one DMMA N-tile)
 constexpr int kPost2Warps = 8;  // one warp per element in the solve phase
 constexpr int kPost2LDG = kPost2EB;  // G rows [q][e]: B-fragment reads are conflict-free at 8
-constexpr int kPost2MaxNS = 40 * 41 / 2;
 
 struct Post2Dims {
   int n, nq, nq4, d3k, npad, ns, nsp;
@@ -40,7 +39,8 @@ struct Post2Dims {
     off_gm = off_qc + 3 * d3k * kPost2EB;             // 12 x EB (rows 9..11 zero)
     off_R = off_gm + 12 * kPost2EB;                   // npad x EB
     off_Rp = off_R + npad * kPost2EB;                 // warps x npad x EB partials
-    off_GS = off_Rp + kPost2Warps * npad * kPost2EB;  // G (3 nq4 x LDG) | S (EB x nsp)
+    const int rp = kPost2Warps * npad * kPost2EB, solve = kPost2Warps * (128 + 64);
+    off_GS = off_Rp + (rp > solve ? rp : solve);      // G (3 nq4 x LDG) | S (EB x nsp)
     const int g = 3 * nq4 * kPost2LDG, sgs = kPost2EB * nsp;
     total = off_GS + (g > sgs ? g : sgs);
   }
@@ -48,20 +48,13 @@ struct Post2Dims {
 
 __device__ __forceinline__ int pk_lower(int i, int j, int n) { return j * n - j * (j - 1) / 2 + (i - j); }
 
-__global__ void __launch_bounds__(kPost2Warps * 32)
+template <int M_>  // trailing system size n - 1
+__global__ void __launch_bounds__(kPost2Warps * 32, 2)
 postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, const double* __restrict__ qx,
                     const double* __restrict__ qy, const double* __restrict__ qz, const double* __restrict__ u,
                     double* __restrict__ ustar) {
   extern __shared__ double psm[];
-  __shared__ unsigned char pk_i[kPost2MaxNS], pk_j[kPost2MaxNS];  // packed index -> (row, col)
-  __shared__ double invd[kPost2Warps][40];                         // 1 / L(k,k) per warp
   const Post2Dims dm(tp.d3, tp.nq, d3k);
-  for (int j = threadIdx.x; j < tp.d3; j += blockDim.x)
-    for (int i = j; i < tp.d3; ++i) {
-      const int p = pk_lower(i, j, tp.d3);
-      pk_i[p] = static_cast<unsigned char>(i);
-      pk_j[p] = static_cast<unsigned char>(j);
-    }
   const int n = dm.n, nq = dm.nq, nq4 = dm.nq4, npad = dm.npad, ns = dm.ns;
   double* verts = psm + dm.off_verts;
   double* sg = psm + dm.off_sg;
@@ -193,72 +186,89 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
     }
     __syncthreads();
 
-    // ---- per element: mean constraint, Cholesky of the trailing block, solves
+    // ---- per element: mean constraint, then the trailing SPD system
+    //      S' x = r' (m = n - 1 <= 32: register sweep inverse, lane c owns
+    //      column c; 32 < m <= 64: the leading 32 x 32 block the same way and
+    //      the (m - 32) border by its Schur complement)
     {
       const int e = warp;
       const long K = K0 + e;
       if (K < nelt) {
-        double* S = Sp + e * dm.nsp;
+        const double* S = Sp + e * dm.nsp;
         const double u0 = u[K * d3k];
-        const int m = n - 1;  // trailing system rows 1..n-1 -> index 0..m-1
-        double rr[2] = {0.0, 0.0};  // trailing rows lane, lane + 32 (n <= 35)
+        constexpr int MA = M_ < 32 ? M_ : 32, MB = M_ - MA;  // leading block, border
+        double* stage = Rp + warp * 128;                     // Rp is dead after the R reduction
+        double* rs = Rp + kPost2Warps * 128 + warp * 64;     // right-hand side r' (m)
+        for (int i = lane; i < M_; i += 32)
+          rs[i] = R[(i + 1) * kPost2EB + e] - S[pk_lower(i + 1, 0, n)] * u0;
+        auto Sat = [&](int i, int j) {  // S'(i, j), trailing indices, packed symmetric storage
+          return i >= j ? S[pk_lower(i + 1, j + 1, n)] : S[pk_lower(j + 1, i + 1, n)];
+        };
+        double a[MA];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int i = 1 + lane + 32 * j;
-          if (i < n) rr[j] = R[i * kPost2EB + e] - S[pk_lower(i, 0, n)] * u0;
-        }
-        // right-looking Cholesky on packed storage (full indices i, j >= 1):
-        // the trailing triangle of columns > k is one contiguous packed range,
-        // so its rank-1 update runs entry-parallel over all 32 lanes
-        for (int k = 1; k < n; ++k) {
-          const int ck = pk_lower(k, k, n);
-          const double lkk = sqrt(S[ck]);
-          const double inv = 1.0 / lkk;
-          __syncwarp();
-          if (lane == 0) {
-            S[ck] = lkk;
-            invd[warp][k - 1] = inv;
-          }
-          for (int i = k + 1 + lane; i < n; i += 32) S[ck + (i - k)] *= inv;
-          __syncwarp();
-          for (int p = ck + (n - k) + lane; p < ns; p += 32) {
-            const int i = pk_i[p], j = pk_j[p];
-            S[p] = fma(-S[ck + (i - k)], S[ck + (j - k)], S[p]);
-          }
-          __syncwarp();
-        }
-        // forward L y = r, then backward L^T x = y (trailing indices)
-        for (int k = 0; k < m; ++k) {
-          const int owner = k & 31, slot = k >> 5;
-          double rk = slot == 0 ? rr[0] : rr[1];
-          rk = __shfl_sync(0xffffffffu, rk, owner);
-          const int ck = pk_lower(k + 1, k + 1, n);
-          const double yk = rk * invd[warp][k];
+        for (int i = 0; i < MA; ++i) a[i] = lane < MA ? Sat(i, lane) : 0.0;
+        __syncwarp();
+        double pmin = 1e300, pmax = 0.0;
+        warp_gj_inverse<MA>(a, stage, lane, pmin, pmax);  // a = column `lane` of A^-1 (symmetric)
+        // z = A^-1 r_A and, for the border, Y = A^-1 B: lane i holds row i (A^-1 symmetric)
+        double z = 0.0;
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int i = lane + 32 * j;
-            if (i == k) rr[j] = yk;
-            else if (i > k && i < m) rr[j] = fma(-S[ck + (i - k)], yk, rr[j]);
-          }
-        }
-        for (int k = m - 1; k >= 0; --k) {
-          const int owner = k & 31, slot = k >> 5;
-          double yk = slot == 0 ? rr[0] : rr[1];
-          yk = __shfl_sync(0xffffffffu, yk, owner);
-          const double xk = yk * invd[warp][k];
+        for (int j = 0; j < MA; ++j) z = fma(a[j], rs[j], z);
+        double x = z;
+        if constexpr (MB > 0) {
+          double Y[MB];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int i = lane + 32 * j;
-            if (i == k) rr[j] = xk;
-            else if (i < k) rr[j] = fma(-S[pk_lower(k + 1, i + 1, n)], xk, rr[j]);
+          for (int b2 = 0; b2 < MB; ++b2) {
+            double y = 0.0;
+#pragma unroll
+            for (int j = 0; j < MA; ++j) y = fma(a[j], Sat(j, MA + b2), y);
+            Y[b2] = lane < MA ? y : 0.0;
           }
+          // Schur complement Cs = C - B^T Y and rhs2 = r_B - B^T z (warp sums)
+          double Cs[MB][MB], r2[MB];
+#pragma unroll
+          for (int p = 0; p < MB; ++p) {
+            const double bp = lane < MA ? Sat(lane, MA + p) : 0.0;
+            double v = bp * (lane < MA ? z : 0.0);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            r2[p] = rs[MA + p] - v;
+#pragma unroll
+            for (int q = 0; q < MB; ++q) {
+              double w = bp * Y[q];
+#pragma unroll
+              for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+              Cs[p][q] = Sat(MA + p, MA + q) - w;
+            }
+          }
+          // x_B = Cs^-1 r2 (small SPD; Gaussian elimination, every lane redundantly)
+#pragma unroll
+          for (int c = 0; c < MB; ++c) {
+            const double inv = 1.0 / Cs[c][c];
+#pragma unroll
+            for (int r = c + 1; r < MB; ++r) {
+              const double f = Cs[r][c] * inv;
+#pragma unroll
+              for (int q = c; q < MB; ++q) Cs[r][q] -= f * Cs[c][q];
+              r2[r] -= f * r2[c];
+            }
+          }
+          double xb[MB];
+#pragma unroll
+          for (int c = MB - 1; c >= 0; --c) {
+            double v = r2[c];
+#pragma unroll
+            for (int q = c + 1; q < MB; ++q) v -= Cs[c][q] * xb[q];
+            xb[c] = v / Cs[c][c];
+          }
+#pragma unroll
+          for (int b2 = 0; b2 < MB; ++b2) x = fma(-Y[b2], xb[b2], x);
+#pragma unroll
+          for (int b2 = 0; b2 < MB; ++b2)
+            if (lane == b2) ustar[K * n + 1 + MA + b2] = xb[b2];
         }
         if (lane == 0) ustar[K * n] = u0;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int i = lane + 32 * j;
-          if (i < m) ustar[K * n + 1 + i] = rr[j];
-        }
+        if (lane < MA) ustar[K * n + 1 + lane] = x;
       }
     }
     __syncthreads();
