@@ -259,6 +259,8 @@ struct hdg_ctx {
   int condense_variant = 3; // k = 2, 3: 4 = element-batched tasks, 3 = CTA-batched, 2 = per-element teams
   std::string jit_error;    // last JIT failure (kernel then runs interpreted)
   int* d_adj = nullptr;     // boundary face -> 4 K + l (neumann_load)
+  double* d_ksamp = nullptr;  // kappa sampled at the postprocess nodes (JIT sampler)
+  size_t ksamp_len = 0;
   int adj_len = 0;
   cudaEvent_t ev[2 * HDG_NSTAGES] = {};
   bool pending[HDG_NSTAGES] = {};
@@ -729,6 +731,7 @@ void hdg_b200_destroy(hdg_ctx* c) {
   if (c->work) cudaFree(c->work);
   if (c->d_adj) cudaFree(c->d_adj);
   if (c->d_zero_T) cudaFree(c->d_zero_T);
+  if (c->d_ksamp) cudaFree(c->d_ksamp);
   if (c->d_bad) cudaFree(c->d_bad);
   if (c->h_bad) cudaFreeHost(c->h_bad);
   if (c->d_status) cudaFree(c->d_status);
@@ -993,11 +996,39 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
     require(c && qx && qy && qz && u && ustar && nelt > 0, HDG_EINVAL, "bad argument");
     require(c->tab[0].ready && c->tab[1].ready, HDG_ESTATE, "set_postprocess_rule first");
     const GeoDev geo = to_geo(g);
-    const FieldDev fk = to_dev(kappa, "kappa");
+    FieldDev fk = to_dev(kappa, "kappa");
     set_device(c);
     const DevTab& tp = c->tab[1].dev;
     const int n = tp.d3;
     require(n - 1 <= 96, HDG_EINVAL, "postprocess degree too high (d3(k+1) <= 97)");
+    if (c->jit && kappa.kind == HDG_FIELD_PROGRAM) {
+      // a program kappa is sampled once at the P_{k+1} nodes by an NVRTC-compiled
+      // sampler, so the postprocess reads samples instead of interpreting it per node
+      std::string err;
+      CUfunction fn = jit_sample_kernel(kappa, &err);
+      if (fn) {
+        const size_t len = size_t(tp.nq) * nelt;
+        if (c->ksamp_len < len) {
+          if (c->d_ksamp) cudaFree(c->d_ksamp);
+          c->d_ksamp = nullptr;
+          CUDA_OK(cudaMalloc(&c->d_ksamp, len * sizeof(double)));
+          c->ksamp_len = len;
+        }
+        int nel = nelt, nq = tp.nq;
+        const double *bary = tp.bary, *V = geo.verts;
+        double* out = c->d_ksamp;
+        void* args[] = {&nel, &nq, &bary, &V, &out};
+        const int grid = int(std::min<long>((long(len) + 255) / 256, long(c->sms) * 16));
+        if (launch_quad_jit(fn, c->stream, grid, 256, 0, args, &err)) {
+          fk.kind = HDG_FIELD_SAMPLED;
+          fk.samples = c->d_ksamp;
+        } else {
+          c->jit_error = err;
+        }
+      } else {
+        c->jit_error = err;
+      }
+    }
     if (n <= 40) {  // k <= 3: CTA-batched DMMA version (kernels_post2.cuh)
       const Post2Dims pd(n, tp.nq, c->tab[0].dev.d3);
       const size_t smem2 = size_t(pd.total) * sizeof(double);

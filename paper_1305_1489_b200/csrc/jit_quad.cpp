@@ -207,15 +207,15 @@ std::string field_expr(const hdg_field& f, const char* sample_ptr) {
   return st.empty() ? "0.0" : st.back();
 }
 
-CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, std::string* err) {
-  std::string src = "#define EB " + std::to_string(eb) + "\n#define FIELD_KAPPA " + field_expr(kap, "sk") + "\n#define FIELD_C " + field_expr(c, "sc") +
-                    "\n#define FIELD_F " + field_expr(f, "sf") + "\n" + kQuadSource;
+namespace {
+// NVRTC-compile `src` for sm_100a and return its kernel `name` (cached by source text).
+CUfunction compile_cached(const std::string& src, const char* name, std::string* err) {
   Cache& C = cache();
   std::lock_guard<std::mutex> lock(C.mu);
   auto it = C.fn.find(src);
   if (it != C.fn.end()) return it->second;
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src.c_str(), "quad_build_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+  if (nvrtcCreateProgram(&prog, src.c_str(), "hdg_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     if (err) *err = "nvrtcCreateProgram failed";
     return nullptr;
   }
@@ -242,13 +242,49 @@ CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_f
     return nullptr;
   }
   if (drv().loadData(&mod, cubin.data()) != CUDA_SUCCESS ||
-      drv().getFunction(&fn, mod, "quad_build_jit") != CUDA_SUCCESS) {
+      drv().getFunction(&fn, mod, name) != CUDA_SUCCESS) {
     if (err) *err = "cuModuleLoadData/cuModuleGetFunction failed";
     return nullptr;
   }
   C.mods.push_back(mod);
   C.fn.emplace(src, fn);
   return fn;
+}
+
+const char* kSampleSource = R"CUDA(
+// JIT: a field program sampled at every element node (SAMPLED layout K * nq + q).
+extern "C" __global__ void __launch_bounds__(256)
+sample_field_jit(int nelt, int nq, const double* __restrict__ bary, const double* __restrict__ V,
+                 double* __restrict__ out) {
+  const long n = long(nelt) * nq;
+  for (long idx = long(blockIdx.x) * blockDim.x + threadIdx.x; idx < n; idx += long(gridDim.x) * blockDim.x) {
+    const long K = idx / nq;
+    const int q = int(idx - K * nq);
+    const double l0 = __ldg(bary + q), l1 = __ldg(bary + nq + q), l2 = __ldg(bary + 2 * nq + q),
+                 l3 = __ldg(bary + 3 * nq + q);
+    const double x = l0 * V[K] + l1 * V[nelt + K] + l2 * V[2L * nelt + K] + l3 * V[3L * nelt + K];
+    const double y = l0 * V[4L * nelt + K] + l1 * V[5L * nelt + K] + l2 * V[6L * nelt + K] + l3 * V[7L * nelt + K];
+    const double z = l0 * V[8L * nelt + K] + l1 * V[9L * nelt + K] + l2 * V[10L * nelt + K] + l3 * V[11L * nelt + K];
+    out[idx] = FIELD_EXPR;
+  }
+}
+)CUDA";
+}  // namespace
+
+CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, std::string* err) {
+  const std::string src = "#define EB " + std::to_string(eb) + "\n#define FIELD_KAPPA " + field_expr(kap, "sk") +
+                          "\n#define FIELD_C " + field_expr(c, "sc") + "\n#define FIELD_F " + field_expr(f, "sf") +
+                          "\n" + kQuadSource;
+  return compile_cached(src, "quad_build_jit", err);
+}
+
+CUfunction jit_sample_kernel(const hdg_field& f, std::string* err) {
+  if (f.kind != HDG_FIELD_PROGRAM) {
+    if (err) *err = "only program fields are sampled";
+    return nullptr;
+  }
+  return compile_cached("#define FIELD_EXPR " + field_expr(f, "nullptr") + "\n" + kSampleSource, "sample_field_jit",
+                        err);
 }
 
 bool launch_quad_jit(CUfunction fn, cudaStream_t stream, int grid, int block, size_t smem, void** args,

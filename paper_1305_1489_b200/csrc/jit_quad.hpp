@@ -11,6 +11,8 @@ namespace hdgb {
 std::string field_expr(const hdg_field& f, const char* sample_ptr);
 // Compiled (cached) kernel for these fields and EB elements per CTA, or nullptr with *err set.
 CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, std::string* err);
+// Kernel sampling a PROGRAM field at every element node (SAMPLED layout), or nullptr.
+CUfunction jit_sample_kernel(const hdg_field& f, std::string* err);
 bool launch_quad_jit(CUfunction fn, cudaStream_t stream, int grid, int block, size_t smem, void** args,
                      std::string* err);
 }  // namespace hdgb
