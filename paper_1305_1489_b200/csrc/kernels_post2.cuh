@@ -106,7 +106,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
     }
     // ---- G_#(q, e) at the P_{k+1} nodes (rows q >= nq are zero padding)
     for (int idx = threadIdx.x; idx < nq4 * kPost2EB; idx += blockDim.x) {
-      const int q = idx / kPost2EB, e = idx - q * kPost2EB;
+      const int e = idx / nq4, q = idx - e * nq4;  // node fastest: coalesced samples and P rows
       const long K = K0 + e;
       double gv[3] = {0.0, 0.0, 0.0};
       if (q < nq && K < nelt) {
@@ -140,6 +140,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
       double acc[5][2];
 #pragma unroll
       for (int m = 0; m < 5; ++m) acc[m][0] = acc[m][1] = 0.0;
+#pragma unroll 4
       for (int kk = k0; kk < k1; ++kk) {
         const int k = kk * 4 + t, h = k / nq4, q = k - h * nq4;
         const double b = G[k * kPost2LDG + g];
