@@ -33,6 +33,23 @@ __global__ void gj_kernel(double* out, long long* cyc, int reps, int dmma_warps)
   out[blockIdx.x * blockDim.x + threadIdx.x] = s + pmin + pmax;
 }
 
+// same inversion under a 512-thread launch bound (<= 128 registers), as in the condense kernel
+template <int N>
+__global__ void __launch_bounds__(512) gj_kernel_lb(double* out, long long* cyc, int reps) {
+  __shared__ __align__(16) double stage[16 * 128];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double a[N];
+  for (int i = 0; i < N; ++i) a[i] = (i == lane ? 4.0 * N : 0.0) + 1.0 / (1.0 + i + lane);
+  double pmin = 1e300, pmax = 0;
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) warp_gj_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
+  long long t1 = clock64();
+  if (lane == 0) cyc[blockIdx.x * 8 + (warp & 7)] = (t1 - t0) / reps;
+  double s = 0;
+  for (int i = 0; i < N; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s + pmin + pmax;
+}
+
 int main() {
   double* out; long long* cyc;
   cudaMalloc(&out, 148 * 256 * 8); cudaMalloc(&cyc, 148 * 8 * 8);
@@ -47,6 +64,11 @@ int main() {
     gj_kernel<20><<<148, 32 * (4 + dw)>>>(out, cyc, 32, dw);
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
     printf("N=20 4 GJ warps + %d DMMA warps: %lld cycles per inverse\n", dw, h[0]);
+  }
+  for (int warps : {4, 8}) {
+    gj_kernel_lb<20><<<148, 32 * warps>>>(out, cyc, 32);
+    cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("N=20 (launch bound 512) warps/SM=%d: %lld cycles per inverse\n", warps, h[0]);
   }
   gj_kernel<10><<<148, 32>>>(out, cyc, 32, 0);
   cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
