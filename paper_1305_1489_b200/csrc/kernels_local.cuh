@@ -150,55 +150,116 @@ struct Team {
   }
 };
 
-// In-place Cholesky (left-looking, lower) of an n x n SPD matrix at A (ld).
+// In-place Cholesky (left-looking, lower) of an n x n SPD matrix at A (ld),
+// two columns per pass (2 team barriers per column pair). scratch: 2n doubles.
 // Returns the pivot ratio test of local_solver.cpp:50-57 transposed to
 // Cholesky pivots d_j = L_jj^2: singular iff min d < 1e-14 max d or d <= 0.
 template <int NW>
 __device__ bool team_cholesky(const Team<NW>& tm, double* A, int ld, int n, double* scratch) {
   constexpr int NT = NW * 32;
+  double* s0 = scratch;
+  double* s1 = scratch + n;
   double dmax = 0.0, dmin = 1e300;
   bool bad = false;
-  for (int j = 0; j < n; ++j) {
-    // s_i = A(i,j) - sum_{k<j} L(i,k) L(j,k), i >= j
+  int j = 0;
+  for (; j + 1 < n; j += 2) {
+    // s0_i = A(i,j) - sum_{k<j} L(i,k) L(j,k); s1_i likewise for column j+1 (i > j)
     for (int i = j + tm.tid; i < n; i += NT) {
-      double s0 = A[i + j * ld], s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 short chains
+      double a0 = A[i + j * ld], a1 = i > j ? A[i + (j + 1) * ld] : 0.0, b0 = 0.0, b1 = 0.0;
       int k = 0;
-      for (; k + 3 < j; k += 4) {
-        s0 = fma(-A[i + k * ld], A[j + k * ld], s0);
-        s1 = fma(-A[i + (k + 1) * ld], A[j + (k + 1) * ld], s1);
-        s2 = fma(-A[i + (k + 2) * ld], A[j + (k + 2) * ld], s2);
-        s3 = fma(-A[i + (k + 3) * ld], A[j + (k + 3) * ld], s3);
+      for (; k + 1 < j; k += 2) {
+        const double l0 = A[i + k * ld], l1 = A[i + (k + 1) * ld];
+        a0 = fma(-l0, A[j + k * ld], a0);
+        a1 = fma(-l0, A[j + 1 + k * ld], a1);
+        b0 = fma(-l1, A[j + (k + 1) * ld], b0);
+        b1 = fma(-l1, A[j + 1 + (k + 1) * ld], b1);
       }
-      for (; k < j; ++k) s0 = fma(-A[i + k * ld], A[j + k * ld], s0);
-      scratch[i] = (s0 + s1) + (s2 + s3);
+      if (k < j) {
+        const double l0 = A[i + k * ld];
+        a0 = fma(-l0, A[j + k * ld], a0);
+        a1 = fma(-l0, A[j + 1 + k * ld], a1);
+      }
+      s0[i] = a0 + b0;
+      s1[i] = a1 + b1;
     }
     tm.sync();
-    const double d = scratch[j];
+    const double d0 = s0[j];
+    const double l00 = d0 > 0.0 ? sqrt(d0) : 1.0, inv0 = 1.0 / l00;
+    const double l10 = s0[j + 1] * inv0;
+    const double d1 = s1[j + 1] - l10 * l10;
+    const double l11 = d1 > 0.0 ? sqrt(d1) : 1.0, inv1 = 1.0 / l11;
+    if (!(d0 > 0.0) || !(d1 > 0.0)) bad = true;
+    dmax = fmax(dmax, fmax(d0, d1));
+    dmin = fmin(dmin, fmin(d0, d1));
+    for (int i = j + tm.tid; i < n; i += NT) {
+      if (i == j) {
+        A[j + j * ld] = l00;
+      } else {
+        const double li0 = s0[i] * inv0;
+        A[i + j * ld] = li0;
+        A[i + (j + 1) * ld] = i == j + 1 ? l11 : (s1[i] - li0 * l10) * inv1;
+      }
+    }
+    tm.sync();
+  }
+  if (j < n) {  // last column of an odd-sized matrix
+    for (int i = j + tm.tid; i < n; i += NT) {
+      double s = A[i + j * ld];
+      for (int k = 0; k < j; ++k) s = fma(-A[i + k * ld], A[j + k * ld], s);
+      s0[i] = s;
+    }
+    tm.sync();
+    const double d = s0[j];
     if (!(d > 0.0)) bad = true;
     dmax = fmax(dmax, d);
     dmin = fmin(dmin, d);
     const double ljj = d > 0.0 ? sqrt(d) : 1.0;
     const double inv = 1.0 / ljj;
-    for (int i = j + tm.tid; i < n; i += NT) A[i + j * ld] = (i == j) ? ljj : scratch[i] * inv;
+    for (int i = j + tm.tid; i < n; i += NT) A[i + j * ld] = (i == j) ? ljj : s0[i] * inv;
     tm.sync();
   }
   return bad || dmax == 0.0 || dmin < 1e-14 * dmax;
 }
 
-// In-place inverse of a lower-triangular matrix (columns right to left):
-// X(j,j) = 1/L(j,j), X(i,j) = -X(j,j) sum_{k=j+1..i} X(i,k) L(k,j).
+// In-place inverse of a lower-triangular matrix (columns right to left, two
+// per pass): X(j,j) = 1/L(j,j), X(i,j) = -X(j,j) sum_{k=j+1..i} X(i,k) L(k,j).
+// scratch: 2n doubles.
 template <int NW>
 __device__ void team_tri_inverse(const Team<NW>& tm, double* A, int ld, int n, double* scratch) {
   constexpr int NT = NW * 32;
-  for (int j = n - 1; j >= 0; --j) {
-    const double xjj = 1.0 / A[j + j * ld];
-    for (int i = j + 1 + tm.tid; i < n; i += NT) {
-      double s = 0.0;
-      for (int k = j + 1; k <= i; ++k) s += A[i + k * ld] * A[k + j * ld];
-      scratch[i] = -xjj * s;
+  double* x0 = scratch;      // column j
+  double* x1 = scratch + n;  // column j - 1
+  int j = n - 1;
+  for (; j >= 1; j -= 2) {
+    const double xjj = 1.0 / A[j + j * ld], xj1 = 1.0 / A[j - 1 + (j - 1) * ld];
+    const double ljj1 = A[j + (j - 1) * ld];  // L(j, j-1)
+    for (int i = j - 1 + tm.tid; i < n; i += NT) {
+      double sj = 0.0, s1 = 0.0;
+      for (int k = j + 1; k <= i; ++k) {
+        const double xik = A[i + k * ld];
+        sj = fma(xik, A[k + j * ld], sj);
+        s1 = fma(xik, A[k + (j - 1) * ld], s1);
+      }
+      const double xij = i > j ? -xjj * sj : (i == j ? xjj : 0.0);
+      x0[i] = xij;
+      x1[i] = i == j - 1 ? xj1 : -xj1 * (s1 + xij * ljj1);
     }
     tm.sync();
-    for (int i = j + tm.tid; i < n; i += NT) A[i + j * ld] = (i == j) ? xjj : scratch[i];
+    for (int i = j - 1 + tm.tid; i < n; i += NT) {
+      if (i >= j) A[i + j * ld] = x0[i];
+      A[i + (j - 1) * ld] = x1[i];
+    }
+    tm.sync();
+  }
+  if (j == 0) {
+    const double x00 = 1.0 / A[0];
+    for (int i = 1 + tm.tid; i < n; i += NT) {
+      double s = 0.0;
+      for (int k = 1; k <= i; ++k) s = fma(A[i + k * ld], A[k], s);
+      x0[i] = -x00 * s;
+    }
+    tm.sync();
+    for (int i = tm.tid; i < n; i += NT) A[i] = i == 0 ? x00 : x0[i];
     tm.sync();
   }
 }
