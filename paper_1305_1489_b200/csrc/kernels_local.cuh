@@ -163,24 +163,26 @@ __device__ bool team_cholesky(const Team<NW>& tm, double* A, int ld, int n, doub
   bool bad = false;
   int j = 0;
   for (; j + 1 < n; j += 2) {
-    // s0_i = A(i,j) - sum_{k<j} L(i,k) L(j,k); s1_i likewise for column j+1 (i > j)
-    for (int i = j + tm.tid; i < n; i += NT) {
-      double a0 = A[i + j * ld], a1 = i > j ? A[i + (j + 1) * ld] : 0.0, b0 = 0.0, b1 = 0.0;
-      int k = 0;
-      for (; k + 1 < j; k += 2) {
-        const double l0 = A[i + k * ld], l1 = A[i + (k + 1) * ld];
-        a0 = fma(-l0, A[j + k * ld], a0);
-        a1 = fma(-l0, A[j + 1 + k * ld], a1);
-        b0 = fma(-l1, A[j + (k + 1) * ld], b0);
-        b1 = fma(-l1, A[j + 1 + (k + 1) * ld], b1);
+    // s0_i = A(i,j) - sum_{k<j} L(i,k) L(j,k); s1_i likewise for column j+1 (i > j).
+    // Four threads per row split the k range (quad shuffle sum): short chains.
+    for (int base = 0; base < n - j; base += NT / 4) {  // warp-uniform trip count
+      const int i = j + base + (tm.tid >> 2), part = tm.tid & 3;
+      const bool live = i < n;
+      double a0 = 0.0, a1 = 0.0;
+      if (live)
+        for (int k = part; k < j; k += 4) {
+          const double l0 = A[i + k * ld];
+          a0 = fma(-l0, A[j + k * ld], a0);
+          a1 = fma(-l0, A[j + 1 + k * ld], a1);
+        }
+      a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+      a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+      if (live && part == 0) {
+        s0[i] = A[i + j * ld] + a0;
+        s1[i] = i > j ? A[i + (j + 1) * ld] + a1 : 0.0;
       }
-      if (k < j) {
-        const double l0 = A[i + k * ld];
-        a0 = fma(-l0, A[j + k * ld], a0);
-        a1 = fma(-l0, A[j + 1 + k * ld], a1);
-      }
-      s0[i] = a0 + b0;
-      s1[i] = a1 + b1;
     }
     tm.sync();
     const double d0 = s0[j];
@@ -233,16 +235,25 @@ __device__ void team_tri_inverse(const Team<NW>& tm, double* A, int ld, int n, d
   for (; j >= 1; j -= 2) {
     const double xjj = 1.0 / A[j + j * ld], xj1 = 1.0 / A[j - 1 + (j - 1) * ld];
     const double ljj1 = A[j + (j - 1) * ld];  // L(j, j-1)
-    for (int i = j - 1 + tm.tid; i < n; i += NT) {
+    for (int base = 0; base < n - j + 1; base += NT / 4) {  // four threads per row (quad sums)
+      const int i = j - 1 + base + (tm.tid >> 2), part = tm.tid & 3;
+      const bool live = i < n;
       double sj = 0.0, s1 = 0.0;
-      for (int k = j + 1; k <= i; ++k) {
-        const double xik = A[i + k * ld];
-        sj = fma(xik, A[k + j * ld], sj);
-        s1 = fma(xik, A[k + (j - 1) * ld], s1);
+      if (live)
+        for (int k = j + 1 + part; k <= i; k += 4) {
+          const double xik = A[i + k * ld];
+          sj = fma(xik, A[k + j * ld], sj);
+          s1 = fma(xik, A[k + (j - 1) * ld], s1);
+        }
+      sj += __shfl_xor_sync(0xffffffffu, sj, 1);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+      sj += __shfl_xor_sync(0xffffffffu, sj, 2);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+      if (live && part == 0) {
+        const double xij = i > j ? -xjj * sj : (i == j ? xjj : 0.0);
+        x0[i] = xij;
+        x1[i] = i == j - 1 ? xj1 : -xj1 * (s1 + xij * ljj1);
       }
-      const double xij = i > j ? -xjj * sj : (i == j ? xjj : 0.0);
-      x0[i] = xij;
-      x1[i] = i == j - 1 ? xj1 : -xj1 * (s1 + xij * ljj1);
     }
     tm.sync();
     for (int i = j - 1 + tm.tid; i < n; i += NT) {
