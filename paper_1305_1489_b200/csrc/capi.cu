@@ -982,8 +982,20 @@ int hdg_b200_scatter(hdg_ctx* c, int nelt, int d2, const int* d_facebyele, const
             HDG_EINVAL, "bad argument");
     set_device(c);
     stage_begin(c, 4);
-    scatter_kernel<<<(nelt + 7) / 8, 256, 0, c->stream>>>(nelt, d2, d_facebyele, d_slot, d_facebase, d_C,
-                                                         d_Cf, d_vals, d_b);
+    const int m = 4 * d2;
+    const size_t smem = size_t(kScatterWarps) * (m * m + 64) * sizeof(double);
+    if (smem <= 200 * 1024) {
+      CUDA_OK(cudaFuncSetAttribute(scatter2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      int occ = 0;
+      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scatter2_kernel, kScatterWarps * 32, smem));
+      const long need = (long(nelt) + kScatterWarps - 1) / kScatterWarps;
+      const int grid = int(std::min<long>(need, long(c->sms) * std::max(occ, 1)));
+      scatter2_kernel<<<grid, kScatterWarps * 32, smem, c->stream>>>(nelt, d2, d_facebyele, d_slot, d_facebase,
+                                                                     d_C, d_Cf, d_vals, d_b);
+    } else {  // k = 5: the C slice does not fit eight warps' shared memory
+      scatter_kernel<<<(nelt + 7) / 8, 256, 0, c->stream>>>(nelt, d2, d_facebyele, d_slot, d_facebase, d_C,
+                                                           d_Cf, d_vals, d_b);
+    }
     CUDA_OK(cudaGetLastError());
     stage_end(c, 4);
   });

@@ -195,4 +195,49 @@ __global__ void scatter_kernel(int nelt, int d2, const int* __restrict__ facebye
   }
 }
 
+// K4 v2: the element's C slice (contiguous m x m, column-major) is staged in
+// shared memory with 16-byte coalesced loads, then written out block by block
+// with lanes along the block's contiguous column index j, so each 80-byte row
+// segment of a d2 x d2 block goes out in one store instruction (v1 wrote with
+// lanes along rows, 8-byte stores scattered over 32 lines). Diagonal blocks
+// (1-2 contributions) and b stay fp64 atomics onto zero: bit-exact.
+constexpr int kScatterWarps = 8;
+__global__ void __launch_bounds__(kScatterWarps * 32)
+scatter2_kernel(int nelt, int d2, const int* __restrict__ facebyele, const uint8_t* __restrict__ slot,
+                const int64_t* __restrict__ facebase, const double* __restrict__ C, const double* __restrict__ Cf,
+                double* __restrict__ vals, double* __restrict__ b) {
+  extern __shared__ __align__(16) double ssm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = 4 * d2, mm = m * m, dd = d2 * d2;
+  double* Cs = ssm + warp * (mm + 64);
+  int64_t* rowb = reinterpret_cast<int64_t*>(Cs + mm);  // per (l1, l2): first value of the block
+  int* nbw = reinterpret_cast<int*>(rowb + 16);          // per l1: row width n1 * d2
+  for (long K = long(blockIdx.x) * kScatterWarps + warp; K < nelt; K += long(gridDim.x) * kScatterWarps) {
+    const double2* src = reinterpret_cast<const double2*>(C + K * mm);
+    for (int q = lane; q < mm / 2; q += 32) reinterpret_cast<double2*>(Cs)[q] = __ldg(src + q);
+    if (lane < 16) {
+      const int l1 = lane >> 2, l2 = lane & 3;
+      const int f1 = facebyele[long(l1) * nelt + K];
+      const int64_t b0 = facebase[f1];
+      const int nb = int(facebase[f1 + 1] - b0);
+      rowb[lane] = b0 * dd + int64_t(slot[K * 16 + l1 * 4 + l2]) * d2;
+      if (l2 == 0) nbw[l1] = nb * d2;
+    }
+    __syncwarp();
+    for (int idx = lane; idx < 16 * dd; idx += 32) {
+      const int blk = idx / dd, w = idx - blk * dd, i = w / d2, j = w - i * d2;
+      const int l1 = blk >> 2, l2 = blk & 3;
+      const double v = Cs[(l1 * d2 + i) + (l2 * d2 + j) * m];
+      double* dst = vals + rowb[blk] + int64_t(i) * nbw[l1] + j;
+      if (l1 == l2) atomicAdd(dst, v);
+      else *dst = v;
+    }
+    for (int r = lane; r < m; r += 32) {
+      const int l = r / d2;
+      atomicAdd(b + long(facebyele[long(l) * nelt + K]) * d2 + (r - l * d2), Cf[K * m + r]);
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace hdgb
