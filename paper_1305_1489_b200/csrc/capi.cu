@@ -300,13 +300,23 @@ int factor_doubles(int k) {
 // launch shape of the CTA-batched kernel in the (NW, EPB) vocabulary
 template <int K_>
 struct C3Launch {
-  static constexpr int EPB = C3Cfg<K_>::EPB, NW = C3Cfg<K_>::NWT / C3Cfg<K_>::EPB;
+  static constexpr int EPB = C3Cfg<K_>::EPB, THREADS = C3Cfg<K_>::NWT * 32;
 };
 
 template <int K_>
 struct C4Launch {
-  static constexpr int EPB = C4Cfg<K_>::EPB, NW = C4Cfg<K_>::NWT / C4Cfg<K_>::EPB > 0 ? C4Cfg<K_>::NWT / C4Cfg<K_>::EPB : 1;
-  static_assert(C4Cfg<K_>::NWT % C4Cfg<K_>::EPB == 0 || C4Cfg<K_>::EPB % C4Cfg<K_>::NWT == 0, "");
+  static constexpr int EPB = C4Cfg<K_>::EPB, THREADS = C4Cfg<K_>::NWT * 32;
+};
+
+template <int K_>
+struct CondLaunch {
+  static constexpr int EPB = CondCfg<K_>::EPB, THREADS = CondCfg<K_>::NW * 32 * CondCfg<K_>::EPB;
+};
+
+// per-element team kernel (v2): NW warps per element
+template <int K_>
+struct C2Launch {
+  static constexpr int EPB = C2Cfg<K_>::EPB, THREADS = C2Cfg<K_>::NW * 32 * C2Cfg<K_>::EPB;
 };
 
 template <class Dm, class Cg, class Kern>
@@ -315,13 +325,13 @@ void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, co
   const size_t smem = (size_t(Cg::EPB) * Dm::PER_ELT + Dm::CTA_EXTRA) * sizeof(double);
   CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int occ = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cg::NW * 32 * Cg::EPB, smem));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cg::THREADS, smem));
   require(occ > 0, HDG_ECUDA, "condense kernel does not fit on an SM");
   const long need = (long(nelt) + Cg::EPB - 1) / Cg::EPB;
   const int grid = int(std::min<long>(need, long(c->sms) * occ));
   DevTab td = c->tab[0].dev;
   if (c->bdm) td.nu = td.d3 - td.d2;  // bdm_blocks (local_solver.cpp:65-69): u truncated to P_{k-1}
-  kern<<<grid, Cg::NW * 32 * Cg::EPB, smem, c->stream>>>(td, nelt, geo, Ms, Ds, fv, C, Cf, F, c->d_bad);
+  kern<<<grid, Cg::THREADS, smem, c->stream>>>(td, nelt, geo, Ms, Ds, fv, C, Cf, F, c->d_bad);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -335,15 +345,15 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
       return;
     }
     if (c->condense_variant == 2)
-      launch_condense_impl<C2Dims<K_>, C2Cfg<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+      launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
     else if (c->condense_variant == 3)
       launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
     else
       launch_condense_impl<C2Dims<K_>, C4Launch<K_>>(c, condense4_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
   } else if constexpr (K_ <= 3)
-    launch_condense_impl<C2Dims<K_>, C2Cfg<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+    launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
   else
-    launch_condense_impl<CondDims<K_>, CondCfg<K_>>(c, condense_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+    launch_condense_impl<CondDims<K_>, CondLaunch<K_>>(c, condense_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
 }
 
 template <int K_>

@@ -6,7 +6,13 @@
 // tasks of all EPB elements over all warps (better balance, 5 CTA barriers
 // per EPB elements instead of 5 team barriers per element), and in P3 the
 // S^-1 sweeps of the batch run concurrently with the M^-1 sweeps of the next
-// batch and the W Zp tiles.
+// batch.
+//
+// Compact layout: every d3-indexed dimension is stored with stride
+// LD = round_up(d3, 4) (20 at k=3, 12 at k=2), so the contraction loops run
+// exactly KS = LD/4 DMMA k-steps with no predicates. The k-padding rows /
+// columns (k=2 only) are kept zero; tile rows/columns past d3 read whatever
+// follows in shared memory and their outputs are never stored.
 #pragma once
 
 #include "kernels_condense2.cuh"
@@ -28,12 +34,34 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) 
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// C2Dims plus a packed copy of D (filled by cp.async one batch ahead).
 template <int K_>
-struct C3Dims : C2Dims<K_> {
-  static constexpr int OFF_DP = C2Dims<K_>::PER_ELT;
-  static constexpr int PER_ELT = OFF_DP + round_up(C2Dims<K_>::NSYM, 2);
-  static constexpr int CTA_EXTRA = 3 * C2Dims<K_>::D3 * C2Dims<K_>::D3 + C2Dims<K_>::D2 * C2Dims<K_>::D2;  // Chat, DD
+struct C3Dims {
+  static constexpr int D3 = cdim3(K_), D2 = cdim2(K_), M = 4 * cdim2(K_);
+  static constexpr int LD = round_up(D3, 4);        // stride of every d3-indexed dimension
+  static constexpr int KS = LD / 4;                 // DMMA k-steps over d3
+  static constexpr int D3P = round_up(D3, 8), MP = round_up(M, 8);
+  static constexpr int MT = D3P / 8, NTM = MP / 8;  // row tiles over d3, column tiles over m
+  static constexpr int NSYM = D3 * (D3 + 1) / 2;
+  static constexpr int SQ = round_up(LD * LD + D3P - LD, 2);  // d3 x d3 + tile-row overrun
+  static constexpr int RH = LD * D3;                          // one R_# (LD x d3)
+  static constexpr int NY = 3 * RH > LD * MP ? 3 * RH : LD * MP;
+  static constexpr int OFF_MI = 0;
+  static constexpr int OFF_S = OFF_MI + SQ;
+  static constexpr int OFF_Y = OFF_S + SQ;       // R_# (3), then Vs (LD x MP)
+  static constexpr int OFF_Z = OFF_Y + NY;       // Zp (LD x MP)
+  static constexpr int OFF_V = OFF_Z + LD * MP;  // V (LD x MP)
+  static constexpr int OFF_NSC = OFF_V + LD * MP;  // column data (8 x MP), see build_columns
+  static constexpr int OFF_F = OFF_NSC + 8 * MP;   // LD: f
+  static constexpr int OFF_FS = OFF_F + LD;        // LD: Si f
+  static constexpr int OFF_STG = round_up(OFF_FS + LD, 2);  // 128: GJ column stage (16 B aligned)
+  static constexpr int OFF_STG2 = OFF_STG + 128;            // 128: second GJ stage
+  static constexpr int OFF_GEO = OFF_STG2 + 128;            // 2 x 32: geometry records (cur/next)
+  static constexpr int OFF_COL = OFF_GEO + 64;              // second column-data buffer
+  static constexpr int OFF_DP = OFF_COL + 8 * MP;           // packed D
+  static constexpr int PER_ELT = OFF_DP + round_up(NSYM, 2);
+  static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
+  // per CTA: Chat_# [c + k d3] (k < LD, padding zero), tauDD, tile overrun
+  static constexpr int CTA_EXTRA = round_up(3 * D3 * LD + D2 * D2 + D3P, 2);
 };
 
 // Most 8-column tiles one face's d2 columns (starting at l d2) touch.
@@ -48,12 +76,12 @@ constexpr int face_tiles(int d2) {
 
 template <int K_> struct C3Cfg;
 #ifndef HDG_C3_EPB2
-#define HDG_C3_EPB2 8
-#define HDG_C3_NWT2 16
-#define HDG_C3_MINB2 1
+#define HDG_C3_EPB2 6
+#define HDG_C3_NWT2 8
+#define HDG_C3_MINB2 2
 #endif
 #ifndef HDG_C3_EPB3
-#define HDG_C3_EPB3 4
+#define HDG_C3_EPB3 5
 #define HDG_C3_NWT3 16
 #define HDG_C3_MINB3 1
 #endif
@@ -68,36 +96,36 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
                  long long* bad_element) {
   using Dm = C3Dims<K_>;
   constexpr int EPB = C3Cfg<K_>::EPB, NWT = C3Cfg<K_>::NWT, NT = NWT * 32;
-  constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, D3P = Dm::D3P, MP = Dm::MP, LD = Dm::LD;
+  constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, MP = Dm::MP, LD = Dm::LD, RH = Dm::RH;
   constexpr int MT = Dm::MT, NTM = Dm::NTM, KS = Dm::KS;
   constexpr int NLOW = NTM * (NTM + 1) / 2;  // lower tiles of the m x m output
   constexpr int NLS = MT * (MT + 1) / 2;     // lower tiles of S
   constexpr int NTF = face_tiles(D2);        // N-tiles one face's columns span
   constexpr int NGJ = 2 * EPB;               // GJ tasks in P3
   constexpr bool GJ_SEP = NWT > NGJ;         // GJ warps do nothing else in P3
-  static_assert(NLOW * 64 <= 3 * D3P * LD, "W Zp tiles must fit in the R buffer");
   extern __shared__ double smem[];
   __shared__ unsigned short pk_rc[Dm::NSYM];  // packed lower index -> row | col << 8
-  for (int i = threadIdx.x; i < EPB * Dm::PER_ELT; i += blockDim.x) smem[i] = 0.0;
+  for (int i = threadIdx.x; i < EPB * Dm::PER_ELT + Dm::CTA_EXTRA; i += blockDim.x) smem[i] = 0.0;
   for (int j = threadIdx.x; j < D3; j += blockDim.x)
     for (int i = j; i < D3; ++i) pk_rc[sym_idx(i, j, D3)] = static_cast<unsigned short>(i | (j << 8));
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const double* Wlm = tab.Wlm;
-  // CTA copy of Chat (3 d3^2): its fragments are re-read every phase, and the
-  // L1 left beside ~218 KB of shared memory does not hold the tables
+  // CTA copy of Chat_# and tauDD: their fragments are re-read every phase
   double* Ch = smem + EPB * Dm::PER_ELT;
-  double* DDs = Ch + 3 * D3 * D3;  // tauDD reference block (d2 x d2)
-  for (int i = threadIdx.x; i < 3 * D3 * D3; i += NT) Ch[i] = tab.Chat[i];
+  double* DDs = Ch + 3 * D3 * LD;
+  for (int i = threadIdx.x; i < 3 * D3 * D3; i += NT) {
+    const int h = i / (D3 * D3);
+    Ch[h * D3 * LD + (i - h * D3 * D3)] = tab.Chat[i];
+  }
   for (int i = threadIdx.x; i < D2 * D2; i += NT) DDs[i] = tab.DD[i];
   __syncthreads();
-#define CH_LD(p) (*(p))
   auto B = [&](int e) { return smem + e * Dm::PER_ELT; };
   auto Mi = [&](int e) { return B(e) + Dm::OFF_MI; };
   auto Sb = [&](int e) { return B(e) + Dm::OFF_S; };
-  auto Yb = [&](int e) { return B(e) + Dm::OFF_Y; };  // R_#, then W Zp tiles
-  auto Zb = [&](int e) { return B(e) + Dm::OFF_Z; };  // Zp, then Vs
+  auto Yb = [&](int e) { return B(e) + Dm::OFF_Y; };            // R_#, then Vs
+  auto Zb = [&](int e) { return B(e) + Dm::OFF_Z; };            // Zp
   auto Vb = [&](int e) { return B(e) + Dm::OFF_V; };
   auto fv = [&](int e) { return B(e) + Dm::OFF_F; };
   auto fs = [&](int e) { return B(e) + Dm::OFF_FS; };
@@ -123,8 +151,8 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  auto load_geometry = [&](long Kb, int which) {
-    for (int idx = threadIdx.x; idx < EPB * 32; idx += NT) {
+  auto load_geometry = [&](long Kb, int which, int tid, int nthr) {
+    for (int idx = tid; idx < EPB * 32; idx += nthr) {
       const int e = idx >> 5, i = idx & 31;
       if (Kb + e < nelt && i < 30) {
         const long K = Kb + e;
@@ -148,11 +176,11 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     __syncwarp();
     double pmin = 1e300, pmax = 0.0;
-    warp_gj_inverse<D3>(a, stM(e), lane, pmin, pmax);
+    warp_gj_inverse2<D3>(a, stM(e), lane, pmin, pmax);
     const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
-    if (lane < D3) {
+    if (lane < D3) {  // symmetric: row-wise stores are conflict-free
 #pragma unroll
-      for (int i = 0; i < D3; ++i) Mi(e)[i + lane * LD] = a[i];
+      for (int i = 0; i < D3; ++i) Mi(e)[lane + i * LD] = a[i];
     }
     if (bad && lane == 0) flag_bad(bad_element, K);
   };
@@ -178,7 +206,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   // ---- prologue: first batch
   if (K0 < nelt) {
     load_Df_async(K0);
-    load_geometry(K0, 0);
+    load_geometry(K0, 0, threadIdx.x, NT);
     for (int e = warp; e < EPB; e += NWT)
       if (K0 + e < nelt) invert_M(e, K0 + e);
     cp_async_wait_all();
@@ -206,23 +234,24 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
           const int k = kk * 4 + t;
-          const bool in = k < D3 && c < D3;
           const int o = c + k * D3;
           const double a = mi[(m * 8 + g) + k * LD];
-          dmma(q[0][0], q[0][1], a, in ? CH_LD(Ch + o) : 0.0);
-          dmma(q[1][0], q[1][1], a, in ? CH_LD(Ch + D3 * D3 + o) : 0.0);
-          dmma(q[2][0], q[2][1], a, in ? CH_LD(Ch + 2 * D3 * D3 + o) : 0.0);
+          dmma(q[0][0], q[0][1], a, Ch[o]);
+          dmma(q[1][0], q[1][1], a, Ch[D3 * LD + o]);
+          dmma(q[2][0], q[2][1], a, Ch[2 * D3 * LD + o]);
         }
         const double* a9 = sg + 1;
         const int c0 = nt * 8 + 2 * t, r = m * 8 + g;
+        if (r < LD) {
 #pragma unroll
-        for (int h = 0; h < 3; ++h) {
-          const double g0 = a9[h] * a9[0] + a9[3 + h] * a9[3] + a9[6 + h] * a9[6];
-          const double g1 = a9[h] * a9[1] + a9[3 + h] * a9[4] + a9[6 + h] * a9[7];
-          const double g2 = a9[h] * a9[2] + a9[3 + h] * a9[5] + a9[6 + h] * a9[8];
-          double* R = Yb(e) + h * D3P * LD;
-          R[r + c0 * LD] = g0 * q[0][0] + g1 * q[1][0] + g2 * q[2][0];
-          R[r + (c0 + 1) * LD] = g0 * q[0][1] + g1 * q[1][1] + g2 * q[2][1];
+          for (int h = 0; h < 3; ++h) {
+            const double g0 = a9[h] * a9[0] + a9[3 + h] * a9[3] + a9[6 + h] * a9[6];
+            const double g1 = a9[h] * a9[1] + a9[3 + h] * a9[4] + a9[6 + h] * a9[7];
+            const double g2 = a9[h] * a9[2] + a9[3 + h] * a9[5] + a9[6 + h] * a9[8];
+            double* R = Yb(e) + h * RH;
+            if (c0 < D3) R[r + c0 * LD] = r < D3 ? g0 * q[0][0] + g1 * q[1][0] + g2 * q[2][0] : 0.0;
+            if (c0 + 1 < D3) R[r + (c0 + 1) * LD] = r < D3 ? g0 * q[0][1] + g1 * q[1][1] + g2 * q[2][1] : 0.0;
+          }
         }
       } else {
         const int nt = sub - MT * MT;
@@ -242,8 +271,11 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         double* Z = Zb(e);
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
-          Z[(m * 8 + g) + c0 * LD] = acc[m][0];
-          Z[(m * 8 + g) + (c0 + 1) * LD] = acc[m][1];
+          const int r = m * 8 + g;
+          if (r < LD) {
+            Z[r + c0 * LD] = r < D3 ? acc[m][0] : 0.0;
+            Z[r + (c0 + 1) * LD] = r < D3 ? acc[m][1] : 0.0;
+          }
         }
       }
     }
@@ -269,12 +301,12 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         double p0 = 0, p1 = 0, q0 = 0, q1 = 0;
 #pragma unroll
         for (int h = 0; h < 3; ++h) {
-          const double* R = Yb(e) + h * D3P * LD;
-          const double* C = Ch + h * D3 * D3;
+          const double* R = Yb(e) + h * RH;
+          const double* C = Ch + h * D3 * LD;
 #pragma unroll
           for (int kk = 0; kk < KS; ++kk) {
             const int k = kk * 4 + t;
-            const double a = (r < D3 && k < D3) ? CH_LD(C + r + k * D3) : 0.0;
+            const double a = C[r + k * D3];
             if (kk & 1) dmma(q0, q1, a, R[k + (j * 8 + g) * LD]);
             else dmma(p0, p1, a, R[k + (j * 8 + g) * LD]);
           }
@@ -283,10 +315,12 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = j * 8 + 2 * t + h;
-          if (r < D3 && c <= r)  // BDM (tab.nu < D3): decoupled diagonal outside the P_{k-1} block
-            S[r + c * LD] = (r >= tab.nu || c >= tab.nu)
-                                ? (r == c ? 6.0 * sgb(e, cur)[0] : 0.0)
-                                : Dp(e)[sym_idx(r, c, D3)] + (h ? p1 + q1 : p0 + q0);
+          if (r < D3 && c <= r) {  // BDM (tab.nu < D3): decoupled diagonal outside the P_{k-1} block
+            const double v = (r >= tab.nu || c >= tab.nu) ? (r == c ? 6.0 * sgb(e, cur)[0] : 0.0)
+                                                          : Dp(e)[sym_idx(r, c, D3)] + (h ? p1 + q1 : p0 + q0);
+            S[r + c * LD] = v;
+            S[c + r * LD] = v;
+          }
         }
       } else {
         const int mt = (sub - NLS) >> 2, l = (sub - NLS) & 3;
@@ -309,11 +343,8 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
           const int k = kk * 4 + t;
-          double a = 0.0;
-          if (r < D3 && k < D3) {
-            const int o = r + k * D3;
-            a = b0 * CH_LD(Ch + o) + b1 * CH_LD(Ch + D3 * D3 + o) + b2 * CH_LD(Ch + 2 * D3 * D3 + o);
-          }
+          const int o = r + k * D3;
+          const double a = b0 * Ch[o] + b1 * Ch[D3 * LD + o] + b2 * Ch[2 * D3 * LD + o];
 #pragma unroll
           for (int j = 0; j < NTF; ++j) {
             const int c = (nt0 + j) * 8 + g;
@@ -322,21 +353,23 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           }
         }
         double* V = Vb(e);
+        if (r < LD) {
 #pragma unroll
-        for (int j = 0; j < NTF; ++j)
+          for (int j = 0; j < NTF; ++j)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = (nt0 + j) * 8 + 2 * t + h;
-            if (c >= cl0 && c < cl1 && r < D3) V[r + c * LD] = r < tab.nu ? acc[j][h] : 0.0;
-          }
+            for (int h = 0; h < 2; ++h) {
+              const int c = (nt0 + j) * 8 + 2 * t + h;
+              if (c >= cl0 && c < cl1) V[r + c * LD] = r < tab.nu ? acc[j][h] : 0.0;
+            }
+        }
       }
     }
     cp_async_wait_all();
     __syncthreads();
 
     PHASE_MARK(batch, 2);
-    // ---- P3: S^-1 of the batch || M^-1 of the next batch || (W Zp) tiles -> Yb
-    //      || V, f -> recovery cache
+    // ---- P3: S^-1 of the batch || M^-1 of the next batch || V, f -> recovery
+    //      cache, next geometry
     {
       const bool gj_warp = warp < NGJ;
       if (gj_warp || !GJ_SEP) {
@@ -345,21 +378,25 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           if (task < EPB) {
             if (e >= nb) continue;
             const long K = K0 + e;
-            double a[D3];
+            double a[D3];  // S is stored full (P2), so column `lane` is read row-wise
 #pragma unroll
-            for (int i = 0; i < D3; ++i) {
-              const int r = i > lane ? i : lane, c = i > lane ? lane : i;
-              a[i] = lane < D3 ? Sb(e)[r + c * LD] : 0.0;
-            }
+            for (int i = 0; i < D3; ++i) a[i] = lane < D3 ? Sb(e)[lane + i * LD] : 0.0;
             double pmin = 1e300, pmax = 0.0;
-            warp_gj_inverse<D3>(a, stS(e), lane, pmin, pmax);
+#ifndef HDG_DIAG_NO_GJ
+            warp_gj_inverse2<D3>(a, stS(e), lane, pmin, pmax);
+#else
+            pmin = pmax = 1.0;
+#endif
             const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
             if (lane < D3) {
 #pragma unroll
-              for (int i = 0; i < D3; ++i) Sb(e)[i + lane * LD] = a[i];
+              for (int i = 0; i < D3; ++i) Sb(e)[lane + i * LD] = a[i];
             }
             if (bad && lane == 0) flag_bad(bad_element, K);
           } else if (has_next && Kn0 + e < nelt) {
+#ifdef HDG_DIAG_NO_GJ
+            continue;
+#endif
             invert_M_staged(e, Kn0 + e);  // packed M copied into the dead Mi(e) during P2
           }
         }
@@ -368,6 +405,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         // No FP64 here: the sweeps' dependent DFMA chains stall badly behind
         // DMMA traffic on the same pipe, so this phase only moves data.
         const int w0 = GJ_SEP ? warp - NGJ : warp, nw = GJ_SEP ? NWT - NGJ : NWT;
+#ifndef HDG_DIAG_NO_P3MEM
         if (factors) {  // V (D3 x M) and f of each element, contiguous in the cache record
           constexpr int NVF = D3 * M + D3;
           for (int q = w0 * 32 + lane; q < nb * NVF; q += nw * 32) {
@@ -376,27 +414,14 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
                 c < M ? Vb(e)[r + c * LD] : (r < tab.nu ? fv(e)[r] : 0.0);
           }
         }
-        if (has_next) {
-          for (int idx = w0 * 32 + lane; idx < EPB * 32; idx += nw * 32) {
-            const int e = idx >> 5, i = idx & 31;
-            const long K = Kn0 + e;
-            if (K < nelt && i < 30) {
-              double v;
-              if (i == 0) v = geo.volume[K];
-              else if (i < 10) v = geo.piola[long(i - 1) * nelt + K];
-              else if (i < 22) v = geo.normals[long(i - 10) * nelt + K];
-              else if (i < 26) v = geo.T[long(i - 22) * nelt + K];
-              else v = double(geo.perm[long(i - 26) * nelt + K]);
-              sgb(e, cur ^ 1)[i] = v;
-            }
-          }
-        }
+#endif
+        if (has_next) load_geometry(Kn0, cur ^ 1, w0 * 32 + lane, nw * 32);
       }
     }
     __syncthreads();
 
     PHASE_MARK(batch, 3);
-    // ---- P4: Vs = Si V (into Zb) | fs = Si f | next batch's geometry + columns
+    // ---- P4: Vs = Si V (into Yb) | fs = Si f | next batch's columns
     for (int task = warp; task < nb * NTM; task += NWT) {  // one column strip per task:
       const int e = task / NTM, nt = task % NTM;           // the V fragment feeds MT chains
       const double* S = Sb(e);
@@ -416,8 +441,10 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         const int r = m * 8 + g;
-        Yb(e)[r + c0 * LD] = acc[m][0];  // Vs (R_# is dead)
-        Yb(e)[r + (c0 + 1) * LD] = acc[m][1];
+        if (r < LD) {
+          Yb(e)[r + c0 * LD] = r < D3 ? acc[m][0] : 0.0;  // Vs (R_# is dead)
+          Yb(e)[r + (c0 + 1) * LD] = r < D3 ? acc[m][1] : 0.0;
+        }
       }
     }
     for (int idx = threadIdx.x; idx < nb * D3; idx += NT) {
@@ -428,7 +455,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       fs(e)[r] = s;
     }
     if (factors) {
-      write_factor(K0, Dm::NSYM, true);       // S^-1 of this batch
+      write_factor(K0, Dm::NSYM, true);           // S^-1 of this batch
       if (has_next) write_factor(Kn0, 0, false);  // M^-1 of the next batch
     }
     __syncthreads();
@@ -452,8 +479,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
         const int k = kk * 4 + t;
-        const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
-        dmma(z0, z1, aw, Z[k + (nt * 8 + g) * LD]);
+        dmma(z0, z1, (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0, Z[k + (nt * 8 + g) * LD]);
         dmma(v0, v1, V[k + r * LD], Vs[k + (nt * 8 + g) * LD]);
       }
       if (r < M) {
@@ -488,7 +514,5 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     cur ^= 1;
   }
 }
-
-#undef CH_LD
 
 }  // namespace hdgb
