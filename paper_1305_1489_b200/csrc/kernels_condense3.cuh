@@ -98,9 +98,13 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int EPB = C3Cfg<K_>::EPB, NWT = C3Cfg<K_>::NWT, NT = NWT * 32;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, MP = Dm::MP, LD = Dm::LD, RH = Dm::RH;
   constexpr int MT = Dm::MT, NTM = Dm::NTM, KS = Dm::KS;
-  constexpr int NLOW = NTM * (NTM + 1) / 2;  // lower tiles of the m x m output
+  constexpr int NLP = (NTM / 2 + 1) * ((NTM + 1) / 2);  // lower tile pairs of the m x m output
   constexpr int NLS = MT * (MT + 1) / 2;     // lower tiles of S
   constexpr int NTF = face_tiles(D2);        // N-tiles one face's columns span
+#ifndef HDG_C3_FPT
+#define HDG_C3_FPT 4
+#endif
+  constexpr int FPT = HDG_C3_FPT;            // faces per V task (1, 2 or 4)
   constexpr int NGJ = 2 * EPB;               // GJ tasks in P3
   constexpr bool GJ_SEP = NWT > NGJ;         // GJ warps do nothing else in P3
   extern __shared__ double smem[];
@@ -292,8 +296,9 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
     // ---- P2: S += sum_# Chat_# R_# (lower tiles) | V_l = Chat_l Zp_l + T_l W_l^T
-    for (int task = warp; task < nb * (NLS + 4 * MT); task += NWT) {
-      const int e = task / (NLS + 4 * MT), sub = task % (NLS + 4 * MT);
+    constexpr int NP2 = NLS + (4 / FPT) * MT;  // P2 tasks per element
+    for (int task = warp; task < nb * NP2; task += NWT) {
+      const int e = task / NP2, sub = task % NP2;
       if (sub < NLS) {
         int mt = 0, rem = sub;
         while (rem > mt) { rem -= mt + 1; ++mt; }
@@ -322,45 +327,59 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             S[c + r * LD] = v;
           }
         }
-      } else {
-        const int mt = (sub - NLS) >> 2, l = (sub - NLS) & 3;
+      } else {  // V rows of row tile mt for FPT faces: the Chat_# fragments feed every face
+        const int mt = (sub - NLS) / (4 / FPT), l0 = ((sub - NLS) % (4 / FPT)) * FPT;
         const int r = mt * 8 + g;
-        const int cl0 = l * D2, cl1 = cl0 + D2, nt0 = cl0 / 8;
         const double* col = colb(e, cur);
         const double* Tc = col + 3 * MP;
         const int* wb = reinterpret_cast<const int*>(col + 4 * MP);
         const double* beta = col + 5 * MP;
-        const double b0 = beta[cl0], b1 = beta[MP + cl0], b2 = beta[2 * MP + cl0];
         const double* Z = Zb(e);
-        double acc[NTF][2];  // starts at T_l W_l^T (its loads overlap the DMMA chain)
+        double bl[FPT][3];
+        double acc[FPT][NTF][2];  // starts at T_l W_l^T (its loads overlap the DMMA chains)
 #pragma unroll
-        for (int j = 0; j < NTF; ++j)
+        for (int f = 0; f < FPT; ++f) {
+          const int cl0 = (l0 + f) * D2, cl1 = cl0 + D2, nt0 = cl0 / 8;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = (nt0 + j) * 8 + 2 * t + h;
-            acc[j][h] = (c >= cl0 && c < cl1 && r < D3) ? Tc[c] * __ldg(Wlm + wb[c] + r * D2) : 0.0;
-          }
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-          const int k = kk * 4 + t;
-          const int o = r + k * D3;
-          const double a = b0 * Ch[o] + b1 * Ch[D3 * LD + o] + b2 * Ch[2 * D3 * LD + o];
-#pragma unroll
-          for (int j = 0; j < NTF; ++j) {
-            const int c = (nt0 + j) * 8 + g;
-            const double b = (c >= cl0 && c < cl1) ? Z[k + c * LD] : 0.0;
-            if ((nt0 + j) * 8 < cl1) dmma(acc[j][0], acc[j][1], a, b);
-          }
-        }
-        double* V = Vb(e);
-        if (r < LD) {
+          for (int h = 0; h < 3; ++h) bl[f][h] = beta[h * MP + cl0];
 #pragma unroll
           for (int j = 0; j < NTF; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int c = (nt0 + j) * 8 + 2 * t + h;
-              if (c >= cl0 && c < cl1) V[r + c * LD] = r < tab.nu ? acc[j][h] : 0.0;
+              acc[f][j][h] = (c >= cl0 && c < cl1 && r < D3) ? Tc[c] * __ldg(Wlm + wb[c] + r * D2) : 0.0;
             }
+        }
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          const int o = r + k * D3;
+          const double c0 = Ch[o], c1 = Ch[D3 * LD + o], c2 = Ch[2 * D3 * LD + o];
+#pragma unroll
+          for (int f = 0; f < FPT; ++f) {
+            const int cl0 = (l0 + f) * D2, cl1 = cl0 + D2, nt0 = cl0 / 8;
+            const double a = bl[f][0] * c0 + bl[f][1] * c1 + bl[f][2] * c2;
+#pragma unroll
+            for (int j = 0; j < NTF; ++j) {
+              const int c = (nt0 + j) * 8 + g;
+              const double b = (c >= cl0 && c < cl1) ? Z[k + c * LD] : 0.0;
+              if ((nt0 + j) * 8 < cl1) dmma(acc[f][j][0], acc[f][j][1], a, b);
+            }
+          }
+        }
+        double* V = Vb(e);
+        if (r < LD) {
+#pragma unroll
+          for (int f = 0; f < FPT; ++f) {
+            const int cl0 = (l0 + f) * D2, cl1 = cl0 + D2, nt0 = cl0 / 8;
+#pragma unroll
+            for (int j = 0; j < NTF; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int c = (nt0 + j) * 8 + 2 * t + h;
+                if (c >= cl0 && c < cl1) V[r + c * LD] = r < tab.nu ? acc[f][j][h] : 0.0;
+              }
+          }
         }
       }
     }
@@ -466,21 +485,29 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     PHASE_MARK(batch, 4);
     if (has_next) load_Df_async(Kn0);  // D, f of this batch are dead after P4
     // ---- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (lower tiles, mirrored) | Cf
-    for (int task = warp; task < nb * NLOW; task += NWT) {
-      const int e = task / NLOW, tile = task % NLOW;
-      int mt = 0, rem = tile;
-      while (rem > mt) { rem -= mt + 1; ++mt; }
-      const int nt = rem, r = mt * 8 + g;
+    for (int task = warp; task < nb * NLP; task += NWT) {  // tile pairs (mt, nt0..nt0+1) of a row
+      const int e = task / NLP;
+      int mt = 0, rem = task % NLP;
+      while (rem >= (mt + 2) / 2) { rem -= (mt + 2) / 2; ++mt; }
+      const int nt0 = 2 * rem, r = mt * 8 + g;
+      const bool two = nt0 + 1 <= mt;
       const double* V = Vb(e);
       const double* Vs = Yb(e);
       const double* Z = Zb(e);
       const int wbr = reinterpret_cast<const int*>(colb(e, cur) + 4 * MP)[r];
-      double v0 = 0, v1 = 0, z0 = 0, z1 = 0;
+      double z[2][2] = {{0, 0}, {0, 0}}, v[2][2] = {{0, 0}, {0, 0}};
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
         const int k = kk * 4 + t;
-        dmma(z0, z1, (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0, Z[k + (nt * 8 + g) * LD]);
-        dmma(v0, v1, V[k + r * LD], Vs[k + (nt * 8 + g) * LD]);
+        const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
+        const double av = V[k + r * LD];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+          const int cn = (nt0 + u) * 8 + g;
+          dmma(z[u][0], z[u][1], aw, Z[k + cn * LD]);
+          dmma(v[u][0], v[u][1], av, Vs[k + cn * LD]);
+        }
       }
       if (r < M) {
         const double* sg = sgb(e, cur);
@@ -490,15 +517,19 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
         double* Ck = Cout + (K0 + e) * M * M;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = nt * 8 + 2 * t + h;
-          if (c > r || c >= M) continue;
-          const int l2 = c / D2;
-          const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
-          double v = nn * (h ? z1 : z0) - (h ? v1 : v0);
-          if (l1 == l2) v += Tc[c] * DDs[(r - l1 * D2) + (c - l2 * D2) * D2];
-          Ck[r + c * M] = v;
-          if (c != r) Ck[c + r * M] = v;
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = (nt0 + u) * 8 + 2 * t + h;
+            if (c > r || c >= M) continue;
+            const int l2 = c / D2;
+            const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
+            double val = nn * z[u][h] - v[u][h];
+            if (l1 == l2) val += Tc[c] * DDs[(r - l1 * D2) + (c - l2 * D2) * D2];
+            Ck[r + c * M] = val;
+            if (c != r) Ck[c + r * M] = val;
+          }
         }
       }
     }
