@@ -1,0 +1,103 @@
+// Warp-register sweep inverse of a small SPD matrix (used by the v3
+// condensation kernel, kernels_condense3.cuh). Self-contained: no includes.
+#pragma once
+
+// 1/x to full double precision: MUFU reciprocal seed + two Newton steps.
+__device__ __forceinline__ double gj_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Inverse of the SPD N x N matrix held by a warp (lane c owns column c in
+// a[]) by the symmetric sweep operator with 2 x 2 pivots (no pivoting; the
+// pivots are the Cholesky pivots and feed the 1e-14 test of
+// local_solver.cpp:50-57 through pmin / pmax). The pivot block columns are
+// exchanged through `stage` (2 x 64 doubles, 16-byte aligned). The pivot
+// lanes take their diagonal entry minus one into w = P^-1 a_K, which yields
+// their special update weights (rows of I - P^-1) without selects, and each
+// lane records its own pivot (one warp reduction at the end).
+template <int N>
+__device__ __forceinline__ void gj_sweep_inverse(double (&a)[N], double* stage, int lane, double& pmin,
+                                                 double& pmax) {
+  double piv = 1.0;  // lane c: Cholesky pivot c (odd c: its reciprocal until the end)
+#pragma unroll
+  for (int k = 0; k + 1 < N; k += 2) {
+    double* st = stage + ((k >> 1) & 1) * 64;
+    if (lane < N) {
+      st[lane] = a[k];
+      st[32 + lane] = a[k + 1];
+    }
+    const double p00 = __shfl_sync(0xffffffffu, a[k], k);
+    const double p01 = __shfl_sync(0xffffffffu, a[k + 1], k);
+    const double p11 = __shfl_sync(0xffffffffu, a[k + 1], k + 1);
+    // next pivot pair's rows of the stage by shuffle: keeps shared memory off
+    // the step-to-step dependency chain
+    double n0x = 0.0, n0y = 0.0, n1x = 0.0, n1y = 0.0;
+    if (k + 2 < N) {
+      n0x = __shfl_sync(0xffffffffu, a[k], k + 2);
+      n1x = __shfl_sync(0xffffffffu, a[k + 1], k + 2);
+      if (k + 3 < N) {
+        n0y = __shfl_sync(0xffffffffu, a[k], k + 3);
+        n1y = __shfl_sync(0xffffffffu, a[k + 1], k + 3);
+      }
+    }
+    const double det = fma(p00, p11, -p01 * p01);
+    const double id = gj_rcp(det);
+    const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;
+    const bool m0 = lane == k, m1 = lane == k + 1;
+    if (m0) piv = p00;
+    if (m1) piv = i11;
+    const double ak0 = m0 ? a[k] - 1.0 : a[k];
+    const double ak1 = m1 ? a[k + 1] - 1.0 : a[k + 1];
+    const double w0 = fma(i00, ak0, i01 * ak1);
+    const double w1 = fma(i01, ak0, i11 * ak1);
+    if (k + 2 < N) {
+      a[k + 2] = fma(-n0x, w0, fma(-n1x, w1, a[k + 2]));
+      if (k + 3 < N) a[k + 3] = fma(-n0y, w0, fma(-n1y, w1, a[k + 3]));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i0 = 0; i0 < N; i0 += 2) {
+      if (i0 == k || i0 == k + 2) continue;
+      const double2 v0 = *reinterpret_cast<const double2*>(st + i0);
+      const double2 v1 = *reinterpret_cast<const double2*>(st + 32 + i0);
+      a[i0] = fma(-v0.x, w0, fma(-v1.x, w1, a[i0]));
+      if (i0 + 1 < N) a[i0 + 1] = fma(-v0.y, w0, fma(-v1.y, w1, a[i0 + 1]));
+    }
+    a[k] = m0 ? w0 - 1.0 : w0;
+    a[k + 1] = m1 ? w1 - 1.0 : w1;
+  }
+  if (N % 2) {  // trailing scalar pivot
+    constexpr int k = N - 1;
+    double* st = stage + (((k >> 1)) & 1) * 64;
+    if (lane < N) st[lane] = a[k];
+    const double p = __shfl_sync(0xffffffffu, a[k], k);
+    const double ip = gj_rcp(p);
+    const bool me = lane == k;
+    if (me) piv = p;
+    const double w = (me ? a[k] - 1.0 : a[k]) * ip;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < k; ++i) a[i] = fma(-st[i], w, a[i]);
+    a[k] = me ? w - 1.0 : w;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = -a[i];
+  // pivots: even lanes hold p00, odd lanes 1/d1 (the trailing scalar pivot as is)
+  double d = (lane & 1) && lane < N - (N % 2) ? 1.0 / piv : piv;
+  const bool bad = lane < N && !(d > 0.0);
+  double mn = lane < N ? d : 1e300, mx = lane < N ? d : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (__any_sync(0xffffffffu, bad)) mn = -1.0;
+  pmin = fmin(pmin, mn);
+  pmax = fmax(pmax, mx);
+}

@@ -180,7 +180,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     __syncwarp();
     double pmin = 1e300, pmax = 0.0;
-    warp_gj_inverse2<D3>(a, stM(e), lane, pmin, pmax);
+    gj_sweep_inverse<D3>(a, stM(e), lane, pmin, pmax);
     const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
     if (lane < D3) {  // symmetric: row-wise stores are conflict-free
 #pragma unroll
@@ -402,7 +402,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             for (int i = 0; i < D3; ++i) a[i] = lane < D3 ? Sb(e)[lane + i * LD] : 0.0;
             double pmin = 1e300, pmax = 0.0;
 #ifndef HDG_DIAG_NO_GJ
-            warp_gj_inverse2<D3>(a, stS(e), lane, pmin, pmax);
+            gj_sweep_inverse<D3>(a, stS(e), lane, pmin, pmax);
 #else
             pmin = pmax = 1.0;
 #endif

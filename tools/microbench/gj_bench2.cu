@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(512) gj_smem(double* out, long long* cyc, int 
         else a[i] = lane < N ? S[rr + c * LD] : 0.0;
       }
       if (V == 1) warp_gj_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
-      else warp_gj_inverse2<N>(a, stage + warp * 128, lane, pmin, pmax);
+      else gj_sweep_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
       if (lane < N) {
 #pragma unroll
         for (int i = 0; i < N; ++i) {
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(512) gj_reg(double* out, long long* cyc, int r
     long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
       if (V == 1) warp_gj_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
-      else warp_gj_inverse2<N>(a, stage + warp * 128, lane, pmin, pmax);
+      else gj_sweep_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
     }
     long long t1 = clock64();
     if (lane == 0) cyc[blockIdx.x * 16 + warp] = (t1 - t0) / reps;
