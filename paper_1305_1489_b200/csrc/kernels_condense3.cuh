@@ -55,8 +55,10 @@ struct C3Dims {
   static constexpr int OFF_FS = OFF_F + LD;        // LD: Si f
   static constexpr int OFF_STG = round_up(OFF_FS + LD, 2);  // 128: GJ column stage (16 B aligned)
   static constexpr int OFF_STG2 = OFF_STG + 128;            // 128: second GJ stage
-  static constexpr int OFF_GEO = OFF_STG2 + 128;            // 2 x 32: geometry records (cur/next)
-  static constexpr int OFF_COL = OFF_GEO + 64;              // second column-data buffer
+  // 2 x 64: element records (cur/next): [0,30) geometry, [32,41) metric
+  // G(h,h') = sum_s a(s,h) a(s,h'), [48,64) face normal products n_l1 . n_l2
+  static constexpr int OFF_GEO = OFF_STG2 + 128;
+  static constexpr int OFF_COL = OFF_GEO + 128;             // second column-data buffer
   static constexpr int OFF_DP = OFF_COL + 8 * MP;           // packed D
   static constexpr int PER_ELT = OFF_DP + round_up(NSYM, 2);
   static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
@@ -108,10 +110,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int NGJ = 2 * EPB;               // GJ tasks in P3
   constexpr bool GJ_SEP = NWT > NGJ;         // GJ warps do nothing else in P3
   extern __shared__ double smem[];
-  __shared__ unsigned short pk_rc[Dm::NSYM];  // packed lower index -> row | col << 8
   for (int i = threadIdx.x; i < EPB * Dm::PER_ELT + Dm::CTA_EXTRA; i += blockDim.x) smem[i] = 0.0;
-  for (int j = threadIdx.x; j < D3; j += blockDim.x)
-    for (int i = j; i < D3; ++i) pk_rc[sym_idx(i, j, D3)] = static_cast<unsigned short>(i | (j << 8));
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -137,7 +136,27 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   auto stS = [&](int e) { return B(e) + Dm::OFF_STG; };
   auto stM = [&](int e) { return B(e) + Dm::OFF_STG2; };
   auto colb = [&](int e, int b) { return B(e) + (b ? Dm::OFF_COL : Dm::OFF_NSC); };
-  auto sgb = [&](int e, int b) { return B(e) + Dm::OFF_GEO + 32 * b; };
+  auto sgb = [&](int e, int b) { return B(e) + Dm::OFF_GEO + 64 * b; };
+  // per-element tables derived from the geometry record (warp-wide)
+  auto build_tables = [&](double* sg) {
+    if (lane < 9) {
+      const int h = lane / 3, h2 = lane % 3;
+      sg[32 + lane] = sg[1 + h] * sg[1 + h2] + sg[4 + h] * sg[4 + h2] + sg[7 + h] * sg[7 + h2];
+    } else if (lane >= 16) {
+      const int l1 = (lane - 16) >> 2, l2 = lane & 3;
+      sg[48 + (lane - 16)] = sg[10 + 3 * l1] * sg[10 + 3 * l2] + sg[11 + 3 * l1] * sg[11 + 3 * l2] +
+                             sg[12 + 3 * l1] * sg[12 + 3 * l2];
+    }
+  };
+  // packed lower column `lane` of a symmetric inverse held in registers -> recovery cache
+  auto store_factor = [&](const double (&a)[D3], long K, int off) {
+    if (factors && lane < D3) {
+      double* dst = factors + K * Dm::FACTORS + off + lane * (2 * D3 - lane + 1) / 2 - lane;
+#pragma unroll
+      for (int i = 0; i < D3; ++i)
+        if (i >= lane) dst[i] = a[i];
+    }
+  };
 
   const long stride = long(gridDim.x) * EPB;
   long K0 = long(blockIdx.x) * EPB;
@@ -170,9 +189,11 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
     }
   };
-  auto invert_M_staged = [&](int e, long K) {  // packed M staged in Mi(e) by cp.async (warp-wide)
+  // M^-1 of element K (packed M at P, global or the staging copy in Mi(e)):
+  // warp-register sweep, full LD-strided result into Mi(e), packed lower part
+  // straight from the registers into the recovery cache (warp-wide)
+  auto invert_M = [&](int e, long K, const double* P) {
     double a[D3];
-    const double* P = Mi(e);
 #pragma unroll
     for (int i = 0; i < D3; ++i) {
       const int r = i > lane ? i : lane, c = i > lane ? lane : i;
@@ -186,25 +207,8 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int i = 0; i < D3; ++i) Mi(e)[lane + i * LD] = a[i];
     }
+    store_factor(a, K, 0);
     if (bad && lane == 0) flag_bad(bad_element, K);
-  };
-  auto invert_M = [&](int e, long K) {  // warp-wide
-    double a[D3];
-    const bool bad = warp_inverse_packed<D3>(Msym + K * Dm::NSYM, a, stM(e), lane);
-    if (lane < D3) {
-#pragma unroll
-      for (int i = 0; i < D3; ++i) Mi(e)[i + lane * LD] = a[i];
-    }
-    if (bad && lane == 0) flag_bad(bad_element, K);
-  };
-  // packed lower triangle of an LD-strided symmetric smem matrix -> recovery cache (all threads)
-  auto write_factor = [&](long Kb, int off, bool si) {
-    for (int idx = threadIdx.x; idx < EPB * Dm::NSYM; idx += NT) {
-      const int e = idx / Dm::NSYM, p = idx - e * Dm::NSYM;
-      const int rc = pk_rc[p];
-      if (Kb + e < nelt)
-        factors[(Kb + e) * Dm::FACTORS + off + p] = (si ? Sb(e) : Mi(e))[(rc & 255) + (rc >> 8) * LD];
-    }
   };
 
   // ---- prologue: first batch
@@ -212,11 +216,13 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     load_Df_async(K0);
     load_geometry(K0, 0, threadIdx.x, NT);
     for (int e = warp; e < EPB; e += NWT)
-      if (K0 + e < nelt) invert_M(e, K0 + e);
+      if (K0 + e < nelt) invert_M(e, K0 + e, Msym + (K0 + e) * Dm::NSYM);
     cp_async_wait_all();
     __syncthreads();
-    if (factors) write_factor(K0, 0, false);
-    for (int e = warp; e < EPB; e += NWT) build_columns<D2, D3, M, MP>(sgb(e, 0), colb(e, 0), lane);
+    for (int e = warp; e < EPB; e += NWT) {
+      build_columns<D2, D3, M, MP>(sgb(e, 0), colb(e, 0), lane);
+      build_tables(sgb(e, 0));
+    }
     __syncthreads();
   }
 
@@ -244,14 +250,11 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           dmma(q[1][0], q[1][1], a, Ch[D3 * LD + o]);
           dmma(q[2][0], q[2][1], a, Ch[2 * D3 * LD + o]);
         }
-        const double* a9 = sg + 1;
         const int c0 = nt * 8 + 2 * t, r = m * 8 + g;
         if (r < LD) {
 #pragma unroll
           for (int h = 0; h < 3; ++h) {
-            const double g0 = a9[h] * a9[0] + a9[3 + h] * a9[3] + a9[6 + h] * a9[6];
-            const double g1 = a9[h] * a9[1] + a9[3 + h] * a9[4] + a9[6 + h] * a9[7];
-            const double g2 = a9[h] * a9[2] + a9[3 + h] * a9[5] + a9[6 + h] * a9[8];
+            const double g0 = sg[32 + 3 * h], g1 = sg[33 + 3 * h], g2 = sg[34 + 3 * h];
             double* R = Yb(e) + h * RH;
             if (c0 < D3) R[r + c0 * LD] = r < D3 ? g0 * q[0][0] + g1 * q[1][0] + g2 * q[2][0] : 0.0;
             if (c0 + 1 < D3) R[r + (c0 + 1) * LD] = r < D3 ? g0 * q[0][1] + g1 * q[1][1] + g2 * q[2][1] : 0.0;
@@ -259,8 +262,11 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         }
       } else {
         const int nt = sub - MT * MT;
-        const int* wb = reinterpret_cast<const int*>(colb(e, cur) + 4 * MP);
-        const int wbc = wb[nt * 8 + g];
+        const double* col = colb(e, cur);
+        const int* wb = reinterpret_cast<const int*>(col + 4 * MP);
+        const int cz = nt * 8 + g, wbc = wb[cz];
+        const double tc = col[3 * MP + cz];
+        double* Vi = Vb(e) + cz * LD;  // V starts as T_l W_l^T (the W fragment is at hand)
         double acc[MT][2];
 #pragma unroll
         for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
@@ -268,6 +274,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         for (int kk = 0; kk < KS; ++kk) {
           const int k = kk * 4 + t;
           const double b = (wbc >= 0 && k < D3) ? __ldg(Wlm + wbc + k * D2) : 0.0;
+          Vi[k] = tc * b;
 #pragma unroll
           for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], mi[(m * 8 + g) + k * LD], b);
         }
@@ -330,26 +337,14 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       } else {  // V rows of row tile mt for FPT faces: the Chat_# fragments feed every face
         const int mt = (sub - NLS) / (4 / FPT), l0 = ((sub - NLS) % (4 / FPT)) * FPT;
         const int r = mt * 8 + g;
-        const double* col = colb(e, cur);
-        const double* Tc = col + 3 * MP;
-        const int* wb = reinterpret_cast<const int*>(col + 4 * MP);
-        const double* beta = col + 5 * MP;
+        const double* beta = colb(e, cur) + 5 * MP;
         const double* Z = Zb(e);
         double bl[FPT][3];
-        double acc[FPT][NTF][2];  // starts at T_l W_l^T (its loads overlap the DMMA chains)
+        double acc[FPT][NTF][2] = {};
 #pragma unroll
-        for (int f = 0; f < FPT; ++f) {
-          const int cl0 = (l0 + f) * D2, cl1 = cl0 + D2, nt0 = cl0 / 8;
+        for (int f = 0; f < FPT; ++f)
 #pragma unroll
-          for (int h = 0; h < 3; ++h) bl[f][h] = beta[h * MP + cl0];
-#pragma unroll
-          for (int j = 0; j < NTF; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int c = (nt0 + j) * 8 + 2 * t + h;
-              acc[f][j][h] = (c >= cl0 && c < cl1 && r < D3) ? Tc[c] * __ldg(Wlm + wb[c] + r * D2) : 0.0;
-            }
-        }
+          for (int h = 0; h < 3; ++h) bl[f][h] = beta[h * MP + (l0 + f) * D2];
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
           const int k = kk * 4 + t;
@@ -377,7 +372,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int c = (nt0 + j) * 8 + 2 * t + h;
-                if (c >= cl0 && c < cl1) V[r + c * LD] = r < tab.nu ? acc[f][j][h] : 0.0;
+                if (c >= cl0 && c < cl1) V[r + c * LD] = r < tab.nu ? acc[f][j][h] + V[r + c * LD] : 0.0;
               }
           }
         }
@@ -411,12 +406,13 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
               for (int i = 0; i < D3; ++i) Sb(e)[lane + i * LD] = a[i];
             }
+            store_factor(a, K, Dm::NSYM);
             if (bad && lane == 0) flag_bad(bad_element, K);
           } else if (has_next && Kn0 + e < nelt) {
 #ifdef HDG_DIAG_NO_GJ
             continue;
 #endif
-            invert_M_staged(e, Kn0 + e);  // packed M copied into the dead Mi(e) during P2
+            invert_M(e, Kn0 + e, Mi(e));  // packed M copied into the dead Mi(e) during P2
           }
         }
       }
@@ -473,23 +469,22 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       for (int k = 0; k < D3; ++k) s += Sb(e)[r + k * LD] * fv(e)[k];
       fs(e)[r] = s;
     }
-    if (factors) {
-      write_factor(K0, Dm::NSYM, true);           // S^-1 of this batch
-      if (has_next) write_factor(Kn0, 0, false);  // M^-1 of the next batch
-    }
     __syncthreads();
     if (has_next)
       for (int e = warp; e < EPB; e += NWT)
-        if (Kn0 + e < nelt) build_columns<D2, D3, M, MP>(sgb(e, cur ^ 1), colb(e, cur ^ 1), lane);
+        if (Kn0 + e < nelt) {
+          build_columns<D2, D3, M, MP>(sgb(e, cur ^ 1), colb(e, cur ^ 1), lane);
+          build_tables(sgb(e, cur ^ 1));
+        }
 
     PHASE_MARK(batch, 4);
     if (has_next) load_Df_async(Kn0);  // D, f of this batch are dead after P4
     // ---- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (lower tiles, mirrored) | Cf
     for (int task = warp; task < nb * NLP; task += NWT) {  // tile pairs (mt, nt0..nt0+1) of a row
       const int e = task / NLP;
-      int mt = 0, rem = task % NLP;
-      while (rem >= (mt + 2) / 2) { rem -= (mt + 2) / 2; ++mt; }
-      const int nt0 = 2 * rem, r = mt * 8 + g;
+      const int tp = task % NLP;  // row mt holds (mt + 2) / 2 pairs; rows < mt hold (mt + 1)^2 / 4
+      const int mt = int(2.0f * sqrtf(float(tp) + 0.25f)) - 1;
+      const int nt0 = 2 * (tp - (mt + 1) * (mt + 1) / 4), r = mt * 8 + g;
       const bool two = nt0 + 1 <= mt;
       const double* V = Vb(e);
       const double* Vs = Yb(e);
@@ -510,11 +505,9 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         }
       }
       if (r < M) {
-        const double* sg = sgb(e, cur);
-        const double* nsc = colb(e, cur);
-        const double* Tc = nsc + 3 * MP;
         const int l1 = r / D2;
-        const double n1x = sg[10 + 3 * l1], n1y = sg[11 + 3 * l1], n1z = sg[12 + 3 * l1];
+        const double* nn4 = sgb(e, cur) + 48 + 4 * l1;
+        const double* Tc = colb(e, cur) + 3 * MP;
         double* Ck = Cout + (K0 + e) * M * M;
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -524,8 +517,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             const int c = (nt0 + u) * 8 + 2 * t + h;
             if (c > r || c >= M) continue;
             const int l2 = c / D2;
-            const double nn = n1x * nsc[c] + n1y * nsc[MP + c] + n1z * nsc[2 * MP + c];
-            double val = nn * z[u][h] - v[u][h];
+            double val = nn4[l2] * z[u][h] - v[u][h];
             if (l1 == l2) val += Tc[c] * DDs[(r - l1 * D2) + (c - l2 * D2) * D2];
             Ck[r + c * M] = val;
             if (c != r) Ck[c + r * M] = val;
