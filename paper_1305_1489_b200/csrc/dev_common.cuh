@@ -89,6 +89,13 @@ __device__ __forceinline__ double eval_field(const FieldDev& F, double x, double
   return run_program(F, x, y, z);
 }
 
+// ------------------------------------------------------------- cp.async
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // ------------------------------------------------------------------ DMMA
 // D(8x8) += A(8x4, row) * B(4x8, col), fp64 tensor-core MMA (SASS DMMA.8x8x4).
 // Lane layout: a = A[g][t], b = B[t][g], c = {C[g][2t], C[g][2t+1]}, g = lane/4, t = lane%4.

@@ -27,7 +27,7 @@ constexpr int kPost2LDG = kPost2EB;  // G rows [q][e]: B-fragment reads are conf
 
 struct Post2Dims {
   int n, nq, nq4, d3k, npad, ns, nsp;
-  int off_verts, off_sg, off_qc, off_gm, off_R, off_Rp, off_GS, total;
+  int off_verts, off_sg, off_qc, off_gm, off_R, off_Rp, off_GS, off_ks, total;
   __host__ __device__ Post2Dims(int n_, int nq_, int d3k_) : n(n_), nq(nq_), d3k(d3k_) {
     nq4 = (nq + 3) / 4 * 4;
     npad = (n + 7) / 8 * 8;
@@ -42,7 +42,8 @@ struct Post2Dims {
     const int rp = kPost2Warps * npad * kPost2EB, solve = kPost2Warps * (128 + 64);
     off_GS = off_Rp + (rp > solve ? rp : solve);      // G (3 nq4 x LDG) | S (EB x nsp)
     const int g = 3 * nq4 * kPost2LDG, sgs = kPost2EB * nsp;
-    total = off_GS + (g > sgs ? g : sgs);
+    off_ks = off_GS + (g > sgs ? g : sgs);            // 2 x nq x EB: sampled kappa (double buffer)
+    total = off_ks + 2 * nq * kPost2EB;
   }
 };
 
@@ -66,8 +67,22 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
   double* Sp = psm + dm.off_GS;  // after R: packed S per element
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const double* qs[3] = {qx, qy, qz};
+  // sampled kappa^-1 at the nodes: the next batch's samples stream in by
+  // cp.async while this batch computes (the samples are the kernel's main
+  // HBM stream)
+  const bool sampled = kap.kind == HDG_FIELD_SAMPLED;
+  auto prefetch_kappa = [&](long Kb, int buf) {
+    const long cnt = (nelt - Kb < kPost2EB ? nelt - Kb : kPost2EB) * long(nq);
+    double* dst = psm + dm.off_ks + buf * nq * kPost2EB;
+    for (long i = threadIdx.x; i < cnt; i += blockDim.x) cp_async8(dst + i, kap.samples + Kb * nq + i);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int kbuf = 0;
+  if (sampled && long(blockIdx.x) * kPost2EB < nelt) prefetch_kappa(long(blockIdx.x) * kPost2EB, 0);
 
-  for (long K0 = long(blockIdx.x) * kPost2EB; K0 < nelt; K0 += long(gridDim.x) * kPost2EB) {
+  for (long K0 = long(blockIdx.x) * kPost2EB; K0 < nelt; K0 += long(gridDim.x) * kPost2EB, kbuf ^= 1) {
+    const long Kn0 = K0 + long(gridDim.x) * kPost2EB;
+    if (sampled && Kn0 < nelt) prefetch_kappa(Kn0, kbuf ^ 1);
     // ---- stage geometry, vertices, coefficients
     for (int idx = threadIdx.x; idx < kPost2EB * 32; idx += blockDim.x) {
       const int e = idx >> 5, i = idx & 31;
@@ -92,6 +107,10 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
       const long K = K0 + e;
       qc[idx] = K < nelt ? qs[s][K * d3k + i] : 0.0;
     }
+    if (sampled) {  // this batch's kappa samples (the next batch's group may stay in flight)
+      if (Kn0 < nelt) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     __syncthreads();
     for (int idx = threadIdx.x; idx < 12 * kPost2EB; idx += blockDim.x) {
       const int h = idx / kPost2EB, e = idx - h * kPost2EB;
@@ -104,32 +123,51 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
       }
       gm[idx] = v;
     }
-    // ---- G_#(q, e) at the P_{k+1} nodes (rows q >= nq are zero padding)
-    for (int idx = threadIdx.x; idx < nq4 * kPost2EB; idx += blockDim.x) {
-      const int e = idx / nq4, q = idx - e * nq4;  // node fastest: coalesced samples and P rows
-      const long K = K0 + e;
-      double gv[3] = {0.0, 0.0, 0.0};
-      if (q < nq && K < nelt) {
-        const double l0 = __ldg(tp.bary + q), l1 = __ldg(tp.bary + nq + q), l2 = __ldg(tp.bary + 2 * nq + q),
-                     l3 = __ldg(tp.bary + 3 * nq + q);
-        const double* V = verts + e;
-        const double x = l0 * V[0] + l1 * V[kPost2EB] + l2 * V[2 * kPost2EB] + l3 * V[3 * kPost2EB];
-        const double y = l0 * V[4 * kPost2EB] + l1 * V[5 * kPost2EB] + l2 * V[6 * kPost2EB] + l3 * V[7 * kPost2EB];
-        const double z = l0 * V[8 * kPost2EB] + l1 * V[9 * kPost2EB] + l2 * V[10 * kPost2EB] + l3 * V[11 * kPost2EB];
-        const double wk = __ldg(tp.w + q) / eval_field(kap, x, y, z, q, K, nq);
-        double Q0 = 0.0, Q1 = 0.0, Q2 = 0.0;
-        for (int i = 0; i < d3k; ++i) {
-          const double p = __ldg(tp.P + long(i) * nq + q);
-          Q0 = fma(p, qc[(0 * d3k + i) * kPost2EB + e], Q0);
-          Q1 = fma(p, qc[(1 * d3k + i) * kPost2EB + e], Q1);
-          Q2 = fma(p, qc[(2 * d3k + i) * kPost2EB + e], Q2);
+    // ---- G_#(q, e) at the P_{k+1} nodes (rows q >= nq are zero padding):
+    //      Q_s = P_k^T qc_s as DMMA tiles (node rows, the 8 elements as N), the
+    //      P_k fragment feeding the three components; then the Piola mix,
+    //      weight and kappa^-1 in the epilogue
+    {
+      const int mts = (nq4 + 7) / 8, ksk = (d3k + 3) / 4;
+      for (int mt = warp; mt < mts; mt += kPost2Warps) {
+        double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        const int qa = mt * 8 + g;
+        for (int kk = 0; kk < ksk; ++kk) {
+          const int i = kk * 4 + t;
+          const double a = (qa < nq && i < d3k) ? __ldg(tp.P + long(i) * nq + qa) : 0.0;
+#pragma unroll
+          for (int s = 0; s < 3; ++s)
+            dmma(acc[s][0], acc[s][1], a, i < d3k ? qc[(s * d3k + i) * kPost2EB + g] : 0.0);
         }
-        const double* a9 = sg + 32 * e + 1;
 #pragma unroll
-        for (int h = 0; h < 3; ++h) gv[h] = (Q0 * a9[h] + Q1 * a9[3 + h] + Q2 * a9[6 + h]) * wk;
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int e = 2 * t + h2;
+          const long K = K0 + e;
+          double gv[3] = {0.0, 0.0, 0.0};
+          if (qa < nq && K < nelt) {
+            double x = 0.0, y = 0.0, z = 0.0;
+            if (kap.kind == HDG_FIELD_PROGRAM) {
+              const double l0 = __ldg(tp.bary + qa), l1 = __ldg(tp.bary + nq + qa),
+                           l2 = __ldg(tp.bary + 2 * nq + qa), l3 = __ldg(tp.bary + 3 * nq + qa);
+              const double* V = verts + e;
+              x = l0 * V[0] + l1 * V[kPost2EB] + l2 * V[2 * kPost2EB] + l3 * V[3 * kPost2EB];
+              y = l0 * V[4 * kPost2EB] + l1 * V[5 * kPost2EB] + l2 * V[6 * kPost2EB] + l3 * V[7 * kPost2EB];
+              z = l0 * V[8 * kPost2EB] + l1 * V[9 * kPost2EB] + l2 * V[10 * kPost2EB] + l3 * V[11 * kPost2EB];
+            }
+            const double kq = sampled ? psm[dm.off_ks + kbuf * nq * kPost2EB + e * nq + qa]
+                                      : eval_field(kap, x, y, z, qa, K, nq);
+            const double wk = __ldg(tp.w + qa) / kq;
+            const double* a9 = sg + 32 * e + 1;
+#pragma unroll
+            for (int h = 0; h < 3; ++h)
+              gv[h] = (acc[0][h2] * a9[h] + acc[1][h2] * a9[3 + h] + acc[2][h2] * a9[6 + h]) * wk;
+          }
+          if (qa < nq4) {
+#pragma unroll
+            for (int h = 0; h < 3; ++h) G[(h * nq4 + qa) * kPost2LDG + e] = gv[h];
+          }
+        }
       }
-#pragma unroll
-      for (int h = 0; h < 3; ++h) G[(h * nq4 + q) * kPost2LDG + e] = gv[h];
     }
     __syncthreads();
 
@@ -140,9 +178,11 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
       double acc[5][2];
 #pragma unroll
       for (int m = 0; m < 5; ++m) acc[m][0] = acc[m][1] = 0.0;
+      int h = (k0 * 4) / nq4, q0 = k0 * 4 - h * nq4;  // nq4 % 4 == 0: one component per k-step
 #pragma unroll 4
-      for (int kk = k0; kk < k1; ++kk) {
-        const int k = kk * 4 + t, h = k / nq4, q = k - h * nq4;
+      for (int kk = k0; kk < k1; ++kk, q0 += 4) {
+        if (q0 >= nq4) { q0 -= nq4; ++h; }
+        const int k = kk * 4 + t, q = q0 + t;
         const double b = G[k * kPost2LDG + g];
         const double* Pd = tp.Pd + long(h) * nq * n;
 #pragma unroll
@@ -210,7 +250,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
         for (int i = 0; i < MA; ++i) a[i] = lane < MA ? Sat(i, lane) : 0.0;
         __syncwarp();
         double pmin = 1e300, pmax = 0.0;
-        warp_gj_inverse<MA>(a, stage, lane, pmin, pmax);  // a = column `lane` of A^-1 (symmetric)
+        gj_sweep_inverse<MA>(a, stage, lane, pmin, pmax);  // a = column `lane` of A^-1 (symmetric)
         // z = A^-1 r_A and, for the border, Y = A^-1 B: lane i holds row i (A^-1 symmetric)
         double z = 0.0;
 #pragma unroll
