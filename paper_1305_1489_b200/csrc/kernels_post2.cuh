@@ -21,9 +21,10 @@
 
 namespace hdgb {
 
-constexpr int kPost2EB = 8;     // elements per CTA (one DMMA N-tile)
-constexpr int kPost2Warps = 8;  // one warp per element in the solve phase
-constexpr int kPost2LDG = kPost2EB;  // G rows [q][e]: B-fragment reads are conflict-free at 8
+constexpr int kPost2EB = 16;    // elements per CTA (two DMMA N-tiles)
+constexpr int kPost2NT = kPost2EB / 8;
+constexpr int kPost2Warps = 16;  // one warp per element in the solve phase
+constexpr int kPost2LDE = kPost2EB + 4;  // [row][e] operand rows: B-fragment reads conflict-free
 
 struct Post2Dims {
   int n, nq, nq4, d3k, npad, ns, nsp;
@@ -35,13 +36,13 @@ struct Post2Dims {
     nsp = (ns + 7) / 8 * 8;
     off_verts = 0;                                    // 12 x EB
     off_sg = off_verts + 12 * kPost2EB;               // 32 x EB geometry records
-    off_qc = off_sg + 32 * kPost2EB;                  // 3 x d3k x EB
-    off_gm = off_qc + 3 * d3k * kPost2EB;             // 12 x EB (rows 9..11 zero)
-    off_R = off_gm + 12 * kPost2EB;                   // npad x EB
-    off_Rp = off_R + npad * kPost2EB;                 // warps x npad x EB partials
-    const int rp = kPost2Warps * npad * kPost2EB, solve = kPost2Warps * (128 + 64);
-    off_GS = off_Rp + (rp > solve ? rp : solve);      // G (3 nq4 x LDG) | S (EB x nsp)
-    const int g = 3 * nq4 * kPost2LDG, sgs = kPost2EB * nsp;
+    off_qc = off_sg + 32 * kPost2EB;                  // 3 x d3k x LDE
+    off_gm = off_qc + 3 * d3k * kPost2LDE;            // 12 x LDE (rows 9..11 zero)
+    off_R = off_gm + 12 * kPost2LDE;                  // npad x EB
+    off_Rp = off_R + npad * kPost2EB;                 // 3 x npad x EB partials | solve scratch
+    const int rp = 3 * npad * kPost2EB, solve = kPost2Warps * (128 + 64);
+    off_GS = off_Rp + (rp > solve ? rp : solve);      // G (3 nq4 x LDE) | S (EB x nsp)
+    const int g = 3 * nq4 * kPost2LDE, sgs = kPost2EB * nsp;
     off_ks = off_GS + (g > sgs ? g : sgs);            // 2 x nq x EB: sampled kappa (double buffer)
     total = off_ks + 2 * nq * kPost2EB;
   }
@@ -50,7 +51,7 @@ struct Post2Dims {
 __device__ __forceinline__ int pk_lower(int i, int j, int n) { return j * n - j * (j - 1) / 2 + (i - j); }
 
 template <int M_>  // trailing system size n - 1
-__global__ void __launch_bounds__(kPost2Warps * 32, 2)
+__global__ void __launch_bounds__(kPost2Warps * 32, 1)
 postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, const double* __restrict__ qx,
                     const double* __restrict__ qy, const double* __restrict__ qz, const double* __restrict__ u,
                     double* __restrict__ ustar) {
@@ -105,7 +106,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
     for (int idx = threadIdx.x; idx < 3 * d3k * kPost2EB; idx += blockDim.x) {
       const int e = idx % kPost2EB, si = idx / kPost2EB, s = si / d3k, i = si - s * d3k;
       const long K = K0 + e;
-      qc[idx] = K < nelt ? qs[s][K * d3k + i] : 0.0;
+      qc[si * kPost2LDE + e] = K < nelt ? qs[s][K * d3k + i] : 0.0;
     }
     if (sampled) {  // this batch's kappa samples (the next batch's group may stay in flight)
       if (Kn0 < nelt) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -121,7 +122,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
         const int p = h / 3, r = h % 3;
         v = detB > 0.0 ? (a9[p] * a9[r] + a9[3 + p] * a9[3 + r] + a9[6 + p] * a9[6 + r]) / detB : 0.0;
       }
-      gm[idx] = v;
+      gm[h * kPost2LDE + e] = v;
     }
     // ---- G_#(q, e) at the P_{k+1} nodes (rows q >= nq are zero padding):
     //      Q_s = P_k^T qc_s as DMMA tiles (node rows, the 8 elements as N), the
@@ -130,18 +131,21 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
     {
       const int mts = (nq4 + 7) / 8, ksk = (d3k + 3) / 4;
       for (int mt = warp; mt < mts; mt += kPost2Warps) {
-        double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        double acc[3][kPost2NT][2] = {};
         const int qa = mt * 8 + g;
         for (int kk = 0; kk < ksk; ++kk) {
           const int i = kk * 4 + t;
           const double a = (qa < nq && i < d3k) ? __ldg(tp.P + long(i) * nq + qa) : 0.0;
 #pragma unroll
           for (int s = 0; s < 3; ++s)
-            dmma(acc[s][0], acc[s][1], a, i < d3k ? qc[(s * d3k + i) * kPost2EB + g] : 0.0);
+#pragma unroll
+            for (int j = 0; j < kPost2NT; ++j)
+              dmma(acc[s][j][0], acc[s][j][1], a, i < d3k ? qc[(s * d3k + i) * kPost2LDE + 8 * j + g] : 0.0);
         }
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int e = 2 * t + h2;
+        for (int jh = 0; jh < 2 * kPost2NT; ++jh) {
+          const int j = jh >> 1, h2 = jh & 1;
+          const int e = 8 * j + 2 * t + h2;
           const long K = K0 + e;
           double gv[3] = {0.0, 0.0, 0.0};
           if (qa < nq && K < nelt) {
@@ -160,68 +164,64 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
             const double* a9 = sg + 32 * e + 1;
 #pragma unroll
             for (int h = 0; h < 3; ++h)
-              gv[h] = (acc[0][h2] * a9[h] + acc[1][h2] * a9[3 + h] + acc[2][h2] * a9[6 + h]) * wk;
+              gv[h] = (acc[0][j][h2] * a9[h] + acc[1][j][h2] * a9[3 + h] + acc[2][j][h2] * a9[6 + h]) * wk;
           }
           if (qa < nq4) {
 #pragma unroll
-            for (int h = 0; h < 3; ++h) G[(h * nq4 + qa) * kPost2LDG + e] = gv[h];
+            for (int h = 0; h < 3; ++h) G[(h * nq4 + qa) * kPost2LDE + e] = gv[h];
           }
         }
       }
     }
     __syncthreads();
 
-    // ---- R = -(1/6) Pd^T G: K split over the warps, all M-tiles per warp
+    // ---- R = -(1/6) sum_# Pd_#^T G_#: one (row tile, component #) per warp,
+    //      the Pd fragment feeding both element tiles; 3 partials reduced below
     {
-      const int mts = npad / 8, ks = 3 * nq4 / 4;
-      const int k0 = warp * ks / kPost2Warps, k1 = (warp + 1) * ks / kPost2Warps;
-      double acc[5][2];
-#pragma unroll
-      for (int m = 0; m < 5; ++m) acc[m][0] = acc[m][1] = 0.0;
-      int h = (k0 * 4) / nq4, q0 = k0 * 4 - h * nq4;  // nq4 % 4 == 0: one component per k-step
+      const int mts = npad / 8;
+      for (int task = warp; task < 3 * mts; task += kPost2Warps) {
+        const int h = task / mts, m = task - h * mts, i = m * 8 + g;
+        const double* Pd = tp.Pd + long(h) * nq * n + long(i) * nq;
+        const double* Gh = G + h * nq4 * kPost2LDE;
+        double acc[kPost2NT][2][2] = {};  // two chains per tile (k-step parity)
 #pragma unroll 4
-      for (int kk = k0; kk < k1; ++kk, q0 += 4) {
-        if (q0 >= nq4) { q0 -= nq4; ++h; }
-        const int k = kk * 4 + t, q = q0 + t;
-        const double b = G[k * kPost2LDG + g];
-        const double* Pd = tp.Pd + long(h) * nq * n;
+        for (int kk = 0; kk < nq4 / 4; ++kk) {
+          const int q = kk * 4 + t;
+          const double a = (q < nq && i < n) ? __ldg(Pd + q) : 0.0;
 #pragma unroll
-        for (int m = 0; m < 5; ++m) {
-          if (m >= mts) break;
-          const int i = m * 8 + g;
-          const double a = (q < nq && i < n) ? __ldg(Pd + long(i) * nq + q) : 0.0;
-          dmma(acc[m][0], acc[m][1], a, b);
+          for (int j = 0; j < kPost2NT; ++j)
+            dmma(acc[j][kk & 1][0], acc[j][kk & 1][1], a, Gh[q * kPost2LDE + 8 * j + g]);
         }
-      }
-      for (int m = 0; m < mts; ++m) {
-        double* P = Rp + (warp * npad + m * 8 + g) * kPost2EB + 2 * t;
-        P[0] = acc[m][0];
-        P[1] = acc[m][1];
+#pragma unroll
+        for (int j = 0; j < kPost2NT; ++j) {
+          double* P = Rp + (h * npad + m * 8 + g) * kPost2EB + 8 * j + 2 * t;
+          P[0] = acc[j][0][0] + acc[j][1][0];
+          P[1] = acc[j][0][1] + acc[j][1][1];
+        }
       }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < npad * kPost2EB; idx += blockDim.x) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kPost2Warps; ++w) s += Rp[w * npad * kPost2EB + idx];
-      R[idx] = -(1.0 / 6.0) * s;
-    }
+    for (int idx = threadIdx.x; idx < npad * kPost2EB; idx += blockDim.x)
+      R[idx] = -(1.0 / 6.0) * (Rp[idx] + Rp[npad * kPost2EB + idx] + Rp[2 * npad * kPost2EB + idx]);
     // ---- S packed lower = ShatP^T-combination gm (G is dead: S overwrites it)
     {
       const int mts = dm.nsp / 8;
       for (int mt = warp; mt < mts; mt += kPost2Warps) {
-        double c0 = 0.0, c1 = 0.0;
+        double c[kPost2NT][2] = {};
         const int idx = mt * 8 + g;
 #pragma unroll
         for (int kk = 0; kk < 3; ++kk) {
           const int h = kk * 4 + t;
           const double a = (h < 9 && idx < ns) ? __ldg(tp.ShatP + long(h) * ns + idx) : 0.0;
-          dmma(c0, c1, a, gm[h * kPost2EB + g]);
+#pragma unroll
+          for (int j = 0; j < kPost2NT; ++j) dmma(c[j][0], c[j][1], a, gm[h * kPost2LDE + 8 * j + g]);
         }
-        __syncwarp();
         if (idx < ns) {
-          Sp[(2 * t) * dm.nsp + idx] = c0;
-          Sp[(2 * t + 1) * dm.nsp + idx] = c1;
+#pragma unroll
+          for (int j = 0; j < kPost2NT; ++j) {
+            Sp[(8 * j + 2 * t) * dm.nsp + idx] = c[j][0];
+            Sp[(8 * j + 2 * t + 1) * dm.nsp + idx] = c[j][1];
+          }
         }
       }
     }
