@@ -183,6 +183,17 @@ int hdg_b200_pattern_fill(hdg_ctx* ctx, int nfc, int d2, const int64_t* d_faceba
 int hdg_b200_scatter(hdg_ctx* ctx, int nelt, int d2, const int* d_facebyele,
                      const uint8_t* d_slot, const int64_t* d_facebase, const double* d_C,
                      const double* d_Cf, double* d_vals, double* d_b);
+/* Face-ordered K4 (same result as hdg_b200_scatter, bit for bit): each face's
+ * block row of H is one contiguous run, gathered from its elements' C
+ * (symmetric: the contiguous column block l is the transposed row block) and
+ * written once; the interior diagonal blocks and b sum the two sides in
+ * registers. Every entry of d_vals and d_b is written (no zeroing needed).
+ * d_sides (nfc x 2) comes from hdg_b200_face_sides: e*4 + l of the face's
+ * elements, lower element first, -1 for a one-sided face.                  */
+int hdg_b200_face_sides(hdg_ctx* ctx, int nelt, int nfc, const int* d_facebyele, int* d_sides);
+int hdg_b200_scatter_faces(hdg_ctx* ctx, int nfc, int d2, const int* d_sides,
+                           const uint8_t* d_slot, const int64_t* d_facebase, const double* d_C,
+                           const double* d_Cf, double* d_vals, double* d_b);
 
 /* --------------------------------------------------- K6: postprocess
  * Replaces postprocess_star (postprocess.cpp:33-74) with stiffness_matrices

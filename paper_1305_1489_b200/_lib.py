@@ -98,6 +98,8 @@ _SIGS = {
     "hdg_b200_recover": (C.c_int, [P, C.c_int, C.POINTER(hdg_geometry), P, P, P, P, P, P, P]),
     "hdg_b200_pattern_fill": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P]),
     "hdg_b200_scatter": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P, P, P, P]),
+    "hdg_b200_face_sides": (C.c_int, [P, C.c_int, C.c_int, P, P]),
+    "hdg_b200_scatter_faces": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P, P, P, P]),
     "hdg_b200_postprocess": (C.c_int, [P, C.c_int, C.POINTER(hdg_geometry), hdg_field, P, P, P, P, P]),
     "hdg_b200_convection_block": (C.c_int, [P, C.c_int, C.POINTER(hdg_geometry), hdg_field, hdg_field,
                                             hdg_field, P, P, P]),

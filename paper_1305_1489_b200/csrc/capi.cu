@@ -1011,6 +1011,56 @@ int hdg_b200_scatter(hdg_ctx* c, int nelt, int d2, const int* d_facebyele, const
   });
 }
 
+int hdg_b200_face_sides(hdg_ctx* c, int nelt, int nfc, const int* d_facebyele, int* d_sides) {
+  return guarded([&] {
+    require(c && d_facebyele && d_sides && nelt > 0 && nfc > 0, HDG_EINVAL, "bad argument");
+    set_device(c);
+    const int grid = int(std::min<long>((long(nfc) + 255) / 256, long(c->sms) * 8));
+    face_sides_init_kernel<<<grid, 256, 0, c->stream>>>(nfc, d_sides);
+    const int grid2 = int(std::min<long>((4L * nelt + 255) / 256, long(c->sms) * 8));
+    face_sides_kernel<<<grid2, 256, 0, c->stream>>>(nelt, d_facebyele, d_sides);
+    face_sides_fix_kernel<<<grid, 256, 0, c->stream>>>(nfc, d_sides);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_scatter_faces(hdg_ctx* c, int nfc, int d2, const int* d_sides, const uint8_t* d_slot,
+                           const int64_t* d_facebase, const double* d_C, const double* d_Cf, double* d_vals,
+                           double* d_b) {
+  return guarded([&] {
+    require(c && d_sides && d_slot && d_facebase && d_C && d_Cf && d_vals && d_b && nfc > 0, HDG_EINVAL,
+            "bad argument");
+    set_device(c);
+    stage_begin(c, 4);
+    auto go = [&](auto kern, int D2) {
+      const int m = 4 * D2;
+      const size_t per_warp = size_t(2 * m * D2 + 8) * sizeof(double);
+      const int nw = int(std::min<size_t>(kFaceRowWarps, (200 * 1024) / per_warp));
+      const size_t smem = per_warp * kFaceRowWarps;  // every warp's slice (the surplus warps exit)
+      const size_t smem_used = per_warp * nw;
+      CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_used)));
+      int occ = 0;
+      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFaceRowWarps * 32, smem_used));
+      const long need = (long(nfc) + nw - 1) / nw;
+      const int grid = int(std::min<long>(need, long(c->sms) * std::max(occ, 1)));
+      (void)smem;
+      kern<<<grid, kFaceRowWarps * 32, smem_used, c->stream>>>(nfc, d_sides, d_slot, d_facebase, d_C, d_Cf, d_vals,
+                                                            d_b, nw);
+    };
+    switch (d2) {
+      case 1: go(scatter_faces_kernel<1>, 1); break;
+      case 3: go(scatter_faces_kernel<3>, 3); break;
+      case 6: go(scatter_faces_kernel<6>, 6); break;
+      case 10: go(scatter_faces_kernel<10>, 10); break;
+      case 15: go(scatter_faces_kernel<15>, 15); break;
+      case 21: go(scatter_faces_kernel<21>, 21); break;
+      default: throw HdgError{HDG_EINVAL, "scatter_faces: d2 must be dim P_k(triangle), k <= 5"};
+    }
+    CUDA_OK(cudaGetLastError());
+    stage_end(c, 4);
+  });
+}
+
 // ------------------------------------------------------------------- K6
 int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field kappa, const double* qx,
                          const double* qy, const double* qz, const double* u, double* ustar) {

@@ -3,6 +3,8 @@
 // element index fastest in every SoA array so loads and stores coalesce.
 #pragma once
 
+#include <climits>
+
 #include "dev_common.cuh"
 #include "kernels_local.cuh"
 
@@ -235,6 +237,89 @@ scatter2_kernel(int nelt, int d2, const int* __restrict__ facebyele, const uint8
     for (int r = lane; r < m; r += 32) {
       const int l = r / d2;
       atomicAdd(b + long(facebyele[long(l) * nelt + K]) * d2 + (r - l * d2), Cf[K * m + r]);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------- face sides
+// sides[2f], sides[2f+1] = element-local codes e*4+l of face f's two elements
+// (lower element first), or -1 for a face with one element.
+__global__ void face_sides_init_kernel(int nfc, int* __restrict__ sides) {
+  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < nfc; i += long(gridDim.x) * blockDim.x) {
+    sides[2 * i] = INT_MAX;
+    sides[2 * i + 1] = -1;
+  }
+}
+__global__ void face_sides_kernel(int nelt, const int* __restrict__ facebyele, int* __restrict__ sides) {
+  const long n = 4L * nelt;
+  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+    const int l = int(i / nelt), K = int(i - long(l) * nelt);
+    const int f = facebyele[i], code = K * 4 + l;
+    atomicMin(sides + 2 * f, code);
+    atomicMax(sides + 2 * f + 1, code);
+  }
+}
+__global__ void face_sides_fix_kernel(int nfc, int* __restrict__ sides) {
+  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < nfc; i += long(gridDim.x) * blockDim.x)
+    if (sides[2 * i + 1] == sides[2 * i]) sides[2 * i + 1] = -1;
+}
+
+// ------------------------------------------------- K4 v3: face-row gather
+// One warp per face: the face's d2 x (nb d2) block row of the CSR values is
+// one contiguous run, assembled from its (one or two) elements' C column
+// blocks C_e[:, l d2 .. l d2 + d2) (C is symmetric, so that contiguous column
+// block is the transposed row block) and written once, coalesced. The
+// diagonal block sums both sides in registers (a + b, order-free), so no
+// atomics and no zero fill; b = sum of the sides' Cf rows the same way.
+constexpr int kFaceRowWarps = 8;
+template <int D2>
+__global__ void __launch_bounds__(kFaceRowWarps * 32)
+scatter_faces_kernel(int nfc, const int* __restrict__ sides, const uint8_t* __restrict__ slot,
+                     const int64_t* __restrict__ facebase, const double* __restrict__ C,
+                     const double* __restrict__ Cf, double* __restrict__ vals, double* __restrict__ b, int nwarps) {
+  extern __shared__ __align__(16) double fsm[];
+  constexpr int m = 4 * D2, md = m * D2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ch = fsm + warp * (2 * md + 8);         // two column blocks
+  int* inv = reinterpret_cast<int*>(ch + 2 * md);  // slot -> side * 4 + l2 (8 = diagonal)
+  if (warp >= nwarps) return;
+  for (long f = long(blockIdx.x) * nwarps + warp; f < nfc; f += long(gridDim.x) * nwarps) {
+    const int s0 = sides[2 * f], s1 = sides[2 * f + 1];
+    const int ns = s1 >= 0 ? 2 : 1;
+    const int64_t base = facebase[f];
+    const int nb = int(facebase[f + 1] - base), W = nb * D2;
+    for (int s = 0; s < ns; ++s) {
+      const int code = s ? s1 : s0, e = code >> 2, l = code & 3;
+      const double2* src = reinterpret_cast<const double2*>(C + long(e) * m * m + long(l) * md);
+      for (int q = lane; q < md / 2; q += 32) reinterpret_cast<double2*>(ch + s * md)[q] = __ldg(src + q);
+      if (lane < 4) {
+        const int q = slot[long(e) * 16 + l * 4 + lane];
+        inv[q] = lane == l ? 8 : s * 4 + lane;
+      }
+    }
+    __syncwarp();
+    const int l0 = s0 & 3, l1 = s1 & 3;
+    double* dst = vals + base * D2 * D2;
+#pragma unroll 1
+    for (int i = 0; i < D2; ++i) {
+      for (int p = lane; p < W; p += 32) {
+        const int q = p / D2, j = p - q * D2;
+        const int src = inv[q];
+        double v;
+        if (src == 8) {
+          v = ch[l0 * D2 + j + i * m];
+          if (ns == 2) v += ch[md + l1 * D2 + j + i * m];
+        } else {
+          v = ch[(src >> 2) * md + (src & 3) * D2 + j + i * m];
+        }
+        dst[i * W + p] = v;
+      }
+    }
+    if (lane < D2) {
+      double v = Cf[long(s0 >> 2) * m + l0 * D2 + lane];
+      if (ns == 2) v += Cf[long(s1 >> 2) * m + l1 * D2 + lane];
+      b[f * D2 + lane] = v;
     }
     __syncwarp();
   }

@@ -262,6 +262,7 @@ class DevicePattern:
     slot: torch.Tensor      # uint8 (nelt, 16)
     rowptr: Optional[torch.Tensor] = None
     colidx: Optional[torch.Tensor] = None
+    sides: Optional[torch.Tensor] = None  # int32 (nfc, 2): e*4+l of each face's elements (K4 by faces)
 
 
 class Engine:
@@ -480,11 +481,30 @@ class Engine:
                                                   _ptr(p.rowptr), _ptr(p.colidx)))
         return p
 
+    def face_sides(self, dm: DeviceMesh) -> torch.Tensor:
+        """(nfc, 2) int32: e*4+l of each face's elements, lower element first, -1 if one-sided."""
+        sides = torch.empty(dm.nfc, 2, dtype=torch.int32, device=self.device)
+        L.check(L.lib().hdg_b200_face_sides(self._ctx, dm.nelt, dm.nfc, _ptr(dm.facebyele), _ptr(sides)))
+        return sides
+
     def assemble(self, dm: DeviceMesh, pat: DevicePattern, cs: CondensedSystem,
-                 out: Optional[SkeletonSystem] = None) -> SkeletonSystem:
-        """global_system.cpp:31-56: CSR values of H and b = sum Cf."""
+                 out: Optional[SkeletonSystem] = None, by: str = "faces") -> SkeletonSystem:
+        """global_system.cpp:31-56: CSR values of H and b = sum Cf.
+        by="faces": each face's block row gathered and written once (no zero fill);
+        by="elements": each element's C slice scattered (atomics on the diagonal blocks)."""
         d2 = self.dims["d2"]
         nnz = int(pat.facebase[-1].item()) * d2 * d2 if out is None else out.vals.numel()
+        if by == "faces":
+            if out is None:
+                out = SkeletonSystem(pat.rowptr, pat.colidx,
+                                     torch.empty(nnz, dtype=torch.float64, device=self.device),
+                                     torch.empty(dm.nfc * d2, dtype=torch.float64, device=self.device), d2)
+            if pat.sides is None:
+                pat.sides = self.face_sides(dm)
+            L.check(L.lib().hdg_b200_scatter_faces(self._ctx, dm.nfc, d2, _ptr(pat.sides), _ptr(pat.slot),
+                                                   _ptr(pat.facebase), _ptr(cs.C), _ptr(cs.Cf), _ptr(out.vals),
+                                                   _ptr(out.b)))
+            return out
         if out is None:
             out = SkeletonSystem(pat.rowptr, pat.colidx, torch.zeros(nnz, dtype=torch.float64, device=self.device),
                                  torch.zeros(dm.nfc * d2, dtype=torch.float64, device=self.device), d2)

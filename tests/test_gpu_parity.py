@@ -170,9 +170,34 @@ def test_scatter_pattern_and_values(k, bc):
     Ho = sp.csc_matrix((vals, rowidx, colptr), shape=(nd, nd))
     assert abs(Hg - Ho).max() <= 1e-13 * abs(Ho).max()
     assert np.max(np.abs(np_(sys.b) - b)) <= 1e-13 * np.max(np.abs(b))
-    # two runs bit-identical (fp64 atomics onto zero commute)
+    # two runs bit-identical, and the element-ordered K4 (fp64 atomics onto
+    # zero on the diagonal blocks: a + b commutes) gives the same bits
     sys2 = eng.assemble(dm, pat, cs)
     assert torch.equal(sys.vals, sys2.vals) and torch.equal(sys.b, sys2.b)
+    sys3 = eng.assemble(dm, pat, cs, by="elements")
+    assert torch.equal(sys.vals, sys3.vals) and torch.equal(sys.b, sys3.b)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 4, 5])
+def test_scatter_by_faces_matches_by_elements(k):
+    """Face-ordered K4 == element-ordered K4 bit for bit, every degree, with a
+    mixed-BC mesh (one- and two-sided faces) and random C, Cf."""
+    mesh = HostMesh.box(2, 2, 3, bc="dirichlet_x")
+    eng = Engine(0)
+    eng.set_degree(k)
+    dm = eng.upload(mesh)
+    pat = eng.pattern_device(dm)
+    d2 = (k + 1) * (k + 2) // 2
+    m = 4 * d2
+    gen = torch.Generator(device="cuda").manual_seed(7 + k)
+    Cr = torch.randn(dm.nelt, m, m, dtype=torch.float64, device="cuda", generator=gen)
+    Cr = (Cr + Cr.transpose(1, 2)).contiguous()  # K4 by faces relies on C's symmetry (as the reference's H does)
+    Cf = torch.randn(dm.nelt, m, dtype=torch.float64, device="cuda", generator=gen)
+    from paper_1305_1489_b200.engine import CondensedSystem
+    cs = CondensedSystem(Cr.reshape(-1), Cf.reshape(-1), None, m)
+    a = eng.assemble(dm, pat, cs, by="faces")
+    b = eng.assemble(dm, pat, cs, by="elements")
+    assert torch.equal(a.vals, b.vals) and torch.equal(a.b, b.b)
 
 
 # ------------------------------------------------ a11: postprocess
