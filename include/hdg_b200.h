@@ -328,7 +328,10 @@ int hdg_b200_stage_times(hdg_ctx* ctx, double ms[HDG_NSTAGES]);
  * the last JIT failure ("" if none; on failure the interpreter runs).      */
 int hdg_b200_set_jit(hdg_ctx* ctx, int enabled);
 /* k = 2, 3 condensation kernel: 3 = CTA-batched phases (default), 4 = element-batched
- * tasks, 2 = per-element warp teams (all equivalent; kept for comparison). */
+ * tasks, 2 = per-element warp teams. k = 4, 5: 1 = triangular-factor kernel, any other
+ * value = v5 (one element per CTA, explicit inverses; default). All are equivalent
+ * (kept for comparison); the recovery-cache layout follows the variant in use at
+ * build_condense time, so recover with the same context setting.            */
 int hdg_b200_set_variant(hdg_ctx* ctx, int variant);
 /* k = 1..3 recovery kernel: 3 = TMA-streamed cache records (default), 2 = one warp
  * per element with direct loads (equivalent; kept for comparison). */

@@ -19,6 +19,7 @@
 #include "kernels_post.cuh"
 #include "kernels_condense2.cuh"
 #include "kernels_condense3.cuh"
+#include "kernels_condense5.cuh"
 #include "kernels_condense4.cuh"
 #include "kernels_recover3.cuh"
 #include "kernels_boundary.cuh"
@@ -256,7 +257,9 @@ struct hdg_ctx {
   double* d_zero_T = nullptr;  // tau = 0 for the BDM variant
   long zero_T_len = 0;
   int recover_variant = 3;  // k = 1..3: 3 = TMA-streamed cache, 2 = warp per element
-  int condense_variant = 3; // k = 2, 3: 4 = element-batched tasks, 3 = CTA-batched, 2 = per-element teams
+  int condense_variant = 3; // k = 2, 3: 4 = element-batched tasks, 3 = CTA-batched, 2 = per-element teams;
+                            // k = 4, 5: 1 = triangular factors (kernels_local.cuh), else v5
+  bool tri_factors = false;  // recovery-cache layout of the last k >= 4 condensation
   std::string jit_error;    // last JIT failure (kernel then runs interpreted)
   int* d_adj = nullptr;     // boundary face -> 4 K + l (neumann_load)
   double* d_ksamp = nullptr;  // kappa sampled at the postprocess nodes (JIT sampler)
@@ -309,6 +312,11 @@ struct C4Launch {
 };
 
 template <int K_>
+struct C5Launch {  // one element per CTA iteration
+  static constexpr int EPB = 1, THREADS = C5Cfg<K_>::NWT * 32;
+};
+
+template <int K_>
 struct CondLaunch {
   static constexpr int EPB = CondCfg<K_>::EPB, THREADS = CondCfg<K_>::NW * 32 * CondCfg<K_>::EPB;
 };
@@ -350,10 +358,18 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
       launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
     else
       launch_condense_impl<C2Dims<K_>, C4Launch<K_>>(c, condense4_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-  } else if constexpr (K_ <= 3)
+  } else if constexpr (K_ <= 3) {
     launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-  else
+  } else if constexpr (K_ <= 5) {
+    c->tri_factors = c->condense_variant == 1;
+    if (c->tri_factors)  // triangular-factor kernel (kernels_local.cuh)
+      launch_condense_impl<CondDims<K_>, CondLaunch<K_>>(c, condense_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+    else
+      launch_condense_impl<C5Dims<K_>, C5Launch<K_>>(c, condense5_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+  } else {
+    c->tri_factors = true;
     launch_condense_impl<CondDims<K_>, CondLaunch<K_>>(c, condense_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+  }
 }
 
 template <int K_>
@@ -373,8 +389,23 @@ void launch_recover(hdg_ctx* c, int nelt, const GeoDev& geo, const int* fbe, con
       return;
     }
   }
+  if constexpr (K_ >= 4 && K_ <= 5) {
+    if (!c->tri_factors) {  // v5 cache {M^-1, S^-1, V, f}: one record per CTA iteration
+      using Rd = Rec5Dims<K_>;
+      const size_t smem = size_t(Rd::TOTAL) * sizeof(double);
+      CUDA_OK(cudaFuncSetAttribute(recover5_kernel<K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      int occ = 0;
+      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, recover5_kernel<K_>, kRec5Threads, smem));
+      const int grid5 = int(std::min<long>(nelt, long(c->sms) * std::max(occ, 1)));
+      recover5_kernel<K_><<<grid5, kRec5Threads, smem, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat, qx, qy,
+                                                                    qz, u);
+      CUDA_OK(cudaGetLastError());
+      return;
+    }
+  }
   const int grid = (nelt + kRecWarps - 1) / kRecWarps;
-  if constexpr (K_ <= 3)
+  // cache layout: {M^-1, S^-1, V, f} (v2..v5) or {L^-1, L_S^-1, Vt, ft} (triangular-factor kernel)
+  if (K_ <= 3 || !c->tri_factors)
     recover2_kernel<K_><<<grid, kRecWarps * 32, 0, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat, qx,
                                                                  qy, qz, u);
   else
@@ -1433,7 +1464,7 @@ const char* hdg_b200_jit_status(const hdg_ctx* c) { return c ? c->jit_error.c_st
 
 int hdg_b200_set_variant(hdg_ctx* c, int variant) {
   return guarded([&] {
-    require(c != nullptr && variant >= 2 && variant <= 4, HDG_EINVAL, "variant must be 2, 3 or 4");
+    require(c != nullptr && variant >= 1 && variant <= 4, HDG_EINVAL, "variant must be 1, 2, 3 or 4");
     c->condense_variant = variant;
   });
 }

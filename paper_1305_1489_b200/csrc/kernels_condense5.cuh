@@ -1,0 +1,443 @@
+// K3 v5 (k = 4, 5): static condensation with the v3 algebra (explicit M^-1
+// and S^-1, every contraction a DMMA tile loop) for element matrices too
+// large for several elements per CTA: d3 = 35 / 56, m = 60 / 84.
+//
+// One element per CTA iteration, all warps on it:
+//   P1  M^-1: M expanded to a full LD-strided matrix, CTA-wide sweep inverse
+//   P2  Zp = M^-1 W^T (strips; T_l W_l^T staged into V) | T0 = M^-1 Chat_0^T
+//   P3  S = D + Chat'_0 T0 (lower tiles) | T1 = M^-1 Chat_1^T
+//   P4  S += Chat'_1 T1 | T0 = M^-1 Chat_2^T
+//   P5  S += Chat'_2 T0 | V_l = Chat_l Zp_l (+ T_l W_l^T)
+//   P6  S^-1: CTA-wide sweep inverse (S stored full by P3..P5)
+//   P7  Vs = S^-1 V (into the dead M^-1 | T0 space) | fs = S^-1 f
+//   P8  C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (lower tile pairs) | Cf
+// with Chat'_h = sum_# g(#,h) Chat_# (g = a^T a; the 3 loads + FMAs per
+// k-step form the A fragment) and Chat_l = sum_# beta_#(l) Chat_#. The
+// reference tables (Chat, W) are read through L1/L2 (they do not fit beside
+// the element's 180-220 KB of operands). Only two 56 x 56 product buffers
+// (T0, T1) exist: the three T_h alternate between them so each S update runs
+// beside the next T product.
+//
+// CTA-wide sweep (cta_sweep_inverse): 2 x 2 pivots as the warp version, each
+// thread owning ~N^2/NT entries of the full symmetric matrix; a step reads
+// the old pivot rows (registers), barrier, writes, barrier.
+#pragma once
+
+#include "kernels_condense2.cuh"
+#include "kernels_condense3.cuh"
+
+namespace hdgb {
+
+template <int K_>
+struct C5Dims {
+  static constexpr int D3 = cdim3(K_), D2 = cdim2(K_), M = 4 * cdim2(K_);
+  static constexpr int D34 = round_up(D3, 4);                    // contraction length over d3
+  static constexpr int KS = D34 / 4;
+  static constexpr int LD = (D34 % 16 == 4 || D34 % 16 == 12) ? D34 : D34 + 4;  // conflict-free stride
+  static constexpr int D3P = round_up(D3, 8), MP = round_up(M, 8);
+  static constexpr int MT = D3P / 8, NTM = MP / 8;
+  static constexpr int NSYM = D3 * (D3 + 1) / 2;
+  static constexpr int SQ = round_up(LD * LD + (D3P > LD ? D3P - LD : 0), 2);
+  static constexpr int OFF_S = 0;
+  static constexpr int OFF_MI = OFF_S + SQ;
+  static constexpr int OFF_T0 = OFF_MI + SQ;
+  static constexpr int OFF_T1 = OFF_T0 + SQ;
+  static constexpr int OFF_Z = OFF_T1 + SQ;
+  static constexpr int OFF_V = OFF_Z + LD * MP;
+  static constexpr int OFF_DP = OFF_V + LD * MP;
+  static constexpr int OFF_F = OFF_DP + round_up(NSYM, 2);
+  static constexpr int OFF_FS = OFF_F + LD;
+  static constexpr int OFF_COL = OFF_FS + LD;
+  static constexpr int OFF_SG = OFF_COL + 8 * MP;
+  static constexpr int OFF_RED = OFF_SG + 64;
+  static constexpr int TOTAL = OFF_RED + 8;
+  static constexpr int PER_ELT = TOTAL, CTA_EXTRA = 0;  // launch_condense_impl vocabulary (EPB = 1)
+  static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
+  static_assert(2 * SQ >= LD * MP, "Vs must fit in the M^-1 | T0 space");
+};
+
+template <int K_> struct C5Cfg { static constexpr int NWT = 16; };
+
+// In-place inverse of the full symmetric N x N matrix X (stride LD, shared
+// memory) by the sweep operator with 2 x 2 pivots, all NT threads of the
+// CTA. Returns the pivot test of local_solver.cpp:50-57 (Cholesky pivots).
+template <int N, int LD, int NT>
+__device__ __forceinline__ bool cta_sweep_inverse(double* X) {
+  constexpr int NN = N * N, PER = (NN + NT - 1) / NT;
+  double nv[PER];
+  double pmin = 1e300, pmax = 0.0;
+  bool bad = false;
+  auto step2 = [&](int k) {
+    const double p00 = X[k + k * LD], p01 = X[k + 1 + k * LD], p11 = X[k + 1 + (k + 1) * LD];
+    const double det = fma(p00, p11, -p01 * p01);
+    const double id = gj_rcp(det);
+    const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;
+    if (!(p00 > 0.0) || !(det > 0.0)) bad = true;
+    const double d1 = 1.0 / i11;
+    pmin = fmin(pmin, fmin(p00, d1));
+    pmax = fmax(pmax, fmax(p00, d1));
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * NT;
+      if (idx < NN) {
+        const int c = idx / N, i = idx - c * N;
+        const double a0 = X[k + c * LD] - (c == k ? 1.0 : 0.0);
+        const double a1 = X[k + 1 + c * LD] - (c == k + 1 ? 1.0 : 0.0);
+        const double w0 = fma(i00, a0, i01 * a1), w1 = fma(i01, a0, i11 * a1);
+        double v;
+        if (i == k) v = w0 - (c == k ? 1.0 : 0.0);
+        else if (i == k + 1) v = w1 - (c == k + 1 ? 1.0 : 0.0);
+        else v = X[i + c * LD] - fma(X[i + k * LD], w0, X[i + (k + 1) * LD] * w1);
+        nv[u] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * NT;
+      if (idx < NN) {
+        const int c = idx / N, i = idx - c * N;
+        X[i + c * LD] = nv[u];
+      }
+    }
+    __syncthreads();
+  };
+  for (int k = 0; k + 1 < N; k += 2) step2(k);
+  if (N % 2) {  // trailing scalar pivot
+    constexpr int k = N - 1;
+    const double p = X[k + k * LD];
+    if (!(p > 0.0)) bad = true;
+    pmin = fmin(pmin, p);
+    pmax = fmax(pmax, p);
+    const double ip = gj_rcp(p);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * NT;
+      if (idx < NN) {
+        const int c = idx / N, i = idx - c * N;
+        const double w = (X[k + c * LD] - (c == k ? 1.0 : 0.0)) * ip;
+        nv[u] = i == k ? w - (c == k ? 1.0 : 0.0) : X[i + c * LD] - X[i + k * LD] * w;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * NT;
+      if (idx < NN) {
+        const int c = idx / N, i = idx - c * N;
+        X[i + c * LD] = nv[u];
+      }
+    }
+    __syncthreads();
+  }
+  // the sweep leaves -X^-1
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int idx = threadIdx.x + u * NT;
+    if (idx < NN) {
+      const int c = idx / N, i = idx - c * N;
+      X[i + c * LD] = -X[i + c * LD];
+    }
+  }
+  __syncthreads();
+  return bad || pmin < 1e-14 * pmax;
+}
+
+template <int K_>
+__global__ void __launch_bounds__(C5Cfg<K_>::NWT * 32, 1)
+condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
+                 const double* __restrict__ Dsym, const double* __restrict__ fvec,
+                 double* __restrict__ Cout, double* __restrict__ Cfout, double* __restrict__ factors,
+                 long long* bad_element) {
+  using Dm = C5Dims<K_>;
+  constexpr int NWT = C5Cfg<K_>::NWT, NT = NWT * 32;
+  constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, MP = Dm::MP, LD = Dm::LD, KS = Dm::KS;
+  constexpr int MT = Dm::MT, NTM = Dm::NTM, NSYM = Dm::NSYM;
+  constexpr int NLS = MT * (MT + 1) / 2;                 // lower tiles of S
+  constexpr int NTF = face_tiles(D2);
+  constexpr int NLP = (NTM / 2 + 1) * ((NTM + 1) / 2);  // C tile pairs (rows' pairs and singles)
+  constexpr bool PAD = Dm::D34 != D3;                    // k-padding present (k = 4)
+  extern __shared__ double smem[];
+  for (int i = threadIdx.x; i < Dm::TOTAL; i += NT) smem[i] = 0.0;
+  __syncthreads();
+  double* S = smem + Dm::OFF_S;
+  double* Mi = smem + Dm::OFF_MI;
+  double* T0 = smem + Dm::OFF_T0;
+  double* T1 = smem + Dm::OFF_T1;
+  double* Z = smem + Dm::OFF_Z;
+  double* V = smem + Dm::OFF_V;
+  double* Vs = smem + Dm::OFF_MI;  // P7..P8: M^-1 and T0 are dead
+  double* Dp = smem + Dm::OFF_DP;
+  double* fv = smem + Dm::OFF_F;
+  double* fs = smem + Dm::OFF_FS;
+  double* col = smem + Dm::OFF_COL;
+  double* sg = smem + Dm::OFF_SG;
+  const double* Tc = col + 3 * MP;
+  const int* wb = reinterpret_cast<const int*>(col + 4 * MP);
+  const double* beta = col + 5 * MP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const double* Wlm = tab.Wlm;
+  const double* Ch = tab.Chat;
+
+  // Chat_h(r, k) from L1/L2 (k-padding and tile rows past d3 read as zero)
+  auto chat = [&](int h, int r, int k) -> double {
+    if (PAD || D3 % 8) {
+      if (r >= D3 || k >= D3) return 0.0;
+    }
+    return __ldg(Ch + h * D3 * D3 + r + k * D3);
+  };
+  // T_h = M^-1 Chat_h^T: one 8 x 8 tile (two chains)
+  auto t_tile = [&](double* Tb, int h, int tile) {
+    const int mt = tile / MT, nt = tile - mt * MT;
+    const int r = mt * 8 + g, c = nt * 8 + g;
+    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+      const int k = kk * 4 + t;
+      const double a = Mi[r + k * LD], b = chat(h, c, k);
+      if (kk & 1) dmma(q[0], q[1], a, b);
+      else dmma(p[0], p[1], a, b);
+    }
+    const int rr = mt * 8 + g, c0 = nt * 8 + 2 * t;
+    if (rr < LD) {
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2)
+        if (c0 + h2 < D3) Tb[rr + (c0 + h2) * LD] = rr < D3 ? p[h2] + q[h2] : 0.0;
+    }
+  };
+  // S (+)= Chat'_h Tb over the lower tiles, Chat'_h = sum_# G(#,h) Chat_#
+  auto s_tile = [&](const double* Tb, int h, int tile, bool first) {
+    int mt = 0, rem = tile;
+    while (rem > mt) { rem -= mt + 1; ++mt; }
+    const int j = rem, r = mt * 8 + g;
+    const double g0 = sg[32 + h], g1 = sg[35 + h], g2 = sg[38 + h];  // G symmetric: G(#, h)
+    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+#pragma unroll 7
+    for (int kk = 0; kk < KS; ++kk) {
+      const int k = kk * 4 + t;
+      const double a = g0 * chat(0, r, k) + g1 * chat(1, r, k) + g2 * chat(2, r, k);
+      const double b = Tb[k + (j * 8 + g) * LD];
+      if (kk & 1) dmma(q[0], q[1], a, b);
+      else dmma(p[0], p[1], a, b);
+    }
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int c = j * 8 + 2 * t + h2;
+      if (r < D3 && c <= r) {
+        const double v = (first ? Dp[sym_idx(r, c, D3)] : S[r + c * LD]) + p[h2] + q[h2];
+        S[r + c * LD] = v;
+        S[c + r * LD] = v;
+      }
+    }
+  };
+
+  for (long K = blockIdx.x; K < nelt; K += gridDim.x) {
+    // ---- prologue: geometry, column data, packed M / D / f
+    if (threadIdx.x < 30) {
+      const int i = threadIdx.x;
+      double v;
+      if (i == 0) v = geo.volume[K];
+      else if (i < 10) v = geo.piola[long(i - 1) * nelt + K];
+      else if (i < 22) v = geo.normals[long(i - 10) * nelt + K];
+      else if (i < 26) v = geo.T[long(i - 22) * nelt + K];
+      else v = double(geo.perm[long(i - 26) * nelt + K]);
+      sg[i] = v;
+    }
+    for (int p = threadIdx.x; p < NSYM; p += NT) {
+      cp_async8(T1 + p, Msym + K * NSYM + p);
+      cp_async8(Dp + p, Dsym + K * NSYM + p);
+    }
+    for (int i = threadIdx.x; i < D3; i += NT) cp_async8(fv + i, fvec + K * D3 + i);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    cp_async_wait_all();
+    __syncthreads();
+    if (warp == 0) {
+      build_columns<D2, D3, M, MP>(sg, col, lane);
+      if (lane < 9) {
+        const int h = lane / 3, h2 = lane % 3;
+        sg[32 + lane] = sg[1 + h] * sg[1 + h2] + sg[4 + h] * sg[4 + h2] + sg[7 + h] * sg[7 + h2];
+      } else if (lane >= 16) {
+        const int l1 = (lane - 16) >> 2, l2 = lane & 3;
+        sg[48 + (lane - 16)] = sg[10 + 3 * l1] * sg[10 + 3 * l2] + sg[11 + 3 * l1] * sg[11 + 3 * l2] +
+                               sg[12 + 3 * l1] * sg[12 + 3 * l2];
+      }
+    }
+    // expand packed M (in T1) to the full LD-strided matrix, padding zero
+    for (int idx = threadIdx.x; idx < LD * LD; idx += NT) {
+      const int c = idx / LD, r = idx - c * LD;
+      Mi[idx] = (r < D3 && c < D3) ? T1[r >= c ? sym_idx(r, c, D3) : sym_idx(c, r, D3)] : 0.0;
+    }
+    __syncthreads();
+
+    // ---- P1: M^-1 (CTA sweep), packed lower part into the recovery cache
+    if (cta_sweep_inverse<D3, LD, NT>(Mi) && threadIdx.x == 0) flag_bad(bad_element, K);
+    if (factors)  // packed lower, column-major: column c at sym_idx(c, c)
+      for (int c = warp; c < D3; c += NWT)
+        for (int i = c + lane; i < D3; i += 32) factors[K * Dm::FACTORS + sym_idx(i, c, D3)] = Mi[i + c * LD];
+
+    // ---- P2: Zp strips (T_l W_l^T staged into V) | T0 = M^-1 Chat_0^T
+    for (int task = warp; task < NTM + MT * MT; task += NWT) {
+      if (task < NTM) {
+        const int nt = task, cz = nt * 8 + g, wbc = wb[cz];
+        const double tc = Tc[cz];
+        double acc[MT][2];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+#pragma unroll 2
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          const double b = (wbc >= 0 && k < D3) ? __ldg(Wlm + wbc + k * D2) : 0.0;
+          V[k + cz * LD] = tc * b;
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], Mi[(m * 8 + g) + k * LD], b);
+        }
+        const int c0 = nt * 8 + 2 * t;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const int r = m * 8 + g;
+          if (r < LD) {
+            Z[r + c0 * LD] = r < D3 ? acc[m][0] : 0.0;
+            Z[r + (c0 + 1) * LD] = r < D3 ? acc[m][1] : 0.0;
+          }
+        }
+      } else {
+        t_tile(T0, 0, task - NTM);
+      }
+    }
+    __syncthreads();
+    // ---- P3..P5: S accumulation beside the next T product / the V rows
+    for (int task = warp; task < NLS + MT * MT; task += NWT) {
+      if (task < NLS) s_tile(T0, 0, task, true);
+      else t_tile(T1, 1, task - NLS);
+    }
+    __syncthreads();
+    for (int task = warp; task < NLS + MT * MT; task += NWT) {
+      if (task < NLS) s_tile(T1, 1, task, false);
+      else t_tile(T0, 2, task - NLS);
+    }
+    __syncthreads();
+    for (int task = warp; task < NLS + 4 * MT; task += NWT) {
+      if (task < NLS) {
+        s_tile(T0, 2, task, false);
+      } else {  // V rows of row tile mt, face l
+        const int mt = (task - NLS) >> 2, l = (task - NLS) & 3;
+        const int r = mt * 8 + g;
+        const int cl0 = l * D2, cl1 = cl0 + D2, nt0 = cl0 / 8;
+        const double b0 = beta[cl0], b1 = beta[MP + cl0], b2 = beta[2 * MP + cl0];
+        double acc[NTF][2] = {};
+#pragma unroll 2
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = kk * 4 + t;
+          const double a = b0 * chat(0, r, k) + b1 * chat(1, r, k) + b2 * chat(2, r, k);
+#pragma unroll
+          for (int j = 0; j < NTF; ++j) {
+            const int c = (nt0 + j) * 8 + g;
+            const double b = (c >= cl0 && c < cl1) ? Z[k + c * LD] : 0.0;
+            if ((nt0 + j) * 8 < cl1) dmma(acc[j][0], acc[j][1], a, b);
+          }
+        }
+        if (r < LD) {
+#pragma unroll
+          for (int j = 0; j < NTF; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = (nt0 + j) * 8 + 2 * t + h;
+              if (c >= cl0 && c < cl1) V[r + c * LD] = r < D3 ? acc[j][h] + V[r + c * LD] : 0.0;
+            }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- P6: S^-1 (CTA sweep); cache: S^-1 packed, V, f
+    if (cta_sweep_inverse<D3, LD, NT>(S) && threadIdx.x == 0) flag_bad(bad_element, K);
+    if (factors) {
+      for (int c = warp; c < D3; c += NWT)
+        for (int i = c + lane; i < D3; i += 32) factors[K * Dm::FACTORS + NSYM + sym_idx(i, c, D3)] = S[i + c * LD];
+      constexpr int NVF = D3 * M + D3;
+      for (int q = threadIdx.x; q < NVF; q += NT) {
+        const int c = q / D3, r = q - c * D3;
+        factors[K * Dm::FACTORS + 2 * NSYM + q] = c < M ? V[r + c * LD] : fv[r];
+      }
+    }
+
+    // ---- P7: Vs = S^-1 V strips | fs = S^-1 f
+    for (int task = warp; task < NTM; task += NWT) {
+      const int nt = task, c = nt * 8 + g;
+      double acc[MT][2];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+#pragma unroll 2
+      for (int kk = 0; kk < KS; ++kk) {
+        const int k = kk * 4 + t;
+        const double b = V[k + c * LD];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], S[(m * 8 + g) + k * LD], b);
+      }
+      const int c0 = nt * 8 + 2 * t;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int r = m * 8 + g;
+        if (r < LD) {
+          Vs[r + c0 * LD] = r < D3 ? acc[m][0] : 0.0;
+          Vs[r + (c0 + 1) * LD] = r < D3 ? acc[m][1] : 0.0;
+        }
+      }
+    }
+    for (int r = threadIdx.x; r < D3; r += NT) {
+      double s = 0.0;
+      for (int k = 0; k < D3; ++k) s += S[r + k * LD] * fv[k];
+      fs[r] = s;
+    }
+    __syncthreads();
+
+    // ---- P8: C (lower tile pairs, mirrored) | Cf
+    for (int task = warp; task < NLP; task += NWT) {
+      const int mt = int(2.0f * sqrtf(float(task) + 0.25f)) - 1;
+      const int nt0 = 2 * (task - (mt + 1) * (mt + 1) / 4), r = mt * 8 + g;
+      const bool two = nt0 + 1 <= mt;
+      const int wbr = wb[r];
+      double z[2][2] = {{0, 0}, {0, 0}}, v[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll 2
+      for (int kk = 0; kk < KS; ++kk) {
+        const int k = kk * 4 + t;
+        const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
+        const double av = V[k + r * LD];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+          const int cn = (nt0 + u) * 8 + g;
+          dmma(z[u][0], z[u][1], aw, Z[k + cn * LD]);
+          dmma(v[u][0], v[u][1], av, Vs[k + cn * LD]);
+        }
+      }
+      if (r < M) {
+        const int l1 = r / D2;
+        const double* nn4 = sg + 48 + 4 * l1;
+        double* Ck = Cout + K * M * M;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = (nt0 + u) * 8 + 2 * t + h;
+            if (c > r || c >= M) continue;
+            const int l2 = c / D2;
+            double val = nn4[l2] * z[u][h] - v[u][h];
+            if (l1 == l2) val += Tc[c] * __ldg(tab.DD + (r - l1 * D2) + (c - l2 * D2) * D2);
+            Ck[r + c * M] = val;
+            if (c != r) Ck[c + r * M] = val;
+          }
+        }
+      }
+    }
+    for (int r = threadIdx.x; r < M; r += NT) {
+      double s = 0.0;
+      for (int k = 0; k < D3; ++k) s += V[k + r * LD] * fs[k];
+      Cfout[K * M + r] = s;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace hdgb

@@ -334,7 +334,10 @@ template <> struct CondCfg<1> { static constexpr int NW = 1, EPB = 16; };
 template <> struct CondCfg<2> { static constexpr int NW = 2, EPB = 8; };
 template <> struct CondCfg<3> { static constexpr int NW = 2, EPB = 4; };
 template <> struct CondCfg<4> { static constexpr int NW = 8, EPB = 1; };
-template <> struct CondCfg<5> { static constexpr int NW = 8, EPB = 1; };
+#ifndef HDG_COND5_NW
+#define HDG_COND5_NW 8
+#endif
+template <> struct CondCfg<5> { static constexpr int NW = HDG_COND5_NW, EPB = 1; };
 template <> struct CondCfg<6> { static constexpr int NW = 8, EPB = 1; };
 
 // Stage element K's geometry record into sg[0..31].

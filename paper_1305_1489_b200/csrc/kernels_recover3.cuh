@@ -225,4 +225,145 @@ recover3_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ faceby
   }
 }
 
+// K5 v5 (k = 4, 5): the cache record of one element (k=5: 63.6 KB) per CTA
+// iteration, one TMA bulk copy into shared memory; all 256 threads recover
+// from it (row-parallel matrix-vector products, 4 threads per row with a
+// shuffle reduction). Three CTAs per SM keep three records in flight.
+constexpr int kRec5Threads = 256;
+template <int K_>
+struct Rec5Dims {
+  static constexpr int D3 = cdim3(K_), D2 = cdim2(K_), M = 4 * cdim2(K_), NS = D3 * (D3 + 1) / 2;
+  static constexpr int FACTORS = 2 * NS + D3 * M + D3;
+  static constexpr int REC = round_up(FACTORS, 2);
+  static constexpr int SCR = round_up(M, 2) + 3 * D3 + 7 * D3 + 3 * D3 + 32;  // lambda, t/u, p|w, r_s, geometry
+  static constexpr int TOTAL = REC + SCR;
+  static constexpr bool BULK = FACTORS % 2 == 0;  // 16-byte records: one TMA bulk copy (else cp.async)
+};
+
+template <int K_>
+__global__ void __launch_bounds__(kRec5Threads)
+recover5_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ facebyele,
+                const double* __restrict__ factors, const double* __restrict__ uhat,
+                double* __restrict__ qx, double* __restrict__ qy, double* __restrict__ qz,
+                double* __restrict__ uout) {
+  using Rd = Rec5Dims<K_>;
+  constexpr int D3 = Rd::D3, D2 = Rd::D2, M = Rd::M, NS = Rd::NS, F = Rd::FACTORS;
+  static_assert(4 * D3 <= kRec5Threads, "four threads per row");
+  extern __shared__ __align__(16) double r5[];
+  __shared__ unsigned long long bar;
+  double* rec = r5;
+  double* lam = r5 + Rd::REC;
+  double* tv = lam + round_up(M, 2);
+  double* uu = tv + D3;
+  double* pw = uu + 2 * D3;  // p_# (3 D3) then w_l (4 D3)
+  double* rs = pw + 7 * D3;  // r_s (3 D3)
+  double* sg = rs + 3 * D3;
+  const double* Mi = rec;
+  const double* Si = rec + NS;
+  const double* V = rec + 2 * NS;
+  const double* f = V + D3 * M;
+  const int tid = threadIdx.x, row = tid >> 2, part = tid & 3;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned phase = 0u;
+  for (long K = blockIdx.x; K < nelt; K += gridDim.x) {
+    if constexpr (Rd::BULK) {
+      if (tid == 0) bulk_load(rec, factors + K * F, F * 8, &bar);
+    } else {
+      for (int i = tid; i < F; i += kRec5Threads) cp_async8(rec + i, factors + K * F + i);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    for (int i = tid; i < M; i += kRec5Threads) {
+      const int l = i / D2;
+      lam[i] = uhat[long(facebyele[long(l) * nelt + K]) * D2 + (i - l * D2)];
+    }
+    if (tid < 30) {
+      double v;
+      if (tid == 0) v = geo.volume[K];
+      else if (tid < 10) v = geo.piola[long(tid - 1) * nelt + K];
+      else if (tid < 22) v = geo.normals[long(tid - 10) * nelt + K];
+      else if (tid < 26) v = geo.T[long(tid - 22) * nelt + K];
+      else v = double(geo.perm[long(tid - 26) * nelt + K]);
+      sg[tid] = v;
+    }
+    if constexpr (Rd::BULK) {
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    // t = f + V lambda
+    double s = 0.0;
+    if (row < D3) {
+      for (int c = part; c < M; c += 4) s = fma(V[row + c * D3], lam[c], s);
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (row < D3 && part == 0) tv[row] = f[row] + s;
+    __syncthreads();
+    // u = S^-1 t (packed lower)
+    s = 0.0;
+    if (row < D3) {
+      for (int r = part; r < D3; r += 4)
+        s = fma(Si[r >= row ? sym_idx(r, row, D3) : sym_idx(row, r, D3)], tv[r], s);
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (row < D3 && part == 0) {
+      uu[row] = s;
+      uout[K * D3 + row] = s;
+    }
+    __syncthreads();
+    // p_#(j) = (Chat_# u)(j) over the rows of Chat_#^T, w_l(j) = (W_l lambda_l)(j)
+    for (int it = tid; it < 7 * D3; it += kRec5Threads) {
+      const int h = it / D3, j = it - h * D3;
+      double acc = 0.0;
+      if (h < 3) {
+        const double* C = tab.ChatT + h * D3 * D3 + j;
+        for (int i = 0; i < D3; ++i) acc = fma(__ldg(C + i * D3), uu[i], acc);
+      } else {
+        const int l = h - 3;
+        const double* W = tab.WlmT + (6 * l + int(sg[26 + l]) - 1) * D2 * D3 + j;
+        for (int i = 0; i < D2; ++i) acc = fma(__ldg(W + i * D3), lam[l * D2 + i], acc);
+      }
+      pw[it] = acc;
+    }
+    __syncthreads();
+    for (int it = tid; it < 3 * D3; it += kRec5Threads) {
+      const int sd = it / D3, j = it - sd * D3;
+      double r = sg[1 + 3 * sd] * pw[j] + sg[2 + 3 * sd] * pw[D3 + j] + sg[3 + 3 * sd] * pw[2 * D3 + j];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) r -= sg[10 + 3 * l + sd] * pw[(3 + l) * D3 + j];
+      rs[it] = r;
+    }
+    __syncthreads();
+    // q_s = M^-1 r_s
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (row < D3) {
+      for (int j = part; j < D3; j += 4) {
+        const double m = Mi[j >= row ? sym_idx(j, row, D3) : sym_idx(row, j, D3)];
+        a0 = fma(m, rs[j], a0);
+        a1 = fma(m, rs[D3 + j], a1);
+        a2 = fma(m, rs[2 * D3 + j], a2);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (row < D3 && part == 0) {
+      qx[K * D3 + row] = a0;
+      qy[K * D3 + row] = a1;
+      qz[K * D3 + row] = a2;
+    }
+    __syncthreads();  // the record buffer is refilled next
+  }
+}
+
 }  // namespace hdgb

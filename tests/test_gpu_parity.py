@@ -463,6 +463,31 @@ def test_condense_variants_agree(k):
         assert max_slice_relerr(np_(out[v].factors.view(dm.nelt, -1)), np_(cs3.factors.view(dm.nelt, -1))) < 1e-12
 
 
+@pytest.mark.parametrize("k", [4, 5])
+def test_condense_v5_matches_triangular_kernel(k):
+    """k = 4, 5: the one-element-per-CTA explicit-inverse kernel (v5, default)
+    and the triangular-factor kernel (variant 1) agree with the oracle on C, Cf
+    and, each through its own recovery cache, on the recovered q, u; 162 tets
+    > 148 CTAs, so CTAs run more than one element."""
+    mesh = HostMesh.box(3, bc="dirichlet_x", perturb=0.1)
+    em = oracle_mesh(mesh)
+    eng, dm, g, cs5 = gpu_pipeline(mesh, k, KAP, CC, FF)
+    d2 = dim2(k)
+    uhat = torch.from_numpy(np.sin(np.arange(dm.nfc * d2) * 0.37)).cuda()
+    ls5 = eng.recover(g, dm, cs5, uhat)
+    eng.set_variant(1)
+    cs1 = eng.build_condense(g, KAP, CC, FF)
+    ls1 = eng.recover(g, dm, cs1, uhat)
+    _, _, lb, C, Cf = oracle_condense(em, k, KAP, CC, FF, 1.0)
+    for cs in (cs5, cs1):
+        assert max_slice_relerr(np_(cs.C_slices()), C) < TOL
+        assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
+    qx, qy, qz, u = core.local_recover(lb, core.gather_traces(em, d2, uhat.cpu().numpy()), 4)
+    for ls in (ls5, ls1):
+        for got, want in ((ls.qx, qx), (ls.qy, qy), (ls.qz, qz), (ls.u, u)):
+            assert max_slice_relerr(np_(got), want.T) < TOL
+
+
 @pytest.mark.parametrize("k", [1, 2, 3])
 def test_recover_variants_agree(k):
     """TMA-streamed recovery (v3, default) and the direct-load kernel (v2) agree;
