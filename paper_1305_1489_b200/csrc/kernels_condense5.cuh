@@ -19,8 +19,8 @@
 // beside the next T product.
 //
 // CTA-wide sweep (cta_sweep_inverse): 2 x 2 pivots as the warp version, each
-// thread owning ~N^2/NT entries of the full symmetric matrix; a step reads
-// the old pivot rows (registers), barrier, writes, barrier.
+// thread owning a run of rows of one column, ping-ponging between the matrix
+// and a free product buffer (one barrier per pivot pair).
 #pragma once
 
 #include "kernels_condense2.cuh"
@@ -58,85 +58,76 @@ struct C5Dims {
 
 template <int K_> struct C5Cfg { static constexpr int NWT = 16; };
 
-// In-place inverse of the full symmetric N x N matrix X (stride LD, shared
-// memory) by the sweep operator with 2 x 2 pivots, all NT threads of the
-// CTA. Returns the pivot test of local_solver.cpp:50-57 (Cholesky pivots).
+// Inverse of the full symmetric N x N matrix X (stride LD, shared memory) by
+// the sweep operator with 2 x 2 pivots, all NT threads of the CTA; Y is a
+// second N x N buffer (same stride): each step reads one buffer and writes
+// the other (one barrier per step). The result ends in X (the step count is
+// made even by a final copy when needed). Thread layout: NT / N row groups
+// per column, each thread owns one column c and a run of rows, so the
+// column's pivot-row weights are computed once per step.
+// Returns the pivot test of local_solver.cpp:50-57 (Cholesky pivots).
 template <int N, int LD, int NT>
-__device__ __forceinline__ bool cta_sweep_inverse(double* X) {
-  constexpr int NN = N * N, PER = (NN + NT - 1) / NT;
-  double nv[PER];
+__device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
+  constexpr int RG = NT / N;                  // row groups per column
+  constexpr int RPT = (N + RG - 1) / RG;      // rows per thread
+  const int c = threadIdx.x / RG, i0 = (threadIdx.x - c * RG) * RPT;
+  const bool live = c < N;
   double pmin = 1e300, pmax = 0.0;
   bool bad = false;
-  auto step2 = [&](int k) {
-    const double p00 = X[k + k * LD], p01 = X[k + 1 + k * LD], p11 = X[k + 1 + (k + 1) * LD];
-    const double det = fma(p00, p11, -p01 * p01);
-    const double id = gj_rcp(det);
-    const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;
-    if (!(p00 > 0.0) || !(det > 0.0)) bad = true;
-    const double d1 = 1.0 / i11;
-    pmin = fmin(pmin, fmin(p00, d1));
-    pmax = fmax(pmax, fmax(p00, d1));
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int idx = threadIdx.x + u * NT;
-      if (idx < NN) {
-        const int c = idx / N, i = idx - c * N;
-        const double a0 = X[k + c * LD] - (c == k ? 1.0 : 0.0);
-        const double a1 = X[k + 1 + c * LD] - (c == k + 1 ? 1.0 : 0.0);
+  double* src = X;
+  double* dst = Y;
+  int nsteps = 0;
+  for (int k = 0; k < N; k += 2, ++nsteps) {
+    if (k + 1 < N) {
+      const double p00 = src[k + k * LD], p01 = src[k + 1 + k * LD], p11 = src[k + 1 + (k + 1) * LD];
+      const double det = fma(p00, p11, -p01 * p01);
+      const double id = gj_rcp(det);
+      const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;
+      if (!(p00 > 0.0) || !(det > 0.0)) bad = true;
+      const double d1 = 1.0 / i11;
+      pmin = fmin(pmin, fmin(p00, d1));
+      pmax = fmax(pmax, fmax(p00, d1));
+      if (live) {
+        const double a0 = src[k + c * LD] - (c == k ? 1.0 : 0.0);
+        const double a1 = src[k + 1 + c * LD] - (c == k + 1 ? 1.0 : 0.0);
         const double w0 = fma(i00, a0, i01 * a1), w1 = fma(i01, a0, i11 * a1);
-        double v;
-        if (i == k) v = w0 - (c == k ? 1.0 : 0.0);
-        else if (i == k + 1) v = w1 - (c == k + 1 ? 1.0 : 0.0);
-        else v = X[i + c * LD] - fma(X[i + k * LD], w0, X[i + (k + 1) * LD] * w1);
-        nv[u] = v;
-      }
-    }
-    __syncthreads();
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int idx = threadIdx.x + u * NT;
-      if (idx < NN) {
-        const int c = idx / N, i = idx - c * N;
-        X[i + c * LD] = nv[u];
+        for (int u = 0; u < RPT; ++u) {
+          const int i = i0 + u;
+          if (i < N) {
+            double v = src[i + c * LD] - fma(src[i + k * LD], w0, src[i + (k + 1) * LD] * w1);
+            if (i == k) v = w0 - (c == k ? 1.0 : 0.0);
+            if (i == k + 1) v = w1 - (c == k + 1 ? 1.0 : 0.0);
+            dst[i + c * LD] = v;
+          }
+        }
       }
-    }
-    __syncthreads();
-  };
-  for (int k = 0; k + 1 < N; k += 2) step2(k);
-  if (N % 2) {  // trailing scalar pivot
-    constexpr int k = N - 1;
-    const double p = X[k + k * LD];
-    if (!(p > 0.0)) bad = true;
-    pmin = fmin(pmin, p);
-    pmax = fmax(pmax, p);
-    const double ip = gj_rcp(p);
+    } else {  // trailing scalar pivot
+      const double p = src[k + k * LD];
+      if (!(p > 0.0)) bad = true;
+      pmin = fmin(pmin, p);
+      pmax = fmax(pmax, p);
+      const double ip = gj_rcp(p);
+      if (live) {
+        const double w = (src[k + c * LD] - (c == k ? 1.0 : 0.0)) * ip;
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int idx = threadIdx.x + u * NT;
-      if (idx < NN) {
-        const int c = idx / N, i = idx - c * N;
-        const double w = (X[k + c * LD] - (c == k ? 1.0 : 0.0)) * ip;
-        nv[u] = i == k ? w - (c == k ? 1.0 : 0.0) : X[i + c * LD] - X[i + k * LD] * w;
+        for (int u = 0; u < RPT; ++u) {
+          const int i = i0 + u;
+          if (i < N) dst[i + c * LD] = i == k ? w - (c == k ? 1.0 : 0.0) : src[i + c * LD] - src[i + k * LD] * w;
+        }
       }
     }
     __syncthreads();
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int idx = threadIdx.x + u * NT;
-      if (idx < NN) {
-        const int c = idx / N, i = idx - c * N;
-        X[i + c * LD] = nv[u];
-      }
-    }
-    __syncthreads();
+    double* tmp = src;
+    src = dst;
+    dst = tmp;
   }
-  // the sweep leaves -X^-1
+  // the sweep leaves -X^-1 in src; negate into X
+  if (live) {
 #pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int idx = threadIdx.x + u * NT;
-    if (idx < NN) {
-      const int c = idx / N, i = idx - c * N;
-      X[i + c * LD] = -X[i + c * LD];
+    for (int u = 0; u < RPT; ++u) {
+      const int i = i0 + u;
+      if (i < N) X[i + c * LD] = -src[i + c * LD];
     }
   }
   __syncthreads();
@@ -270,7 +261,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     __syncthreads();
 
     // ---- P1: M^-1 (CTA sweep), packed lower part into the recovery cache
-    if (cta_sweep_inverse<D3, LD, NT>(Mi) && threadIdx.x == 0) flag_bad(bad_element, K);
+    if (cta_sweep_inverse<D3, LD, NT>(Mi, T0) && threadIdx.x == 0) flag_bad(bad_element, K);
     if (factors)  // packed lower, column-major: column c at sym_idx(c, c)
       for (int c = warp; c < D3; c += NWT)
         for (int i = c + lane; i < D3; i += 32) factors[K * Dm::FACTORS + sym_idx(i, c, D3)] = Mi[i + c * LD];
@@ -350,7 +341,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     __syncthreads();
 
     // ---- P6: S^-1 (CTA sweep); cache: S^-1 packed, V, f
-    if (cta_sweep_inverse<D3, LD, NT>(S) && threadIdx.x == 0) flag_bad(bad_element, K);
+    if (cta_sweep_inverse<D3, LD, NT>(S, T1) && threadIdx.x == 0) flag_bad(bad_element, K);
     if (factors) {
       for (int c = warp; c < D3; c += NWT)
         for (int i = c + lane; i < D3; i += 32) factors[K * Dm::FACTORS + NSYM + sym_idx(i, c, D3)] = S[i + c * LD];
