@@ -98,6 +98,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int NLP = (NTM / 2 + 1) * ((NTM + 1) / 2);  // lower tile pairs of the m x m output
   constexpr int NLS = MT * (MT + 1) / 2;     // lower tiles of S
   constexpr int NTF = face_tiles(D2);        // N-tiles one face's columns span
+  static_assert(M % 8 == 0, "P5 pairs columns c0, c0 + 1 < M");
 #ifndef HDG_C3_FPT
 #define HDG_C3_FPT 4
 #endif
@@ -507,16 +508,20 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           if (u == 1 && !two) break;
+          const int c0 = (nt0 + u) * 8 + 2 * t;  // c0 + 1 < M: M and the tiles are whole
+          double val[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int c = (nt0 + u) * 8 + 2 * t + h;
-            if (c > r || c >= M) continue;
-            const int l2 = c / D2;
-            double val = nn4[l2] * z[u][h] - v[u][h];
-            if (l1 == l2) val += Tc[c] * DDs[(r - l1 * D2) + (c - l2 * D2) * D2];
-            Ck[r + c * M] = val;
-            if (c != r) Ck[c + r * M] = val;
+            const int c = c0 + h, l2 = c / D2;
+            val[h] = nn4[l2] * z[u][h] - v[u][h];
+            if (l1 == l2) val[h] += Tc[c] * DDs[(r - l1 * D2) + (c - l2 * D2) * D2];
           }
+          // lower entries (c <= r); the mirrored upper ones as one 16-byte
+          // store where both columns are strictly below the diagonal
+          if (c0 <= r) Ck[r + c0 * M] = val[0];
+          if (c0 + 1 <= r) Ck[r + (c0 + 1) * M] = val[1];
+          if (c0 + 1 < r) *reinterpret_cast<double2*>(Ck + c0 + r * M) = make_double2(val[0], val[1]);
+          else if (c0 < r) Ck[c0 + r * M] = val[0];
         }
       }
     }
