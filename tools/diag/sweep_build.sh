@@ -2,8 +2,10 @@
 # Build libhdg_b200 variants with different CTA-batched condensation shapes
 # into tools/diag/sweep/ (diagnostics only; the product .so is untouched).
 set -e
-cd "$(dirname "$0")/../../paper_1305_1489_b200/csrc"
-out=../../tools/diag/sweep
+ROOT="$(cd "$(dirname "$0")/../.." && pwd)"
+cd "$ROOT/paper_1305_1489_b200/csrc"
+out="$ROOT/tools/diag/sweep"
+mkdir -p "$out"
 build() {  # name, extra nvcc flags
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
     --expt-relaxed-constexpr $2 -c capi.cu -o /tmp/capi_$1.o
