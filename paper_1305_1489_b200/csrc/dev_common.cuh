@@ -96,6 +96,22 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) 
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// ------------------------------------------------------ TMA bulk stores
+// Shared -> global bulk copy (16-byte aligned addresses, size a multiple of
+// 16), tracked by the issuing thread's bulk async-group.
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
+  asm volatile(
+      "fence.proxy.async.shared::cta;\n"
+      "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+      "cp.async.bulk.commit_group;\n" ::"l"(gdst), "r"(s), "r"(bytes)
+      : "memory");
+}
+// Wait until the issuing thread's bulk stores have finished reading shared memory.
+__device__ __forceinline__ void bulk_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
 // ------------------------------------------------------------------ DMMA
 // D(8x8) += A(8x4, row) * B(4x8, col), fp64 tensor-core MMA (SASS DMMA.8x8x4).
 // Lane layout: a = A[g][t], b = B[t][g], c = {C[g][2t], C[g][2t+1]}, g = lane/4, t = lane%4.

@@ -105,6 +105,11 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int FPT = HDG_C3_FPT;            // faces per V task (1, 2 or 4)
   constexpr int NGJ = 2 * EPB;               // GJ tasks in P3
   constexpr bool GJ_SEP = NWT > NGJ;         // GJ warps do nothing else in P3
+#ifndef HDG_C3_NO_BULK
+  const bool BULK_VF = LD == D3 && tab.nu == D3 && GJ_SEP;  // record layout == shared layout
+#else
+  const bool BULK_VF = false;
+#endif
   extern __shared__ double smem[];
   for (int i = threadIdx.x; i < EPB * Dm::PER_ELT + Dm::CTA_EXTRA; i += blockDim.x) smem[i] = 0.0;
   __syncthreads();
@@ -417,7 +422,16 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         // DMMA traffic on the same pipe, so this phase only moves data.
         const int w0 = GJ_SEP ? warp - NGJ : warp, nw = GJ_SEP ? NWT - NGJ : NWT;
 #ifndef HDG_DIAG_NO_P3MEM
-        if (factors) {  // V (D3 x M) and f of each element, contiguous in the cache record
+        if (factors && BULK_VF) {
+          // V and f are already in the record's layout in shared memory (LD ==
+          // d3): one TMA bulk store each, off the LSU path
+          if (lane == 0)
+            for (int e = w0; e < nb; e += nw) {
+              double* rec = factors + (K0 + e) * Dm::FACTORS + 2 * Dm::NSYM;
+              bulk_store(rec, Vb(e), D3 * M * 8);
+              bulk_store(rec + D3 * M, fv(e), D3 * 8);
+            }
+        } else if (factors) {  // V (D3 x M) and f of each element, contiguous in the cache record
           constexpr int NVF = D3 * M + D3;
           for (int q = w0 * 32 + lane; q < nb * NVF; q += nw * 32) {
             const int e = q / NVF, rem = q - e * NVF, c = rem / D3, r = rem - c * D3;
@@ -465,6 +479,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       for (int k = 0; k < D3; ++k) s += Sb(e)[r + k * LD] * fv(e)[k];
       fs(e)[r] = s;
     }
+    if (BULK_VF && lane == 0) bulk_store_wait_read();  // V, f are rewritten from P5 on
     __syncthreads();
     if (has_next)
       for (int e = warp; e < EPB; e += NWT)
