@@ -20,6 +20,10 @@
 #include "../../include/hdg_b200.h"
 #include "jit_quad.hpp"
 
+#ifndef HDG_QUAD_UNROLL
+#define HDG_QUAD_UNROLL 8  // k-steps of the node GEMM unrolled (A fragments in flight)
+#endif
+
 namespace hdgb {
 
 namespace {
@@ -47,18 +51,24 @@ quad_build_jit(int nelt, int nq, int nqp, int nsym, int nsymp, int d3, int d3p,
   double* Bc = Bk + rows * LDB;
   double* Bf = Bc + rows * LDB;
   const long K0 = long(blockIdx.x) * EB;
-  for (int idx = threadIdx.x; idx < rows * EB; idx += blockDim.x) {
-    const int q = idx / EB, e = idx % EB;
-    const long K = K0 + e;
+  // blockDim is a multiple of EB: each thread keeps one element (its vertex
+  // coordinates and volume in registers) and walks that element's nodes
+  const int e = threadIdx.x % EB;
+  const long K = K0 + e;
+  double vx[12], vk = 0.0;
+#pragma unroll
+  for (int j = 0; j < 12; ++j) vx[j] = K < nelt ? V[long(j) * nelt + K] : 0.0;
+  if (K < nelt) vk = vol[K];
+  for (int q = threadIdx.x / EB; q < rows; q += blockDim.x / EB) {
     double bk = 0.0, bc = 0.0, bf = 0.0;
     if (K < nelt) {
       if (q < nq) {
         const double l0 = __ldg(bary + q), l1 = __ldg(bary + nq + q), l2 = __ldg(bary + 2 * nq + q),
                      l3 = __ldg(bary + 3 * nq + q);
-        const double x = l0 * V[K] + l1 * V[nelt + K] + l2 * V[2L * nelt + K] + l3 * V[3L * nelt + K];
-        const double y = l0 * V[4L * nelt + K] + l1 * V[5L * nelt + K] + l2 * V[6L * nelt + K] + l3 * V[7L * nelt + K];
-        const double z = l0 * V[8L * nelt + K] + l1 * V[9L * nelt + K] + l2 * V[10L * nelt + K] + l3 * V[11L * nelt + K];
-        const double wv = __ldg(wq + q) * vol[K];
+        const double x = l0 * vx[0] + l1 * vx[1] + l2 * vx[2] + l3 * vx[3];
+        const double y = l0 * vx[4] + l1 * vx[5] + l2 * vx[6] + l3 * vx[7];
+        const double z = l0 * vx[8] + l1 * vx[9] + l2 * vx[10] + l3 * vx[11];
+        const double wv = __ldg(wq + q) * vk;
         bk = wv / (FIELD_KAPPA);
         bc = wv * (FIELD_C);
         bf = wv * (FIELD_F);
@@ -86,7 +96,7 @@ quad_build_jit(int nelt, int nq, int nqp, int nsym, int nsymp, int d3, int d3p,
     const double* Arow = sym ? Asym + (long(mt) * ((nqp + 4) / 4)) * 32 + lane
                              : Af + (long(mt) * (nqp / 4)) * 32 + lane;
     const double* B0 = sym ? Bk : Bf;
-#pragma unroll 4
+#pragma unroll QUAD_UNROLL
     for (int kk = 0; kk < nqp / 4; ++kk) {
       const double a = __ldg(Arow + kk * 32);
       const int o = (kk * 4 + t) * LDB + g;
@@ -272,7 +282,8 @@ sample_field_jit(int nelt, int nq, const double* __restrict__ bary, const double
 }  // namespace
 
 CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, std::string* err) {
-  const std::string src = "#define EB " + std::to_string(eb) + "\n#define FIELD_KAPPA " + field_expr(kap, "sk") +
+  const std::string src = "#define EB " + std::to_string(eb) + "\n#define QUAD_UNROLL " +
+                          std::to_string(HDG_QUAD_UNROLL) + "\n#define FIELD_KAPPA " + field_expr(kap, "sk") +
                           "\n#define FIELD_C " + field_expr(c, "sc") + "\n#define FIELD_F " + field_expr(f, "sf") +
                           "\n" + kQuadSource;
   return compile_cached(src, "quad_build_jit", err);

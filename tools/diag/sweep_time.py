@@ -22,7 +22,7 @@ if len(sys.argv) > 3:
 dm = eng.upload(mesh)
 g = eng.geometry(dm, cfg.tau)
 eng.set_timing(True)
-ts, tr = [], []
+ts, tr, tb = [], [], []
 d2 = (cfg.k + 1) * (cfg.k + 2) // 2
 uhat = torch.sin(torch.arange(dm.nfc * d2, dtype=torch.float64, device="cuda") * 0.37)
 for i in range(8):
@@ -32,6 +32,8 @@ for i in range(8):
     st = eng.stage_times()
     if i >= 2:
         ts.append(st["condense"])
+        tb.append(st["node_build"])
         tr.append(st["recover"])
-print(f"{os.path.basename(sys.argv[1])} {cfg.name}: condense median {np.median(ts):.3f} ms  "
+print(f"{os.path.basename(sys.argv[1])} {cfg.name}: node build median {np.median(tb):.3f} ms  "
+      f"condense median {np.median(ts):.3f} ms  "
       f"recover median {np.median(tr):.3f} ms")
