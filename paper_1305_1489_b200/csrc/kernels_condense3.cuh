@@ -106,7 +106,8 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int NGJ = 2 * EPB;               // GJ tasks in P3
   constexpr bool GJ_SEP = NWT > NGJ;         // GJ warps do nothing else in P3
 #ifndef HDG_C3_NO_BULK
-  const bool BULK_VF = LD == D3 && tab.nu == D3 && GJ_SEP;  // record layout == shared layout
+  // record layout == shared layout (k = 3), packed factors a 16-byte multiple
+  const bool BULK_VF = LD == D3 && (Dm::NSYM * 8) % 16 == 0 && tab.nu == D3 && GJ_SEP;
 #else
   const bool BULK_VF = false;
 #endif
@@ -149,9 +150,23 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
                              sg[12 + 3 * l1] * sg[12 + 3 * l2];
     }
   };
-  // packed lower column `lane` of a symmetric inverse held in registers -> recovery cache
-  auto store_factor = [&](const double (&a)[D3], long K, int off) {
-    if (factors && lane < D3) {
+  // packed lower column `lane` of a symmetric inverse held in registers -> recovery cache.
+  // With a shared-memory staging area (k = 3: the packed record is a 16-byte
+  // multiple) the packed matrix is assembled there and written by one TMA bulk
+  // store, which the caller's lane 0 must retire (bulk_store_wait_read) before
+  // the staging area is reused; otherwise straight from the registers.
+  auto store_factor = [&](const double (&a)[D3], long K, int off, double* stage) {
+    if (!factors) return;
+    if (BULK_VF && stage) {
+      if (lane < D3) {
+        double* dst = stage + lane * (2 * D3 - lane + 1) / 2 - lane;
+#pragma unroll
+        for (int i = 0; i < D3; ++i)
+          if (i >= lane) dst[i] = a[i];
+      }
+      __syncwarp();
+      if (lane == 0) bulk_store(factors + K * Dm::FACTORS + off, stage, Dm::NSYM * 8);
+    } else if (lane < D3) {
       double* dst = factors + K * Dm::FACTORS + off + lane * (2 * D3 - lane + 1) / 2 - lane;
 #pragma unroll
       for (int i = 0; i < D3; ++i)
@@ -208,7 +223,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int i = 0; i < D3; ++i) Mi(e)[lane + i * LD] = a[i];
     }
-    store_factor(a, K, 0);
+    store_factor(a, K, 0, Yb(e));  // R_# of this slot is dead until the next P1
     if (bad && lane == 0) flag_bad(bad_element, K);
   };
 
@@ -218,6 +233,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     load_geometry(K0, 0, threadIdx.x, NT);
     for (int e = warp; e < EPB; e += NWT)
       if (K0 + e < nelt) invert_M(e, K0 + e, Msym + (K0 + e) * Dm::NSYM);
+    if (BULK_VF && lane == 0) bulk_store_wait_read();  // staged M^-1 read before P1 reuses Yb
     cp_async_wait_all();
     __syncthreads();
     for (int e = warp; e < EPB; e += NWT) {
@@ -407,7 +423,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
               for (int i = 0; i < D3; ++i) Sb(e)[lane + i * LD] = a[i];
             }
-            store_factor(a, K, Dm::NSYM);
+            store_factor(a, K, Dm::NSYM, Dp(e));  // packed D is dead after P2
             if (bad && lane == 0) flag_bad(bad_element, K);
           } else if (has_next && Kn0 + e < nelt) {
 #ifdef HDG_DIAG_NO_GJ
@@ -416,6 +432,8 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             invert_M(e, Kn0 + e, Mi(e));  // packed M copied into the dead Mi(e) during P2
           }
         }
+        // the staged factors (Dp, Yb) are read before P4 / P5 reuse them
+        if (BULK_VF && lane == 0) bulk_store_wait_read();
       }
       if (!gj_warp || !GJ_SEP) {
         // No FP64 here: the sweeps' dependent DFMA chains stall badly behind
