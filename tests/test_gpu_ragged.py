@@ -72,3 +72,24 @@ def test_postprocess_ragged(k, n):
     t1 = core.tables(k + 1, 2 * (k + 1) + 2, 2 * k + 2)
     want = core.postprocess_star(em, t1, field(KAP), *(np.asfortranarray(a.T) for a in arrs))
     assert max_slice_relerr(np_(us), want.T) < TOL
+
+
+@pytest.mark.parametrize("k", range(6))
+def test_lowest_singular_element_across_ctas(k):
+    """local_solver.cpp:89-98 (test_local_solver.cpp:279-290): the lowest
+    singular element is reported, here with two singular elements far apart
+    (different CTAs / batches of every condensation kernel)."""
+    from paper_1305_1489_b200._lib import LocalSolverError
+    from paper_1305_1489_b200.engine import Engine
+    mesh = HostMesh.box(5)  # 750 tets
+    eng = Engine(0)
+    eng.set_degree(k)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 1.0)
+    X, _, _ = eng.quad_points(g)
+    kap = torch.ones_like(X)
+    kap[613] = float("inf")  # kappa^-1 = 0 -> M = 0 -> singular
+    kap[401] = float("inf")
+    with pytest.raises(LocalSolverError) as ei:
+        eng.build_condense(g, kap.contiguous(), 1.0, 1.0)
+    assert ei.value.element == 401
