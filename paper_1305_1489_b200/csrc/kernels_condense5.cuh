@@ -59,12 +59,18 @@ struct C5Dims {
 template <int K_> struct C5Cfg { static constexpr int NWT = 16; };
 
 // Inverse of the full symmetric N x N matrix X (stride LD, shared memory) by
-// the sweep operator with 2 x 2 pivots, all NT threads of the CTA; Y is a
-// second N x N buffer (same stride): each step reads one buffer and writes
-// the other (one barrier per step). The result ends in X (the step count is
-// made even by a final copy when needed). Thread layout: NT / N row groups
-// per column, each thread owns one column c and a run of rows, so the
-// column's pivot-row weights are computed once per step.
+// the sweep operator with 2 x 2 pivots, all NT threads of the CTA. Thread
+// layout: NT / N row groups per column, each thread owns one column c and a
+// run of rows of it IN REGISTERS for the whole sweep. Each step the owners of
+// the pivot rows k, k+1 and the threads of the pivot columns publish them
+// (4 N doubles) to a double-buffered stage in Y (8 N doubles), one barrier
+// per step, and every thread reads its column's pivot-row entries and its
+// rows' pivot-column entries from there: the whole matrix no longer
+// round-trips through shared memory each step. (Rows and columns are both
+// published although the swept matrix is symmetric in exact arithmetic: the
+// pivot columns carry the cancellation A - A (I - P^-1) of the sweep, the rows
+// do not, and the update must use the same triangle as the reference order.)
+// The result (X^-1, full) is written back to X.
 // Returns the pivot test of local_solver.cpp:50-57 (Cholesky pivots).
 template <int N, int LD, int NT>
 __device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
@@ -72,63 +78,83 @@ __device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
   constexpr int RPT = (N + RG - 1) / RG;      // rows per thread
   const int c = threadIdx.x / RG, i0 = (threadIdx.x - c * RG) * RPT;
   const bool live = c < N;
+  double a[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) a[u] = (live && i0 + u < N) ? X[i0 + u + c * LD] : 0.0;
   double pmin = 1e300, pmax = 0.0;
   bool bad = false;
-  double* src = X;
-  double* dst = Y;
-  int nsteps = 0;
-  for (int k = 0; k < N; k += 2, ++nsteps) {
+  // stage of the pivot pair (k, k+1): [0, N) row k by column, [N, 2N) row
+  // k+1, [2N, 3N) column k by row, [3N, 4N) column k+1. The entries a step
+  // produces for the next pair are staged from the update loop itself.
+  auto put = [&](double* st, int k, int u, bool colk, bool colk1, double v) {
+    const int i = i0 + u;
+    if (i == k) st[c] = v;
+    if (i == k + 1) st[N + c] = v;
+    if (colk) st[2 * N + i] = v;
+    if (colk1) st[3 * N + i] = v;
+  };
+  if (live) {
+#pragma unroll
+    for (int u = 0; u < RPT; ++u)
+      if (i0 + u < N) put(Y, 0, u, c == 0, c == 1, a[u]);
+  }
+  const bool stats = threadIdx.x < 32;  // the pivot test is returned to thread 0
+  int buf = 0;
+  for (int k = 0; k < N; k += 2, buf ^= 1) {
+    double* st = Y + buf * 4 * N;
+    double* nx = Y + (buf ^ 1) * 4 * N;
+    const bool colk = c == k + 2, colk1 = c == k + 3;
+    __syncthreads();
     if (k + 1 < N) {
-      const double p00 = src[k + k * LD], p01 = src[k + 1 + k * LD], p11 = src[k + 1 + (k + 1) * LD];
+      const double p00 = st[k], p01 = st[2 * N + k + 1], p11 = st[N + k + 1];
       const double det = fma(p00, p11, -p01 * p01);
       const double id = gj_rcp(det);
       const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;
-      if (!(p00 > 0.0) || !(det > 0.0)) bad = true;
-      const double d1 = 1.0 / i11;
-      pmin = fmin(pmin, fmin(p00, d1));
-      pmax = fmax(pmax, fmax(p00, d1));
+      if (stats) {
+        if (!(p00 > 0.0) || !(det > 0.0)) bad = true;
+        const double d1 = det * gj_rcp(p00);  // second Cholesky pivot of the pair
+        pmin = fmin(pmin, fmin(p00, d1));
+        pmax = fmax(pmax, fmax(p00, d1));
+      }
       if (live) {
-        const double a0 = src[k + c * LD] - (c == k ? 1.0 : 0.0);
-        const double a1 = src[k + 1 + c * LD] - (c == k + 1 ? 1.0 : 0.0);
+        const double a0 = st[c] - (c == k ? 1.0 : 0.0);
+        const double a1 = st[N + c] - (c == k + 1 ? 1.0 : 0.0);
         const double w0 = fma(i00, a0, i01 * a1), w1 = fma(i01, a0, i11 * a1);
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
           const int i = i0 + u;
           if (i < N) {
-            double v = src[i + c * LD] - fma(src[i + k * LD], w0, src[i + (k + 1) * LD] * w1);
+            double v = a[u] - fma(st[2 * N + i], w0, st[3 * N + i] * w1);
             if (i == k) v = w0 - (c == k ? 1.0 : 0.0);
             if (i == k + 1) v = w1 - (c == k + 1 ? 1.0 : 0.0);
-            dst[i + c * LD] = v;
+            a[u] = v;
+            put(nx, k + 2, u, colk, colk1, v);
           }
         }
       }
     } else {  // trailing scalar pivot
-      const double p = src[k + k * LD];
-      if (!(p > 0.0)) bad = true;
-      pmin = fmin(pmin, p);
-      pmax = fmax(pmax, p);
+      const double p = st[k];
+      if (stats) {
+        if (!(p > 0.0)) bad = true;
+        pmin = fmin(pmin, p);
+        pmax = fmax(pmax, p);
+      }
       const double ip = gj_rcp(p);
       if (live) {
-        const double w = (src[k + c * LD] - (c == k ? 1.0 : 0.0)) * ip;
+        const double w = (st[c] - (c == k ? 1.0 : 0.0)) * ip;
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
           const int i = i0 + u;
-          if (i < N) dst[i + c * LD] = i == k ? w - (c == k ? 1.0 : 0.0) : src[i + c * LD] - src[i + k * LD] * w;
+          if (i < N) a[u] = i == k ? w - (c == k ? 1.0 : 0.0) : a[u] - st[2 * N + i] * w;
         }
       }
     }
-    __syncthreads();
-    double* tmp = src;
-    src = dst;
-    dst = tmp;
   }
-  // the sweep leaves -X^-1 in src; negate into X
+  // the sweep leaves -X^-1; negate into X
   if (live) {
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      const int i = i0 + u;
-      if (i < N) X[i + c * LD] = -src[i + c * LD];
-    }
+    for (int u = 0; u < RPT; ++u)
+      if (i0 + u < N) X[i0 + u + c * LD] = -a[u];
   }
   __syncthreads();
   return bad || pmin < 1e-14 * pmax;
