@@ -170,7 +170,6 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int NWT = C5Cfg<K_>::NWT, NT = NWT * 32;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, MP = Dm::MP, LD = Dm::LD, KS = Dm::KS;
   constexpr int MT = Dm::MT, NTM = Dm::NTM, NSYM = Dm::NSYM;
-  constexpr int NLS = MT * (MT + 1) / 2;                 // lower tiles of S
   constexpr int NTF = face_tiles(D2);
   constexpr int NLP = (NTM / 2 + 1) * ((NTM + 1) / 2);  // C tile pairs (rows' pairs and singles)
   constexpr bool PAD = Dm::D34 != D3;                    // k-padding present (k = 4)
@@ -203,47 +202,75 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     return __ldg(Ch + h * D3 * D3 + r + k * D3);
   };
-  // T_h = M^-1 Chat_h^T: one 8 x 8 tile (two chains)
-  auto t_tile = [&](double* Tb, int h, int tile) {
-    const int mt = tile / MT, nt = tile - mt * MT;
-    const int r = mt * 8 + g, c = nt * 8 + g;
-    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+  // T_h = M^-1 Chat_h^T by column strips: column tile nt, row tiles [lo, hi)
+  // (three row groups per column): the Chat fragment of a k-step (L1/L2)
+  // feeds every row tile of the group
+  constexpr int TSG = 3;                           // row groups per column strip
+  constexpr int NTS = MT * TSG;                    // T strip tasks
+  auto t_strip = [&](double* Tb, int h, int task) {
+    const int nt = task / TSG, part = task - nt * TSG;
+    const int lo = part * MT / TSG, hi = (part + 1) * MT / TSG;
+    const int c = nt * 8 + g;
+    double acc[(MT + TSG - 1) / TSG][2];
 #pragma unroll
+    for (int u = 0; u < (MT + TSG - 1) / TSG; ++u) acc[u][0] = acc[u][1] = 0.0;
+#pragma unroll 2
     for (int kk = 0; kk < KS; ++kk) {
       const int k = kk * 4 + t;
-      const double a = Mi[r + k * LD], b = chat(h, c, k);
-      if (kk & 1) dmma(q[0], q[1], a, b);
-      else dmma(p[0], p[1], a, b);
-    }
-    const int rr = mt * 8 + g, c0 = nt * 8 + 2 * t;
-    if (rr < LD) {
+      const double b = chat(h, c, k);
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2)
-        if (c0 + h2 < D3) Tb[rr + (c0 + h2) * LD] = rr < D3 ? p[h2] + q[h2] : 0.0;
+      for (int u = 0; u < (MT + TSG - 1) / TSG; ++u)
+        if (lo + u < hi) dmma(acc[u][0], acc[u][1], Mi[((lo + u) * 8 + g) + k * LD], b);
+    }
+    const int c0 = nt * 8 + 2 * t;
+#pragma unroll
+    for (int u = 0; u < (MT + TSG - 1) / TSG; ++u) {
+      const int rr = (lo + u) * 8 + g;
+      if (lo + u < hi && rr < LD) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2)
+          if (c0 + h2 < D3) Tb[rr + (c0 + h2) * LD] = rr < D3 ? acc[u][h2] : 0.0;
+      }
     }
   };
-  // S (+)= Chat'_h Tb over the lower tiles, Chat'_h = sum_# G(#,h) Chat_#
-  auto s_tile = [&](const double* Tb, int h, int tile, bool first) {
-    int mt = 0, rem = tile;
-    while (rem > mt) { rem -= mt + 1; ++mt; }
-    const int j = rem, r = mt * 8 + g;
+  // S (+)= Chat'_h Tb by row strips: row tile mt, column tiles of one chunk
+  // (rows split into chunks of <= 3 lower tiles): the combined Chat'_h
+  // fragment (3 L1/L2 loads + FMAs) of a k-step feeds the whole chunk
+  constexpr int SCH = 3;                           // lower tiles per S task at most
+  constexpr int NSS = [] {
+    int n = 0;
+    for (int mt = 0; mt < MT; ++mt) n += (mt + SCH) / SCH;
+    return n;
+  }();
+  auto s_strip = [&](const double* Tb, int h, int task, bool first) {
+    int mt = 0, rem = task;
+    while (rem >= (mt + SCH) / SCH) { rem -= (mt + SCH) / SCH; ++mt; }
+    const int nch = (mt + SCH) / SCH;
+    const int jlo = rem * (mt + 1) / nch, jhi = (rem + 1) * (mt + 1) / nch;
+    const int r = mt * 8 + g;
     const double g0 = sg[32 + h], g1 = sg[35 + h], g2 = sg[38 + h];  // G symmetric: G(#, h)
-    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
-#pragma unroll 7
+    double acc[SCH][2];
+#pragma unroll
+    for (int u = 0; u < SCH; ++u) acc[u][0] = acc[u][1] = 0.0;
+#pragma unroll 2
     for (int kk = 0; kk < KS; ++kk) {
       const int k = kk * 4 + t;
       const double a = g0 * chat(0, r, k) + g1 * chat(1, r, k) + g2 * chat(2, r, k);
-      const double b = Tb[k + (j * 8 + g) * LD];
-      if (kk & 1) dmma(q[0], q[1], a, b);
-      else dmma(p[0], p[1], a, b);
+#pragma unroll
+      for (int u = 0; u < SCH; ++u)
+        if (jlo + u < jhi) dmma(acc[u][0], acc[u][1], a, Tb[k + ((jlo + u) * 8 + g) * LD]);
     }
 #pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const int c = j * 8 + 2 * t + h2;
-      if (r < D3 && c <= r) {
-        const double v = (first ? Dp[sym_idx(r, c, D3)] : S[r + c * LD]) + p[h2] + q[h2];
-        S[r + c * LD] = v;
-        S[c + r * LD] = v;
+    for (int u = 0; u < SCH; ++u) {
+      if (jlo + u >= jhi) break;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int c = (jlo + u) * 8 + 2 * t + h2;
+        if (r < D3 && c <= r) {
+          const double v = (first ? Dp[sym_idx(r, c, D3)] : S[r + c * LD]) + acc[u][h2];
+          S[r + c * LD] = v;
+          S[c + r * LD] = v;
+        }
       }
     }
   };
@@ -293,7 +320,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         for (int i = c + lane; i < D3; i += 32) factors[K * Dm::FACTORS + sym_idx(i, c, D3)] = Mi[i + c * LD];
 
     // ---- P2: Zp strips (T_l W_l^T staged into V) | T0 = M^-1 Chat_0^T
-    for (int task = warp; task < NTM + MT * MT; task += NWT) {
+    for (int task = warp; task < NTM + NTS; task += NWT) {
       if (task < NTM) {
         const int nt = task, cz = nt * 8 + g, wbc = wb[cz];
         const double tc = Tc[cz];
@@ -318,26 +345,26 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           }
         }
       } else {
-        t_tile(T0, 0, task - NTM);
+        t_strip(T0, 0, task - NTM);
       }
     }
     __syncthreads();
     // ---- P3..P5: S accumulation beside the next T product / the V rows
-    for (int task = warp; task < NLS + MT * MT; task += NWT) {
-      if (task < NLS) s_tile(T0, 0, task, true);
-      else t_tile(T1, 1, task - NLS);
+    for (int task = warp; task < NSS + NTS; task += NWT) {
+      if (task < NSS) s_strip(T0, 0, task, true);
+      else t_strip(T1, 1, task - NSS);
     }
     __syncthreads();
-    for (int task = warp; task < NLS + MT * MT; task += NWT) {
-      if (task < NLS) s_tile(T1, 1, task, false);
-      else t_tile(T0, 2, task - NLS);
+    for (int task = warp; task < NSS + NTS; task += NWT) {
+      if (task < NSS) s_strip(T1, 1, task, false);
+      else t_strip(T0, 2, task - NSS);
     }
     __syncthreads();
-    for (int task = warp; task < NLS + 4 * MT; task += NWT) {
-      if (task < NLS) {
-        s_tile(T0, 2, task, false);
+    for (int task = warp; task < NSS + 4 * MT; task += NWT) {
+      if (task < NSS) {
+        s_strip(T0, 2, task, false);
       } else {  // V rows of row tile mt, face l
-        const int mt = (task - NLS) >> 2, l = (task - NLS) & 3;
+        const int mt = (task - NSS) >> 2, l = (task - NSS) & 3;
         const int r = mt * 8 + g;
         const int cl0 = l * D2, cl1 = cl0 + D2, nt0 = cl0 / 8;
         const double b0 = beta[cl0], b1 = beta[MP + cl0], b2 = beta[2 * MP + cl0];
