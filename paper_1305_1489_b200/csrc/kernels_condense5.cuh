@@ -93,6 +93,16 @@ __device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
     if (colk) st[2 * N + i] = v;
     if (colk1) st[3 * N + i] = v;
   };
+  // the pivot columns of the next pair: only their RG threads store (after
+  // the update loop, so the other warps skip it)
+  auto put_cols = [&](double* st, int k) {
+    if (c == k || c == k + 1) {
+      double* col = st + (c == k ? 2 : 3) * N;
+#pragma unroll
+      for (int u = 0; u < RPT; ++u)
+        if (i0 + u < N) col[i0 + u] = a[u];
+    }
+  };
   if (live) {
 #pragma unroll
     for (int u = 0; u < RPT; ++u)
@@ -103,7 +113,6 @@ __device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
   for (int k = 0; k < N; k += 2, buf ^= 1) {
     double* st = Y + buf * 4 * N;
     double* nx = Y + (buf ^ 1) * 4 * N;
-    const bool colk = c == k + 2, colk1 = c == k + 3;
     __syncthreads();
     if (k + 1 < N) {
       const double p00 = st[k], p01 = st[2 * N + k + 1], p11 = st[N + k + 1];
@@ -128,9 +137,10 @@ __device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
             if (i == k) v = w0 - (c == k ? 1.0 : 0.0);
             if (i == k + 1) v = w1 - (c == k + 1 ? 1.0 : 0.0);
             a[u] = v;
-            put(nx, k + 2, u, colk, colk1, v);
+            put(nx, k + 2, u, false, false, v);
           }
         }
+        put_cols(nx, k + 2);
       }
     } else {  // trailing scalar pivot
       const double p = st[k];
