@@ -10,6 +10,7 @@
 #include <cuda.h>
 #include <nvrtc.h>
 
+#include <cmath>
 #include <cstdio>
 #include <mutex>
 #include <sstream>
@@ -69,6 +70,7 @@ quad_build_jit(int nelt, int nq, int nqp, int nsym, int nsymp, int d3, int d3p,
         const double y = l0 * vx[4] + l1 * vx[5] + l2 * vx[6] + l3 * vx[7];
         const double z = l0 * vx[8] + l1 * vx[9] + l2 * vx[10] + l3 * vx[11];
         const double wv = __ldg(wq + q) * vk;
+        FIELD_STMTS
         bk = wv / (FIELD_KAPPA);
         bc = wv * (FIELD_C);
         bf = wv * (FIELD_F);
@@ -180,41 +182,91 @@ Cache& cache() {
 
 }  // namespace
 
-// Infix C expression of a field at (x, y, z) for node q of element K.
-std::string field_expr(const hdg_field& f, const char* sample_ptr) {
+// Straight-line device code for the field programs of one kernel. Every
+// operation becomes one named temporary, hash-consed across all the fields
+// the kernel evaluates (C2's f repeats kappa's sin/cos terms, and x + y feeds
+// both exp and cos), products of literals are folded on the host (the same
+// IEEE double product the reference's callback computes), and sin/cos of an
+// exact multiple of pi use sinpi/cospi (exact argument reduction, no
+// Cody-Waite / Payne-Hanek path; differs from sin(fl(pi) m E) by ~1e-16 E).
+std::string FieldEmitter::emit(const hdg_field& f, const char* sample_ptr) {
   if (f.kind == HDG_FIELD_CONST) return lit(f.value);
   if (f.kind == HDG_FIELD_SAMPLED) return std::string("__ldg(") + sample_ptr + " + K * nq + q)";
-  std::vector<std::string> st;
+  struct Val {
+    std::string s;            // temporary, literal or coordinate
+    bool is_const = false;
+    double c = 0.0;
+    double mul_c = 0.0;       // MUL by a literal: the literal and the other operand
+    std::string mul_e;
+  };
+  auto temp = [&](const std::string& expr) {
+    auto it = memo_.find(expr);
+    if (it != memo_.end()) return it->second;
+    const std::string name = "_t" + std::to_string(ntemp_++);
+    stmts_ += "const double " + name + " = " + expr + "; ";
+    memo_.emplace(expr, name);
+    return name;
+  };
+  auto konst = [&](double v) { Val r; r.s = lit(v); r.is_const = true; r.c = v; return r; };
+  auto node = [&](const std::string& expr) { Val r; r.s = temp(expr); return r; };
+  // m with c == m * fl(pi) exactly, m a small multiple of 1/4 (else 0)
+  auto pi_multiple = [](double c) {
+    const double m = c / 3.141592653589793;
+    const double mq = std::nearbyint(m * 4.0) / 4.0;
+    return (mq != 0.0 && std::fabs(mq) <= 64.0 && mq * 3.141592653589793 == c) ? mq : 0.0;
+  };
+  std::vector<Val> st;
   int ci = 0;
   for (int i = 0; i < f.nops; ++i) {
     const int op = f.ops[i];
-    auto pop = [&]() { std::string v = st.back(); st.pop_back(); return v; };
+    auto pop = [&]() { Val v = st.back(); st.pop_back(); return v; };
     switch (op) {
-      case HDG_OP_X: st.push_back("x"); break;
-      case HDG_OP_Y: st.push_back("y"); break;
-      case HDG_OP_Z: st.push_back("z"); break;
-      case HDG_OP_CONST: st.push_back(lit(f.consts[ci++])); break;
-      case HDG_OP_NEG: st.back() = "(-" + st.back() + ")"; break;
-      case HDG_OP_SIN: st.back() = "sin(" + st.back() + ")"; break;
-      case HDG_OP_COS: st.back() = "cos(" + st.back() + ")"; break;
-      case HDG_OP_EXP: st.back() = "exp(" + st.back() + ")"; break;
-      case HDG_OP_SQRT: st.back() = "sqrt(" + st.back() + ")"; break;
-      case HDG_OP_ABS: st.back() = "fabs(" + st.back() + ")"; break;
+      case HDG_OP_X: { Val v; v.s = "x"; st.push_back(v); break; }
+      case HDG_OP_Y: { Val v; v.s = "y"; st.push_back(v); break; }
+      case HDG_OP_Z: { Val v; v.s = "z"; st.push_back(v); break; }
+      case HDG_OP_CONST: st.push_back(konst(f.consts[ci++])); break;
+      case HDG_OP_NEG: {
+        const Val a = pop();
+        st.push_back(a.is_const ? konst(-a.c) : node("(-" + a.s + ")"));
+        break;
+      }
+      case HDG_OP_SIN:
+      case HDG_OP_COS: {
+        const Val a = pop();
+        const double m = a.mul_e.empty() ? 0.0 : pi_multiple(a.mul_c);
+        const char* fn = op == HDG_OP_SIN ? (m != 0.0 ? "sinpi" : "sin") : (m != 0.0 ? "cospi" : "cos");
+        st.push_back(node(std::string(fn) + "(" + (m != 0.0 ? (m == 1.0 ? a.mul_e : lit(m) + " * " + a.mul_e) : a.s) + ")"));
+        break;
+      }
+      case HDG_OP_EXP: st.push_back(node("exp(" + pop().s + ")")); break;
+      case HDG_OP_SQRT: st.push_back(node("sqrt(" + pop().s + ")")); break;
+      case HDG_OP_ABS: st.push_back(node("fabs(" + pop().s + ")")); break;
       default: {
-        const std::string b = pop(), a = pop();
+        const Val b = pop(), a = pop();
+        if (a.is_const && b.is_const && op >= HDG_OP_ADD && op <= HDG_OP_DIV) {
+          st.push_back(konst(op == HDG_OP_ADD ? a.c + b.c : op == HDG_OP_SUB ? a.c - b.c
+                             : op == HDG_OP_MUL ? a.c * b.c : a.c / b.c));
+          break;
+        }
         switch (op) {
-          case HDG_OP_ADD: st.push_back("(" + a + " + " + b + ")"); break;
-          case HDG_OP_SUB: st.push_back("(" + a + " - " + b + ")"); break;
-          case HDG_OP_MUL: st.push_back("(" + a + " * " + b + ")"); break;
-          case HDG_OP_DIV: st.push_back("(" + a + " / " + b + ")"); break;
-          case HDG_OP_LT: st.push_back("((" + a + ") < (" + b + ") ? 1.0 : 0.0)"); break;
-          case HDG_OP_POW: st.push_back("pow(" + a + ", " + b + ")"); break;
-          default: st.push_back("0.0");
+          case HDG_OP_ADD: st.push_back(node("(" + a.s + " + " + b.s + ")")); break;
+          case HDG_OP_SUB: st.push_back(node("(" + a.s + " - " + b.s + ")")); break;
+          case HDG_OP_MUL: {
+            Val r = node("(" + a.s + " * " + b.s + ")");
+            if (a.is_const) { r.mul_c = a.c; r.mul_e = b.s; }
+            else if (b.is_const) { r.mul_c = b.c; r.mul_e = a.s; }
+            st.push_back(r);
+            break;
+          }
+          case HDG_OP_DIV: st.push_back(node("(" + a.s + " / " + b.s + ")")); break;
+          case HDG_OP_LT: st.push_back(node("((" + a.s + ") < (" + b.s + ") ? 1.0 : 0.0)")); break;
+          case HDG_OP_POW: st.push_back(node("pow(" + a.s + ", " + b.s + ")")); break;
+          default: st.push_back(konst(0.0));
         }
       }
     }
   }
-  return st.empty() ? "0.0" : st.back();
+  return st.empty() ? "0.0" : st.back().s;
 }
 
 namespace {
@@ -275,6 +327,7 @@ sample_field_jit(int nelt, int nq, const double* __restrict__ bary, const double
     const double x = l0 * V[K] + l1 * V[nelt + K] + l2 * V[2L * nelt + K] + l3 * V[3L * nelt + K];
     const double y = l0 * V[4L * nelt + K] + l1 * V[5L * nelt + K] + l2 * V[6L * nelt + K] + l3 * V[7L * nelt + K];
     const double z = l0 * V[8L * nelt + K] + l1 * V[9L * nelt + K] + l2 * V[10L * nelt + K] + l3 * V[11L * nelt + K];
+    FIELD_STMTS
     out[idx] = FIELD_EXPR;
   }
 }
@@ -282,9 +335,11 @@ sample_field_jit(int nelt, int nq, const double* __restrict__ bary, const double
 }  // namespace
 
 CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, std::string* err) {
+  FieldEmitter fe;
+  const std::string ek = fe.emit(kap, "sk"), ec = fe.emit(c, "sc"), ef = fe.emit(f, "sf");
   const std::string src = "#define EB " + std::to_string(eb) + "\n#define QUAD_UNROLL " +
-                          std::to_string(HDG_QUAD_UNROLL) + "\n#define FIELD_KAPPA " + field_expr(kap, "sk") +
-                          "\n#define FIELD_C " + field_expr(c, "sc") + "\n#define FIELD_F " + field_expr(f, "sf") +
+                          std::to_string(HDG_QUAD_UNROLL) + "\n#define FIELD_STMTS " + fe.stmts() +
+                          "\n#define FIELD_KAPPA " + ek + "\n#define FIELD_C " + ec + "\n#define FIELD_F " + ef +
                           "\n" + kQuadSource;
   return compile_cached(src, "quad_build_jit", err);
 }
@@ -294,8 +349,10 @@ CUfunction jit_sample_kernel(const hdg_field& f, std::string* err) {
     if (err) *err = "only program fields are sampled";
     return nullptr;
   }
-  return compile_cached("#define FIELD_EXPR " + field_expr(f, "nullptr") + "\n" + kSampleSource, "sample_field_jit",
-                        err);
+  FieldEmitter fe;
+  const std::string e = fe.emit(f, "nullptr");
+  return compile_cached("#define FIELD_STMTS " + fe.stmts() + "\n#define FIELD_EXPR " + e + "\n" + kSampleSource,
+                        "sample_field_jit", err);
 }
 
 bool launch_quad_jit(CUfunction fn, cudaStream_t stream, int grid, int block, size_t smem, void** args,

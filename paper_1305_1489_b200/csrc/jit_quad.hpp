@@ -4,11 +4,24 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <unordered_map>
 
 #include "../../include/hdg_b200.h"
 
 namespace hdgb {
-std::string field_expr(const hdg_field& f, const char* sample_ptr);
+// Field programs -> straight-line device code (shared temporaries across the
+// fields of one kernel): emit() returns the expression naming the field's
+// value; stmts() the declarations to place before its first use.
+class FieldEmitter {
+ public:
+  std::string emit(const hdg_field& f, const char* sample_ptr);
+  const std::string& stmts() const { return stmts_; }
+
+ private:
+  std::string stmts_;
+  std::unordered_map<std::string, std::string> memo_;
+  int ntemp_ = 0;
+};
 // Compiled (cached) kernel for these fields and EB elements per CTA, or nullptr with *err set.
 CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, std::string* err);
 // Kernel sampling a PROGRAM field at every element node (SAMPLED layout), or nullptr.
