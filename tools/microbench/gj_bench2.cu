@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cuda_runtime.h>
 #include "../../paper_1305_1489_b200/csrc/kernels_condense2.cuh"
+#include "gj_sweep_v3.cuh"
 using namespace hdgb;
 
 template <int N, int LD, int V, bool ROW = false>
@@ -30,6 +31,9 @@ __global__ void __launch_bounds__(512) gj_smem(double* out, long long* cyc, int 
         else a[i] = lane < N ? S[rr + c * LD] : 0.0;
       }
       if (V == 1) warp_gj_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
+      else if (V == 3) gj_sweep_inverse3<N>(a, stage + warp * 128, lane, pmin, pmax);
+      else if (V == 4) gj_sweep_inverse3<N, true>(a, stage + warp * 128, lane, pmin, pmax);
+      else if (V >= 5) gj_sweep_inverse3<N, false, V - 4>(a, stage + warp * 128, lane, pmin, pmax);
       else gj_sweep_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
       if (lane < N) {
 #pragma unroll
@@ -61,6 +65,9 @@ __global__ void __launch_bounds__(512) gj_reg(double* out, long long* cyc, int r
     long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
       if (V == 1) warp_gj_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
+      else if (V == 3) gj_sweep_inverse3<N>(a, stage + warp * 128, lane, pmin, pmax);
+      else if (V == 4) gj_sweep_inverse3<N, true>(a, stage + warp * 128, lane, pmin, pmax);
+      else if (V >= 5) gj_sweep_inverse3<N, false, V - 4>(a, stage + warp * 128, lane, pmin, pmax);
       else gj_sweep_inverse<N>(a, stage + warp * 128, lane, pmin, pmax);
     }
     long long t1 = clock64();
@@ -76,7 +83,7 @@ void run(const char* name) {
   double* out; long long* cyc;
   cudaMalloc(&out, 4096 * 8); cudaMalloc(&cyc, 148 * 16 * 8);
   long long h[148 * 16];
-  for (int act : {1, 4, 8}) {
+  for (int act : {1, 4, 8, 12, 16}) {
     gj_smem<N, (N + 3) / 4 * 4, V><<<148, 512>>>(out, cyc, 32, act);
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
     printf("%s N=%d %d active warps: %lld cycles per inverse\n", name, N, act, h[0]);
@@ -96,6 +103,32 @@ void run(const char* name) {
   cudaFree(out); cudaFree(cyc);
 }
 
+__global__ void rcp_err(double* out, int n) {
+  double mx = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double x = 1.0 + (double)i / n * 3.0 + 1e-7 * (i % 977);
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    mx = fmax(mx, fabs(fma(-x, r, 1.0)));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)out, (unsigned long long)__double_as_longlong(mx));
+}
+
+template <int N, int VA, int VB>
+void check2() {
+  double *o1, *o2; long long* cyc;
+  cudaMalloc(&o1, 4096 * 8); cudaMalloc(&o2, 4096 * 8); cudaMalloc(&cyc, 148 * 16 * 8);
+  gj_smem<N, (N + 3) / 4 * 4, VA><<<1, 512>>>(o1, cyc, 1, 1);
+  gj_smem<N, (N + 3) / 4 * 4, VB><<<1, 512>>>(o2, cyc, 1, 1);
+  double h1[N * N + 2], h2[N * N + 2];
+  cudaMemcpy(h1, o1, sizeof(h1), cudaMemcpyDeviceToHost);
+  cudaMemcpy(h2, o2, sizeof(h2), cudaMemcpyDeviceToHost);
+  double md = 0, mx = 0;
+  for (int i = 0; i < N * N; ++i) { md = fmax(md, fabs(h1[i] - h2[i])); mx = fmax(mx, fabs(h1[i])); }
+  printf("N=%d v%d vs v%d max|diff|/max|inv| = %.3e  pmin %.6e/%.6e\n", N, VA, VB, md / mx, h1[N * N], h2[N * N]);
+}
+
 template <int N>
 void check() {
   double *o1, *o2; long long* cyc;
@@ -113,7 +146,15 @@ void check() {
 
 int main() {
   check<20>(); check<10>(); check<19>(); check<4>(); check<1>();
-  run<20, 1>("v1"); run<20, 2>("v2");
-  run<10, 1>("v1"); run<10, 2>("v2");
+  check2<20, 2, 3>(); check2<20, 2, 4>(); check2<19, 2, 3>(); check2<20, 1, 3>();
+  {
+    double* e; cudaMalloc(&e, 8); cudaMemset(e, 0, 8);
+    rcp_err<<<148, 256>>>(e, 1 << 24);
+    double h; cudaMemcpy(&h, e, 8, cudaMemcpyDeviceToHost);
+    printf("rcp.approx.f64 max |1 - x r| = %.3e (2^%.1f)\n", h, log2(h));
+  }
+  check2<20, 2, 5>(); check2<20, 2, 7>();
+  run<20, 2>("v2"); run<20, 3>("v3"); run<20, 5>("lds64"); run<20, 6>("noload"); run<20, 7>("shfl");
+
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }

@@ -1,15 +1,24 @@
 // Warp-register sweep inverse of a small SPD matrix (used by the v3
 // condensation kernel, kernels_condense3.cuh). Self-contained: no includes.
 #pragma once
+// microbench candidate (v3 step: adjugate weights, fused pivot-row update)
 
 // 1/x to full double precision: MUFU reciprocal seed + two Newton steps.
-__device__ __forceinline__ double gj_rcp(double x) {
+__device__ __forceinline__ double gj_rcp_v3(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
   double e = fma(-x, r, 1.0);
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
+}
+
+// 1/x by one cubic refinement of the MUFU seed: r (1 + e + e^2), e = 1 - x r
+__device__ __forceinline__ double gj_rcp_cubic3(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 
 // Inverse of the SPD N x N matrix held by a warp (lane c owns column c in
@@ -20,9 +29,10 @@ __device__ __forceinline__ double gj_rcp(double x) {
 // lanes take their diagonal entry minus one into w = P^-1 a_K, which yields
 // their special update weights (rows of I - P^-1) without selects, and each
 // lane records its own pivot (one warp reduction at the end).
-template <int N>
-__device__ __forceinline__ void gj_sweep_inverse(double (&a)[N], double* stage, int lane, double& pmin,
+template <int N, bool CUBIC = false, int MODE = 0>
+__device__ __forceinline__ void gj_sweep_inverse3(double (&a)[N], double* stage, int lane, double& pmin,
                                                  double& pmax) {
+  auto RCP = [](double x) { return CUBIC ? gj_rcp_cubic3(x) : gj_rcp_v3(x); };
   double piv = 1.0;  // lane c: Cholesky pivot c (odd c: its reciprocal until the end)
 #pragma unroll
   for (int k = 0; k + 1 < N; k += 2) {
@@ -50,7 +60,7 @@ __device__ __forceinline__ void gj_sweep_inverse(double (&a)[N], double* stage, 
     const double ak0 = m0 ? a[k] - 1.0 : a[k];
     const double ak1 = m1 ? a[k + 1] - 1.0 : a[k + 1];
     // w = P^-1 a_K = adj(P) a_K / det: the adjugate products and the next
-    // pivot rows' contractions overlap the reciprocal, one FMA follows it
+    // pivot rows' contractions overlap the reciprocal, so one FMA follows it
     const double u0 = fma(p11, ak0, -p01 * ak1);
     const double u1 = fma(p00, ak1, -p01 * ak0);
     double s0 = 0.0, s1 = 0.0;
@@ -58,7 +68,7 @@ __device__ __forceinline__ void gj_sweep_inverse(double (&a)[N], double* stage, 
       s0 = fma(n0x, u0, n1x * u1);
       if (k + 3 < N) s1 = fma(n0y, u0, n1y * u1);
     }
-    const double id = gj_rcp(det);
+    const double id = RCP(det);
     if (k + 2 < N) {
       a[k + 2] = fma(-s0, id, a[k + 2]);
       if (k + 3 < N) a[k + 3] = fma(-s1, id, a[k + 3]);
@@ -70,8 +80,18 @@ __device__ __forceinline__ void gj_sweep_inverse(double (&a)[N], double* stage, 
 #pragma unroll
     for (int i0 = 0; i0 < N; i0 += 2) {
       if (i0 == k || i0 == k + 2) continue;
-      const double2 v0 = *reinterpret_cast<const double2*>(st + i0);
-      const double2 v1 = *reinterpret_cast<const double2*>(st + 32 + i0);
+      double2 v0, v1;
+      if (MODE == 0) {
+        v0 = *reinterpret_cast<const double2*>(st + i0);
+        v1 = *reinterpret_cast<const double2*>(st + 32 + i0);
+      } else if (MODE == 1) {
+        v0.x = st[i0]; v0.y = st[i0 + 1]; v1.x = st[32 + i0]; v1.y = st[33 + i0];
+      } else if (MODE == 2) {  // timing only (wrong values)
+        v0.x = n0x + i0; v0.y = n0y; v1.x = n1x; v1.y = n1y + i0;
+      } else {
+        v0.x = __shfl_sync(0xffffffffu, ak0, i0); v0.y = __shfl_sync(0xffffffffu, ak0, i0 + 1);
+        v1.x = __shfl_sync(0xffffffffu, ak1, i0); v1.y = __shfl_sync(0xffffffffu, ak1, i0 + 1);
+      }
       a[i0] = fma(-v0.x, w0, fma(-v1.x, w1, a[i0]));
       if (i0 + 1 < N) a[i0 + 1] = fma(-v0.y, w0, fma(-v1.y, w1, a[i0 + 1]));
     }
@@ -83,7 +103,7 @@ __device__ __forceinline__ void gj_sweep_inverse(double (&a)[N], double* stage, 
     double* st = stage + (((k >> 1)) & 1) * 64;
     if (lane < N) st[lane] = a[k];
     const double p = __shfl_sync(0xffffffffu, a[k], k);
-    const double ip = gj_rcp(p);
+    const double ip = RCP(p);
     const bool me = lane == k;
     if (me) piv = p;
     const double w = (me ? a[k] - 1.0 : a[k]) * ip;
