@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include "../../paper_1305_1489_b200/csrc/kernels_condense2.cuh"
 #include "gj_sweep_v3.cuh"
+#include "gj_pair.cuh"
 using namespace hdgb;
 
 template <int N, int LD, int V, bool ROW = false>
@@ -115,6 +116,74 @@ __global__ void rcp_err(double* out, int n) {
   if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)out, (unsigned long long)__double_as_longlong(mx));
 }
 
+
+// two 20 x 20 inverses per warp (gj_pair.cuh): cycles per PAIR
+template <int LD>
+__global__ void __launch_bounds__(512) gj_pair_smem(double* out, long long* cyc, int reps, int active) {
+  __shared__ __align__(16) double stage[6 * 384];
+  __shared__ double Sm[8][24 * LD];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int N = 20;
+  if (warp < active) {
+    double* S = Sm[(2 * warp + (lane >> 4)) & 7];
+    const int c = lane & 15;
+    for (int i = c; i < 24 * LD; i += 16) S[i] = 0.0;
+    __syncwarp();
+    for (int col = c; col < N; col += 16)
+      for (int i = 0; i < N; ++i) S[i + col * LD] = (i == col ? 4.0 * N : 0.0) + 1.0 / (1.0 + i + col);
+    __syncwarp();
+    double pmin = 1e300, pmax = 0;
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      double a[20], cc[10], zi[10];
+#pragma unroll
+      for (int i = 0; i < 20; ++i) a[i] = S[i + c * LD];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int jj = 0; jj <= j; ++jj) cc[j * (j + 1) / 2 + jj] = S[16 + j + (16 + jj) * LD];
+      __syncwarp();
+      gj_pair_inverse20(a, cc, zi, stage + warp * 384, lane, pmin, pmax);
+#pragma unroll
+      for (int i = 0; i < 20; ++i) S[i + c * LD] = a[i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) S[c + (16 + j) * LD] = a[16 + j];
+      if (c < 4) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) S[16 + j + (16 + c) * LD] = zi[j >= c ? j * (j + 1) / 2 + c : c * (c + 1) / 2 + j];
+      }
+      __syncwarp();
+    }
+    long long t1 = clock64();
+    if (lane == 0) cyc[blockIdx.x * 16 + warp] = (t1 - t0) / reps;
+    if (blockIdx.x == 0 && warp == 0) {
+      for (int i = lane; i < N * N; i += 32) out[i] = Sm[0][(i % N) + (i / N) * LD];
+      if (lane == 0) { out[N * N] = pmin; out[N * N + 1] = pmax; }
+    }
+  }
+  __syncthreads();
+}
+
+void run_pair() {
+  double* out; long long* cyc;
+  cudaMalloc(&out, 4096 * 8); cudaMalloc(&cyc, 148 * 16 * 8);
+  long long h[148 * 16];
+  double *o1; cudaMalloc(&o1, 4096 * 8);
+  gj_smem<20, 20, 2><<<1, 512>>>(o1, cyc, 1, 1);
+  gj_pair_smem<20><<<1, 512>>>(out, cyc, 1, 1);
+  double h1[402], h2[402];
+  cudaMemcpy(h1, o1, sizeof(h1), cudaMemcpyDeviceToHost);
+  cudaMemcpy(h2, out, sizeof(h2), cudaMemcpyDeviceToHost);
+  double md = 0, mx = 0;
+  for (int i = 0; i < 400; ++i) { md = fmax(md, fabs(h1[i] - h2[i])); mx = fmax(mx, fabs(h1[i])); }
+  printf("pair vs v2 max|diff|/max|inv| = %.3e  pmin %.6e/%.6e pmax %.6e/%.6e\n", md / mx, h1[400], h2[400], h1[401], h2[401]);
+  for (int act : {1, 2, 4, 5, 6}) {
+    gj_pair_smem<20><<<148, 512>>>(out, cyc, 32, act);
+    cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("pair N=20 %d active warps (%d inverses): %lld cycles per pair\n", act, 2 * act, h[0]);
+  }
+}
+
 template <int N, int VA, int VB>
 void check2() {
   double *o1, *o2; long long* cyc;
@@ -154,7 +223,8 @@ int main() {
     printf("rcp.approx.f64 max |1 - x r| = %.3e (2^%.1f)\n", h, log2(h));
   }
   check2<20, 2, 5>(); check2<20, 2, 7>();
-  run<20, 2>("v2"); run<20, 3>("v3"); run<20, 5>("lds64"); run<20, 6>("noload"); run<20, 7>("shfl");
+  run_pair();
+  run<20, 2>("v2");
 
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
