@@ -399,6 +399,31 @@ def test_jit_and_interpreter_agree():
     assert max_slice_relerr(np_(cs_jit.Cf_cols()), np_(cs_vm.Cf_cols())) < 1e-10
 
 
+# Field programs exercising the JIT emitter's rewrites (jit_quad.cpp
+# FieldEmitter): sin/cos of exact multiples of pi as sinpi/cospi (m = 3, 1/2,
+# -2, 2, 1), a non-multiple (pi*pi stays sin), folded literal products,
+# subexpressions shared across kappa, c and f (sin(3*pi*x), sin(2*pi*x)), and
+# the remaining operators (pow, sqrt, abs, lt, division, negation).
+EMIT_FIELDS = [
+    ("2 + sin(3*pi*x)*cos(pi/2*y)", "1 + 0.5*sin(pi*pi*z)**2",
+     "cos(-2*pi*(x + y))*sin(3*pi*x) + sqrt(abs(x - y) + 1)"),
+    ("1.5 + 0.25*lt(z, 0.5) + 0.5*sin(2*pi*x)", "exp(-x*y)",
+     "(2 + sin(2*pi*x))/(1 + z*z) - cos(pi*z)**3"),
+]
+
+
+@pytest.mark.parametrize("kap,c,f", EMIT_FIELDS)
+def test_jit_field_emitter_vs_oracle(kap, c, f):
+    k = 2
+    mesh = HostMesh.box(2, bc="dirichlet_x", perturb=0.1, seed=3)
+    em = oracle_mesh(mesh)
+    eng, dm, g, cs = gpu_pipeline(mesh, k, kap, c, f)
+    assert eng.jit_status == "", eng.jit_status
+    _, _, _, C, Cf = oracle_condense(em, k, kap, c, f, 1.0)
+    assert max_slice_relerr(np_(cs.C_slices()), C) < TOL
+    assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
+
+
 def test_two_slab_scatter_exchange_matches_global():
     """z-slab scatter on the GPU (K4 into slab-local CSR) + interface exchange
     == the single-mesh GPU assembly, bit for bit."""
