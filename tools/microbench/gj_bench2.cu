@@ -184,6 +184,37 @@ void run_pair() {
   }
 }
 
+// P3 mix: warps 0..npair-1 invert pairs (gj_pair.cuh), warps npair..npair+nsingle-1 single matrices (v2)
+__global__ void __launch_bounds__(512) gj_mix(long long* cyc, int reps, int npair, int nsingle) {
+  __shared__ __align__(16) double stage[6 * 384];
+  __shared__ __align__(16) double st1[10 * 128];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane & 15;
+  long long t0 = clock64();
+  if (warp < npair) {
+    double a[20], cc[10], zi[10], pmin = 1e300, pmax = 0;
+    for (int i = 0; i < 20; ++i) a[i] = (i == c ? 80.0 : 0.0) + 1.0 / (1.0 + i + c);
+    for (int j = 0; j < 10; ++j) cc[j] = (j == 0 || j == 2 || j == 5 || j == 9) ? 80.0 : 0.01;
+    for (int r = 0; r < reps; ++r) gj_pair_inverse20(a, cc, zi, stage + warp * 384, lane, pmin, pmax);
+    if (a[3] == 12345.0 && zi[2] == 1.0) cyc[1000] = 1;
+  } else if (warp < npair + nsingle) {
+    double a[20], pmin = 1e300, pmax = 0;
+    for (int i = 0; i < 20; ++i) a[i] = lane < 20 ? (i == lane ? 80.0 : 0.0) + 1.0 / (1.0 + i + lane) : 0.0;
+    for (int r = 0; r < reps; ++r) gj_sweep_inverse<20>(a, st1 + (warp - npair) * 128, lane, pmin, pmax);
+    if (a[3] == 12345.0) cyc[1000] = 1;
+  }
+  long long t1 = clock64();
+  if (lane == 0 && blockIdx.x == 0) cyc[warp] = (t1 - t0) / reps;
+}
+
+void run_mix(int np, int ns) {
+  long long* cyc; cudaMalloc(&cyc, 2048 * 8); cudaMemset(cyc, 0, 2048 * 8);
+  gj_mix<<<148, 512>>>(cyc, 32, np, ns);
+  long long h[16]; cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  long long mx = 0; for (int i = 0; i < np + ns; ++i) mx = h[i] > mx ? h[i] : mx;
+  printf("mix %d pair warps + %d single warps (%d inverses): max %lld cycles per round\n", np, ns, 2 * np + ns, mx);
+}
+
 template <int N, int VA, int VB>
 void check2() {
   double *o1, *o2; long long* cyc;
@@ -224,6 +255,7 @@ int main() {
   }
   check2<20, 2, 5>(); check2<20, 2, 7>();
   run_pair();
+  run_mix(0, 10); run_mix(5, 0); run_mix(4, 2); run_mix(4, 0); run_mix(0, 8); run_mix(3, 4);
   run<20, 2>("v2");
 
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
