@@ -103,7 +103,13 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #define HDG_C3_FPT 4
 #endif
   constexpr int FPT = HDG_C3_FPT;            // faces per V task (1, 2 or 4)
-  constexpr int NGJ = 2 * EPB;               // GJ tasks in P3
+#ifndef HDG_C3_PAIR
+#define HDG_C3_PAIR 1
+#endif
+  // d3 <= 16 (k = 2): one warp sweeps two matrices, S of element e and M of
+  // the next batch's element e, one per 16-lane half (gj_sweep_seg)
+  constexpr bool PAIR = HDG_C3_PAIR && D3 % 2 == 0 && D3 <= 16;
+  constexpr int NGJ = PAIR ? EPB : 2 * EPB;  // GJ tasks in P3
   constexpr bool GJ_SEP = NWT > NGJ;         // GJ warps do nothing else in P3
 #ifndef HDG_C3_NO_BULK
   // record layout == shared layout (k = 3), packed factors a 16-byte multiple
@@ -406,6 +412,38 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       if (gj_warp || !GJ_SEP) {
         for (int task = warp; task < NGJ; task += (GJ_SEP ? NGJ : NWT)) {
           const int e = task % EPB;
+          if constexpr (PAIR) {
+            const int h = lane >> 4, c = lane & 15;
+            const bool live = h == 0 ? e < nb : (has_next && Kn0 + e < nelt);
+            const long K = h == 0 ? K0 + e : Kn0 + e;
+            double* dst = h == 0 ? Sb(e) : Mi(e);  // S stored full (P2); packed M copied into Mi(e) in P2
+            double a[D3];
+#pragma unroll
+            for (int i = 0; i < D3; ++i) {
+              double v = i == c ? 1.0 : 0.0;  // dead half / padding lanes: identity
+              if (live && c < D3) {
+                const int r = i > c ? i : c, cc = i > c ? c : i;
+                v = h == 0 ? dst[c + i * LD] : dst[sym_idx(r, cc, D3)];
+              }
+              a[i] = v;
+            }
+            __syncwarp();
+            double pmin = 1e300, pmax = 0.0;
+            gj_sweep_seg<D3, 16, D3>(a, h == 0 ? stS(e) : stM(e), c, pmin, pmax);
+            const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
+            if (live && c < D3) {
+#pragma unroll
+              for (int i = 0; i < D3; ++i) dst[c + i * LD] = a[i];
+              if (factors) {
+                double* fd = factors + K * Dm::FACTORS + (h == 0 ? Dm::NSYM : 0) + c * (2 * D3 - c + 1) / 2 - c;
+#pragma unroll
+                for (int i = 0; i < D3; ++i)
+                  if (i >= c) fd[i] = a[i];
+              }
+            }
+            if (live && bad && c == 0) flag_bad(bad_element, K);
+            continue;
+          }
           if (task < EPB) {
             if (e >= nb) continue;
             const long K = K0 + e;

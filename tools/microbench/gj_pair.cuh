@@ -7,79 +7,6 @@
 
 #include "../../paper_1305_1489_b200/csrc/gj_sweep.cuh"
 
-// Sweep inverse of the leading N x N block held by a W-lane segment of the
-// warp (lane c < N of the segment owns column c in a[0..N-1]; rows N..R-1 of
-// a[] are left untouched). Same algebra as gj_sweep_inverse; shuffles stay
-// inside the segment; `stage` is the segment's own 2 x 64 doubles. pmin/pmax
-// reduce the Cholesky pivots over the segment (a non-positive pivot as -1).
-template <int N, int W, int R>
-__device__ __forceinline__ void gj_sweep_seg(double (&a)[R], double* stage, int c, double& pmin, double& pmax) {
-  static_assert(N % 2 == 0 && N <= W && N <= R, "even N on one segment");
-  constexpr unsigned FULL = 0xffffffffu;
-  double piv = 1.0;
-#pragma unroll
-  for (int k = 0; k + 1 < N; k += 2) {
-    double* st = stage + ((k >> 1) & 1) * 64;
-    if (c < N) {
-      st[c] = a[k];
-      st[32 + c] = a[k + 1];
-    }
-    const double p00 = __shfl_sync(FULL, a[k], k, W);
-    const double p01 = __shfl_sync(FULL, a[k + 1], k, W);
-    const double p11 = __shfl_sync(FULL, a[k + 1], k + 1, W);
-    double n0x = 0.0, n0y = 0.0, n1x = 0.0, n1y = 0.0;
-    if (k + 2 < N) {
-      n0x = __shfl_sync(FULL, a[k], k + 2, W);
-      n1x = __shfl_sync(FULL, a[k + 1], k + 2, W);
-      n0y = __shfl_sync(FULL, a[k], k + 3, W);
-      n1y = __shfl_sync(FULL, a[k + 1], k + 3, W);
-    }
-    const double det = fma(p00, p11, -p01 * p01);
-    const bool m0 = c == k, m1 = c == k + 1;
-    const double ak0 = m0 ? a[k] - 1.0 : a[k];
-    const double ak1 = m1 ? a[k + 1] - 1.0 : a[k + 1];
-    const double u0 = fma(p11, ak0, -p01 * ak1);
-    const double u1 = fma(p00, ak1, -p01 * ak0);
-    double s0 = 0.0, s1 = 0.0;
-    if (k + 2 < N) {
-      s0 = fma(n0x, u0, n1x * u1);
-      s1 = fma(n0y, u0, n1y * u1);
-    }
-    const double id = gj_rcp(det);
-    if (k + 2 < N) {
-      a[k + 2] = fma(-s0, id, a[k + 2]);
-      a[k + 3] = fma(-s1, id, a[k + 3]);
-    }
-    const double w0 = u0 * id, w1 = u1 * id;
-    if (m0) piv = p00;
-    if (m1) piv = p00 * id;
-    __syncwarp();
-#pragma unroll
-    for (int i0 = 0; i0 < N; i0 += 2) {
-      if (i0 == k || i0 == k + 2) continue;
-      const double2 v0 = *reinterpret_cast<const double2*>(st + i0);
-      const double2 v1 = *reinterpret_cast<const double2*>(st + 32 + i0);
-      a[i0] = fma(-v0.x, w0, fma(-v1.x, w1, a[i0]));
-      a[i0 + 1] = fma(-v0.y, w0, fma(-v1.y, w1, a[i0 + 1]));
-    }
-    a[k] = m0 ? w0 - 1.0 : w0;
-    a[k + 1] = m1 ? w1 - 1.0 : w1;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < N; ++i) a[i] = -a[i];
-  double d = (c & 1) && c < N ? 1.0 / piv : piv;
-  if (!(d > 0.0)) d = -1.0;
-  double mn = c < N ? d : 1e300, mx = c < N ? d : 0.0;
-#pragma unroll
-  for (int o = W / 2; o > 0; o >>= 1) {
-    mn = fmin(mn, __shfl_xor_sync(FULL, mn, o));
-    mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
-  }
-  pmin = fmin(pmin, mn);
-  pmax = fmax(pmax, mx);
-}
-
 // Inverse of one 20 x 20 SPD matrix per 16-lane half. On entry lane c of the
 // half holds column c (rows 0..19) of its matrix in a[] and every lane the
 // trailing 4 x 4 block C packed lower in cc[] ((j, j'), j >= j', at
