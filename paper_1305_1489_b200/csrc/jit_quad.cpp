@@ -21,6 +21,9 @@
 #include "../../include/hdg_b200.h"
 #include "jit_quad.hpp"
 
+#ifndef HDG_QUAD_MINB32
+#define HDG_QUAD_MINB32 "2"  // EB = 32: two CTAs per SM must fit the registers
+#endif
 #ifndef HDG_QUAD_UNROLL
 #define HDG_QUAD_UNROLL 8  // k-steps of the node GEMM unrolled (A fragments in flight)
 #endif
@@ -31,15 +34,16 @@ namespace {
 
 const char* kQuadSource = R"CUDA(
 // JIT: K2 node build with inlined coefficient fields (see kernels_local.cuh quad_build_kernel).
-// EB (elements per CTA, a multiple of 8) and QUAD_THREADS (the block size) are
-// defined by the host before this text
+// EB (elements per CTA, a multiple of 8), QUAD_THREADS (the block size) and
+// QUAD_MINB (CTAs per SM the registers must allow) are defined by the host
+// before this text
 #define LDB (EB + 4)
 #define NTI (EB / 8)
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
-extern "C" __global__ void __launch_bounds__(QUAD_THREADS)
+extern "C" __global__ void __launch_bounds__(QUAD_THREADS, QUAD_MINB)
 quad_build_jit(int nelt, int nq, int nqp, int nsym, int nsymp, int d3, int d3p,
                const double* __restrict__ bary, const double* __restrict__ wq,
                const double* __restrict__ Asym, const double* __restrict__ Af,
@@ -339,7 +343,8 @@ CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_f
   FieldEmitter fe;
   const std::string ek = fe.emit(kap, "sk"), ec = fe.emit(c, "sc"), ef = fe.emit(f, "sf");
   const std::string src = "#define EB " + std::to_string(eb) + "\n#define QUAD_THREADS " +
-                          std::to_string(jit_quad_threads(eb)) + "\n#define QUAD_UNROLL " +
+                          std::to_string(jit_quad_threads(eb)) + "\n#define QUAD_MINB " + (eb == 32 ? HDG_QUAD_MINB32 : "1") +
+                          "\n#define QUAD_UNROLL " +
                           std::to_string(HDG_QUAD_UNROLL) + "\n#define FIELD_STMTS " + fe.stmts() +
                           "\n#define FIELD_KAPPA " + ek + "\n#define FIELD_C " + ec + "\n#define FIELD_F " + ef +
                           "\n" + kQuadSource;

@@ -23,11 +23,14 @@ class FieldEmitter {
   int ntemp_ = 0;
 };
 #ifndef HDG_QUAD_THREADS16
-#define HDG_QUAD_THREADS16 512
+#define HDG_QUAD_THREADS16 1024
 #endif
-// Block size of the JIT node build: EB = 32 runs two 256-thread CTAs per SM;
-// EB = 16 (k >= 4, one CTA per SM by shared memory) gets 16 warps for the GEMM.
-inline int jit_quad_threads(int eb) { return eb == 16 ? HDG_QUAD_THREADS16 : 256; }
+// Block size of the JIT node build (measured): EB = 32 runs two 384-thread CTAs per SM;
+// EB = 16 (k >= 4, one CTA per SM by shared memory) one 1024-thread CTA.
+#ifndef HDG_QUAD_THREADS32
+#define HDG_QUAD_THREADS32 384
+#endif
+inline int jit_quad_threads(int eb) { return eb == 16 ? HDG_QUAD_THREADS16 : HDG_QUAD_THREADS32; }
 // Compiled (cached) kernel for these fields and EB elements per CTA, or nullptr with *err set.
 CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, std::string* err);
 // Kernel sampling a PROGRAM field at every element node (SAMPLED layout), or nullptr.
