@@ -950,7 +950,7 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     CUfunction jfn = nullptr;
     if (c->jit && any_prog) {
       std::string err;
-      jfn = jit_quad_kernel(kappa, cf, f, eb, &err);
+      jfn = jit_quad_kernel(kappa, cf, f, eb, t.nqp, &err);
       if (!jfn) c->jit_error = err;
     }
     stage_begin(c, 1);
@@ -962,7 +962,7 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
       void* args[] = {&nel, &nq, &nqp, &nsym, &nsymp, &d3, &d3p, &bary, &w, &As, &Af, &vol, &T, &V,
                       &sk, &sc, &sf, &Ms, &Ds, &fv};
       std::string err;
-      launched = launch_quad_jit(jfn, c->stream, qgrid, jit_quad_threads(eb), qsmem, args, &err);
+      launched = launch_quad_jit(jfn, c->stream, qgrid, jit_quad_threads(eb, t.nqp), qsmem, args, &err);
       if (!launched) c->jit_error = err;
     }
     if (!launched) {

@@ -339,11 +339,12 @@ sample_field_jit(int nelt, int nq, const double* __restrict__ bary, const double
 )CUDA";
 }  // namespace
 
-CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, std::string* err) {
+CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, int nqp,
+                           std::string* err) {
   FieldEmitter fe;
   const std::string ek = fe.emit(kap, "sk"), ec = fe.emit(c, "sc"), ef = fe.emit(f, "sf");
   const std::string src = "#define EB " + std::to_string(eb) + "\n#define QUAD_THREADS " +
-                          std::to_string(jit_quad_threads(eb)) + "\n#define QUAD_MINB " + (eb == 32 ? HDG_QUAD_MINB32 : "1") +
+                          std::to_string(jit_quad_threads(eb, nqp)) + "\n#define QUAD_MINB " + (jit_quad_threads(eb, nqp) == 384 ? HDG_QUAD_MINB32 : "1") +
                           "\n#define QUAD_UNROLL " +
                           std::to_string(HDG_QUAD_UNROLL) + "\n#define FIELD_STMTS " + fe.stmts() +
                           "\n#define FIELD_KAPPA " + ek + "\n#define FIELD_C " + ec + "\n#define FIELD_F " + ef +
