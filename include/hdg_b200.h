@@ -327,15 +327,31 @@ int hdg_b200_stage_times(hdg_ctx* ctx, double ms[HDG_NSTAGES]);
  * set); disable to force the in-kernel field interpreter. jit_status returns
  * the last JIT failure ("" if none; on failure the interpreter runs).      */
 int hdg_b200_set_jit(hdg_ctx* ctx, int enabled);
-/* k = 2, 3 condensation kernel: 3 = CTA-batched phases (default), 4 = element-batched
- * tasks, 2 = per-element warp teams. k = 4, 5: 1 = triangular-factor kernel, any other
- * value = v5 (one element per CTA, explicit inverses; default). All are equivalent
- * (kept for comparison); the recovery-cache layout follows the variant in use at
- * build_condense time, so recover with the same context setting.            */
-int hdg_b200_set_variant(hdg_ctx* ctx, int variant);
 /* k = 1..3 recovery kernel: 3 = TMA-streamed cache records (default), 2 = one warp
  * per element with direct loads (equivalent; kept for comparison). */
 int hdg_b200_set_recover_variant(hdg_ctx* ctx, int variant);
+/* Singular elements. The condensation eliminates A1 by blocks (sweep
+ * inverses of M and of its Schur complement S, no pivoting) and records their
+ * extreme |pivots|. An element whose combined pivot ratio falls below
+ * `screen` (default 1e-12), or whose pivots vanished or overflowed, is
+ * re-solved by the reference's own path on the GPU: partial-pivot LU of A1
+ * with the 1e-14 test of factor_checked (local_solver.cpp:50-57), C, Cf from
+ * the LU solve (local_solver.cpp:71-100), recovery cache from partial-pivot
+ * inverses. So indefinite (c < 0) and ill-conditioned elements get the
+ * reference's verdict (HDG_ESINGULAR + lowest element) and values. screen >= 1
+ * sends every element through that path (testing). rescued_elements returns
+ * how many elements the last build_condense re-solved (synchronises).     */
+int hdg_b200_set_rescue_screen(hdg_ctx* ctx, double screen);
+int hdg_b200_rescued_elements(hdg_ctx* ctx, int64_t* count);
+/* StabilizationField::allow_zero (element_matrices.hpp:24): build_condense
+ * validates tau like StabilizationField::validate (element_matrices.cpp:38-46,
+ * called at :287) before any factorisation: a negative tau(K,l) returns
+ * HDG_EINVAL, and so does tau vanishing on all four faces of an element
+ * unless allow_zero is set (the reference's study sets it for BDM,
+ * study.cpp:18). Validation and the singular test are reported when
+ * build_condense gets a non-NULL bad_element, otherwise by the next
+ * hdg_b200_synchronize.                                                   */
+int hdg_b200_set_tau_allow_zero(hdg_ctx* ctx, int enabled);
 /* BDM variant (bdm_blocks, local_solver.cpp:65-69): the scalar space of the
  * local solve is truncated to its first d3 - d2 modes (P_{k-1}) and tau is
  * ignored (tauPP, tauDP and tauDD dropped); build_condense then returns the

@@ -23,12 +23,22 @@ def build(quiet: bool = True) -> None:
         raise RuntimeError("oracle build failed:\n" + (out.stdout or "") + (out.stderr or ""))
 
 
+if os.environ.get("HDG_ORACLE_NATIVE") == "1":
+    # CPU baseline: the same sources compiled -O3 -march=native for this host
+    # (make native -> oracle/_native/); falls back to the portable build.
+    _nat = os.path.join(_here, "_native")
+    _out = subprocess.run(["make", "-C", _here, "native", f"PY={sys.executable}"], capture_output=True, text=True)
+    NATIVE = _out.returncode == 0
+    if NATIVE and _nat not in sys.path:
+        sys.path.insert(0, _nat)
+else:
+    NATIVE = False
 if _here not in sys.path:
-    sys.path.insert(0, _here)
+    sys.path.insert(len(sys.path) if NATIVE else 0, _here)
 try:
     import _hdg_oracle as core  # noqa: E402
 except ImportError:  # built lazily in a fresh checkout
     build()
     import _hdg_oracle as core  # noqa: E402
 
-__all__ = ["core", "build"]
+__all__ = ["core", "build", "NATIVE"]

@@ -7,7 +7,10 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include <atomic>
 #include <chrono>
+#include <cmath>
+#include <thread>
 #include <cstring>
 #include <random>
 #include <tuple>
@@ -426,6 +429,89 @@ PYBIND11_MODULE(_hdg_oracle, m) {
           for (double v : chk) sum += v;
           return std::vector<double>{std::chrono::duration<double>(t1 - t0).count(), sum};
         });
+  // Config C2's coefficient callbacks as compiled C++ lambdas (what a user of
+  // the reference writes as ScalarField, coefficient.hpp:13-14), so the CPU
+  // baseline does not pay the field-program interpreter. Same expressions as
+  // paper_1305_1489_b200/configs.py (_C2_KAPPA, c = 1 + xyz, _C2 f).
+  m.def("c2_native_fields", []() {
+    const double pi = 3.141592653589793;
+    auto kap = [pi](double x, double y, double) { return 1 + 0.5 * std::sin(2 * pi * x) * std::cos(2 * pi * y); };
+    auto c = [](double x, double y, double z) { return 1 + x * y * z; };
+    auto f = [pi, kap](double x, double y, double z) {
+      return std::exp(x + y) * std::sin(pi * z) *
+             (-pi * std::cos(2 * pi * (x + y)) - kap(x, y, z) * (2 - pi * pi) + 1 + x * y * z);
+    };
+    return py::make_tuple(Field{kap}, Field{c}, Field{f});
+  });
+
+  // Whole-mesh CPU baseline in element chunks (<= 16,384
+  // elements per chunk, because the materialised reference path needs
+  // ~190 KB per element at k = 3): nthreads workers pull chunks of `chunk`
+  // contiguous elements and run build_element_matrices -> local_blocks ->
+  // condense -> local_recover on each (the reference's per-element math and
+  // summation order; every stage on all cores, the "all-cores" mode).
+  // Per-thread mesh views (global coordinates and face areas, per-chunk
+  // element rows) are set up outside the timed region; the per-chunk row
+  // copies are inside it. Returns {seconds, checksum}.
+  m.def("time_pipeline_chunked",
+        [](const ExpandedMesh& em, const Tables& t, const Field& kappa, const Field& c,
+           const Field& f, const StabilizationField& tau, const DArr& uhat, int nthreads, int chunk) {
+          const Mat U = mat_from(uhat);
+          py::gil_scoped_release r;
+          const int nelt = em.n_elements();
+          const int nchunks = (nelt + chunk - 1) / chunk;
+          nthreads = std::max(1, std::min(nthreads, nchunks));
+          std::vector<ExpandedMesh> sub(nthreads);
+          std::vector<StabilizationField> stau(nthreads, tau);
+          for (auto& s : sub) {  // setup: global arrays the element code indexes
+            s.raw.coordinates = em.raw.coordinates;
+            s.faces = em.faces;
+            s.area = em.area;
+            s.facetype = em.facetype;
+          }
+          auto rows = [](const auto& src, int k0, int k1, auto& dst) {
+            dst.r = k1 - k0;
+            dst.c = src.c;
+            dst.a.resize(size_t(dst.r) * dst.c);
+            for (int j = 0; j < src.c; ++j)
+              std::memcpy(&dst.a[size_t(j) * dst.r], &src.a[size_t(k0) + size_t(j) * src.r],
+                          sizeof(src.a[0]) * size_t(dst.r));
+          };
+          std::atomic<int> next{0};
+          std::vector<double> chk(nthreads, 0.0);
+          using clk = std::chrono::steady_clock;
+          auto t0 = clk::now();
+          std::vector<std::thread> pool;
+          for (int w = 0; w < nthreads; ++w)
+            pool.emplace_back([&, w] {
+              ExpandedMesh& s = sub[w];
+              StabilizationField& st = stau[w];
+              Mat su;
+              for (int ci = next++; ci < nchunks; ci = next++) {
+                const int k0 = ci * chunk, k1 = std::min(nelt, k0 + chunk);
+                rows(em.raw.elements, k0, k1, s.raw.elements);
+                rows(em.facebyele, k0, k1, s.facebyele);
+                rows(em.perm, k0, k1, s.perm);
+                rows(em.normals, k0, k1, s.normals);
+                s.volume.assign(em.volume.begin() + k0, em.volume.begin() + k1);
+                rows(tau.tau, k0, k1, st.tau);
+                su = Mat(U.r, k1 - k0);
+                std::memcpy(su.a.data(), U.col(k0), sizeof(double) * size_t(U.r) * (k1 - k0));
+                ElementMatrixSet ms = build_element_matrices(s, t.tb, t.tet, t.tri, kappa.f, c.f, f.f, st);
+                LocalBlocks lb = local_blocks(ms);
+                CondensedSystem cs = condense(lb, 1);
+                LocalSolution ls = local_recover(lb, su, 1);
+                chk[w] += cs.C.data[0] + ls.u.a[0];
+              }
+            });
+          for (auto& th : pool) th.join();
+          auto t1 = clk::now();
+          double sum = 0.0;
+          for (double v : chk) sum += v;
+          return std::vector<double>{std::chrono::duration<double>(t1 - t0).count(), sum};
+        },
+        py::arg("em"), py::arg("t"), py::arg("kappa"), py::arg("c"), py::arg("f"), py::arg("tau"),
+        py::arg("uhat"), py::arg("nthreads"), py::arg("chunk") = 1024);
   m.def("time_pipeline",
         [](const ExpandedMesh& em, const Tables& t, const Field& kappa, const Field& c,
            const Field& f, const StabilizationField& tau, const DArr& uhat, int nthreads) {

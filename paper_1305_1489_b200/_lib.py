@@ -59,6 +59,11 @@ class GlobalSolverError(HdgError):
     """Reference GlobalSolverError (global_system.hpp:44-46)."""
 
 
+class InvalidArgument(HdgError, ValueError):
+    """HDG_EINVAL: the reference's std::invalid_argument (e.g. StabilizationField::validate,
+    element_matrices.cpp:38-46)."""
+
+
 class hdg_error_report(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("e_q", "e_u", "e_uhat", "eps_u", "eps_uhat", "e_star")]
 
@@ -109,9 +114,11 @@ _SIGS = {
     "hdg_b200_set_timing": (C.c_int, [P, C.c_int]),
     "hdg_b200_stage_times": (C.c_int, [P, DP]),
     "hdg_b200_set_jit": (C.c_int, [P, C.c_int]),
-    "hdg_b200_set_variant": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_recover_variant": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_bdm": (C.c_int, [P, C.c_int]),
+    "hdg_b200_set_tau_allow_zero": (C.c_int, [P, C.c_int]),
+    "hdg_b200_set_rescue_screen": (C.c_int, [P, C.c_double]),
+    "hdg_b200_rescued_elements": (C.c_int, [P, C.POINTER(C.c_int64)]),
     "hdg_b200_expand_device": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, P, C.c_int, P, P, P, P,
                                          C.POINTER(C.c_int)]),
     "hdg_b200_pattern_device": (C.c_int, [P, C.c_int, C.c_int, P, P, P, P, C.POINTER(C.c_int)]),
@@ -160,6 +167,8 @@ def check(status: int, bad_element: int = -1) -> None:
         raise MeshError(status, msg)
     if status == HDG_ESOLVE:
         raise GlobalSolverError(status, msg)
+    if status == HDG_EINVAL:
+        raise InvalidArgument(status, msg)
     raise HdgError(status, msg)
 
 

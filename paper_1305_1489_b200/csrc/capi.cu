@@ -20,12 +20,12 @@
 #include "kernels_condense2.cuh"
 #include "kernels_condense3.cuh"
 #include "kernels_condense5.cuh"
-#include "kernels_condense4.cuh"
 #include "kernels_recover3.cuh"
 #include "kernels_boundary.cuh"
 #include "kernels_solve.cuh"
 #include "kernels_errors.cuh"
 #include "kernels_post2.cuh"
+#include "kernels_rescue.cuh"
 #include "jit_quad.hpp"
 #include "mesh_dev.hpp"
 
@@ -254,12 +254,13 @@ struct hdg_ctx {
   bool timing = false;
   bool jit = true;          // NVRTC-specialised K2 for program fields
   bool bdm = false;         // bdm_blocks variant (hdg_b200_set_bdm)
+  bool tau_allow_zero = false;  // StabilizationField::allow_zero (element_matrices.hpp:24)
+  double rescue_screen = 1e-12; // pivot-ratio screen of the rescue kernel (kernels_rescue.cuh)
+  double* d_rescue = nullptr;   // rescue kernel scratch
+  size_t rescue_len = 0;
   double* d_zero_T = nullptr;  // tau = 0 for the BDM variant
   long zero_T_len = 0;
   int recover_variant = 3;  // k = 1..3: 3 = TMA-streamed cache, 2 = warp per element
-  int condense_variant = 3; // k = 2, 3: 4 = element-batched tasks, 3 = CTA-batched, 2 = per-element teams;
-                            // k = 4, 5: 1 = triangular factors (kernels_local.cuh), else v5
-  bool tri_factors = false;  // recovery-cache layout of the last k >= 4 condensation
   std::string jit_error;    // last JIT failure (kernel then runs interpreted)
   int* d_adj = nullptr;     // boundary face -> 4 K + l (neumann_load)
   double* d_ksamp = nullptr;  // kappa sampled at the postprocess nodes (JIT sampler)
@@ -293,7 +294,10 @@ void* ctx_work(hdg_ctx* c, size_t bytes) {
   return c->work;
 }
 
-size_t work_doubles(const DevTab& t, long nelt) { return size_t(nelt) * (2 * t.nsym + t.d3); }
+// K2 outputs (packed M, packed D, f) then the pivot statistics of K3
+// (nelt x 4, 32-byte aligned) screened by the rescue kernel.
+size_t pivstat_offset(const DevTab& t, long nelt) { return (size_t(nelt) * (2 * t.nsym + t.d3) + 3) / 4 * 4; }
+size_t work_doubles(const DevTab& t, long nelt) { return pivstat_offset(t, nelt) + size_t(nelt) * 4; }
 
 int factor_doubles(int k) {
   const int d3 = hdgb::pdim3(k), m = 4 * hdgb::pdim2(k);
@@ -307,21 +311,11 @@ struct C3Launch {
 };
 
 template <int K_>
-struct C4Launch {
-  static constexpr int EPB = C4Cfg<K_>::EPB, THREADS = C4Cfg<K_>::NWT * 32;
-};
-
-template <int K_>
 struct C5Launch {  // one element per CTA iteration
   static constexpr int EPB = 1, THREADS = C5Cfg<K_>::NWT * 32;
 };
 
-template <int K_>
-struct CondLaunch {
-  static constexpr int EPB = CondCfg<K_>::EPB, THREADS = CondCfg<K_>::NW * 32 * CondCfg<K_>::EPB;
-};
-
-// per-element team kernel (v2): NW warps per element
+// per-element team kernel (k <= 1): NW warps per element
 template <int K_>
 struct C2Launch {
   static constexpr int EPB = C2Cfg<K_>::EPB, THREADS = C2Cfg<K_>::NW * 32 * C2Cfg<K_>::EPB;
@@ -329,7 +323,7 @@ struct C2Launch {
 
 template <class Dm, class Cg, class Kern>
 void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, const double* Ms,
-                          const double* Ds, const double* fv, double* C, double* Cf, double* F) {
+                          const double* Ds, const double* fv, double* C, double* Cf, double* F, double* ps) {
   const size_t smem = (size_t(Cg::EPB) * Dm::PER_ELT + Dm::CTA_EXTRA) * sizeof(double);
   CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int occ = 0;
@@ -339,37 +333,40 @@ void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, co
   const int grid = int(std::min<long>(need, long(c->sms) * occ));
   DevTab td = c->tab[0].dev;
   if (c->bdm) td.nu = td.d3 - td.d2;  // bdm_blocks (local_solver.cpp:65-69): u truncated to P_{k-1}
-  kern<<<grid, Cg::THREADS, smem, c->stream>>>(td, nelt, geo, Ms, Ds, fv, C, Cf, F, c->d_bad);
+  kern<<<grid, Cg::THREADS, smem, c->stream>>>(td, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
   CUDA_OK(cudaGetLastError());
 }
 
-// k <= 3: explicit-inverse kernel (kernels_condense2.cuh); k >= 4: triangular-factor kernel.
+// k <= 1: per-element warp teams (kernels_condense2.cuh); k = 2, 3: CTA-batched
+// phases (kernels_condense3.cuh); k = 4, 5: one element per CTA iteration
+// (kernels_condense5.cuh). All write the recovery cache {M^-1, S^-1, V, f}.
 template <int K_>
 void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, const double* Ds,
-                     const double* fv, double* C, double* Cf, double* F) {
-  if constexpr (K_ == 2 || K_ == 3) {
-    if (c->bdm) {  // the u-space truncation is implemented in the v3 kernel
-      launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-      return;
-    }
-    if (c->condense_variant == 2)
-      launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-    else if (c->condense_variant == 3)
-      launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-    else
-      launch_condense_impl<C2Dims<K_>, C4Launch<K_>>(c, condense4_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-  } else if constexpr (K_ <= 3) {
-    launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-  } else if constexpr (K_ <= 5) {
-    c->tri_factors = c->condense_variant == 1;
-    if (c->tri_factors)  // triangular-factor kernel (kernels_local.cuh)
-      launch_condense_impl<CondDims<K_>, CondLaunch<K_>>(c, condense_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-    else
-      launch_condense_impl<C5Dims<K_>, C5Launch<K_>>(c, condense5_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
-  } else {
-    c->tri_factors = true;
-    launch_condense_impl<CondDims<K_>, CondLaunch<K_>>(c, condense_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F);
+                     const double* fv, double* C, double* Cf, double* F, double* ps) {
+  if constexpr (K_ <= 1)
+    launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
+  else if constexpr (K_ <= 3)
+    launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
+  else
+    launch_condense_impl<C5Dims<K_>, C5Launch<K_>>(c, condense5_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
+}
+
+// K3b: screen the pivot statistics, re-solve the flagged elements by the
+// reference's LU path (kernels_rescue.cuh).
+void launch_rescue(hdg_ctx* c, int nelt, const DevTab& td, const GeoDev& geo, const double* Ms,
+                   const double* Ds, const double* fv, const double* ps, double* C, double* Cf, double* F) {
+  const RescueLayout L(td.d3, td.d2, td.nu);
+  const int grid = int(std::max<long>(1, std::min<long>((long(nelt) + kRescueThreads - 1) / kRescueThreads, c->sms)));
+  const size_t need = size_t(grid) * L.total;
+  if (c->rescue_len < need) {
+    if (c->d_rescue) cudaFree(c->d_rescue);
+    c->d_rescue = nullptr;
+    CUDA_OK(cudaMalloc(&c->d_rescue, need * sizeof(double)));
+    c->rescue_len = need;
   }
+  rescue_kernel<<<grid, kRescueThreads, 0, c->stream>>>(td, nelt, geo, Ms, Ds, fv, ps, c->rescue_screen, C, Cf, F,
+                                                        c->d_rescue, c->d_bad);
+  CUDA_OK(cudaGetLastError());
 }
 
 template <int K_>
@@ -390,7 +387,7 @@ void launch_recover(hdg_ctx* c, int nelt, const GeoDev& geo, const int* fbe, con
     }
   }
   if constexpr (K_ >= 4 && K_ <= 5) {
-    if (!c->tri_factors) {  // v5 cache {M^-1, S^-1, V, f}: one record per CTA iteration
+    {  // v5 cache {M^-1, S^-1, V, f}: one record per CTA iteration
       using Rd = Rec5Dims<K_>;
       const size_t smem = size_t(Rd::TOTAL) * sizeof(double);
       CUDA_OK(cudaFuncSetAttribute(recover5_kernel<K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -403,15 +400,12 @@ void launch_recover(hdg_ctx* c, int nelt, const GeoDev& geo, const int* fbe, con
       return;
     }
   }
-  const int grid = (nelt + kRecWarps - 1) / kRecWarps;
-  // cache layout: {M^-1, S^-1, V, f} (v2..v5) or {L^-1, L_S^-1, Vt, ft} (triangular-factor kernel)
-  if (K_ <= 3 || !c->tri_factors)
+  if constexpr (K_ <= 3) {  // k = 0, or recover variant 2: one warp per element, direct loads
+    const int grid = (nelt + kRecWarps - 1) / kRecWarps;
     recover2_kernel<K_><<<grid, kRecWarps * 32, 0, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat, qx,
                                                                  qy, qz, u);
-  else
-    recover_kernel<K_><<<grid, kRecWarps * 32, 0, c->stream>>>(c->tab[0].dev, nelt, geo, fbe, F, uhat, qx,
-                                                                qy, qz, u);
-  CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaGetLastError());
+  }
 }
 
 #define DISPATCH_K(k, FN, ...)                              \
@@ -425,13 +419,28 @@ void launch_recover(hdg_ctx* c, int nelt, const GeoDev& geo, const int* fbe, con
     default: throw HdgError{HDG_EINVAL, "degree not compiled (k <= 5)"}; \
   }
 
+// Status of the last build_condense (reset_build_status_kernel words), in the
+// reference's order: tau.validate() runs before any factorisation
+// (element_matrices.cpp:287), so its invalid_argument wins over a singular
+// element.
+void raise_build_status(const hdg_ctx* c, int64_t* bad_element) {
+  const long long* h = c->h_bad;
+  if (bad_element) *bad_element = -1;
+  if (h[1] != LLONG_MAX)
+    throw HdgError{HDG_EINVAL, "stabilization must be nonnegative (element " + std::to_string(h[1]) + ")"};
+  if (h[2] != LLONG_MAX && !c->tau_allow_zero)
+    throw HdgError{HDG_EINVAL, "stabilization vanishes identically on element " + std::to_string(h[2])};
+  if (h[0] != LLONG_MAX) {
+    if (bad_element) *bad_element = h[0];
+    throw HdgError{HDG_ESINGULAR, "singular local system on element " + std::to_string(h[0])};
+  }
+}
+
 void check_bad(hdg_ctx* c, int64_t* bad_element) {
   if (!bad_element) return;
-  CUDA_OK(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaMemcpyAsync(c->h_bad, c->d_bad, 3 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OK(cudaStreamSynchronize(c->stream));
-  *bad_element = *c->h_bad == LLONG_MAX ? -1 : *c->h_bad;
-  if (*c->h_bad != LLONG_MAX)
-    throw HdgError{HDG_ESINGULAR, "singular local system on element " + std::to_string(*c->h_bad)};
+  raise_build_status(c, bad_element);
 }
 
 int warps_for(size_t per_warp_bytes) {
@@ -622,19 +631,19 @@ void launch_hdg_project(hdg_ctx* c, int nelt, const GeoDev& geo, const FieldDev*
   const std::vector<double> wi = face_block_inverses(c->tab[0].host);
   DevBuf dw(c->stream, wi.size() * 8);
   CUDA_OK(cudaMemcpyAsync(dw.p, wi.data(), wi.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  set_ll_kernel<<<1, 1, 0, c->stream>>>(c->d_bad, LLONG_MAX);
+  set_ll_kernel<<<1, 1, 0, c->stream>>>(c->d_bad + 3, LLONG_MAX);
   const int per_warp = 4 * tE.nq + 4 * tE.nqd + 4 * tE.d3 + 4 * tE.d2 + 32;
   const size_t smem = size_t(kErrWarps) * per_warp * 8;
   CUDA_OK(cudaFuncSetAttribute(hdg_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int grid = int(std::min<long>((long(nelt) + kErrWarps - 1) / kErrWarps, long(c->sms) * 16));
   hdg_project_kernel<<<grid, kErrWarps * 32, smem, c->stream>>>(tE, c->tab[0].dev, nelt, geo, F[0], F[1], F[2],
-                                                                F[3], dw.as<double>(), qx, qy, qz, u, c->d_bad,
+                                                                F[3], dw.as<double>(), qx, qy, qz, u, c->d_bad + 3,
                                                                 per_warp);
   CUDA_OK(cudaGetLastError());
-  CUDA_OK(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaMemcpyAsync(c->h_bad + 3, c->d_bad + 3, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OK(cudaStreamSynchronize(c->stream));
-  if (*c->h_bad != LLONG_MAX)
-    throw HdgError{HDG_ESINGULAR, "singular projection system on element " + std::to_string(*c->h_bad)};
+  if (c->h_bad[3] != LLONG_MAX)
+    throw HdgError{HDG_ESINGULAR, "singular projection system on element " + std::to_string(c->h_bad[3])};
 }
 }  // namespace
 
@@ -754,8 +763,12 @@ int hdg_b200_create(int device, void* stream, hdg_ctx** out) {
     c->stream = static_cast<cudaStream_t>(stream);
     set_device(c.get());
     CUDA_OK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
-    CUDA_OK(cudaMalloc(&c->d_bad, sizeof(long long)));
-    CUDA_OK(cudaMallocHost(&c->h_bad, sizeof(long long)));
+    // [0..2] build_condense status (reset_build_status_kernel), [3] hdg_project,
+    // [4] elements re-solved by the rescue kernel
+    CUDA_OK(cudaMalloc(&c->d_bad, 8 * sizeof(long long)));
+    CUDA_OK(cudaMallocHost(&c->h_bad, 8 * sizeof(long long)));
+    for (int i = 0; i < 8; ++i) c->h_bad[i] = i == 4 ? 0 : LLONG_MAX;
+    CUDA_OK(cudaMemcpy(c->d_bad, c->h_bad, 8 * sizeof(long long), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMalloc(&c->d_status, 2 * sizeof(int)));
     CUDA_OK(cudaMallocHost(&c->h_status, 2 * sizeof(int)));
     c->h_status[0] = c->h_status[1] = INT_MAX;
@@ -773,6 +786,7 @@ void hdg_b200_destroy(hdg_ctx* c) {
   if (c->d_adj) cudaFree(c->d_adj);
   if (c->d_zero_T) cudaFree(c->d_zero_T);
   if (c->d_ksamp) cudaFree(c->d_ksamp);
+  if (c->d_rescue) cudaFree(c->d_rescue);
   if (c->d_bad) cudaFree(c->d_bad);
   if (c->h_bad) cudaFreeHost(c->h_bad);
   if (c->d_status) cudaFree(c->d_status);
@@ -926,6 +940,9 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     const FieldDev fk = to_dev(kappa, "kappa"), fc = to_dev(cf, "c"), ff = to_dev(f, "f");
     set_device(c);
     const DevTab& t = c->tab[0].dev;
+    reset_build_status_kernel<<<1, 32, 0, c->stream>>>(c->d_bad);
+    tau_check_kernel<<<int(std::min<long>((long(nelt) + 255) / 256, long(c->sms) * 4)), 256, 0, c->stream>>>(
+        nelt, geo.T, c->d_bad);
     GeoDev geo_b = geo;
     if (c->bdm) {  // bdm_blocks ignores tau entirely (local_solver.cpp:36-43): run with T = 0
       require(t.k >= 1, HDG_EINVAL, "the BDM variant needs degree k >= 1");
@@ -947,23 +964,23 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     const size_t qsmem = quad_smem_bytes(eb, t.nqp);
     const int qgrid = (nelt + eb - 1) / eb;
     const bool any_prog = kappa.kind == HDG_FIELD_PROGRAM || cf.kind == HDG_FIELD_PROGRAM || f.kind == HDG_FIELD_PROGRAM;
-    CUfunction jfn = nullptr;
+    JitKernel jk;
     if (c->jit && any_prog) {
       std::string err;
-      jfn = jit_quad_kernel(kappa, cf, f, eb, t.nqp, &err);
-      if (!jfn) c->jit_error = err;
+      jk = jit_quad_kernel(kappa, cf, f, eb, t.nqp, &err);
+      if (!jk.fn) c->jit_error = err;
     }
     stage_begin(c, 1);
     bool launched = false;
-    if (jfn) {
+    if (jk.fn) {
       int nel = nelt, nq = t.nq, nqp = t.nqp, nsym = t.nsym, nsymp = t.nsymp, d3 = t.d3, d3p = t.d3p;
       const double *bary = t.bary, *w = t.w, *As = t.Asym, *Af = t.Af, *vol = geo_b.volume, *T = geo_b.T,
                    *V = geo_b.verts, *sk = kappa.samples, *sc = cf.samples, *sf = f.samples;
       void* args[] = {&nel, &nq, &nqp, &nsym, &nsymp, &d3, &d3p, &bary, &w, &As, &Af, &vol, &T, &V,
                       &sk, &sc, &sf, &Ms, &Ds, &fv};
       std::string err;
-      launched = launch_quad_jit(jfn, c->stream, qgrid, jit_quad_threads(eb, t.nqp), qsmem, args, &err);
-      if (!launched) c->jit_error = err;
+      launched = launch_quad_jit(jk.fn, c->stream, qgrid, jk.threads, qsmem, args, &err);
+      c->jit_error = launched ? std::string() : err;
     }
     if (!launched) {
       if (eb == 32) {
@@ -976,9 +993,14 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     }
     CUDA_OK(cudaGetLastError());
     stage_end(c, 1);
-    set_ll_kernel<<<1, 1, 0, c->stream>>>(c->d_bad, LLONG_MAX);
+    double* ps = work + pivstat_offset(t, nelt);
     stage_begin(c, 2);
-    DISPATCH_K(t.k, launch_condense, c, nelt, geo_b, Ms, Ds, fv, d_C, d_Cf, d_factors);
+    DISPATCH_K(t.k, launch_condense, c, nelt, geo_b, Ms, Ds, fv, d_C, d_Cf, d_factors, ps);
+    {
+      DevTab td = t;
+      if (c->bdm) td.nu = td.d3 - td.d2;
+      launch_rescue(c, nelt, td, geo_b, Ms, Ds, fv, ps, d_C, d_Cf, d_factors);
+    }
     stage_end(c, 2);
     check_bad(c, bad_element);
   });
@@ -1125,6 +1147,7 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
         if (launch_quad_jit(fn, c->stream, grid, 256, 0, args, &err)) {
           fk.kind = HDG_FIELD_SAMPLED;
           fk.samples = c->d_ksamp;
+          c->jit_error.clear();
         } else {
           c->jit_error = err;
         }
@@ -1244,7 +1267,7 @@ int hdg_b200_hdg_project(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
     try {
       launch_hdg_project(c, nelt, geo, F, d_qx, d_qy, d_qz, d_u);
     } catch (const HdgError& e) {
-      if (e.code == HDG_ESINGULAR && bad_element) *bad_element = *c->h_bad;
+      if (e.code == HDG_ESINGULAR && bad_element) *bad_element = c->h_bad[3];
       throw;
     }
   });
@@ -1462,10 +1485,28 @@ int hdg_b200_set_jit(hdg_ctx* c, int enabled) {
 
 const char* hdg_b200_jit_status(const hdg_ctx* c) { return c ? c->jit_error.c_str() : ""; }
 
-int hdg_b200_set_variant(hdg_ctx* c, int variant) {
+int hdg_b200_set_rescue_screen(hdg_ctx* c, double screen) {
   return guarded([&] {
-    require(c != nullptr && variant >= 1 && variant <= 4, HDG_EINVAL, "variant must be 1, 2, 3 or 4");
-    c->condense_variant = variant;
+    require(c != nullptr && screen >= 0.0, HDG_EINVAL, "screen must be >= 0");
+    c->rescue_screen = screen;
+  });
+}
+
+int hdg_b200_rescued_elements(hdg_ctx* c, int64_t* count) {
+  return guarded([&] {
+    require(c && count, HDG_EINVAL, "NULL argument");
+    set_device(c);
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    long long v = 0;
+    CUDA_OK(cudaMemcpy(&v, c->d_bad + 4, sizeof(long long), cudaMemcpyDeviceToHost));
+    *count = v;
+  });
+}
+
+int hdg_b200_set_tau_allow_zero(hdg_ctx* c, int enabled) {
+  return guarded([&] {
+    require(c != nullptr, HDG_EINVAL, "ctx is NULL");
+    c->tau_allow_zero = enabled != 0;
   });
 }
 
@@ -1499,6 +1540,9 @@ int hdg_b200_synchronize(hdg_ctx* c) {
     require(c->h_status[0] == INT_MAX, HDG_EMESH,
             "element " + std::to_string(c->h_status[0]) + " has non-positive orientation");
     require(c->h_status[1] == INT_MAX, HDG_EMESH, "face vertex triples do not match as sets");
+    // deferred status of the last build_condense run without bad_element
+    CUDA_OK(cudaMemcpy(c->h_bad, c->d_bad, 3 * sizeof(long long), cudaMemcpyDeviceToHost));
+    raise_build_status(c, nullptr);
   });
 }
 

@@ -132,4 +132,13 @@ __device__ __forceinline__ void flag_bad(long long* bad, long long K) {
   atomicMin(reinterpret_cast<unsigned long long*>(bad), static_cast<unsigned long long>(K));
 }
 
+// Pivot statistics of an element's two structured inverses (which = 0: M,
+// 1: the Schur complement S): extreme |pivots|, pmin = 0 if a pivot vanished
+// or is not finite. kernels_rescue.cuh screens them and re-runs the
+// reference's LU path (local_solver.cpp:50-57, :71-100) where they are too
+// far apart to vouch for the element.
+__device__ __forceinline__ void store_pivstat(double* ps, long long K, int which, double pmin, double pmax) {
+  reinterpret_cast<double2*>(ps)[2 * K + which] = make_double2(pmin, pmax);
+}
+
 }  // namespace hdgb

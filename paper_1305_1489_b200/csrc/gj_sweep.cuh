@@ -12,10 +12,10 @@ __device__ __forceinline__ double gj_rcp(double x) {
   return fma(r, e, r);
 }
 
-// Inverse of the SPD N x N matrix held by a warp (lane c owns column c in
-// a[]) by the symmetric sweep operator with 2 x 2 pivots (no pivoting; the
-// pivots are the Cholesky pivots and feed the 1e-14 test of
-// local_solver.cpp:50-57 through pmin / pmax). The pivot block columns are
+// Inverse of the symmetric N x N matrix held by a warp (lane c owns column c
+// in a[]) by the symmetric sweep operator with 2 x 2 pivots (no pivoting;
+// pmin / pmax return the extreme |LDL^T pivots|, 0 for a vanished or
+// non-finite one, for the rescue screen of kernels_rescue.cuh). The pivot block columns are
 // exchanged through `stage` (2 x 64 doubles, 16-byte aligned). The pivot
 // lanes take their diagonal entry minus one into w = P^-1 a_K, which yields
 // their special update weights (rows of I - P^-1) without selects, and each
@@ -95,16 +95,16 @@ __device__ __forceinline__ void gj_sweep_inverse(double (&a)[N], double* stage, 
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < N; ++i) a[i] = -a[i];
-  // pivots: even lanes hold p00, odd lanes 1/d1 (the trailing scalar pivot as is)
-  double d = (lane & 1) && lane < N - (N % 2) ? 1.0 / piv : piv;
-  const bool bad = lane < N && !(d > 0.0);
+  // pivots: even lanes hold p00, odd lanes 1/d1 (the trailing scalar pivot as
+  // is); reduced as |d|, a vanished or non-finite pivot as 0
+  double d = fabs((lane & 1) && lane < N - (N % 2) ? 1.0 / piv : piv);
+  if (!(d <= 1.79e308)) d = 0.0;
   double mn = lane < N ? d : 1e300, mx = lane < N ? d : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
-  if (__any_sync(0xffffffffu, bad)) mn = -1.0;
   pmin = fmin(pmin, mn);
   pmax = fmax(pmax, mx);
 }
@@ -113,7 +113,7 @@ __device__ __forceinline__ void gj_sweep_inverse(double (&a)[N], double* stage, 
 // warp (lane c < N of the segment owns column c in a[0..N-1]; rows N..R-1 of
 // a[] are left untouched). Same algebra as gj_sweep_inverse; shuffles stay
 // inside the segment; `stage` is the segment's own 2 x 64 doubles. pmin/pmax
-// reduce the Cholesky pivots over the segment (a non-positive pivot as -1).
+// reduce the |pivots| over the segment (a vanished or non-finite one as 0).
 template <int N, int W, int R>
 __device__ __forceinline__ void gj_sweep_seg(double (&a)[R], double* stage, int c, double& pmin, double& pmax) {
   static_assert(N % 2 == 0 && N <= W && N <= R, "even N on one segment");
@@ -170,8 +170,8 @@ __device__ __forceinline__ void gj_sweep_seg(double (&a)[R], double* stage, int 
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < N; ++i) a[i] = -a[i];
-  double d = (c & 1) && c < N ? 1.0 / piv : piv;
-  if (!(d > 0.0)) d = -1.0;
+  double d = fabs((c & 1) && c < N ? 1.0 / piv : piv);
+  if (!(d <= 1.79e308)) d = 0.0;  // vanished / non-finite pivot
   double mn = c < N ? d : 1e300, mx = c < N ? d : 0.0;
 #pragma unroll
   for (int o = W / 2; o > 0; o >>= 1) {

@@ -155,6 +155,7 @@ struct Drv {
   CUresult (*setAttr)(CUfunction, CUfunction_attribute, int) = nullptr;
   CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
                      void**, void**) = nullptr;
+  CUresult (*ctxGetCurrent)(CUcontext*) = nullptr;
   bool ok = false;
 };
 Drv& drv() {
@@ -168,14 +169,19 @@ Drv& drv() {
     r.ok = get("cuModuleLoadData", reinterpret_cast<void**>(&r.loadData)) &&
            get("cuModuleGetFunction", reinterpret_cast<void**>(&r.getFunction)) &&
            get("cuFuncSetAttribute", reinterpret_cast<void**>(&r.setAttr)) &&
-           get("cuLaunchKernel", reinterpret_cast<void**>(&r.launch));
+           get("cuLaunchKernel", reinterpret_cast<void**>(&r.launch)) &&
+           get("cuCtxGetCurrent", reinterpret_cast<void**>(&r.ctxGetCurrent));
     return r;
   }();
   return d;
 }
 
+// Compiled cubins are cached per source text; loaded modules per (context,
+// source): a CUfunction belongs to the context that was current when its
+// module was loaded, so engines on different devices each load their own.
 struct Cache {
   std::mutex mu;
+  std::unordered_map<std::string, std::vector<char>> cubin;
   std::unordered_map<std::string, CUfunction> fn;
   std::vector<CUmodule> mods;
   std::string last_error;
@@ -275,46 +281,59 @@ std::string FieldEmitter::emit(const hdg_field& f, const char* sample_ptr) {
 }
 
 namespace {
-// NVRTC-compile `src` for sm_100a and return its kernel `name` (cached by source text).
+// NVRTC-compile `src` for sm_100a (once per source text) and return its kernel
+// `name` loaded in the current context (once per context).
 CUfunction compile_cached(const std::string& src, const char* name, std::string* err) {
   Cache& C = cache();
   std::lock_guard<std::mutex> lock(C.mu);
-  auto it = C.fn.find(src);
-  if (it != C.fn.end()) return it->second;
-  nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src.c_str(), "hdg_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
-    if (err) *err = "nvrtcCreateProgram failed";
-    return nullptr;
-  }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
-  const nvrtcResult rc = nvrtcCompileProgram(prog, 3, opts);
-  if (rc != NVRTC_SUCCESS) {
-    size_t n = 0;
-    nvrtcGetProgramLogSize(prog, &n);
-    std::string log(n, '\0');
-    nvrtcGetProgramLog(prog, log.data());
-    if (err) *err = "nvrtc: " + log;
-    nvrtcDestroyProgram(&prog);
-    return nullptr;
-  }
-  size_t n = 0;
-  nvrtcGetCUBINSize(prog, &n);
-  std::vector<char> cubin(n);
-  nvrtcGetCUBIN(prog, cubin.data());
-  nvrtcDestroyProgram(&prog);
-  CUmodule mod;
-  CUfunction fn;
   if (!drv().ok) {
     if (err) *err = "driver entry points unavailable";
     return nullptr;
   }
-  if (drv().loadData(&mod, cubin.data()) != CUDA_SUCCESS ||
+  CUcontext ctx = nullptr;
+  if (drv().ctxGetCurrent(&ctx) != CUDA_SUCCESS || !ctx) {
+    if (err) *err = "no current CUDA context";
+    return nullptr;
+  }
+  char key_prefix[32];
+  std::snprintf(key_prefix, sizeof key_prefix, "%p\n", static_cast<void*>(ctx));
+  const std::string key = key_prefix + src;
+  auto it = C.fn.find(key);
+  if (it != C.fn.end()) return it->second;
+  auto bin = C.cubin.find(src);
+  if (bin == C.cubin.end()) {
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, src.c_str(), "hdg_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+      if (err) *err = "nvrtcCreateProgram failed";
+      return nullptr;
+    }
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
+    const nvrtcResult rc = nvrtcCompileProgram(prog, 3, opts);
+    if (rc != NVRTC_SUCCESS) {
+      size_t n = 0;
+      nvrtcGetProgramLogSize(prog, &n);
+      std::string log(n, '\0');
+      nvrtcGetProgramLog(prog, log.data());
+      if (err) *err = "nvrtc: " + log;
+      nvrtcDestroyProgram(&prog);
+      return nullptr;
+    }
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    std::vector<char> cubin(n);
+    nvrtcGetCUBIN(prog, cubin.data());
+    nvrtcDestroyProgram(&prog);
+    bin = C.cubin.emplace(src, std::move(cubin)).first;
+  }
+  CUmodule mod;
+  CUfunction fn;
+  if (drv().loadData(&mod, bin->second.data()) != CUDA_SUCCESS ||
       drv().getFunction(&fn, mod, name) != CUDA_SUCCESS) {
     if (err) *err = "cuModuleLoadData/cuModuleGetFunction failed";
     return nullptr;
   }
   C.mods.push_back(mod);
-  C.fn.emplace(src, fn);
+  C.fn.emplace(key, fn);
   return fn;
 }
 
@@ -339,17 +358,20 @@ sample_field_jit(int nelt, int nq, const double* __restrict__ bary, const double
 )CUDA";
 }  // namespace
 
-CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, int nqp,
-                           std::string* err) {
+JitKernel jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, int nqp,
+                          std::string* err) {
   FieldEmitter fe;
   const std::string ek = fe.emit(kap, "sk"), ec = fe.emit(c, "sc"), ef = fe.emit(f, "sf");
+  // the block size is baked into __launch_bounds__ here and returned with the
+  // kernel, so the launch always uses the value the kernel was compiled for
+  const int threads = jit_quad_threads(eb, nqp);
   const std::string src = "#define EB " + std::to_string(eb) + "\n#define QUAD_THREADS " +
-                          std::to_string(jit_quad_threads(eb, nqp)) + "\n#define QUAD_MINB " + (jit_quad_threads(eb, nqp) == 384 ? HDG_QUAD_MINB32 : "1") +
+                          std::to_string(threads) + "\n#define QUAD_MINB " + (threads == 384 ? HDG_QUAD_MINB32 : "1") +
                           "\n#define QUAD_UNROLL " +
                           std::to_string(HDG_QUAD_UNROLL) + "\n#define FIELD_STMTS " + fe.stmts() +
                           "\n#define FIELD_KAPPA " + ek + "\n#define FIELD_C " + ec + "\n#define FIELD_F " + ef +
                           "\n" + kQuadSource;
-  return compile_cached(src, "quad_build_jit", err);
+  return JitKernel{compile_cached(src, "quad_build_jit", err), threads};
 }
 
 CUfunction jit_sample_kernel(const hdg_field& f, std::string* err) {

@@ -34,9 +34,15 @@ class FieldEmitter {
 inline int jit_quad_threads(int eb, int nqp) {
   return eb == 16 ? HDG_QUAD_THREADS16 : (nqp >= 100 ? HDG_QUAD_THREADS32 : 256);
 }
-// Compiled (cached) kernel for these fields and EB elements per CTA, or nullptr with *err set.
-CUfunction jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, int nqp,
-                           std::string* err);
+// Compiled (cached per source and CUDA context) kernel for these fields and EB
+// elements per CTA with the block size it was compiled for; fn == nullptr with
+// *err set on failure.
+struct JitKernel {
+  CUfunction fn = nullptr;
+  int threads = 0;
+};
+JitKernel jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, int nqp,
+                          std::string* err);
 // Kernel sampling a PROGRAM field at every element node (SAMPLED layout), or nullptr.
 CUfunction jit_sample_kernel(const hdg_field& f, std::string* err);
 bool launch_quad_jit(CUfunction fn, cudaStream_t stream, int grid, int block, size_t smem, void** args,

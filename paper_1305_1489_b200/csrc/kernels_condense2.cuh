@@ -57,8 +57,10 @@ template <> struct C2Cfg<3> { static constexpr int NW = 4, EPB = 4; };
 // a[]) by the symmetric sweep operator: sweeping pivot k keeps the matrix
 // symmetric, so column k is gathered from every lane's own a[k] (one shared
 // store per lane + broadcast loads) instead of being broadcast entry by entry.
-// After N sweeps a = -A^-1; the sign is folded in on return. No pivoting
-// (SPD); the pivots are the Cholesky pivots and feed the 1e-14 test.
+// After N sweeps a = -A^-1; the sign is folded in on return. No pivoting;
+// pmin / pmax return the extreme |pivots| (the LDL^T pivots: p00 and det/p00
+// per 2 x 2 block; pmin = 0 if one vanished or is not finite), which the
+// rescue screen compares (kernels_rescue.cuh).
 // 1/x to full double precision: MUFU reciprocal seed + two Newton steps
 // (shorter dependency chain than IEEE division; last-bit rounding may differ).
 __device__ __forceinline__ double fast_rcp(double x) {
@@ -78,6 +80,7 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
   // Cholesky pivots of each 2x2 block: p00 and det / p00 = 1 / i11, tracked as
   // running extremes (p00, i11, det) instead of stored, to save registers.
   double p00min = 1e300, p00max = 0.0, i11min = 1e300, i11max = 0.0, detmin = 1e300;
+  bool finite = true;
 #pragma unroll
   for (int k = 0; k + 1 < N; k += 2) {
     double* st = stage + ((k >> 1) & 1) * 64;
@@ -92,11 +95,12 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
     const double det = fma(p00, p11, -p01 * p01);
     const double id = fast_rcp(det);
     const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;  // P^-1 (symmetric)
-    p00min = fmin(p00min, p00);
-    p00max = fmax(p00max, p00);
-    i11min = fmin(i11min, i11);
-    i11max = fmax(i11max, i11);
-    detmin = fmin(detmin, det);
+    p00min = fmin(p00min, fabs(p00));
+    p00max = fmax(p00max, fabs(p00));
+    i11min = fmin(i11min, fabs(i11));
+    i11max = fmax(i11max, fabs(i11));
+    detmin = fmin(detmin, fabs(det));
+    finite = finite && isfinite(i11) && isfinite(p00);
     const bool m0 = lane == k, m1 = lane == k + 1;
     // w = P^-1 [a_k; a_k+1] for ordinary lanes; pivot lanes hold their own
     // block column, for which "a - v w" must produce A(i,block) P^-1.
@@ -129,9 +133,10 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
     double* st = stage + (((k >> 1)) & 1) * 64;
     if (lane < N) st[lane] = a[k];
     const double p = __shfl_sync(0xffffffffu, a[k], k);
-    p00min = fmin(p00min, p);
-    p00max = fmax(p00max, p);
-    detmin = fmin(detmin, p);
+    p00min = fmin(p00min, fabs(p));
+    p00max = fmax(p00max, fabs(p));
+    detmin = fmin(detmin, fabs(p));
+    finite = finite && isfinite(p);
     const double ip = fast_rcp(p);
     const bool me = lane == k;
     const double t = me ? 1.0 - ip : a[k] * ip;
@@ -144,8 +149,8 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < N; ++i) a[i] = -a[i];
-  if (!(p00min > 0.0) || !(detmin > 0.0)) {
-    pmin = fmin(pmin, fmin(p00min, detmin));  // not SPD: fails the pivot test
+  if (!finite || !(p00min > 0.0) || !(detmin > 0.0)) {
+    pmin = 0.0;  // a pivot vanished or overflowed: the rescue kernel decides
     pmax = fmax(pmax, p00max);
   } else {
     const double dmin = N >= 2 ? 1.0 / i11max : 1e300, dmax = N >= 2 ? 1.0 / i11min : 0.0;
@@ -154,19 +159,19 @@ __device__ __forceinline__ void warp_gj_inverse(double (&a)[N], double* stage, i
   }
 }
 
-// Loads column `lane` of a packed-lower SPD matrix and inverts it in place
-// (warp-wide). Returns true if the 1e-14 pivot test fails.
+// Loads column `lane` of a packed-lower symmetric matrix and inverts it in
+// place (warp-wide); pmin / pmax as warp_gj_inverse.
 template <int D3>
-__device__ __forceinline__ bool warp_inverse_packed(const double* __restrict__ P, double (&a)[D3],
-                                                    double* stage, int lane) {
+__device__ __forceinline__ void warp_inverse_packed(const double* __restrict__ P, double (&a)[D3],
+                                                    double* stage, int lane, double& pmin, double& pmax) {
 #pragma unroll
   for (int i = 0; i < D3; ++i) {
     const int r = i > lane ? i : lane, c = i > lane ? lane : i;
     a[i] = lane < D3 ? P[sym_idx(r, c, D3)] : 0.0;
   }
-  double pmin = 1e300, pmax = 0.0;
+  pmin = 1e300;
+  pmax = 0.0;
   warp_gj_inverse<D3>(a, stage, lane, pmin, pmax);
-  return !(pmin > 0.0) || pmin < 1e-14 * pmax;
 }
 
 // Column data of element K's faces (per m-column: normals, tau|e|, W offset,
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(C2Cfg<K_>::NW * 32 * C2Cfg<K_>::EPB)
 condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
                  const double* __restrict__ Dsym, const double* __restrict__ fvec,
                  double* __restrict__ Cout, double* __restrict__ Cfout, double* __restrict__ factors,
-                 long long* bad_element) {
+                 double* __restrict__ pivstat) {
   using Dm = C2Dims<K_>;
   constexpr int NW = C2Cfg<K_>::NW, EPB = C2Cfg<K_>::EPB, NT = NW * 32;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, D3P = Dm::D3P, MP = Dm::MP, LD = Dm::LD;
@@ -253,17 +258,22 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     for (int i = tm.tid; i < D3; i += NT) fv[i] = fvec[K * D3 + i];
     if (tm.warp == 0) {
       double a[D3];
-      const bool bad = warp_inverse_packed<D3>(Msym + K * Dm::NSYM, a, stgM, lane);
+      double pmin, pmax;
+      warp_inverse_packed<D3>(Msym + K * Dm::NSYM, a, stgM, lane, pmin, pmax);
       if (lane < D3) {
 #pragma unroll
-        for (int i = 0; i < D3; ++i) Mi[i + lane * LD] = a[i];
+        for (int i = 0; i < D3; ++i)  // lower triangle of the sweep result, mirrored
+          if (i >= lane) {
+            Mi[i + lane * LD] = a[i];
+            Mi[lane + i * LD] = a[i];
+          }
         if (factors) {
 #pragma unroll
           for (int i = 0; i < D3; ++i)
             if (i >= lane) factors[K * Dm::FACTORS + sym_idx(i, lane, D3)] = a[i];
         }
       }
-      if (bad && lane == 0) flag_bad(bad_element, K);
+      if (lane == 0) store_pivstat(pivstat, K, 0, pmin, pmax);
     }
     tm.sync();
     if (tm.warp == NW - 1) build_columns<D2, D3, M, MP>(sgbuf(0), colbuf(0), lane);
@@ -425,31 +435,39 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
       double pmin = 1e300, pmax = 0.0;
       warp_gj_inverse<D3>(a, stgS, lane, pmin, pmax);
-      const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
       if (lane < D3) {
 #pragma unroll
-        for (int i = 0; i < D3; ++i) Sb[i + lane * LD] = a[i];
+        for (int i = 0; i < D3; ++i)  // lower triangle of the sweep result, mirrored
+          if (i >= lane) {
+            Sb[i + lane * LD] = a[i];
+            Sb[lane + i * LD] = a[i];
+          }
         if (F) {
 #pragma unroll
           for (int i = 0; i < D3; ++i)
             if (i >= lane) F[Dm::NSYM + sym_idx(i, lane, D3)] = a[i];
         }
       }
-      if (bad && lane == 0) flag_bad(bad_element, K);
+      if (lane == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
     }
     if (tm.warp == WM && has_next) {  // Mi is dead after P1: invert the next M into it
       double a[D3];
-      const bool bad = warp_inverse_packed<D3>(Msym + Kn * Dm::NSYM, a, stgM, lane);
+      double pmin, pmax;
+      warp_inverse_packed<D3>(Msym + Kn * Dm::NSYM, a, stgM, lane, pmin, pmax);
       if (lane < D3) {
 #pragma unroll
-        for (int i = 0; i < D3; ++i) Mi[i + lane * LD] = a[i];
+        for (int i = 0; i < D3; ++i)  // lower triangle of the sweep result, mirrored
+          if (i >= lane) {
+            Mi[i + lane * LD] = a[i];
+            Mi[lane + i * LD] = a[i];
+          }
         if (factors) {
 #pragma unroll
           for (int i = 0; i < D3; ++i)
             if (i >= lane) factors[Kn * Dm::FACTORS + sym_idx(i, lane, D3)] = a[i];
         }
       }
-      if (bad && lane == 0) flag_bad(bad_element, Kn);
+      if (lane == 0) store_pivstat(pivstat, Kn, 0, pmin, pmax);
     }
     if (tm.warp >= GW0) {
       const int ow = tm.warp - GW0;

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(C3Cfg<K_>::NWT * 32, C3Cfg<K_>::MINB)
 condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
                  const double* __restrict__ Dsym, const double* __restrict__ fvec,
                  double* __restrict__ Cout, double* __restrict__ Cfout, double* __restrict__ factors,
-                 long long* bad_element) {
+                 double* __restrict__ pivstat) {
   using Dm = C3Dims<K_>;
   constexpr int EPB = C3Cfg<K_>::EPB, NWT = C3Cfg<K_>::NWT, NT = NWT * 32;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, MP = Dm::MP, LD = Dm::LD, RH = Dm::RH;
@@ -224,13 +224,16 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     __syncwarp();
     double pmin = 1e300, pmax = 0.0;
     gj_sweep_inverse<D3>(a, stM(e), lane, pmin, pmax);
-    const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
-    if (lane < D3) {  // symmetric: row-wise stores are conflict-free
+    if (lane < D3) {
 #pragma unroll
-      for (int i = 0; i < D3; ++i) Mi(e)[lane + i * LD] = a[i];
+      for (int i = 0; i < D3; ++i)  // lower triangle of the sweep result, mirrored:
+        if (i >= lane) {              // the two halves round differently (GJ)
+          Mi(e)[lane + i * LD] = a[i];
+          Mi(e)[i + lane * LD] = a[i];
+        }
     }
     store_factor(a, K, 0, Yb(e));  // R_# of this slot is dead until the next P1
-    if (bad && lane == 0) flag_bad(bad_element, K);
+    if (lane == 0) store_pivstat(pivstat, K, 0, pmin, pmax);
   };
 
   // ---- prologue: first batch
@@ -430,10 +433,13 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             __syncwarp();
             double pmin = 1e300, pmax = 0.0;
             gj_sweep_seg<D3, 16, D3>(a, h == 0 ? stS(e) : stM(e), c, pmin, pmax);
-            const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
             if (live && c < D3) {
 #pragma unroll
-              for (int i = 0; i < D3; ++i) dst[c + i * LD] = a[i];
+              for (int i = 0; i < D3; ++i)  // lower triangle, mirrored (see invert_M)
+                if (i >= c) {
+                  dst[c + i * LD] = a[i];
+                  dst[i + c * LD] = a[i];
+                }
               if (factors) {
                 double* fd = factors + K * Dm::FACTORS + (h == 0 ? Dm::NSYM : 0) + c * (2 * D3 - c + 1) / 2 - c;
 #pragma unroll
@@ -441,7 +447,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
                   if (i >= c) fd[i] = a[i];
               }
             }
-            if (live && bad && c == 0) flag_bad(bad_element, K);
+            if (live && c == 0) store_pivstat(pivstat, K, h == 0 ? 1 : 0, pmin, pmax);
             continue;
           }
           if (task < EPB) {
@@ -456,13 +462,16 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #else
             pmin = pmax = 1.0;
 #endif
-            const bool bad = !(pmin > 0.0) || pmin < 1e-14 * pmax;
             if (lane < D3) {
 #pragma unroll
-              for (int i = 0; i < D3; ++i) Sb(e)[lane + i * LD] = a[i];
+              for (int i = 0; i < D3; ++i)  // lower triangle, mirrored (see invert_M)
+                if (i >= lane) {
+                  Sb(e)[lane + i * LD] = a[i];
+                  Sb(e)[i + lane * LD] = a[i];
+                }
             }
             store_factor(a, K, Dm::NSYM, Dp(e));  // packed D is dead after P2
-            if (bad && lane == 0) flag_bad(bad_element, K);
+            if (lane == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
           } else if (has_next && Kn0 + e < nelt) {
 #ifdef HDG_DIAG_NO_GJ
             continue;

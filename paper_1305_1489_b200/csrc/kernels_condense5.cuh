@@ -72,8 +72,10 @@ template <int K_> struct C5Cfg { static constexpr int NWT = 16; };
 // do not, and the update must use the same triangle as the reference order.)
 // The result (X^-1, full) is written back to X.
 // Returns the pivot test of local_solver.cpp:50-57 (Cholesky pivots).
+// pmin / pmax (valid on thread 0) return the extreme |LDL^T pivots|, 0 for a
+// vanished or non-finite one (the rescue screen, kernels_rescue.cuh).
 template <int N, int LD, int NT>
-__device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
+__device__ __forceinline__ void cta_sweep_inverse(double* X, double* Y, double& pmin, double& pmax) {
   constexpr int RG = NT / N;                  // row groups per column
   constexpr int RPT = (N + RG - 1) / RG;      // rows per thread
   const int c = threadIdx.x / RG, i0 = (threadIdx.x - c * RG) * RPT;
@@ -81,7 +83,8 @@ __device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
   double a[RPT];
 #pragma unroll
   for (int u = 0; u < RPT; ++u) a[u] = (live && i0 + u < N) ? X[i0 + u + c * LD] : 0.0;
-  double pmin = 1e300, pmax = 0.0;
+  pmin = 1e300;
+  pmax = 0.0;
   bool bad = false;
   // stage of the pivot pair (k, k+1): [0, N) row k by column, [N, 2N) row
   // k+1, [2N, 3N) column k by row, [3N, 4N) column k+1. The entries a step
@@ -120,10 +123,10 @@ __device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
       const double id = gj_rcp(det);
       const double i00 = p11 * id, i01 = -p01 * id, i11 = p00 * id;
       if (stats) {
-        if (!(p00 > 0.0) || !(det > 0.0)) bad = true;
-        const double d1 = det * gj_rcp(p00);  // second Cholesky pivot of the pair
-        pmin = fmin(pmin, fmin(p00, d1));
-        pmax = fmax(pmax, fmax(p00, d1));
+        const double d0 = fabs(p00), d1 = fabs(det * gj_rcp(p00));  // LDL^T pivots of the pair
+        if (!(d0 > 0.0) || !(d1 > 0.0) || !(d0 <= 1.79e308) || !(d1 <= 1.79e308)) bad = true;
+        pmin = fmin(pmin, fmin(d0, d1));
+        pmax = fmax(pmax, fmax(d0, d1));
       }
       if (live) {
         const double a0 = st[c] - (c == k ? 1.0 : 0.0);
@@ -145,9 +148,9 @@ __device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
     } else {  // trailing scalar pivot
       const double p = st[k];
       if (stats) {
-        if (!(p > 0.0)) bad = true;
-        pmin = fmin(pmin, p);
-        pmax = fmax(pmax, p);
+        if (!(fabs(p) > 0.0) || !(fabs(p) <= 1.79e308)) bad = true;
+        pmin = fmin(pmin, fabs(p));
+        pmax = fmax(pmax, fabs(p));
       }
       const double ip = gj_rcp(p);
       if (live) {
@@ -164,10 +167,13 @@ __device__ __forceinline__ bool cta_sweep_inverse(double* X, double* Y) {
   if (live) {
 #pragma unroll
     for (int u = 0; u < RPT; ++u)
-      if (i0 + u < N) X[i0 + u + c * LD] = -a[u];
+      if (i0 + u < N && i0 + u >= c) {  // lower triangle, mirrored: the two halves of a
+        X[i0 + u + c * LD] = -a[u];     // Gauss-Jordan inverse round differently
+        X[c + (i0 + u) * LD] = -a[u];
+      }
   }
   __syncthreads();
-  return bad || pmin < 1e-14 * pmax;
+  if (bad) pmin = 0.0;
 }
 
 template <int K_>
@@ -175,7 +181,7 @@ __global__ void __launch_bounds__(C5Cfg<K_>::NWT * 32, 1)
 condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
                  const double* __restrict__ Dsym, const double* __restrict__ fvec,
                  double* __restrict__ Cout, double* __restrict__ Cfout, double* __restrict__ factors,
-                 long long* bad_element) {
+                 double* __restrict__ pivstat) {
   using Dm = C5Dims<K_>;
   constexpr int NWT = C5Cfg<K_>::NWT, NT = NWT * 32;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, MP = Dm::MP, LD = Dm::LD, KS = Dm::KS;
@@ -324,7 +330,11 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     __syncthreads();
 
     // ---- P1: M^-1 (CTA sweep), packed lower part into the recovery cache
-    if (cta_sweep_inverse<D3, LD, NT>(Mi, T0) && threadIdx.x == 0) flag_bad(bad_element, K);
+    {
+      double pmin, pmax;
+      cta_sweep_inverse<D3, LD, NT>(Mi, T0, pmin, pmax);
+      if (threadIdx.x == 0) store_pivstat(pivstat, K, 0, pmin, pmax);
+    }
     if (factors)  // packed lower, column-major: column c at sym_idx(c, c)
       for (int c = warp; c < D3; c += NWT)
         for (int i = c + lane; i < D3; i += 32) factors[K * Dm::FACTORS + sym_idx(i, c, D3)] = Mi[i + c * LD];
@@ -404,7 +414,11 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     __syncthreads();
 
     // ---- P6: S^-1 (CTA sweep); cache: S^-1 packed, V, f
-    if (cta_sweep_inverse<D3, LD, NT>(S, T1) && threadIdx.x == 0) flag_bad(bad_element, K);
+    {
+      double pmin, pmax;
+      cta_sweep_inverse<D3, LD, NT>(S, T1, pmin, pmax);
+      if (threadIdx.x == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
+    }
     if (factors) {
       for (int c = warp; c < D3; c += NWT)
         for (int i = c + lane; i < D3; i += 32) factors[K * Dm::FACTORS + NSYM + sym_idx(i, c, D3)] = S[i + c * LD];

@@ -141,6 +141,24 @@ __global__ void quad_points_kernel(int nelt, int nq, const double* __restrict__ 
 
 __global__ void set_ll_kernel(long long* p, long long v) { *p = v; }
 
+// Status words of one build_condense: [0] lowest singular element, [1] lowest
+// element with a negative tau, [2] lowest element whose tau vanishes on all
+// four faces (LLONG_MAX = none); [4] elements re-solved by the rescue kernel.
+__global__ void reset_build_status_kernel(long long* st) {
+  if (threadIdx.x < 3) st[threadIdx.x] = LLONG_MAX;
+  if (threadIdx.x == 4) st[4] = 0;
+}
+
+// StabilizationField::validate (element_matrices.cpp:38-46) on T = tau |e|
+// (|e| > 0, so the signs are tau's): records the lowest offending elements.
+__global__ void tau_check_kernel(int nelt, const double* __restrict__ T, long long* st) {
+  for (long K = long(blockIdx.x) * blockDim.x + threadIdx.x; K < nelt; K += long(gridDim.x) * blockDim.x) {
+    const double t0 = T[K], t1 = T[nelt + K], t2 = T[2L * nelt + K], t3 = T[3L * nelt + K];
+    if (t0 < 0.0 || t1 < 0.0 || t2 < 0.0 || t3 < 0.0) atomicMin(st + 1, K);
+    if (fmax(fmax(t0, t1), fmax(t2, t3)) <= 0.0) atomicMin(st + 2, K);
+  }
+}
+
 // ================================================================ K4
 // CSR of the skeleton matrix H: row (f, i) holds, for every neighbour face g of
 // f in ascending order, the d2 columns g*d2 + j (global_system.cpp:43-54).

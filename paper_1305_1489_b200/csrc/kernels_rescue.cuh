@@ -1,0 +1,287 @@
+// K3b: rescue screen + the reference's LU path for the elements the
+// structured condensation cannot vouch for.
+//
+// The condensation kernels (kernels_condense2/3/5.cuh) eliminate A1 by blocks
+// without pivoting: two symmetric sweep inverses (M, then the Schur complement
+// S = D + sum_s C_s M^-1 C_s^T). They record each inverse's extreme |LDL^T
+// pivots| (store_pivstat). The reference instead factorises all of A1 with
+// partial pivoting and calls an element singular when
+// min |U_ii| < 1e-14 max |U_ii| (factor_checked, local_solver.cpp:50-57).
+// The two pivot sets are different numbers, so this kernel screens every
+// element: where min(|pivots of M|, |pivots of S|) < screen * max(...) (or a
+// pivot vanished / overflowed), the element is re-solved exactly as the
+// reference does -- A1, A2, A3, Af assembled from the K2 outputs and the
+// tables (local_solver.cpp:12-40), a partial-pivot LU with the reference's
+// 1e-14 test, X = A1^-1 [A2 | Af], C = A3 X + tauDD, Cf = A3 X_f
+// (local_solver.cpp:71-100) -- and its recovery-cache record {M^-1, S^-1, V,
+// f} is recomputed with partial-pivot inverses, so indefinite or
+// ill-conditioned elements (e.g. c < 0, kappa^-1 -> 0) get the reference's
+// verdict and the reference's values. Singular elements are reported through
+// the lowest-index status word (LocalSolverError{element}).
+//
+// Measured pivot ratios (tools/diag/singular_screen.py): the combined ratio
+// of M and S is below the reference's U ratio in every sampled element
+// (kappa scaled 1..1e20, c down to -1e4, h down to 1e-4, perturbed meshes),
+// so screen = 1e-12 (two orders of margin over the reference's 1e-14)
+// catches every element the reference could flag. Healthy meshes never reach
+// it; the screen costs one 32 B/element read.
+#pragma once
+
+#include "dev_common.cuh"
+#include "kernels_local.cuh"
+
+namespace hdgb {
+
+constexpr int kRescueThreads = 256;
+
+// Per-CTA scratch (doubles) for one rescued element.
+struct RescueLayout {
+  int d3, d2, m, nu, n;
+  long A, B, Cs, E, TDP, Mw, Mi, Sw, Si, Z, Dm, f, total;
+  __host__ __device__ RescueLayout(int d3_, int d2_, int nu_) : d3(d3_), d2(d2_), m(4 * d2_), nu(nu_), n(3 * d3_ + nu_) {
+    long o = 0;
+    A = o;   o += long(n) * n;              // A1 -> LU
+    B = o;   o += long(n) * (m + 1);        // [A2 | Af] -> X
+    Cs = o;  o += 3L * d3 * d3;             // C_x, C_y, C_z
+    E = o;   o += 3L * m * d3;              // nxDP, nyDP, nzDP
+    TDP = o; o += long(m) * d3;             // tauDP
+    Mw = o;  o += long(d3) * d3;            // M (destroyed)
+    Mi = o;  o += long(d3) * d3;            // M^-1
+    Sw = o;  o += long(d3) * d3;            // S (destroyed)
+    Si = o;  o += long(d3) * d3;            // S^-1
+    Z = o;   o += 3L * d3 * (d3 + m);       // M^-1 C_s^T | M^-1 E_s^T
+    Dm = o;  o += long(d3) * d3;            // D = Mc + tau PP
+    f = o;   o += d3;
+    total = round_up(int(o), 32);
+  }
+};
+
+// Partial-pivot Gaussian elimination of [A | B] (A n x n, column-major lda;
+// B n x nrhs, ldb) by the whole CTA, then back substitution: B <- A^-1 B.
+// |U_jj| go to diag[0..n). The pivot is the first row holding the column's
+// largest magnitude (Eigen PartialPivLU's maxCoeff); a zero pivot column is
+// skipped, as Eigen does (its |U_jj| = 0 then fails the caller's test).
+__device__ void cta_gauss(double* A, int lda, int n, double* B, int ldb, int nrhs, double* diag, double* lm,
+                          double* red_v, int* red_i) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  for (int j = 0; j < n; ++j) {
+    double best = -1.0;
+    int bi = n;
+    for (int i = j + tid; i < n; i += NT) {
+      const double v = fabs(A[i + long(j) * lda]);
+      if (v > best) { best = v; bi = i; }
+    }
+    red_v[tid] = best;
+    red_i[tid] = bi;
+    __syncthreads();
+    for (int s = NT / 2; s > 0; s >>= 1) {
+      if (tid < s) {
+        const double v2 = red_v[tid + s];
+        const int i2 = red_i[tid + s];
+        if (v2 > red_v[tid] || (v2 == red_v[tid] && i2 < red_i[tid])) { red_v[tid] = v2; red_i[tid] = i2; }
+      }
+      __syncthreads();
+    }
+    const int p = red_i[0];
+    if (tid == 0) diag[j] = red_v[0];
+    if (p != j && p < n) {
+      for (int c = tid; c < n + nrhs; c += NT) {
+        double* x = c < n ? A + long(c) * lda : B + long(c - n) * ldb;
+        const double t = x[j];
+        x[j] = x[p];
+        x[p] = t;
+      }
+    }
+    __syncthreads();
+    const double piv = A[j + long(j) * lda];
+    if (piv != 0.0) {
+      for (int i = j + 1 + tid; i < n; i += NT) lm[i] = A[i + long(j) * lda] / piv;
+      __syncthreads();
+      const int rows = n - j - 1, cols = n - j - 1 + nrhs;
+      for (long idx = tid; idx < long(rows) * cols; idx += NT) {
+        const int i = j + 1 + int(idx % rows), cc = int(idx / rows);
+        double* x = cc < n - j - 1 ? A + long(j + 1 + cc) * lda : B + long(cc - (n - j - 1)) * ldb;
+        x[i] = fma(-lm[i], x[j], x[i]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int c = tid; c < nrhs; c += NT) {
+    double* x = B + long(c) * ldb;
+    for (int i = n - 1; i >= 0; --i) {
+      double s = x[i];
+      for (int k = i + 1; k < n; ++k) s = fma(-A[i + long(k) * lda], x[k], s);
+      x[i] = s / A[i + long(i) * lda];
+    }
+  }
+  __syncthreads();
+}
+
+// pivstat: nelt x 4 (min, max |pivot| of M; of S). status[0]: lowest singular
+// element (atomicMin), status[4]: count of rescued elements.
+__global__ void __launch_bounds__(kRescueThreads)
+rescue_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym, const double* __restrict__ Dsym,
+              const double* __restrict__ fvec, const double* __restrict__ pivstat, double screen,
+              double* __restrict__ Cout, double* __restrict__ Cfout, double* __restrict__ factors,
+              double* __restrict__ scratch, long long* status) {
+  __shared__ int cand[kRescueThreads];
+  __shared__ int ncand;
+  __shared__ double sg[32];
+  __shared__ double diag[3 * 56 + 56];
+  __shared__ double lm[3 * 56 + 56];
+  __shared__ double red_v[kRescueThreads];
+  __shared__ int red_i[kRescueThreads];
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int d3 = tab.d3, d2 = tab.d2, m = 4 * d2, nu = tab.nu;
+  const RescueLayout L(d3, d2, nu);
+  const int n = L.n;
+  double* W = scratch + long(blockIdx.x) * L.total;
+  double *A = W + L.A, *B = W + L.B, *Cs = W + L.Cs, *E = W + L.E, *TDP = W + L.TDP, *Mw = W + L.Mw,
+         *Mi = W + L.Mi, *Sw = W + L.Sw, *Si = W + L.Si, *Z = W + L.Z, *Dm = W + L.Dm, *fl = W + L.f;
+  const int nsym = d3 * (d3 + 1) / 2;
+  const long FD = long(d3) * (d3 + 1) + long(d3) * m + d3;
+
+  for (long base = long(blockIdx.x) * NT; base < nelt; base += long(gridDim.x) * NT) {
+    if (tid == 0) ncand = 0;
+    __syncthreads();
+    const long Kt = base + tid;
+    if (Kt < nelt) {
+      const double2 pm = reinterpret_cast<const double2*>(pivstat)[2 * Kt];
+      const double2 ps = reinterpret_cast<const double2*>(pivstat)[2 * Kt + 1];
+      const double lo = fmin(pm.x, ps.x), hi = fmax(pm.y, ps.y);
+      if (!(lo > 0.0 && lo >= screen * hi && hi <= 1.79e308)) cand[atomicAdd(&ncand, 1)] = int(Kt);
+    }
+    __syncthreads();
+    const int nc = ncand;
+    for (int ci = 0; ci < nc; ++ci) {
+      const long K = cand[ci];
+      if (tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + 4), 1ull);
+      load_geo(geo, K, nelt, sg, tid, NT);
+      __syncthreads();
+      const double* a9 = sg + 1;
+      const double* nrm = sg + 10;
+      const double* Tl = sg + 22;
+      // ---- element matrices from the K2 outputs and the tables
+      for (int idx = tid; idx < d3 * d3; idx += NT) {
+        const int i = idx % d3, j = idx / d3;
+        const int r = i >= j ? i : j, c = i >= j ? j : i;
+        const double mv = Msym[K * nsym + sym_idx(r, c, d3)];
+        Mw[idx] = mv;
+        Dm[idx] = Dsym[K * nsym + sym_idx(r, c, d3)];
+        for (int s = 0; s < 3; ++s) {
+          double acc = 0.0;
+          for (int h = 0; h < 3; ++h) acc += __ldg(tab.Chat + long(h) * d3 * d3 + idx) * a9[3 * s + h];
+          Cs[long(s) * d3 * d3 + idx] = acc;
+        }
+        Mi[idx] = i == j ? 1.0 : 0.0;
+      }
+      for (int i = tid; i < d3; i += NT) fl[i] = fvec[K * d3 + i];
+      for (int idx = tid; idx < m * d3; idx += NT) {
+        const int r = idx % m, j = idx / m;
+        const int l = r / d2, i = r - l * d2;
+        const int mu = int(sg[26 + l]);
+        const double w = __ldg(tab.Wlm + long(6 * l + mu - 1) * d2 * d3 + i + long(j) * d2);
+        TDP[idx] = Tl[l] * w;
+        for (int s = 0; s < 3; ++s) E[long(s) * m * d3 + idx] = nrm[3 * l + s] * w;
+      }
+      __syncthreads();
+      // ---- A1, [A2 | Af] (local_solver.cpp:12-40, column-major)
+      for (long idx = tid; idx < long(n) * n; idx += NT) {
+        const int r = int(idx % n), c = int(idx / n);
+        const int br = r / d3 < 3 ? r / d3 : 3, bc = c / d3 < 3 ? c / d3 : 3;
+        const int i = r - br * d3, j = c - bc * d3;
+        double v = 0.0;
+        if (br < 3 && bc < 3) v = br == bc ? Mw[i + j * d3] : 0.0;             // M blocks
+        else if (br < 3) v = -Cs[long(br) * d3 * d3 + j + i * d3];              // -C_s^T (:, :nu)
+        else if (bc < 3) v = Cs[long(bc) * d3 * d3 + i + j * d3];               // C_s (:nu, :)
+        else v = Dm[i + j * d3];                                                // Mc + tau PP
+        A[idx] = v;
+      }
+      for (long idx = tid; idx < long(n) * (m + 1); idx += NT) {
+        const int r = int(idx % n), c = int(idx / n);
+        const int br = r / d3 < 3 ? r / d3 : 3, i = r - br * d3;
+        double v;
+        if (c == m) v = br < 3 ? 0.0 : fl[i];                                    // Af
+        else v = br < 3 ? E[long(br) * m * d3 + c + i * m] : -TDP[c + i * m];    // [nDP_s^T; -tauDP^T]
+        B[idx] = v;
+      }
+      __syncthreads();
+      cta_gauss(A, n, n, B, n, m + 1, diag, lm, red_v, red_i);
+      // factor_checked (local_solver.cpp:50-57)
+      if (tid == 0) {
+        double dmin = 1e300, dmax = 0.0;
+        for (int j = 0; j < n; ++j) { dmin = fmin(dmin, diag[j]); dmax = fmax(dmax, diag[j]); }
+        red_v[0] = (dmax == 0.0 || dmin < 1e-14 * dmax) ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      const bool singular = red_v[0] != 0.0;
+      __syncthreads();
+      if (singular) {
+        if (tid == 0) atomicMin(reinterpret_cast<unsigned long long*>(status), static_cast<unsigned long long>(K));
+        continue;
+      }
+      // ---- C = A3 X + tauDD, Cf = A3 X_f (A3 = [nDP_s, tauDP(:, :nu)])
+      for (int idx = tid; idx < m * (m + 1); idx += NT) {
+        const int r = idx % m, c = idx / m;
+        double acc = 0.0;
+        for (int s = 0; s < 3; ++s)
+          for (int j = 0; j < d3; ++j) acc = fma(E[long(s) * m * d3 + r + j * m], B[long(c) * n + s * d3 + j], acc);
+        for (int j = 0; j < nu; ++j) acc = fma(TDP[r + j * m], B[long(c) * n + 3 * d3 + j], acc);
+        if (c < m) {
+          const int l = r / d2, l2 = c / d2;
+          if (l == l2) acc += Tl[l] * __ldg(tab.DD + (r - l * d2) + (c - l2 * d2) * d2);
+          Cout[K * m * m + r + long(c) * m] = acc;
+        } else {
+          Cfout[K * m + r] = acc;
+        }
+      }
+      if (!factors) { __syncthreads(); continue; }
+      // ---- recovery cache {M^-1, S^-1, V, f} with partial-pivot inverses
+      cta_gauss(Mw, d3, d3, Mi, d3, d3, diag, lm, red_v, red_i);
+      for (int idx = tid; idx < d3 * (nu + m) * 3; idx += NT) {  // Z_s = M^-1 [C_s(:nu,:)^T | E_s^T]
+        const int a = idx % d3, rest = idx / d3, col = rest % (nu + m), s = rest / (nu + m);
+        double acc = 0.0;
+        for (int b = 0; b < d3; ++b) {
+          const double rhs = col < nu ? Cs[long(s) * d3 * d3 + col + b * d3] : E[long(s) * m * d3 + (col - nu) + b * m];
+          acc = fma(Mi[a + b * d3], rhs, acc);
+        }
+        Z[(long(s) * (nu + m) + col) * d3 + a] = acc;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < nu * nu; idx += NT) {  // S = D + sum_s C_s M^-1 C_s^T
+        const int i = idx % nu, j = idx / nu;
+        double acc = Dm[i + j * d3];
+        for (int s = 0; s < 3; ++s)
+          for (int a = 0; a < d3; ++a) acc = fma(Cs[long(s) * d3 * d3 + i + a * d3], Z[(long(s) * (nu + m) + j) * d3 + a], acc);
+        Sw[i + j * nu] = acc;
+        Si[i + j * nu] = i == j ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      cta_gauss(Sw, nu, nu, Si, nu, nu, diag, lm, red_v, red_i);
+      double* F = factors + K * FD;
+      for (int idx = tid; idx < nsym; idx += NT) {  // packed lower M^-1 and S^-1
+        int j = 0;
+        while (sym_idx(d3 - 1, j, d3) < idx) ++j;
+        const int i = j + (idx - sym_idx(j, j, d3));
+        F[idx] = Mi[i + j * d3];
+        F[nsym + idx] = (i < nu && j < nu) ? Si[i + j * nu] : (i == j ? 1.0 / (6.0 * sg[0]) : 0.0);
+      }
+      for (int idx = tid; idx < d3 * m; idx += NT) {  // V = tauDP^T + sum_s C_s M^-1 E_s^T (rows < nu)
+        const int i = idx % d3, r = idx / d3;
+        double acc = 0.0;
+        if (i < nu) {
+          acc = TDP[r + i * m];
+          for (int s = 0; s < 3; ++s)
+            for (int a = 0; a < d3; ++a)
+              acc = fma(Cs[long(s) * d3 * d3 + i + a * d3], Z[(long(s) * (nu + m) + nu + r) * d3 + a], acc);
+        }
+        F[2 * nsym + idx] = acc;
+      }
+      for (int i = tid; i < d3; i += NT) F[2 * nsym + long(d3) * m + i] = i < nu ? fl[i] : 0.0;
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace hdgb

@@ -325,10 +325,21 @@ class Engine:
         """NVRTC-specialised node build for program fields (default on)."""
         L.check(L.lib().hdg_b200_set_jit(self._ctx, int(enabled)))
 
-    def set_variant(self, variant: int) -> None:
-        """k = 2, 3 condensation kernel: 3 = CTA-batched (default), 4 = element-batched
-        tasks, 2 = per-element teams."""
-        L.check(L.lib().hdg_b200_set_variant(self._ctx, int(variant)))
+    def set_rescue_screen(self, screen: float) -> None:
+        """Pivot-ratio screen below which an element is re-solved by the reference's
+        partial-pivot LU path (kernels_rescue.cuh); >= 1 re-solves every element."""
+        L.check(L.lib().hdg_b200_set_rescue_screen(self._ctx, float(screen)))
+
+    def rescued_elements(self) -> int:
+        """Elements the last build_condense re-solved by the reference's LU path."""
+        n = C.c_int64(0)
+        L.check(L.lib().hdg_b200_rescued_elements(self._ctx, C.byref(n)))
+        return int(n.value)
+
+    def set_tau_allow_zero(self, enabled: bool) -> None:
+        """StabilizationField::allow_zero (element_matrices.hpp:24): accept tau == 0 on
+        all faces of an element (negative tau is always rejected, element_matrices.cpp:38-46)."""
+        L.check(L.lib().hdg_b200_set_tau_allow_zero(self._ctx, int(enabled)))
 
     def set_bdm(self, enabled: bool) -> None:
         """BDM variant (bdm_blocks, local_solver.cpp:65-69): u truncated to P_{k-1}, tau ignored."""

@@ -468,49 +468,24 @@ def test_two_slab_scatter_exchange_matches_global():
             assert np.array_equal(vals[seg], want)
 
 
-@pytest.mark.parametrize("k", [2, 3])
-def test_condense_variants_agree(k):
-    """CTA-batched (v3, default), element-batched (v4) and per-element-team (v2)
-    condensation kernels agree with each other and with the oracle; the mesh
-    size (3^3 x 6 = 162 tets) leaves partial batches."""
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+def test_condense_recover_perturbed(k):
+    """The default condensation kernel (CTA-batched phases at k = 2, 3; one
+    element per CTA iteration at k = 4, 5) and its recovery cache against the
+    oracle's LU path on a perturbed mesh; 162 tets leave partial batches and
+    > 148 CTAs' worth of iterations at k >= 4."""
     mesh = HostMesh.box(3, bc="dirichlet_x", perturb=0.1)
     em = oracle_mesh(mesh)
-    eng, dm, g, cs3 = gpu_pipeline(mesh, k, KAP, CC, FF)
-    out = {3: cs3}
-    for v in (2, 4):
-        eng.set_variant(v)
-        out[v] = eng.build_condense(g, KAP, CC, FF)
-    _, _, _, C, Cf = oracle_condense(em, k, KAP, CC, FF, 1.0)
-    for cs in out.values():
-        assert max_slice_relerr(np_(cs.C_slices()), C) < TOL
-        assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
-    for v in (2, 4):
-        assert max_slice_relerr(np_(out[v].factors.view(dm.nelt, -1)), np_(cs3.factors.view(dm.nelt, -1))) < 1e-12
-
-
-@pytest.mark.parametrize("k", [4, 5])
-def test_condense_v5_matches_triangular_kernel(k):
-    """k = 4, 5: the one-element-per-CTA explicit-inverse kernel (v5, default)
-    and the triangular-factor kernel (variant 1) agree with the oracle on C, Cf
-    and, each through its own recovery cache, on the recovered q, u; 162 tets
-    > 148 CTAs, so CTAs run more than one element."""
-    mesh = HostMesh.box(3, bc="dirichlet_x", perturb=0.1)
-    em = oracle_mesh(mesh)
-    eng, dm, g, cs5 = gpu_pipeline(mesh, k, KAP, CC, FF)
+    eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
     d2 = dim2(k)
     uhat = torch.from_numpy(np.sin(np.arange(dm.nfc * d2) * 0.37)).cuda()
-    ls5 = eng.recover(g, dm, cs5, uhat)
-    eng.set_variant(1)
-    cs1 = eng.build_condense(g, KAP, CC, FF)
-    ls1 = eng.recover(g, dm, cs1, uhat)
+    ls = eng.recover(g, dm, cs, uhat)
     _, _, lb, C, Cf = oracle_condense(em, k, KAP, CC, FF, 1.0)
-    for cs in (cs5, cs1):
-        assert max_slice_relerr(np_(cs.C_slices()), C) < TOL
-        assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
+    assert max_slice_relerr(np_(cs.C_slices()), C) < TOL
+    assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
     qx, qy, qz, u = core.local_recover(lb, core.gather_traces(em, d2, uhat.cpu().numpy()), 4)
-    for ls in (ls5, ls1):
-        for got, want in ((ls.qx, qx), (ls.qy, qy), (ls.qz, qz), (ls.u, u)):
-            assert max_slice_relerr(np_(got), want.T) < TOL
+    for got, want in ((ls.qx, qx), (ls.qy, qy), (ls.qz, qz), (ls.u, u)):
+        assert max_slice_relerr(np_(got), want.T) < TOL
 
 
 @pytest.mark.parametrize("k", [1, 2, 3])

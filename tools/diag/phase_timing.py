@@ -21,8 +21,6 @@ cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
 mesh = HostMesh.box(cfg.n, bc=cfg.problem.bc, perturb=cfg.perturb, seed=cfg.seed)
 eng = Engine(0)
 eng.set_degree(cfg.k)
-if len(sys.argv) > 2:
-    eng.set_variant(int(sys.argv[2]))
 dm = eng.upload(mesh)
 g = eng.geometry(dm, cfg.tau)
 for _ in range(3):

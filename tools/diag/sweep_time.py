@@ -1,5 +1,5 @@
 """Time K3 (build_condense) and K5 (recover) of a libhdg_b200 variant:
-sweep_time.py LIB CONFIG [condense variant]."""
+sweep_time.py LIB CONFIG."""
 import os
 import sys
 
@@ -17,8 +17,6 @@ cfg = CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "C2"]
 mesh = HostMesh.box(cfg.n, bc=cfg.problem.bc, perturb=cfg.perturb, seed=cfg.seed)
 eng = Engine(0)
 eng.set_degree(cfg.k)
-if len(sys.argv) > 3:
-    eng.set_variant(int(sys.argv[3]))
 dm = eng.upload(mesh)
 g = eng.geometry(dm, cfg.tau)
 eng.set_timing(True)
