@@ -512,6 +512,58 @@ PYBIND11_MODULE(_hdg_oracle, m) {
         },
         py::arg("em"), py::arg("t"), py::arg("kappa"), py::arg("c"), py::arg("f"), py::arg("tau"),
         py::arg("uhat"), py::arg("nthreads"), py::arg("chunk") = 1024);
+  // The reference path (build -> local_blocks -> condense -> local_recover) on
+  // the element range [k0, k1) of a full mesh, over nthreads contiguous
+  // sub-ranges: returns C (k1-k0, m, m), Cf (m, k1-k0), qx, qy, qz, u
+  // (d3, k1-k0). uhat: per-element stacked traces (4 d2, k1-k0). For parity
+  // over whole full-size meshes in bounded-memory chunks (tests).
+  m.def("pipeline_range",
+        [](const ExpandedMesh& em, const Tables& t, const Field& kappa, const Field& c, const Field& f,
+           const StabilizationField& tau, const DArr& uhat, int k0, int k1, int nthreads) {
+          const Mat U = mat_from(uhat);
+          const int ne = k1 - k0, d3 = t.tb.d3, m = 4 * t.tb.d2;
+          if (k0 < 0 || k1 > em.n_elements() || ne <= 0 || U.c != ne || U.r != m)
+            throw std::invalid_argument("pipeline_range: bad range or uhat shape");
+          Batch3 C(m, m, ne);
+          Mat Cf(m, ne), qx(d3, ne), qy(d3, ne), qz(d3, ne), u(d3, ne);
+          {
+            py::gil_scoped_release r;
+            auto rows = [](const auto& src, int a, int b, auto& dst) {
+              dst.r = b - a;
+              dst.c = src.c;
+              dst.a.resize(size_t(dst.r) * dst.c);
+              for (int j = 0; j < src.c; ++j)
+                std::memcpy(&dst.a[size_t(j) * dst.r], &src.a[size_t(a) + size_t(j) * src.r],
+                            sizeof(src.a[0]) * size_t(dst.r));
+            };
+            parallel_for(ne, nthreads, [&](int b, int e) {
+              ExpandedMesh s;
+              s.raw.coordinates = em.raw.coordinates;
+              s.faces = em.faces;
+              s.area = em.area;
+              rows(em.raw.elements, k0 + b, k0 + e, s.raw.elements);
+              rows(em.facebyele, k0 + b, k0 + e, s.facebyele);
+              rows(em.perm, k0 + b, k0 + e, s.perm);
+              rows(em.normals, k0 + b, k0 + e, s.normals);
+              s.volume.assign(em.volume.begin() + k0 + b, em.volume.begin() + k0 + e);
+              StabilizationField st = tau;
+              rows(tau.tau, k0 + b, k0 + e, st.tau);
+              Mat su(m, e - b);
+              std::memcpy(su.a.data(), U.col(b), sizeof(double) * size_t(m) * (e - b));
+              ElementMatrixSet ms = build_element_matrices(s, t.tb, t.tet, t.tri, kappa.f, c.f, f.f, st);
+              LocalBlocks lb = local_blocks(ms);
+              CondensedSystem cs = condense(lb, 1);
+              LocalSolution ls = local_recover(lb, su, 1);
+              std::memcpy(C.slice(b), cs.C.data.data(), cs.C.data.size() * sizeof(double));
+              std::memcpy(Cf.col(b), cs.Cf.a.data(), cs.Cf.a.size() * sizeof(double));
+              std::memcpy(qx.col(b), ls.qx.a.data(), ls.qx.a.size() * sizeof(double));
+              std::memcpy(qy.col(b), ls.qy.a.data(), ls.qy.a.size() * sizeof(double));
+              std::memcpy(qz.col(b), ls.qz.a.data(), ls.qz.a.size() * sizeof(double));
+              std::memcpy(u.col(b), ls.u.a.data(), ls.u.a.size() * sizeof(double));
+            });
+          }
+          return py::make_tuple(np_batch(C), np_mat(Cf), np_mat(qx), np_mat(qy), np_mat(qz), np_mat(u));
+        });
   m.def("time_pipeline",
         [](const ExpandedMesh& em, const Tables& t, const Field& kappa, const Field& c,
            const Field& f, const StabilizationField& tau, const DArr& uhat, int nthreads) {

@@ -11,7 +11,13 @@ from paper_1305_1489_b200.fields import compile_field
 
 
 def field(expr) -> "core.Field":
-    p = compile_field(expr)
+    try:
+        p = compile_field(expr)
+    except ValueError:  # beyond the device VM's limits (e.g. poly-k at k >= 4): a Python callback
+        import math
+        code = compile(str(expr), "<field>", "eval")
+        env = {n: getattr(math, n) for n in ("sin", "cos", "exp", "sqrt", "pi")}
+        return core.Field.python(lambda x, y, z: float(eval(code, env, {"x": x, "y": y, "z": z})))
     return core.Field.program(p.ops, p.consts)
 
 

@@ -380,17 +380,20 @@ def test_full_size_sampled_elements(cfg_name):
         assert max_slice_relerr(np_(us[idx]), want.T) < TOL
 
 
-def test_jit_and_interpreter_agree():
-    """NVRTC-specialised node build == interpreted field programs (both GPU paths)."""
-    k = 3
-    mesh = HostMesh.box(2, bc="dirichlet_x")
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_jit_and_interpreter_agree(k):
+    """NVRTC-specialised node build == interpreted field programs (both GPU paths)
+    at every block-size branch of the JIT kernel (256 threads below 100 nodes,
+    384 at k = 3, 1024 at k >= 4); 107 tets leave a partial last CTA."""
+    from test_gpu_ragged import first_tets
+    mesh = first_tets(107, 3)
     prob = CONFIGS["C2"].problem
     eng = Engine(0)
     eng.set_degree(k)
     dm = eng.upload(mesh)
     g = eng.geometry(dm, 1.0)
     cs_jit = eng.build_condense(g, prob.kappa, prob.c, prob.f)
-    assert eng.jit_status == "", eng.jit_status
+    assert eng.jit_status == "", eng.jit_status   # the compiled kernel ran (no silent fallback)
     eng.set_jit(False)
     cs_vm = eng.build_condense(g, prob.kappa, prob.c, prob.f)
     # fields differ only by FMA contraction in the compiled expressions (~1 ulp
@@ -544,3 +547,28 @@ def test_bdm_rejects_degree_zero():
     g = eng.geometry(dm, 0.0)
     with pytest.raises(HdgError, match="k >= 1"):
         eng.build_condense(g, KAP, CC, FF)
+
+
+def test_upwind_tau_independent():
+    """Config C4's tau = 1 + |beta(x_e) . nu_{K,l}| against a host
+    computation from the oracle's mesh: face centroid of local face l, unit
+    outward normal from the oracle's area-scaled normals (mesh.cpp:153-169)."""
+    cfg = CONFIGS["C4"]
+    mesh = HostMesh.box(3, bc="all_dirichlet", perturb=0.12, seed=3)
+    eng = Engine(0)
+    eng.set_degree(2)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 1.0)
+    tau = np_(eng.upwind_tau(g, cfg.upwind_beta))          # (4, nelt)
+    em = oracle_mesh(mesh)
+    X, el, nrm = em.coordinates, em.elements, em.normals
+    lf = [(0, 1, 2), (0, 1, 3), (0, 2, 3), (3, 1, 2)]
+    beta = lambda x, y, z: np.array([np.sin(np.pi * y), np.cos(np.pi * x), 0.5])
+    assert cfg.upwind_beta == ("sin(pi*y)", "cos(pi*x)", "0.5")
+    want = np.empty_like(tau)
+    for K in range(em.n_elements):
+        for l in range(4):
+            xc = X[el[K, list(lf[l])]].sum(axis=0) / 3.0
+            nu = nrm[K, 3 * l:3 * l + 3] / np.linalg.norm(nrm[K, 3 * l:3 * l + 3])
+            want[l, K] = 1.0 + abs(beta(*xc) @ nu)
+    assert np.max(np.abs(tau - want)) < 1e-13

@@ -68,7 +68,7 @@ def test_gauss_jacobi_against_numpy(n, alpha):
 
 
 # ----------------------------------------------------------------------- basis
-@pytest.mark.parametrize("k", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 4, 5])
 def test_basis_orthonormal(k):
     """tests/test_basis.cpp:33-49 + acceptance.cpp:253-267: Gram = 6I / 2I."""
     t = core.tables(k, 2 * k + 2, 2 * k + 2)
