@@ -94,12 +94,39 @@ def k2_flops(k: int, nq: int) -> float:
     return 2.0 * nsym * nq * 2 + 2.0 * nsym * 4 + 2.0 * d3 * nq
 
 
-def k3_bytes(k: int) -> float:
+def step_algorithmic_bytes(k: int, nq: int, sampled: bool) -> float:
+    """B = 2 x 164 (elements, coords, facebyele, perm for build and
+    for recover) + 3 nq 8 (kappa^-1, c, f samples; SAMPLED fields only)
+    + (m^2 + m) 8 (C, Cf written) + m 8 (lambda gathered) + 4 d3 8 (q, u written)."""
     d3 = (k + 1) * (k + 2) * (k + 3) // 6
     m = 2 * (k + 1) * (k + 2)
-    nsym = d3 * (d3 + 1) // 2
-    fac = 2 * nsym + d3 * m + d3
-    return 8.0 * (2 * nsym + d3 + 30 + m * m + m + fac)
+    return 2 * 164 + (3 * nq * 8 if sampled else 0) + (m * m + m) * 8 + m * 8 + 4 * d3 * 8
+
+
+STEP_KERNELS = ("face_area_kernel", "geometry_kernel", "reset_build_status", "tau_check", "quad_build",
+                "condense", "rescue_kernel", "recover")
+
+
+def ncu_step_traffic():
+    """DRAM bytes of one full-size step (sum over the step's kernels, each the
+    largest launch of its name) from the newest committed ncu launch list."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_launches.csv")))
+    if not files:
+        return None, None
+    best = {}
+    for line in open(files[-1]):
+        parts = line.strip().split(",")
+        if len(parts) < 5:
+            continue
+        try:
+            b = float(parts[3]) + float(parts[4])
+        except ValueError:
+            continue
+        for kn in STEP_KERNELS:
+            if kn in parts[1]:
+                best[kn] = max(best.get(kn, 0.0), b)
+    return (sum(best.values()) if best else None), os.path.relpath(files[-1], ROOT)
 
 
 # ------------------------------------------------------------------ clocks
@@ -248,6 +275,7 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     nthreads = os.cpu_count() or 1
     work = oracle_workload(cfg)
     from oracle import NATIVE
@@ -261,12 +289,13 @@ def run_reference(args):
     v = len(secs) * ne / tot
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot / len(secs), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * tot / len(secs), "higher_is_better": True, "scaling": args.split,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(cfg, 1),
+            "config": workload_config(cfg, world, args.split),
             "cpu_baseline": {"value": v, "unit": "elements/s", "cores": nthreads, "kind": "port",
                              "march_native": bool(NATIVE),
-                             "sample": f"{cfg.name}: the whole {cfg.n}^3 mesh ({ne} tets) per step, every stage of "
+                             "sample": f"{cfg.name}: the whole {cfg.n}^3 mesh ({ne} tets; at N > 1 weak, one GPU's "
+                                       f"slab) per step, every stage of "
                                        f"the reference path (build_element_matrices -> local_blocks -> condense -> "
                                        f"local_recover) over 1024-element chunks on {nthreads} threads; "
                                        f"lambda gathered outside the timed region"},
@@ -318,7 +347,13 @@ def run_ours(args):
     k = cfg.k
     n = cfg.n
     t_setup = time.perf_counter()
-    mesh = HostMesh.box(n, n, n * world, bc=prob.bc, perturb=cfg.perturb, seed=cfg.seed)
+    # weak: rank r owns z-slab r of an n x n x (n * world) box (fixed work per
+    # GPU); strong: the config's own n^3 mesh split into world z-slabs
+    # (BASELINE C5: "split into contiguous z-slabs over 1/2/4/8 B200")
+    nz = n * world if args.split == "weak" else n
+    if args.split == "strong" and n % world:
+        raise SystemExit(f"--split strong needs {world} to divide the {n} cell layers")
+    mesh = HostMesh.box(n, n, nz, bc=prob.bc, perturb=cfg.perturb, seed=cfg.seed)
     sl = partition.slab(mesh, rank, world)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(dev)
@@ -354,7 +389,9 @@ def run_ours(args):
         if cfg.postprocess:
             eng.postprocess_star(g, kap, ls, out=ustar)
 
-    launches_per_step = 2 + 1 + 1 + 1 + 1 + (1 if cfg.postprocess else 0)
+    # geometry 2 (face areas, per element); build_condense 5 (status reset, tau
+    # check, K2, K3, rescue screen); recover 1; postprocess 1 (+1 kappa sampler)
+    launches_per_step = 2 + 5 + 1 + (2 if cfg.postprocess else 0)
     eng.set_timing(True)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -400,12 +437,16 @@ def run_ours(args):
     # faces' diagonal blocks and b summed with the neighbour slabs.
     scatter_info = None
     if not args.no_scatter:
-        from paper_1305_1489_b200.distributed import SlabExchange
+        from paper_1305_1489_b200.distributed import NativeSlabExchange
         fb, nb, slt = partition.slab_pattern(sl)
         with torch.cuda.stream(stream):
             pat = eng.pattern_from_arrays(fb, nb, slt)
             sysH = eng.assemble(dm, pat, cs)
-            ex = SlabExchange(sl, fb, nb, d2, dev)
+            # the engine's own exchange: C-ABI plan, device gather/add, grouped
+            # ncclSend/ncclRecv per neighbour on the engine stream
+            ex = NativeSlabExchange(eng, sl, fb, nb, d2)
+            if world > 1:
+                ex.init_comm(rank, world)
             stream.synchronize()
             if world > 1:
                 dist.barrier()
@@ -422,11 +463,75 @@ def run_ours(args):
                 sc_ms.append(a0.elapsed_time(a1))
                 ex_ms.append(a1.elapsed_time(a2))
         eng.stage_times()
-        scatter_info = {"scatter_ms": float(np.median(sc_ms)), "exchange_ms": float(np.median(ex_ms)),
+        sc_med, ex_med = float(np.median(sc_ms)), float(np.median(ex_ms))
+        if world > 1:
+            t = torch.tensor([sc_med + ex_med], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            both = float(t.item())
+        else:
+            both = sc_med + ex_med
+        scatter_info = {"scatter_ms": sc_med, "exchange_ms": ex_med,
                         "nnz": int(sysH.vals.numel()), "interface_faces": int(len(sl.interface)),
-                        "exchange_bytes": int(sum(v[0].numel() + v[1].numel() for v in ex.peers.values()) * 8),
-                        "scatter_hbm_gbs": 2 * 8.0 * (4 * d2) * (4 * d2 + 1) * nelt / (np.median(sc_ms) / 1e3) / 1e9}
+                        "exchange_bytes": int(sum(ex.entries) * 8),
+                        "exchange": "hdg_b200_exchange_interface (NCCL grouped send/recv)" if world > 1 else "none (1 rank)",
+                        "with_scatter": {"value": world * nelt / ((ms_per_step + both) / 1e3), "unit": "elements/s",
+                                         "ms_per_step": ms_per_step + both,
+                                         "note": "step + K4 scatter + interface exchange, max over ranks"},
+                        # C and Cf read once, every CSR value and b entry written once
+                        "scatter_bytes": 8.0 * ((4 * d2) * (4 * d2 + 1) * nelt + sysH.vals.numel() + sysH.b.numel()),
+                        }
+        scatter_info["scatter_hbm_gbs"] = scatter_info["scatter_bytes"] / (sc_med / 1e3) / 1e9
         del sysH, pat
+
+    # ------------------------------------------------------- SAMPLED leg
+    # The reference's own API shape (ScalarField callbacks, coefficient.hpp:
+    # 13-14): the caller samples its callbacks at the device's physical nodes
+    # (hdg_b200_quad_points; here torch expressions of the same fields) and
+    # passes HDG_FIELD_SAMPLED arrays, which K2 reads (3 nq 8 B per element).
+    # Timed: geometry, quad points, the caller's callbacks, build+condense,
+    # recover.
+    sampled_info = None
+    if not args.no_sampled and not cfg.upwind_beta:
+        import math
+        env = {"sin": torch.sin, "cos": torch.cos, "exp": torch.exp, "sqrt": torch.sqrt, "abs": torch.abs,
+               "pi": math.pi, "lt": lambda a, b: (a < b).double(), "pow": torch.pow}
+        cb = [compile(e, "<field>", "eval") for e in (prob.kappa, prob.c, prob.f)]
+
+        def callbacks(X, Y, Z):
+            loc = {"x": X, "y": Y, "z": Z}
+            return [torch.as_tensor(eval(c_, env, loc), dtype=torch.float64, device=dev).expand_as(X).contiguous()
+                    for c_ in cb]
+
+        def sampled_step():
+            eng.geometry(dm, tau, out=g)
+            X, Y, Z = eng.quad_points(g)
+            sk, sc_, sf = callbacks(X, Y, Z)
+            eng.build_condense(g, Field.sampled(sk), Field.sampled(sc_), Field.sampled(sf), out=cs, work=work,
+                               check=False)
+            eng.recover(g, dm, cs, uhat, out=ls)
+
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                sampled_step()
+            sms = []
+            for _ in range(max(1, min(args.steps, 5))):
+                flush.zero_()
+                b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                b0.record(stream)
+                sampled_step()
+                b1.record(stream)
+                b1.synchronize()
+                sms.append(b0.elapsed_time(b1))
+        eng.stage_times()
+        smed = float(np.median(sms))
+        if world > 1:
+            t = torch.tensor([smed], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            smed = float(t.item())
+        sampled_info = {"value": world * nelt / (smed / 1e3), "unit": "elements/s", "ms_per_step": smed,
+                        "path": "hdg_b200_quad_points -> caller's torch callbacks at the nodes -> HDG_FIELD_SAMPLED "
+                                "build_condense -> recover",
+                        "sample_bytes_per_element": 3 * nq * 8}
 
     # ---------------------------------------------------------------- e2e
     # Through the public API with HOST buffers: H2D of the step's inputs (mesh
@@ -512,14 +617,25 @@ def run_ours(args):
     k3_ms = stage_ms.get("condense", float("nan"))
     achieved = k3_flops(k) * nelt / (k3_ms / 1e3) / 1e12
     kname3 = f"condense3_kernel<{k}>" if k in (2, 3) else (f"condense2_kernel<{k}>" if k <= 1 else
-                                                           f"condense_kernel<{k}>")
+                                                           f"condense5_kernel<{k}>")
     traffic, traffic_src = ncu_traffic(kname3)
     roof = {"kernel": f"{kname3} (K3)", "bound": "tensor", "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
             "traffic": traffic if cfg.name == "C2" and world == 1 else None,
-            "traffic_source": traffic_src, "algorithmic_bytes": k3_bytes(k) * nelt,
+            "traffic_source": traffic_src,
             "peak_source": FP64_PEAK_SOURCE, "flops_per_element": k3_flops(k),
+            "flops_per_launch": k3_flops(k) * nelt, "launch_ms": k3_ms,
             "pipe": "fp64 (DMMA mma.sync m8n8k4)"}
+    # SURVEY §8(d) compulsory HBM bytes of the whole step (mesh + geometry for
+    # build and for recover, coefficient samples when SAMPLED, C + Cf written,
+    # lambda gathered, q + u written); caches and intermediates are not
+    # algorithmic. The fields here are PROGRAMs evaluated at the nodes (no sample reads).
+    alg = step_algorithmic_bytes(k, nq, sampled=False) * nelt
+    step_dram, step_src = ncu_step_traffic()
+    traffic_info = {"algorithmic_bytes": alg, "algorithmic_bytes_per_element": alg / nelt,
+                    "dram_bytes": step_dram if cfg.name == "C2" and world == 1 else None, "source": step_src,
+                    "dram_over_algorithmic": (step_dram / alg) if (step_dram and cfg.name == "C2" and world == 1) else None,
+                    "algorithmic_gbs": alg / (ms_per_step / 1e3) / 1e9, "hbm_peak_gbs": hbm_peak}
     kern = {}
     for kname, v in stage_ms.items():
         kern[kname] = {"ms": v}
@@ -527,24 +643,23 @@ def run_ours(args):
         kern["node_build"]["tflops"] = k2_flops(k, nq) * nelt / (stage_ms["node_build"] / 1e3) / 1e12
     if "condense" in stage_ms:
         kern["condense"]["tflops"] = achieved
-        kern["condense"]["hbm_gbs"] = k3_bytes(k) * nelt / (stage_ms["condense"] / 1e3) / 1e9
     if "recover" in stage_ms:
         rb = 8.0 * (dims["factors"] + 4 * d2 + 30 + 4 * d3)
         kern["recover"]["hbm_gbs"] = rb * nelt / (stage_ms["recover"] / 1e3) / 1e9
         kern["recover"]["hbm_frac"] = kern["recover"]["hbm_gbs"] / hbm_peak
     line = {
         "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.split,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (closed-form fields at the nodes, BASELINE configs)",
-        "config": {"workload": f"{cfg.name}: k={k}, {n}x{n}x{n * world} Kuhn box, {nelt} tets/GPU ({cfg.note})",
-                   "k": k, "tets_per_gpu": nelt, "parallelism": f"z-slabs x{world}",
-                   "l2": "flushed (512 MB write) between timed steps; per-step working set > 1 GB"},
+        "config": workload_config(cfg, world, args.split),
         "roofline": roof,
+        "traffic": traffic_info,
         "kernels_ms": kern,
         "e2e": {"value": world * nelt / (e2e_ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "chunks": E2E_CHUNKS,
                 "path": "pinned host mesh+lambda -> C ABI step in 4 element chunks, D2H of chunk i overlapped with chunk i+1 -> pinned host C, Cf, q, u"},
         "scatter": scatter_info,
+        "sampled_fields": sampled_info,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "setup_s": t_setup,
@@ -567,8 +682,11 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--split", default="weak", choices=["weak", "strong"],
+                    help="multi-GPU: weak = an n^3 slab per GPU, strong = the config's n^3 mesh split in z-slabs")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sampled", action="store_true", help="skip the HDG_FIELD_SAMPLED leg")
     ap.add_argument("--no-scatter", action="store_true",
                     help="skip the separately reported K4 scatter + interface exchange timing")
     args = ap.parse_args()

@@ -202,6 +202,45 @@ int hdg_b200_postprocess(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_fiel
                          const double* d_qx, const double* d_qy, const double* d_qz,
                          const double* d_u, double* d_ustar);
 
+/* ------------------------------------- interface exchange (multi-GPU)
+ * Elements are split into contiguous z-slabs, one per rank; each rank
+ * scatters its slab into a slab-local CSR (faces it touches, global order).
+ * Two tets share at most one face, so the only entries two slabs share are
+ * the interface faces' d2 x d2 diagonal blocks of H and their d2 entries of b:
+ * the reference's assemble sums both sides' triplets (global_system.cpp:
+ * 31-56, setFromTriplets at :53-54). A plan lists, per neighbour rank, the
+ * interface faces (slab-local ids, ascending global order, so both sides pair
+ * entry by entry); exchange_interface gathers those entries, runs one grouped
+ * ncclSend/ncclRecv per neighbour on the context stream and adds what it
+ * receives: both ranks end with a + b == b + a, bit-identical to one GPU.
+ * NCCL failures return HDG_ENCCL. NCCL is loaded at run time (libnccl.so.2).
+ * exchange_positions: the plan's positions for one face list (host only):
+ *   nfaces*d2*d2 value positions (face-major, block row-major), then
+ *   nfaces*d2 positions in b.
+ * exchange_pack / unpack_add: the gather and the add of one peer's entries
+ *   (what exchange_interface does around the transport), for callers with
+ *   their own transport.                                                  */
+typedef struct hdg_exchange hdg_exchange;
+int hdg_b200_exchange_positions(int nfc, int d2, const int64_t* h_facebase, const int* h_nbr, int nfaces,
+                                const int* h_faces, int64_t* h_pos);
+int hdg_b200_exchange_plan(hdg_ctx* ctx, int nfc, int d2, const int64_t* h_facebase, const int* h_nbr,
+                           int npeers, const int* h_peer_rank, const int* h_peer_nfaces,
+                           const int* h_faces /* concatenated per peer */, hdg_exchange** out);
+void hdg_b200_exchange_free(hdg_exchange* plan);
+int hdg_b200_exchange_pack(hdg_ctx* ctx, const hdg_exchange* plan, int peer, const double* d_vals,
+                           const double* d_b, double* d_buf);
+int hdg_b200_exchange_unpack_add(hdg_ctx* ctx, const hdg_exchange* plan, int peer, const double* d_buf,
+                                 double* d_vals, double* d_b);
+/* nccl_comm: an ncclComm_t (from hdg_b200_nccl_comm_init or the caller's own). */
+int hdg_b200_exchange_interface(hdg_ctx* ctx, const hdg_exchange* plan, void* nccl_comm, double* d_vals,
+                                double* d_b);
+/* NCCL communicator plumbing without NCCL types: rank 0 makes the 128-byte
+ * unique id, the caller broadcasts it (e.g. torch.distributed), every rank
+ * initialises on the context's device.                                     */
+int hdg_b200_nccl_get_unique_id(unsigned char id[128]);
+int hdg_b200_nccl_comm_init(hdg_ctx* ctx, int nranks, int rank, const unsigned char id[128], void** comm);
+int hdg_b200_nccl_comm_destroy(void* comm);
+
 /* ------------------------------------------------ device mesh setup
  * expand_device: mesh.cpp:74-171 on the GPU, bit-exact with
  * hdg_b200_mesh_expand (face numbering, parametrisation, facetype,
@@ -316,10 +355,11 @@ int hdg_b200_quad_points(hdg_ctx* ctx, int nelt, const hdg_geometry* g, int whic
 
 /* Per-kernel timing with CUDA events recorded on the context stream around each
  * stage. Stages: 0 geometry (K1), 1 node build (K2), 2 condense (K3),
- * 3 recover (K5), 4 scatter (K4), 5 postprocess (K6). stage_times waits for
+ * 3 recover (K5), 4 scatter (K4), 5 postprocess (K6), 6 rescue screen (K3b,
+ * kernels_rescue.cuh). stage_times waits for
  * the last recorded event of each stage and returns its duration in ms (-1 if
  * the stage did not run since the previous query).                        */
-#define HDG_NSTAGES 6
+#define HDG_NSTAGES 7
 int hdg_b200_set_timing(hdg_ctx* ctx, int enabled);
 int hdg_b200_stage_times(hdg_ctx* ctx, double ms[HDG_NSTAGES]);
 

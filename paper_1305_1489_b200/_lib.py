@@ -15,7 +15,7 @@ HDG_OK, HDG_ESINGULAR, HDG_EINVAL, HDG_ECUDA, HDG_ENCCL, HDG_EMESH, HDG_ESTATE, 
 FIELD_CONST, FIELD_SAMPLED, FIELD_PROGRAM = 0, 1, 2
 BC = {"all_dirichlet": 0, "dirichlet_top_bottom": 1, "dirichlet_x": 2}
 MESH_COORDS, MESH_ELEMENTS, MESH_DIRICHLET, MESH_NEUMANN, MESH_FACES, MESH_FACETYPE, MESH_FACEBYELE = range(7)
-STAGES = ("geometry", "node_build", "condense", "recover", "scatter", "postprocess")
+STAGES = ("geometry", "node_build", "condense", "recover", "scatter", "postprocess", "rescue")
 TABLES = dict(tet_bary=0, tet_w=1, P=2, Chat=3, Wlm=4, PP=5, DD=6, tri_bary=7, tri_w=8)
 
 P = C.c_void_p
@@ -134,6 +134,15 @@ _SIGS = {
     "hdg_b200_skeleton_project": (C.c_int, [P, C.c_int, P, C.c_int, P, hdg_field, P]),
     "hdg_b200_neumann_load": (C.c_int, [P, C.c_int, P, C.c_int, P, C.c_int, P, C.POINTER(hdg_geometry),
                                         C.c_int, C.c_int, hdg_field, hdg_field, hdg_field, C.c_double, P]),
+    "hdg_b200_exchange_positions": (C.c_int, [C.c_int, C.c_int, P, P, C.c_int, P, P]),
+    "hdg_b200_exchange_plan": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_int, P, P, P, C.POINTER(P)]),
+    "hdg_b200_exchange_free": (None, [P]),
+    "hdg_b200_exchange_pack": (C.c_int, [P, P, C.c_int, P, P, P]),
+    "hdg_b200_exchange_unpack_add": (C.c_int, [P, P, C.c_int, P, P, P]),
+    "hdg_b200_exchange_interface": (C.c_int, [P, P, P, P, P]),
+    "hdg_b200_nccl_get_unique_id": (C.c_int, [P]),
+    "hdg_b200_nccl_comm_init": (C.c_int, [P, C.c_int, C.c_int, P, C.POINTER(P)]),
+    "hdg_b200_nccl_comm_destroy": (C.c_int, [P]),
     "hdg_b200_jit_status": (C.c_char_p, [P]),
     "hdg_b200_synchronize": (C.c_int, [P]),
 }

@@ -26,6 +26,7 @@
 #include "kernels_errors.cuh"
 #include "kernels_post2.cuh"
 #include "kernels_rescue.cuh"
+#include "exchange.cuh"
 #include "jit_quad.hpp"
 #include "mesh_dev.hpp"
 
@@ -996,12 +997,14 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     double* ps = work + pivstat_offset(t, nelt);
     stage_begin(c, 2);
     DISPATCH_K(t.k, launch_condense, c, nelt, geo_b, Ms, Ds, fv, d_C, d_Cf, d_factors, ps);
+    stage_end(c, 2);
+    stage_begin(c, 6);
     {
       DevTab td = t;
       if (c->bdm) td.nu = td.d3 - td.d2;
       launch_rescue(c, nelt, td, geo_b, Ms, Ds, fv, ps, d_C, d_Cf, d_factors);
     }
-    stage_end(c, 2);
+    stage_end(c, 6);
     check_bad(c, bad_element);
   });
 }
@@ -1521,6 +1524,173 @@ int hdg_b200_set_recover_variant(hdg_ctx* c, int variant) {
   return guarded([&] {
     require(c != nullptr && (variant == 2 || variant == 3), HDG_EINVAL, "recover variant must be 2 or 3");
     c->recover_variant = variant;
+  });
+}
+
+// ------------------------------------------- interface exchange (§8(e))
+}  // extern "C"
+
+struct hdg_exchange {
+  int device = 0;
+  int d2 = 0;
+  struct Peer {
+    int rank = 0, nfaces = 0;
+    long n = 0, nv = 0;           // entries, of which value positions
+    int64_t* idx = nullptr;       // device positions (values | b)
+    double* send = nullptr;       // device staging
+    double* recv = nullptr;
+  };
+  std::vector<Peer> peers;
+  ~hdg_exchange() {
+    cudaSetDevice(device);
+    for (auto& p : peers) {
+      if (p.idx) cudaFree(p.idx);
+      if (p.send) cudaFree(p.send);
+      if (p.recv) cudaFree(p.recv);
+    }
+  }
+};
+
+namespace {
+void require_nccl() {
+  const NcclApi& a = nccl_api();
+  if (!a.ok) throw HdgError{HDG_ENCCL, a.why};
+}
+void nccl_ok(int rc, const char* what) {
+  if (rc != 0) throw HdgError{HDG_ENCCL, std::string(what) + ": " + nccl_api().errorString(rc)};
+}
+int exchange_grid(const hdg_ctx* c, long n) { return int(std::max<long>(1, std::min<long>((n + 255) / 256, c->sms * 4L))); }
+}  // namespace
+
+extern "C" {
+
+int hdg_b200_exchange_positions(int nfc, int d2, const int64_t* h_facebase, const int* h_nbr, int nfaces,
+                                const int* h_faces, int64_t* h_pos) {
+  return guarded([&] {
+    require(nfc > 0 && d2 > 0 && h_facebase && h_nbr && nfaces >= 0 && (nfaces == 0 || (h_faces && h_pos)),
+            HDG_EINVAL, "bad argument");
+    std::vector<int64_t> pos;
+    std::string err;
+    require(interface_positions(nfc, d2, h_facebase, h_nbr, nfaces, h_faces, pos, &err), HDG_EINVAL, err);
+    std::copy(pos.begin(), pos.end(), h_pos);
+  });
+}
+
+int hdg_b200_exchange_plan(hdg_ctx* c, int nfc, int d2, const int64_t* h_facebase, const int* h_nbr, int npeers,
+                           const int* h_peer_rank, const int* h_peer_nfaces, const int* h_faces,
+                           hdg_exchange** out) {
+  return guarded([&] {
+    require(c && out && nfc > 0 && d2 > 0 && h_facebase && h_nbr && npeers >= 0 &&
+                (npeers == 0 || (h_peer_rank && h_peer_nfaces && h_faces)),
+            HDG_EINVAL, "bad argument");
+    set_device(c);
+    auto plan = std::make_unique<hdg_exchange>();
+    plan->device = c->device;
+    plan->d2 = d2;
+    const int* fp = h_faces;
+    for (int q = 0; q < npeers; ++q) {
+      hdg_exchange::Peer p;
+      p.rank = h_peer_rank[q];
+      p.nfaces = h_peer_nfaces[q];
+      require(p.nfaces >= 0, HDG_EINVAL, "negative interface face count");
+      std::vector<int64_t> pos;
+      std::string err;
+      require(interface_positions(nfc, d2, h_facebase, h_nbr, p.nfaces, fp, pos, &err), HDG_EINVAL, err);
+      fp += p.nfaces;
+      p.n = long(pos.size());
+      p.nv = long(p.nfaces) * d2 * d2;
+      if (p.n) {
+        CUDA_OK(cudaMalloc(&p.idx, size_t(p.n) * sizeof(int64_t)));
+        CUDA_OK(cudaMalloc(&p.send, size_t(p.n) * sizeof(double)));
+        CUDA_OK(cudaMalloc(&p.recv, size_t(p.n) * sizeof(double)));
+        CUDA_OK(cudaMemcpy(p.idx, pos.data(), size_t(p.n) * sizeof(int64_t), cudaMemcpyHostToDevice));
+      }
+      plan->peers.push_back(p);
+    }
+    *out = plan.release();
+  });
+}
+
+void hdg_b200_exchange_free(hdg_exchange* plan) { delete plan; }
+
+int hdg_b200_exchange_pack(hdg_ctx* c, const hdg_exchange* plan, int peer, const double* d_vals, const double* d_b,
+                           double* d_buf) {
+  return guarded([&] {
+    require(c && plan && peer >= 0 && peer < int(plan->peers.size()) && d_vals && d_b && d_buf, HDG_EINVAL,
+            "bad argument");
+    set_device(c);
+    const auto& p = plan->peers[peer];
+    if (!p.n) return;
+    exchange_pack_kernel<<<exchange_grid(c, p.n), 256, 0, c->stream>>>(p.n, p.idx, d_vals, p.nv, d_b, d_buf);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_exchange_unpack_add(hdg_ctx* c, const hdg_exchange* plan, int peer, const double* d_buf,
+                                 double* d_vals, double* d_b) {
+  return guarded([&] {
+    require(c && plan && peer >= 0 && peer < int(plan->peers.size()) && d_vals && d_b && d_buf, HDG_EINVAL,
+            "bad argument");
+    set_device(c);
+    const auto& p = plan->peers[peer];
+    if (!p.n) return;
+    exchange_unpack_add_kernel<<<exchange_grid(c, p.n), 256, 0, c->stream>>>(p.n, p.idx, d_buf, p.nv, d_vals, d_b);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_exchange_interface(hdg_ctx* c, const hdg_exchange* plan, void* comm, double* d_vals, double* d_b) {
+  return guarded([&] {
+    require(c && plan && d_vals && d_b, HDG_EINVAL, "bad argument");
+    set_device(c);
+    if (plan->peers.empty()) return;
+    require(comm != nullptr, HDG_EINVAL, "NULL communicator");
+    require_nccl();
+    const NcclApi& a = nccl_api();
+    for (const auto& p : plan->peers)
+      if (p.n) exchange_pack_kernel<<<exchange_grid(c, p.n), 256, 0, c->stream>>>(p.n, p.idx, d_vals, p.nv, d_b, p.send);
+    CUDA_OK(cudaGetLastError());
+    nccl_ok(a.groupStart(), "ncclGroupStart");
+    for (const auto& p : plan->peers) {
+      if (!p.n) continue;
+      nccl_ok(a.send(p.send, size_t(p.n), kNcclDouble, p.rank, comm, c->stream), "ncclSend");
+      nccl_ok(a.recv(p.recv, size_t(p.n), kNcclDouble, p.rank, comm, c->stream), "ncclRecv");
+    }
+    nccl_ok(a.groupEnd(), "ncclGroupEnd");
+    for (const auto& p : plan->peers)
+      if (p.n)
+        exchange_unpack_add_kernel<<<exchange_grid(c, p.n), 256, 0, c->stream>>>(p.n, p.idx, p.recv, p.nv, d_vals,
+                                                                                 d_b);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int hdg_b200_nccl_get_unique_id(unsigned char id[128]) {
+  return guarded([&] {
+    require(id != nullptr, HDG_EINVAL, "NULL id");
+    require_nccl();
+    NcclApi::UniqueId u;
+    nccl_ok(nccl_api().getUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, u.internal, 128);
+  });
+}
+
+int hdg_b200_nccl_comm_init(hdg_ctx* c, int nranks, int rank, const unsigned char id[128], void** comm) {
+  return guarded([&] {
+    require(c && id && comm && nranks > 0 && rank >= 0 && rank < nranks, HDG_EINVAL, "bad argument");
+    set_device(c);
+    require_nccl();
+    NcclApi::UniqueId u;
+    std::memcpy(u.internal, id, 128);
+    nccl_ok(nccl_api().commInitRank(comm, nranks, u, rank), "ncclCommInitRank");
+  });
+}
+
+int hdg_b200_nccl_comm_destroy(void* comm) {
+  return guarded([&] {
+    if (!comm) return;
+    require_nccl();
+    nccl_ok(nccl_api().commDestroy(comm), "ncclCommDestroy");
   });
 }
 

@@ -358,7 +358,7 @@ class Engine:
 
     def stage_times(self) -> dict:
         """ms per stage since the last query (CUDA events on the engine stream)."""
-        ms = (C.c_double * 6)()
+        ms = (C.c_double * len(L.STAGES))()
         L.check(L.lib().hdg_b200_stage_times(self._ctx, ms))
         return {n: ms[i] for i, n in enumerate(L.STAGES) if ms[i] >= 0}
 

@@ -109,3 +109,19 @@ def test_two_rank_interface_exchange_gloo():
     ret = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), ret), nprocs=2, join=True)
     assert dict(ret) == {0: 1, 1: 1}
+
+
+def test_native_interface_positions_match_host_logic():
+    """hdg_b200_exchange_positions (the C-ABI plan's index sets) == the Python
+    restatement used by the gloo exchange, for every slab of a 4-way split."""
+    from paper_1305_1489_b200.distributed import _diag_indices, interface_positions
+    mesh = HostMesh.box(N, N, 4 * N, bc="dirichlet_x")
+    for k in (1, 3):
+        d2 = (k + 1) * (k + 2) // 2
+        for r in range(4):
+            s = slab(mesh, r, 4)
+            fb, nb, _ = slab_pattern(s)
+            for q in np.unique(s.interface_rank):
+                faces = s.interface[s.interface_rank == q]
+                iv, ib = _diag_indices(fb, nb, faces, d2)
+                assert np.array_equal(interface_positions(fb, nb, faces, d2), np.concatenate([iv, ib]))

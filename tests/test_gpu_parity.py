@@ -427,21 +427,26 @@ def test_jit_field_emitter_vs_oracle(kap, c, f):
     assert max_slice_relerr(np_(cs.Cf_cols()), Cf.T) < TOL
 
 
-def test_two_slab_scatter_exchange_matches_global():
+@pytest.mark.parametrize("nslabs,native", [(2, False), (2, True), (4, True)])
+def test_two_slab_scatter_exchange_matches_global(nslabs, native):
     """z-slab scatter on the GPU (K4 into slab-local CSR) + interface exchange
-    == the single-mesh GPU assembly, bit for bit."""
-    from paper_1305_1489_b200.distributed import SlabExchange, exchange_local
+    == the single-mesh GPU assembly, bit for bit. native: the
+    C-ABI plan's gather / add kernels (hdg_b200_exchange_pack / _unpack_add,
+    what hdg_b200_exchange_interface runs around its NCCL calls), the
+    transport a device copy; 4 slabs give the middle ranks two neighbours."""
+    from paper_1305_1489_b200.distributed import (NativeSlabExchange, SlabExchange, exchange_local,
+                                                  exchange_local_native)
     from paper_1305_1489_b200.partition import slab, slab_pattern, upload_slab
     k = 2
-    mesh = HostMesh.box(3, 3, 6, bc="dirichlet_x")
+    mesh = HostMesh.box(3, 3, 2 * nslabs, bc="dirichlet_x")
     eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
     pat = eng.pattern(mesh)
     full = eng.assemble(dm, pat, cs)
     d2 = dim2(k)
     m = 4 * d2
     exs, systems, slabs = [], [], []
-    for r in range(2):
-        s = slab(mesh, r, 2)
+    for r in range(nslabs):
+        s = slab(mesh, r, nslabs)
         fb, nb, sl = slab_pattern(s)
         sdm = upload_slab(s, torch.device("cuda"))
         sp_ = eng.pattern_from_arrays(fb, nb, sl)
@@ -450,10 +455,10 @@ def test_two_slab_scatter_exchange_matches_global():
         scs = CondensedSystem(cs.C[s.elem_begin * m * m:s.elem_end * m * m], cs.Cf[s.elem_begin * m:s.elem_end * m],
                               None, m)
         ssys = eng.assemble(sdm, sp_, scs)
-        exs.append(SlabExchange(s, fb, nb, d2, torch.device("cuda")))
+        exs.append(NativeSlabExchange(eng, s, fb, nb, d2) if native else SlabExchange(s, fb, nb, d2, torch.device("cuda")))
         systems.append((ssys.vals, ssys.b))
         slabs.append((s, fb, nb, ssys))
-    exchange_local(exs, systems)
+    (exchange_local_native if native else exchange_local)(exs, systems)
     import scipy.sparse as sp
     nd = dm.nfc * d2
     H = sp.csr_matrix((np_(full.vals), np_(full.colidx), np_(full.rowptr)), shape=(nd, nd))
