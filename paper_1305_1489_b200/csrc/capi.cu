@@ -256,6 +256,7 @@ struct hdg_ctx {
   bool jit = true;          // NVRTC-specialised K2 for program fields
   bool bdm = false;         // bdm_blocks variant (hdg_b200_set_bdm)
   bool tau_allow_zero = false;  // StabilizationField::allow_zero (element_matrices.hpp:24)
+  bool build_status_pending = false;  // last build_condense's status not yet reported
   double rescue_screen = 1e-12; // pivot-ratio screen of the rescue kernel (kernels_rescue.cuh)
   double* d_rescue = nullptr;   // rescue kernel scratch
   size_t rescue_len = 0;
@@ -441,6 +442,7 @@ void check_bad(hdg_ctx* c, int64_t* bad_element) {
   if (!bad_element) return;
   CUDA_OK(cudaMemcpyAsync(c->h_bad, c->d_bad, 3 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OK(cudaStreamSynchronize(c->stream));
+  c->build_status_pending = false;
   raise_build_status(c, bad_element);
 }
 
@@ -942,6 +944,7 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     set_device(c);
     const DevTab& t = c->tab[0].dev;
     reset_build_status_kernel<<<1, 32, 0, c->stream>>>(c->d_bad);
+    c->build_status_pending = true;
     tau_check_kernel<<<int(std::min<long>((long(nelt) + 255) / 256, long(c->sms) * 4)), 256, 0, c->stream>>>(
         nelt, geo.T, c->d_bad);
     GeoDev geo_b = geo;
@@ -1711,8 +1714,12 @@ int hdg_b200_synchronize(hdg_ctx* c) {
             "element " + std::to_string(c->h_status[0]) + " has non-positive orientation");
     require(c->h_status[1] == INT_MAX, HDG_EMESH, "face vertex triples do not match as sets");
     // deferred status of the last build_condense run without bad_element
-    CUDA_OK(cudaMemcpy(c->h_bad, c->d_bad, 3 * sizeof(long long), cudaMemcpyDeviceToHost));
-    raise_build_status(c, nullptr);
+    // (reported once)
+    if (c->build_status_pending) {
+      CUDA_OK(cudaMemcpy(c->h_bad, c->d_bad, 3 * sizeof(long long), cudaMemcpyDeviceToHost));
+      c->build_status_pending = false;
+      raise_build_status(c, nullptr);
+    }
   });
 }
 
