@@ -16,7 +16,6 @@
 //     (global_system.hpp:55-56,                    -> LocalSolution {qx,qy,qz,u}
 //     local_solver.hpp:58-59)
 //   postprocess_star (postprocess.hpp:26-28)     postprocess_star(level, kappa, ls)
-//   assemble (global_system.hpp:31)              assemble(level, cs)
 //   LocalSolverError{element}                    LocalSolverError{element}
 //     (local_solver.hpp:45-49)
 //   MeshError (mesh.hpp:75-78)                   MeshError
@@ -278,9 +277,9 @@ inline CondensedSystem condense(Level& lv, const ScalarField& kappa, const Scala
   cs.factors = DeviceArray<double>(size_t(n) * size_t(dims[5]));
   int64_t bad = -1;
   const hdg_geometry g = lv.geometry();
-  check(hdg_b200_build_condense(lv.ctx(), n, &g, sampled(sk), sampled(sc), sampled(sf), cs.d_C.get(),
-                                cs.d_Cf.get(), cs.factors.get(), nullptr, &bad),
-        bad);
+  const int st = hdg_b200_build_condense(lv.ctx(), n, &g, sampled(sk), sampled(sc), sampled(sf), cs.d_C.get(),
+                                         cs.d_Cf.get(), cs.factors.get(), nullptr, &bad);
+  check(st, bad);  // (bad is set by the call: not an argument of the same expression)
   cs.C = Batch3(m, m, n);
   cs.Cf = Matrix(m, n);
   cs.d_C.download(cs.C.data.data());

@@ -158,7 +158,9 @@ int hdg_b200_upwind_tau(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_field
  * local_blocks (local_solver.cpp:124-126) -> condense (local_solver.cpp:71-100)
  * as one call returning the same CondensedSystem: C (m x m x nelt Batch3) and
  * Cf (m x nelt), m = 4*d2. d_factors (nullable) receives the per-element
- * recovery cache used by hdg_b200_recover (dims[5] doubles per element).
+ * recovery cache used by hdg_b200_recover (dims[5] doubles per element:
+ * M^-1 packed lower, Vs = S^-1 V (d3 x m), fs = S^-1 f, padded to 16 bytes;
+ * the reference refactorises A1 in local_recover instead).
  * d_work: scratch of hdg_b200_work_size() bytes.                           */
 int64_t hdg_b200_work_size(const hdg_ctx* ctx, int nelt);
 int hdg_b200_build_condense(hdg_ctx* ctx, int nelt, const hdg_geometry* g, hdg_field kappa,

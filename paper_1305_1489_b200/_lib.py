@@ -10,6 +10,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhdg_b200.so")
+_DEFAULT_LIB = LIB_PATH
 
 HDG_OK, HDG_ESINGULAR, HDG_EINVAL, HDG_ECUDA, HDG_ENCCL, HDG_EMESH, HDG_ESTATE, HDG_ESOLVE = range(8)
 FIELD_CONST, FIELD_SAMPLED, FIELD_PROGRAM = 0, 1, 2
@@ -158,7 +159,10 @@ def lib() -> C.CDLL:
             raise ImportError(f"{LIB_PATH} is missing: build the CUDA extension first "
                               "(python -c 'import __graft_entry__ as g; g.build()')")
         handle = C.CDLL(LIB_PATH)
+        diag = LIB_PATH != _DEFAULT_LIB  # an older diagnostics build may lack newer entry points
         for name, (res, args) in _SIGS.items():
+            if diag and not hasattr(handle, name):
+                continue
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

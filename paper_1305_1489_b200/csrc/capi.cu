@@ -301,9 +301,11 @@ void* ctx_work(hdg_ctx* c, size_t bytes) {
 size_t pivstat_offset(const DevTab& t, long nelt) { return (size_t(nelt) * (2 * t.nsym + t.d3) + 3) / 4 * 4; }
 size_t work_doubles(const DevTab& t, long nelt) { return pivstat_offset(t, nelt) + size_t(nelt) * 4; }
 
+// recovery cache record: {M^-1 packed lower, Vs = S^-1 V (d3 x m), fs = S^-1 f},
+// padded to a 16-byte multiple (TMA bulk copies)
 int factor_doubles(int k) {
   const int d3 = hdgb::pdim3(k), m = 4 * hdgb::pdim2(k);
-  return d3 * (d3 + 1) + d3 * m + d3;
+  return (d3 * (d3 + 1) / 2 + d3 * m + d3 + 1) / 2 * 2;
 }
 
 // launch shape of the CTA-batched kernel in the (NW, EPB) vocabulary
@@ -345,7 +347,10 @@ void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, co
 template <int K_>
 void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, const double* Ds,
                      const double* fv, double* C, double* Cf, double* F, double* ps) {
-  if constexpr (K_ <= 1)
+#ifndef HDG_TEAM_MAXK
+#define HDG_TEAM_MAXK 1  // diagnostics builds: per-element warp teams up to this degree
+#endif
+  if constexpr (K_ <= HDG_TEAM_MAXK)
     launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
   else if constexpr (K_ <= 3)
     launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);

@@ -43,15 +43,23 @@ struct C2Dims {
   static constexpr int OFF_GEO = OFF_STG2 + 128;        // 2 x 32: geometry records (cur/next)
   static constexpr int OFF_COL = OFF_GEO + 64;         // second column-data buffer
   static constexpr int PER_ELT = OFF_COL + 8 * MP;
-  static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
+  static constexpr int FACTORS = round_up(NSYM + D3 * M + D3, 2);  // {M^-1 packed, Vs, fs}, 16-B records
   static constexpr int CTA_EXTRA = 0;  // per-CTA shared doubles beyond EPB * PER_ELT
 };
 
 template <int K_> struct C2Cfg;
 template <> struct C2Cfg<0> { static constexpr int NW = 1, EPB = 8; };
 template <> struct C2Cfg<1> { static constexpr int NW = 1, EPB = 16; };
-template <> struct C2Cfg<2> { static constexpr int NW = 2, EPB = 8; };
-template <> struct C2Cfg<3> { static constexpr int NW = 4, EPB = 4; };
+#ifndef HDG_C2_NW2
+#define HDG_C2_NW2 2
+#define HDG_C2_EPB2 8
+#endif
+#ifndef HDG_C2_NW3
+#define HDG_C2_NW3 4
+#define HDG_C2_EPB3 4
+#endif
+template <> struct C2Cfg<2> { static constexpr int NW = HDG_C2_NW2, EPB = HDG_C2_EPB2; };
+template <> struct C2Cfg<3> { static constexpr int NW = HDG_C2_NW3, EPB = HDG_C2_EPB3; };
 
 // Inverse of the SPD N x N matrix held by a warp (lane c owns column c in
 // a[]) by the symmetric sweep operator: sweeping pivot k keeps the matrix
@@ -442,11 +450,6 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             Sb[i + lane * LD] = a[i];
             Sb[lane + i * LD] = a[i];
           }
-        if (F) {
-#pragma unroll
-          for (int i = 0; i < D3; ++i)
-            if (i >= lane) F[Dm::NSYM + sym_idx(i, lane, D3)] = a[i];
-        }
       }
       if (lane == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
     }
@@ -485,13 +488,6 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           const double aw = (wbr >= 0 && k < D3) ? __ldg(Wlm + wbr + k * D2) : 0.0;
           dmma(accz[i][0], accz[i][1], aw, Zb[k + (nt * 8 + g) * LD]);
         }
-      }
-      if (F && tm.warp == NW - 1) {
-        for (int idx = lane; idx < D3 * M; idx += 32) {
-          const int r = idx % D3, c = idx / D3;
-          F[2 * Dm::NSYM + idx] = Vb[r + c * LD];
-        }
-        for (int i = lane; i < D3; i += 32) F[2 * Dm::NSYM + D3 * M + i] = i < tab.nu ? fv[i] : 0.0;
       }
     }
     tm.sync();
@@ -535,6 +531,11 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       build_columns<D2, D3, M, MP>(sgbuf(nxt), colbuf(nxt), lane);
     }
     tm.sync();
+    if (F)  // recovery cache: Vs = S^-1 V (d3 x m) and fs = S^-1 f after M^-1
+      for (int idx = tm.tid; idx < D3 * M + D3; idx += NT) {
+        const int r = idx % D3, c = idx / D3;
+        F[Dm::NSYM + idx] = c < M ? Vs[r + c * LD] : (r < tab.nu ? fs[r] : 0.0);
+      }
 
     // ---- P5: C = tauDD + (n_l1.n_l2) o (W Zp) - V^T Vs (lower tiles, mirrored);
     //      Cf; then the next element's D and f (Sb, fv are free)
@@ -585,8 +586,8 @@ condense2_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   }
 }
 
-// K5 for the v2 cache {Mi, Si, V, f}:
-//   u = Si (f + V lambda),  q_s = Mi (C_s^T u - E_s^T lambda)
+// K5 for the cache {Mi, Vs = Si V, fs = Si f}:
+//   u = fs + Vs lambda,  q_s = Mi (C_s^T u - E_s^T lambda)
 template <int K_>
 __global__ void __launch_bounds__(kRecWarps * 32)
 recover2_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ facebyele,
@@ -607,25 +608,18 @@ recover2_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ faceby
   if (K >= nelt) return;
   const double* F = factors + K * Dm::FACTORS;
   const double* Mi = F;
-  const double* Si = F + NS;
-  const double* V = F + 2 * NS;
-  const double* f = F + 2 * NS + D3 * M;
+  const double* Vs = F + NS;
+  const double* fs = F + NS + D3 * M;
   load_geo(geo, K, nelt, sg, lane, 32);
   for (int i = lane; i < M; i += 32) {
     const int l = i / D2;
     lam[i] = uhat[long(facebyele[long(l) * nelt + K]) * D2 + (i - l * D2)];
   }
   __syncwarp();
-  for (int r = lane; r < D3; r += 32) {  // t = f + V lambda
-    double s = f[r];
-    for (int c = 0; c < M; ++c) s += V[r + c * D3] * lam[c];
-    tv[r] = s;
-  }
-  __syncwarp();
-  for (int i = lane; i < D3; i += 32) {  // u = Si t (symmetric, packed lower)
-    double s = 0.0;
-    for (int r = 0; r < D3; ++r) s += Si[r >= i ? sym_idx(r, i, D3) : sym_idx(i, r, D3)] * tv[r];
-    uu[i] = s;
+  for (int r = lane; r < D3; r += 32) {  // u = S^-1 (f + V lambda) = fs + Vs lambda
+    double s = fs[r];
+    for (int c = 0; c < M; ++c) s += Vs[r + c * D3] * lam[c];
+    uu[r] = s;
   }
   __syncwarp();
   const double* a9 = sg + 1;

@@ -56,7 +56,7 @@ struct C3Dims {
   static constexpr int OFF_COL = OFF_GEO + 128;             // second column-data buffer
   static constexpr int OFF_DP = OFF_COL + 8 * MP;           // packed D
   static constexpr int PER_ELT = OFF_DP + round_up(NSYM, 2);
-  static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
+  static constexpr int FACTORS = round_up(NSYM + D3 * M + D3, 2);  // {M^-1 packed, Vs, fs}, 16-B records
   // per CTA: Chat_# [c + k d3] (k < LD, padding zero), tauDD, tile overrun
   static constexpr int CTA_EXTRA = round_up(3 * D3 * LD + D2 * D2 + D3P, 2);
 };
@@ -117,6 +117,13 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #else
   const bool BULK_VF = false;
 #endif
+#ifndef HDG_C3_VS_DIRECT
+#define HDG_C3_VS_DIRECT 1
+#endif
+  // Vs, fs go to the recovery cache from P4's registers (1) or by TMA bulk
+  // stores from shared memory under P5 (0: measured slower, P5 is
+  // shared-memory bound)
+  constexpr bool VS_DIRECT = HDG_C3_VS_DIRECT;
   extern __shared__ double smem[];
   for (int i = threadIdx.x; i < EPB * Dm::PER_ELT + Dm::CTA_EXTRA; i += blockDim.x) smem[i] = 0.0;
   __syncthreads();
@@ -440,8 +447,8 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
                   dst[c + i * LD] = a[i];
                   dst[i + c * LD] = a[i];
                 }
-              if (factors) {
-                double* fd = factors + K * Dm::FACTORS + (h == 0 ? Dm::NSYM : 0) + c * (2 * D3 - c + 1) / 2 - c;
+              if (factors && h == 1) {  // M^-1 of the next batch (S^-1 is not cached: Vs, fs are)
+                double* fd = factors + K * Dm::FACTORS + c * (2 * D3 - c + 1) / 2 - c;
 #pragma unroll
                 for (int i = 0; i < D3; ++i)
                   if (i >= c) fd[i] = a[i];
@@ -470,7 +477,6 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
                   Sb(e)[i + lane * LD] = a[i];
                 }
             }
-            store_factor(a, K, Dm::NSYM, Dp(e));  // packed D is dead after P2
             if (lane == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
           } else if (has_next && Kn0 + e < nelt) {
 #ifdef HDG_DIAG_NO_GJ
@@ -486,25 +492,6 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         // No FP64 here: the sweeps' dependent DFMA chains stall badly behind
         // DMMA traffic on the same pipe, so this phase only moves data.
         const int w0 = GJ_SEP ? warp - NGJ : warp, nw = GJ_SEP ? NWT - NGJ : NWT;
-#ifndef HDG_DIAG_NO_P3MEM
-        if (factors && BULK_VF) {
-          // V and f are already in the record's layout in shared memory (LD ==
-          // d3): one TMA bulk store each, off the LSU path
-          if (lane == 0)
-            for (int e = w0; e < nb; e += nw) {
-              double* rec = factors + (K0 + e) * Dm::FACTORS + 2 * Dm::NSYM;
-              bulk_store(rec, Vb(e), D3 * M * 8);
-              bulk_store(rec + D3 * M, fv(e), D3 * 8);
-            }
-        } else if (factors) {  // V (D3 x M) and f of each element, contiguous in the cache record
-          constexpr int NVF = D3 * M + D3;
-          for (int q = w0 * 32 + lane; q < nb * NVF; q += nw * 32) {
-            const int e = q / NVF, rem = q - e * NVF, c = rem / D3, r = rem - c * D3;
-            factors[(K0 + e) * Dm::FACTORS + 2 * Dm::NSYM + rem] =
-                c < M ? Vb(e)[r + c * LD] : (r < tab.nu ? fv(e)[r] : 0.0);
-          }
-        }
-#endif
         if (has_next) load_geometry(Kn0, cur ^ 1, w0 * 32 + lane, nw * 32);
       }
     }
@@ -535,6 +522,11 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           Yb(e)[r + c0 * LD] = r < D3 ? acc[m][0] : 0.0;  // Vs (R_# is dead)
           Yb(e)[r + (c0 + 1) * LD] = r < D3 ? acc[m][1] : 0.0;
         }
+        if (VS_DIRECT && factors && r < D3) {  // recovery cache, straight from the registers
+          double* rec = factors + (K0 + e) * Dm::FACTORS + Dm::NSYM;
+          rec[r + c0 * D3] = acc[m][0];
+          rec[r + (c0 + 1) * D3] = acc[m][1];
+        }
       }
     }
     for (int idx = threadIdx.x; idx < nb * D3; idx += NT) {
@@ -543,9 +535,29 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int k = 0; k < D3; ++k) s += Sb(e)[r + k * LD] * fv(e)[k];
       fs(e)[r] = s;
+      if (VS_DIRECT && factors) factors[(K0 + e) * Dm::FACTORS + Dm::NSYM + D3 * M + r] = r < tab.nu ? s : 0.0;
     }
-    if (BULK_VF && lane == 0) bulk_store_wait_read();  // V, f are rewritten from P5 on
     __syncthreads();
+    // recovery cache: Vs = S^-1 V and fs = S^-1 f after M^-1 (k = 3: already in the
+    // record's layout in shared memory, one TMA bulk store each, retired before
+    // the end of P5, when Vs's slot is rewritten by the next P1)
+    if (VS_DIRECT) {
+      // written from P4's registers
+    } else if (factors && BULK_VF) {
+      if (lane == 0)
+        for (int e = warp; e < nb; e += NWT) {
+          double* rec = factors + (K0 + e) * Dm::FACTORS + Dm::NSYM;
+          bulk_store(rec, Yb(e), D3 * M * 8);
+          bulk_store(rec + D3 * M, fs(e), D3 * 8);
+        }
+    } else if (factors) {
+      constexpr int NVF = D3 * M + D3;
+      for (int q = threadIdx.x; q < nb * NVF; q += NT) {
+        const int e = q / NVF, rem = q - e * NVF, c = rem / D3, r = rem - c * D3;
+        factors[(K0 + e) * Dm::FACTORS + Dm::NSYM + rem] =
+            c < M ? Yb(e)[r + c * LD] : (r < tab.nu ? fs(e)[r] : 0.0);
+      }
+    }
     if (has_next)
       for (int e = warp; e < EPB; e += NWT)
         if (Kn0 + e < nelt) {
@@ -612,6 +624,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       for (int k = 0; k < D3; ++k) s += Vb(e)[k + r * LD] * fs(e)[k];
       Cfout[(K0 + e) * M + r] = s;
     }
+    if (!VS_DIRECT && factors && BULK_VF && lane == 0 && warp < nb) bulk_store_wait_read();  // Vs, fs read out
     __syncthreads();
     PHASE_MARK(batch, 5);
     cur ^= 1;

@@ -52,7 +52,7 @@ struct C5Dims {
   static constexpr int OFF_RED = OFF_SG + 64;
   static constexpr int TOTAL = OFF_RED + 8;
   static constexpr int PER_ELT = TOTAL, CTA_EXTRA = 0;  // launch_condense_impl vocabulary (EPB = 1)
-  static constexpr int FACTORS = 2 * NSYM + D3 * M + D3;
+  static constexpr int FACTORS = round_up(NSYM + D3 * M + D3, 2);  // {M^-1 packed, Vs, fs}, 16-B records
   static_assert(2 * SQ >= LD * MP, "Vs must fit in the M^-1 | T0 space");
 };
 
@@ -413,20 +413,11 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     __syncthreads();
 
-    // ---- P6: S^-1 (CTA sweep); cache: S^-1 packed, V, f
+    // ---- P6: S^-1 (CTA sweep)
     {
       double pmin, pmax;
       cta_sweep_inverse<D3, LD, NT>(S, T1, pmin, pmax);
       if (threadIdx.x == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
-    }
-    if (factors) {
-      for (int c = warp; c < D3; c += NWT)
-        for (int i = c + lane; i < D3; i += 32) factors[K * Dm::FACTORS + NSYM + sym_idx(i, c, D3)] = S[i + c * LD];
-      constexpr int NVF = D3 * M + D3;
-      for (int q = threadIdx.x; q < NVF; q += NT) {
-        const int c = q / D3, r = q - c * D3;
-        factors[K * Dm::FACTORS + 2 * NSYM + q] = c < M ? V[r + c * LD] : fv[r];
-      }
     }
 
     // ---- P7: Vs = S^-1 V strips | fs = S^-1 f
@@ -458,6 +449,13 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       fs[r] = s;
     }
     __syncthreads();
+    if (factors) {  // recovery cache: Vs = S^-1 V (d3 x m) and fs = S^-1 f after M^-1
+      constexpr int NVF = D3 * M + D3;
+      for (int q = threadIdx.x; q < NVF; q += NT) {
+        const int c = q / D3, r = q - c * D3;
+        factors[K * Dm::FACTORS + NSYM + q] = c < M ? Vs[r + c * LD] : fs[r];
+      }
+    }
 
     // ---- P8: C (lower tile pairs, mirrored) | Cf
     for (int task = warp; task < NLP; task += NWT) {

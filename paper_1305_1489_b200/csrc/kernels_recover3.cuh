@@ -1,8 +1,9 @@
 // K5 v3 (k = 1..3): gather + local recovery from the condensation cache,
 // HBM-streaming form.
 //
-// Per element the cache record {M^-1, S^-1 (packed lower), V (d3 x m), f} is
-// read exactly once (k=3: 9,920 B), so the kernel is a stream over the cache.
+// Per element the cache record {M^-1 (packed lower), Vs = S^-1 V (d3 x m),
+// fs = S^-1 f} is read exactly once (k=3: 8,240 B), so the kernel is a stream
+// over the cache.
 // Each warp owns a chain of elements (persistent grid) and double-buffers the
 // records in shared memory with 1-D TMA bulk copies (cp.async.bulk, completion
 // on a per-buffer mbarrier): the copies of the next kRec3Bufs-1 elements of the
@@ -55,7 +56,7 @@ template <> struct Rec3Cfg<3> { static constexpr int WARPS = 8, BUFS = 2; };
 template <int K_>
 struct Rec3Dims {
   static constexpr int D3 = cdim3(K_), D2 = cdim2(K_), M = 4 * cdim2(K_), NS = D3 * (D3 + 1) / 2;
-  static constexpr int FACTORS = 2 * NS + D3 * M + D3;  // doubles per cache record
+  static constexpr int FACTORS = round_up(NS + D3 * M + D3, 2);  // {M^-1 packed, Vs, fs}
   static constexpr int REC = round_up(FACTORS, 2);       // 16-byte multiple
   static constexpr int SCR = round_up(M, 2) + 2 * 32 + 3 * D3 + 32;  // lambda, t, u, r_s, geometry
   static constexpr int PER_WARP = Rec3Cfg<K_>::BUFS * REC + SCR;
@@ -148,29 +149,17 @@ recover3_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ faceby
     mbar_wait(&bars[warp][b], (phase >> b) & 1u);
     phase ^= 1u << b;
     const double* Mi = buf + b * Rd::REC;
-    const double* Si = Mi + NS;
-    const double* V = Mi + 2 * NS;
-    const double* f = V + D3 * M;
+    const double* Vs = Mi + NS;
+    const double* fs = Vs + D3 * M;
 
-    if (lane < D3) {  // t = f + V lambda
-      double s0 = f[lane], s1 = 0.0;
+    if (lane < D3) {  // u = S^-1 (f + V lambda) = fs + Vs lambda
+      double s0 = fs[lane], s1 = 0.0;
 #pragma unroll
       for (int c = 0; c < M; c += 2) {
-        s0 = fma(V[lane + c * D3], lam[c], s0);
-        if (c + 1 < M) s1 = fma(V[lane + (c + 1) * D3], lam[c + 1], s1);
+        s0 = fma(Vs[lane + c * D3], lam[c], s0);
+        if (c + 1 < M) s1 = fma(Vs[lane + (c + 1) * D3], lam[c + 1], s1);
       }
-      tv[lane] = s0 + s1;
-    }
-    __syncwarp();
-    double u = 0.0;
-    if (lane < D3) {  // u = S^-1 t (packed lower)
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int r = 0; r < D3; ++r) {
-        const double v = Si[r >= lane ? sym_idx(r, lane, D3) : sym_idx(lane, r, D3)] * tv[r];
-        if (r & 1) s1 += v; else s0 += v;
-      }
-      u = s0 + s1;
+      const double u = s0 + s1;
       uu[lane] = u;
       uout[K * D3 + lane] = u;
     }
@@ -233,7 +222,7 @@ constexpr int kRec5Threads = 256;
 template <int K_>
 struct Rec5Dims {
   static constexpr int D3 = cdim3(K_), D2 = cdim2(K_), M = 4 * cdim2(K_), NS = D3 * (D3 + 1) / 2;
-  static constexpr int FACTORS = 2 * NS + D3 * M + D3;
+  static constexpr int FACTORS = round_up(NS + D3 * M + D3, 2);  // {M^-1 packed, Vs, fs}
   static constexpr int REC = round_up(FACTORS, 2);
   static constexpr int SCR = round_up(M, 2) + 3 * D3 + 7 * D3 + 3 * D3 + 32;  // lambda, t/u, p|w, r_s, geometry
   static constexpr int TOTAL = REC + SCR;
@@ -259,9 +248,8 @@ recover5_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ faceby
   double* rs = pw + 7 * D3;  // r_s (3 D3)
   double* sg = rs + 3 * D3;
   const double* Mi = rec;
-  const double* Si = rec + NS;
-  const double* V = rec + 2 * NS;
-  const double* f = V + D3 * M;
+  const double* Vs = rec + NS;
+  const double* fs = Vs + D3 * M;
   const int tid = threadIdx.x, row = tid >> 2, part = tid & 3;
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -296,26 +284,16 @@ recover5_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ faceby
       cp_async_wait_all();
     }
     __syncthreads();
-    // t = f + V lambda
+    // u = S^-1 (f + V lambda) = fs + Vs lambda
     double s = 0.0;
     if (row < D3) {
-      for (int c = part; c < M; c += 4) s = fma(V[row + c * D3], lam[c], s);
-    }
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (row < D3 && part == 0) tv[row] = f[row] + s;
-    __syncthreads();
-    // u = S^-1 t (packed lower)
-    s = 0.0;
-    if (row < D3) {
-      for (int r = part; r < D3; r += 4)
-        s = fma(Si[r >= row ? sym_idx(r, row, D3) : sym_idx(row, r, D3)], tv[r], s);
+      for (int c = part; c < M; c += 4) s = fma(Vs[row + c * D3], lam[c], s);
     }
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     if (row < D3 && part == 0) {
-      uu[row] = s;
-      uout[K * D3 + row] = s;
+      uu[row] = fs[row] + s;
+      uout[K * D3 + row] = fs[row] + s;
     }
     __syncthreads();
     // p_#(j) = (Chat_# u)(j) over the rows of Chat_#^T, w_l(j) = (W_l lambda_l)(j)

@@ -140,7 +140,7 @@ rescue_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
   double *A = W + L.A, *B = W + L.B, *Cs = W + L.Cs, *E = W + L.E, *TDP = W + L.TDP, *Mw = W + L.Mw,
          *Mi = W + L.Mi, *Sw = W + L.Sw, *Si = W + L.Si, *Z = W + L.Z, *Dm = W + L.Dm, *fl = W + L.f;
   const int nsym = d3 * (d3 + 1) / 2;
-  const long FD = long(d3) * (d3 + 1) + long(d3) * m + d3;
+  const long FD = (long(nsym) + long(d3) * m + d3 + 1) / 2 * 2;  // {M^-1 packed, Vs, fs}
 
   for (long base = long(blockIdx.x) * NT; base < nelt; base += long(gridDim.x) * NT) {
     if (tid == 0) ncand = 0;
@@ -260,14 +260,14 @@ rescue_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
       __syncthreads();
       cta_gauss(Sw, nu, nu, Si, nu, nu, diag, lm, red_v, red_i);
       double* F = factors + K * FD;
-      for (int idx = tid; idx < nsym; idx += NT) {  // packed lower M^-1 and S^-1
+      for (int idx = tid; idx < nsym; idx += NT) {  // packed lower M^-1
         int j = 0;
         while (sym_idx(d3 - 1, j, d3) < idx) ++j;
         const int i = j + (idx - sym_idx(j, j, d3));
         F[idx] = Mi[i + j * d3];
-        F[nsym + idx] = (i < nu && j < nu) ? Si[i + j * nu] : (i == j ? 1.0 / (6.0 * sg[0]) : 0.0);
       }
-      for (int idx = tid; idx < d3 * m; idx += NT) {  // V = tauDP^T + sum_s C_s M^-1 E_s^T (rows < nu)
+      double* V = B;  // X is dead: V = tauDP^T + sum_s C_s M^-1 E_s^T (rows < nu), d3 x m
+      for (int idx = tid; idx < d3 * m; idx += NT) {
         const int i = idx % d3, r = idx / d3;
         double acc = 0.0;
         if (i < nu) {
@@ -276,9 +276,16 @@ rescue_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
             for (int a = 0; a < d3; ++a)
               acc = fma(Cs[long(s) * d3 * d3 + i + a * d3], Z[(long(s) * (nu + m) + nu + r) * d3 + a], acc);
         }
-        F[2 * nsym + idx] = acc;
+        V[idx] = acc;
       }
-      for (int i = tid; i < d3; i += NT) F[2 * nsym + long(d3) * m + i] = i < nu ? fl[i] : 0.0;
+      __syncthreads();
+      for (int idx = tid; idx < d3 * (m + 1); idx += NT) {  // Vs = S^-1 V, fs = S^-1 f (rows < nu)
+        const int i = idx % d3, r = idx / d3;
+        double acc = 0.0;
+        if (i < nu)
+          for (int j = 0; j < nu; ++j) acc = fma(Si[i + j * nu], r < m ? V[j + r * d3] : fl[j], acc);
+        F[nsym + idx] = acc;
+      }
       __syncthreads();
     }
     __syncthreads();

@@ -79,8 +79,10 @@ int main(int argc, char** argv) {
     bool thrown = false;
     try {
       condense(lv2, kap_sing, constant_field(1.0), constant_field(1.0));
+      std::fprintf(stderr, "condense returned without LocalSolverError\n");
     } catch (const LocalSolverError& e) {
       thrown = e.element == 3;
+      if (!thrown) std::fprintf(stderr, "LocalSolverError on element %d (%s)\n", e.element, e.what());
     }
     expect(thrown && calls == 1, "LocalSolverError on element 3");
     // negative tau on element 2: std::invalid_argument (element_matrices.cpp:38-46)

@@ -1,5 +1,6 @@
 """Diagnostics: per-phase cycle counts of the CTA-batched condensation kernel
-(build with -DHDG_PHASE_TIMING into tools/diag/libhdg_b200_phase.so)."""
+(build with -DHDG_PHASE_TIMING, e.g. tools/diag/sweep_build.sh "pt,-DHDG_PHASE_TIMING"):
+phase_timing.py CONFIG [LIB]."""
 import ctypes as C
 import os
 import sys
@@ -10,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 from paper_1305_1489_b200 import _lib as L  # noqa: E402
 
-L.LIB_PATH = os.path.join(ROOT, "tools", "diag", "libhdg_b200_phase.so")
+L.LIB_PATH = os.path.abspath(sys.argv[2]) if len(sys.argv) > 2 else os.path.join(ROOT, "tools", "diag", "libhdg_b200_phase.so")
 lib = L.lib()
 lib.hdg_b200_debug_phase_clocks.argtypes = [C.c_void_p]
 import torch  # noqa: E402
