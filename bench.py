@@ -382,16 +382,23 @@ def run_ours(args):
     stream.synchronize()
     t_setup = time.perf_counter() - t_setup
 
+    conv_out = None
+    if cfg.upwind_beta:  # C4: the convection block (convdiff.cpp:5-28) is part of the step
+        m_ = 4 * d2
+        conv_out = tuple(torch.empty(nelt * a, dtype=torch.float64, device=dev) for a in (d3 * d3, m_ * d3, m_ * m_))
+
     def step():
         eng.geometry(dm, tau, out=g)
         eng.build_condense(g, kap, cc, ff, out=cs, work=work, check=False)
         eng.recover(g, dm, cs, uhat, out=ls)
         if cfg.postprocess:
             eng.postprocess_star(g, kap, ls, out=ustar)
+        if conv_out is not None:
+            eng.convection_bilinear_matrices(g, cfg.upwind_beta, out=conv_out)
 
     # geometry 2 (face areas, per element); build_condense 5 (status reset, tau
     # check, K2, K3, rescue screen); recover 1; postprocess 1 (+1 kappa sampler)
-    launches_per_step = 2 + 5 + 1 + (2 if cfg.postprocess else 0)
+    launches_per_step = 2 + 5 + 1 + (2 if cfg.postprocess else 0) + (1 if cfg.upwind_beta else 0)
     eng.set_timing(True)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):

@@ -26,6 +26,7 @@
 #include "kernels_errors.cuh"
 #include "kernels_post2.cuh"
 #include "kernels_rescue.cuh"
+#include "kernels_conv2.cuh"
 #include "exchange.cuh"
 #include "jit_quad.hpp"
 #include "mesh_dev.hpp"
@@ -177,6 +178,16 @@ void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
     }
     push(sp);                                                    // 17
   }
+  if (k <= 3) {  // K7 v2 volume table: row i + j d3, column # nqp + q: P_qi dP_qj/dxhat_#
+    const int rows = round_up(d3 * d3, 8), cols = 3 * nqp;
+    std::vector<double> A(size_t(rows) * cols, 0.0);
+    for (int j = 0; j < d3; ++j)
+      for (int i = 0; i < d3; ++i)
+        for (int hh = 0; hh < 3; ++hh)
+          for (int q = 0; q < nq; ++q)
+            A[size_t(i + j * d3) * cols + hh * nqp + q] = h.P[q + size_t(i) * nq] * h.Pd[hh][q + size_t(j) * nq];
+    push(to_fragments(A, rows, cols));                           // 18
+  }
   CUDA_OK(cudaMalloc(&ts.buf, all.size() * sizeof(double)));
   CUDA_OK(cudaMemcpy(ts.buf, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice));
   ts.doubles = all.size();
@@ -189,6 +200,7 @@ void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
   t.tri_bary = b + off[9]; t.tri_w = b + off[10]; t.Pface = b + off[11]; t.Dperm = b + off[12];
   t.Asym = b + off[13]; t.Af = b + off[14]; t.ChatT = b + off[15]; t.WlmT = b + off[16];
   t.ShatP = b + off[17];
+  t.Aconv = k <= 3 ? b + off[18] : nullptr;
   ts.ready = true;
 }
 
@@ -1429,6 +1441,27 @@ int hdg_b200_convection_block(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_f
     const GeoDev geo = to_geo(g);
     set_device(c);
     const DevTab& t = c->tab[0].dev;
+    if (t.Aconv) {  // k <= 3: CTA-batched, the volume block on DMMA (kernels_conv2.cuh)
+      const Conv2Dims cd(t.d3, t.d2, t.nq, t.nqd);
+      const size_t smem = size_t(cd.total) * sizeof(double);
+      auto go = [&](auto kern) {
+        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int occ = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kConv2Threads, smem));
+        const long need = (long(nelt) + kConv2EB - 1) / kConv2EB;
+        const int grid = int(std::min<long>(need, long(c->sms) * std::max(occ, 1)));
+        kern<<<grid, kConv2Threads, smem, c->stream>>>(t, nelt, geo, to_dev(bx, "bx"), to_dev(by, "by"),
+                                                       to_dev(bz, "bz"), vol, dp, dd);
+      };
+      switch (t.k) {
+        case 0: go(convection2_kernel<0>); break;
+        case 1: go(convection2_kernel<1>); break;
+        case 2: go(convection2_kernel<2>); break;
+        default: go(convection2_kernel<3>); break;
+      }
+      CUDA_OK(cudaGetLastError());
+      return;
+    }
     const int per_warp = 3 * t.nq + 4 * t.nqd + 32;
     const int nw = warps_for(size_t(per_warp) * 8);
     const size_t smem = size_t(nw) * per_warp * sizeof(double);

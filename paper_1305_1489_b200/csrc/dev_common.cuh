@@ -40,6 +40,7 @@ struct DevTab {
   const double* ChatT;  // 3 x (d3 x d3), Chat transposed
   const double* WlmT;   // 24 x (d3 x d2), Wlm transposed
   const double* ShatP;  // 9 x d3(d3+1)/2, Shat packed lower (column-major)
+  const double* Aconv;  // k <= 3: fragment-ordered [P_qi dP_qj/dxhat_#], d3^2 x 3 nqp (kernels_conv2.cuh)
 };
 
 // ------------------------------------------------------------------ fields

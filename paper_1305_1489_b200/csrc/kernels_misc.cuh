@@ -307,14 +307,36 @@ scatter_faces_kernel(int nfc, const int* __restrict__ sides, const uint8_t* __re
     const int ns = s1 >= 0 ? 2 : 1;
     const int64_t base = facebase[f];
     const int nb = int(facebase[f + 1] - base), W = nb * D2;
-    for (int s = 0; s < ns; ++s) {
+    // both sides' column blocks: every load issued before the first store
+    // (memory-level parallelism: NQ 16-byte loads per lane and side in flight;
+    // batches of at most 8 per lane and side for the large k = 4, 5 blocks)
+    constexpr int NQALL = (md / 2 + 31) / 32, NQ = NQALL < 8 ? NQALL : 8;
+    for (int u0 = 0; u0 < NQALL; u0 += NQ) {
+    double2 v[2][NQ];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int code = s ? s1 : s0;
+      const double2* src = reinterpret_cast<const double2*>(C + long(code >> 2) * m * m + long(code & 3) * md);
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) {
+        const int q = lane + 32 * (u0 + u);
+        if (s < ns && q < md / 2) v[s][u] = __ldg(src + q);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (s >= ns) break;
       const int code = s ? s1 : s0, e = code >> 2, l = code & 3;
-      const double2* src = reinterpret_cast<const double2*>(C + long(e) * m * m + long(l) * md);
-      for (int q = lane; q < md / 2; q += 32) reinterpret_cast<double2*>(ch + s * md)[q] = __ldg(src + q);
-      if (lane < 4) {
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) {
+        const int q = lane + 32 * (u0 + u);
+        if (q < md / 2) reinterpret_cast<double2*>(ch + s * md)[q] = v[s][u];
+      }
+      if (u0 == 0 && lane < 4) {
         const int q = slot[long(e) * 16 + l * 4 + lane];
         inv[q] = lane == l ? 8 : s * 4 + lane;
       }
+    }
     }
     __syncwarp();
     const int l0 = s0 & 3, l1 = s1 & 3;

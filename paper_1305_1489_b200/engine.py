@@ -622,12 +622,17 @@ class Engine:
         return b
 
     # ---------------------------------------------------------------- K7
-    def convection_bilinear_matrices(self, g: Geometry, beta: Sequence):
+    def convection_bilinear_matrices(self, g: Geometry, beta: Sequence, out=None):
+        """convection_bilinear_matrices (convdiff.cpp:5-28): (vol, dp, dd) Batch3 views;
+        out = (vol, dp, dd) flat buffers from a previous call's .base tensors to reuse."""
         d = self.dims
         d3, m, n = d["d3"], 4 * d["d2"], g.nelt
-        vol = torch.empty(n * d3 * d3, dtype=torch.float64, device=self.device)
-        dp = torch.empty(n * m * d3, dtype=torch.float64, device=self.device)
-        dd = torch.empty(n * m * m, dtype=torch.float64, device=self.device)
+        if out is None:
+            vol = torch.empty(n * d3 * d3, dtype=torch.float64, device=self.device)
+            dp = torch.empty(n * m * d3, dtype=torch.float64, device=self.device)
+            dd = torch.empty(n * m * m, dtype=torch.float64, device=self.device)
+        else:
+            vol, dp, dd = out
         fs = [as_field(b) for b in beta]
         gs = g.c_struct()
         L.check(L.lib().hdg_b200_convection_block(self._ctx, n, C.byref(gs), fs[0].c_struct(), fs[1].c_struct(),

@@ -219,9 +219,11 @@ def test_postprocess(k):
 
 
 # ------------------------------------------------ a6: convection block
-def test_convection_block():
-    k = 2
-    mesh = HostMesh.box(2)
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 4, 5])
+def test_convection_block(k):
+    """convection_bilinear_matrices (convdiff.cpp:5-28): the CTA-batched DMMA
+    kernel at k <= 3 (72 tets: a partial last batch of 16), warp per element beyond."""
+    mesh = HostMesh.box(2, 2, 3, perturb=0.1)
     em = oracle_mesh(mesh)
     beta = ("x*y", "y*z", "x + z*z")
     eng = Engine(0)
