@@ -398,7 +398,7 @@ int hdg_b200_set_tau_allow_zero(hdg_ctx* ctx, int enabled);
  * local solve is truncated to its first d3 - d2 modes (P_{k-1}) and tau is
  * ignored (tauPP, tauDP and tauDD dropped); build_condense then returns the
  * condensed system of the BDM blocks and recover returns u zero-padded to
- * d3, as the reference. k = 1..3 (k = 0 is rejected as in the reference). */
+ * d3, as the reference. k = 1..5 (k = 0 is rejected as in the reference). */
 int hdg_b200_set_bdm(hdg_ctx* ctx, int enabled);
 const char* hdg_b200_jit_status(const hdg_ctx* ctx);
 

@@ -967,7 +967,6 @@ int hdg_b200_build_condense(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_fie
     GeoDev geo_b = geo;
     if (c->bdm) {  // bdm_blocks ignores tau entirely (local_solver.cpp:36-43): run with T = 0
       require(t.k >= 1, HDG_EINVAL, "the BDM variant needs degree k >= 1");
-      require(t.k <= 3, HDG_EINVAL, "the BDM variant is built for k = 1..3");
       if (c->zero_T_len < 4L * nelt) {
         if (c->d_zero_T) cudaFree(c->d_zero_T);
         c->d_zero_T = nullptr;

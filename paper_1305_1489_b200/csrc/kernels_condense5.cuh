@@ -412,6 +412,20 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
     }
     __syncthreads();
+    if (tab.nu < D3) {  // BDM (bdm_blocks, local_solver.cpp:65-69): the scalar space is P_{k-1}:
+      // decouple the remaining modes (identity-scaled S, zero V rows and f)
+      const int nu = tab.nu;
+      for (int idx = threadIdx.x; idx < D3 * D3; idx += NT) {
+        const int r = idx % D3, c = idx / D3;
+        if (r >= nu || c >= nu) S[r + c * LD] = r == c ? 6.0 * sg[0] : 0.0;
+      }
+      for (int idx = threadIdx.x; idx < (D3 - nu) * MP; idx += NT) {
+        const int r = nu + idx % (D3 - nu), c = idx / (D3 - nu);
+        V[r + c * LD] = 0.0;
+      }
+      for (int r = nu + threadIdx.x; r < D3; r += NT) fv[r] = 0.0;
+      __syncthreads();
+    }
 
     // ---- P6: S^-1 (CTA sweep)
     {

@@ -515,7 +515,7 @@ def test_recover_variants_agree(k):
 
 
 # -------------------------------------------- a7: BDM variant (bdm_blocks)
-@pytest.mark.parametrize("k", [1, 2, 3])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
 def test_bdm_variant(k):
     """bdm_blocks (local_solver.cpp:65-69): u truncated to P_{k-1}, tau ignored;
     C, Cf and the recovered (q, u) (u zero-padded) match the oracle."""
