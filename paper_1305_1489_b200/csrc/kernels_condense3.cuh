@@ -125,6 +125,13 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   // shared-memory bound)
   constexpr bool VS_DIRECT = HDG_C3_VS_DIRECT;
   extern __shared__ double smem[];
+  // The sweep inverses' two triangles round differently (each lane computes one
+  // column), and the Schur-complement products amplify that asymmetry (C at
+  // kappa = 1e4 off by 1e-4): every consumer reads one canonical value per
+  // symmetric pair, the one the lower-index lane computed (its column below the
+  // diagonal: the upper half of a sweep column is measurably less accurate),
+  // stored row-wise by that lane at (min, max) = min + max * LD.
+  auto sym_at = [](int r, int k) { return r <= k ? r + k * LD : k + r * LD; };
   for (int i = threadIdx.x; i < EPB * Dm::PER_ELT + Dm::CTA_EXTRA; i += blockDim.x) smem[i] = 0.0;
   __syncthreads();
 
@@ -231,13 +238,9 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     __syncwarp();
     double pmin = 1e300, pmax = 0.0;
     gj_sweep_inverse<D3>(a, stM(e), lane, pmin, pmax);
-    if (lane < D3) {
+    if (lane < D3) {  // row-wise (conflict-free); consumers read the canonical entries (sym_at)
 #pragma unroll
-      for (int i = 0; i < D3; ++i)  // lower triangle of the sweep result, mirrored:
-        if (i >= lane) {              // the two halves round differently (GJ)
-          Mi(e)[lane + i * LD] = a[i];
-          Mi(e)[i + lane * LD] = a[i];
-        }
+      for (int i = 0; i < D3; ++i) Mi(e)[lane + i * LD] = a[i];
     }
     store_factor(a, K, 0, Yb(e));  // R_# of this slot is dead until the next P1
     if (lane == 0) store_pivstat(pivstat, K, 0, pmin, pmax);
@@ -278,7 +281,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         for (int kk = 0; kk < KS; ++kk) {
           const int k = kk * 4 + t;
           const int o = c + k * D3;
-          const double a = mi[(m * 8 + g) + k * LD];
+          const double a = mi[sym_at(m * 8 + g, k)];
           dmma(q[0][0], q[0][1], a, Ch[o]);
           dmma(q[1][0], q[1][1], a, Ch[D3 * LD + o]);
           dmma(q[2][0], q[2][1], a, Ch[2 * D3 * LD + o]);
@@ -309,7 +312,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
           const double b = (wbc >= 0 && k < D3) ? __ldg(Wlm + wbc + k * D2) : 0.0;
           Vi[k] = tc * b;
 #pragma unroll
-          for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], mi[(m * 8 + g) + k * LD], b);
+          for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], mi[sym_at(m * 8 + g, k)], b);
         }
         const int c0 = nt * 8 + 2 * t;
         double* Z = Zb(e);
@@ -442,7 +445,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             gj_sweep_seg<D3, 16, D3>(a, h == 0 ? stS(e) : stM(e), c, pmin, pmax);
             if (live && c < D3) {
 #pragma unroll
-              for (int i = 0; i < D3; ++i)  // lower triangle, mirrored (see invert_M)
+              for (int i = 0; i < D3; ++i)  // lower triangle mirrored: consistent for sym_at
                 if (i >= c) {
                   dst[c + i * LD] = a[i];
                   dst[i + c * LD] = a[i];
@@ -469,13 +472,9 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #else
             pmin = pmax = 1.0;
 #endif
-            if (lane < D3) {
+            if (lane < D3) {  // row-wise; consumers read canonical (max, min) entries (sym_at)
 #pragma unroll
-              for (int i = 0; i < D3; ++i)  // lower triangle, mirrored (see invert_M)
-                if (i >= lane) {
-                  Sb(e)[lane + i * LD] = a[i];
-                  Sb(e)[i + lane * LD] = a[i];
-                }
+              for (int i = 0; i < D3; ++i) Sb(e)[lane + i * LD] = a[i];
             }
             if (lane == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
           } else if (has_next && Kn0 + e < nelt) {
@@ -512,7 +511,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         const int k = kk * 4 + t;
         const double b = V[k + c * LD];
 #pragma unroll
-        for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], S[(m * 8 + g) + k * LD], b);
+        for (int m = 0; m < MT; ++m) dmma(acc[m][0], acc[m][1], S[sym_at(m * 8 + g, k)], b);
       }
       const int c0 = nt * 8 + 2 * t;
 #pragma unroll
@@ -533,7 +532,7 @@ condense3_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       const int e = idx / D3, r = idx % D3;
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < D3; ++k) s += Sb(e)[r + k * LD] * fv(e)[k];
+      for (int k = 0; k < D3; ++k) s += Sb(e)[sym_at(r, k)] * fv(e)[k];
       fs(e)[r] = s;
       if (VS_DIRECT && factors) factors[(K0 + e) * Dm::FACTORS + Dm::NSYM + D3 * M + r] = r < tab.nu ? s : 0.0;
     }
