@@ -175,6 +175,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
     }
     __syncthreads();
 
+#ifndef HDG_K6_SKIP_R
     // ---- R = -(1/6) sum_# Pd_#^T G_#: one (row tile, component #) per warp,
     //      the Pd fragment feeding both element tiles; 3 partials reduced below
     {
@@ -203,6 +204,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
     __syncthreads();
     for (int idx = threadIdx.x; idx < npad * kPost2EB; idx += blockDim.x)
       R[idx] = -(1.0 / 6.0) * (Rp[idx] + Rp[npad * kPost2EB + idx] + Rp[2 * npad * kPost2EB + idx]);
+#endif
     // ---- S packed lower = ShatP^T-combination gm (G is dead: S overwrites it)
     {
       const int mts = dm.nsp / 8;
@@ -227,6 +229,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
     }
     __syncthreads();
 
+#ifndef HDG_K6_SKIP_SOLVE
     // ---- per element: mean constraint, then the trailing SPD system
     //      S' x = r' (m = n - 1 <= 32: register sweep inverse, lane c owns
     //      column c; 32 < m <= 64: the leading 32 x 32 block the same way and
@@ -312,6 +315,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
         if (lane < MA) ustar[K * n + 1 + lane] = x;
       }
     }
+#endif
     __syncthreads();
   }
 }
