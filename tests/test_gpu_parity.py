@@ -579,3 +579,50 @@ def test_upwind_tau_independent():
             nu = nrm[K, 3 * l:3 * l + 3] / np.linalg.norm(nrm[K, 3 * l:3 * l + 3])
             want[l, K] = 1.0 + abs(beta(*xc) @ nu)
     assert np.max(np.abs(tau - want)) < 1e-13
+
+
+def test_nccl_exchange_transport_self_peer():
+    """hdg_b200_exchange_interface over real NCCL on one GPU: a one-rank
+    communicator (unique id, comm init through the C ABI) and a plan whose
+    neighbour is the rank itself, so the grouped ncclSend/ncclRecv returns each
+    interface entry to its sender and the add doubles exactly those entries
+    (every other CSR value and b entry untouched)."""
+    import ctypes as C
+    from paper_1305_1489_b200 import _lib as L
+    from paper_1305_1489_b200.partition import slab, slab_pattern, upload_slab
+    from paper_1305_1489_b200.engine import CondensedSystem
+    from paper_1305_1489_b200.distributed import interface_positions
+    k = 2
+    mesh = HostMesh.box(3, 3, 4, bc="dirichlet_x")
+    eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
+    d2 = dim2(k)
+    m = 4 * d2
+    s = slab(mesh, 0, 2)
+    fb, nb, sl = slab_pattern(s)
+    sdm = upload_slab(s, torch.device("cuda"))
+    scs = CondensedSystem(cs.C[:s.elem_end * m * m], cs.Cf[:s.elem_end * m], None, m)
+    sysH = eng.assemble(sdm, eng.pattern_from_arrays(fb, nb, sl), scs)
+    v0, b0 = sysH.vals.clone(), sysH.b.clone()
+    faces = np.ascontiguousarray(s.interface.astype(np.int32))
+    fbc, nbc = np.ascontiguousarray(fb, np.int64), np.ascontiguousarray(nb, np.int32)
+    plan = C.c_void_p()
+    ranks, nf = np.array([0], np.int32), np.array([len(faces)], np.int32)
+    L.check(L.lib().hdg_b200_exchange_plan(eng._ctx, len(fbc) - 1, d2, fbc.ctypes.data, nbc.ctypes.data, 1,
+                                           ranks.ctypes.data, nf.ctypes.data, faces.ctypes.data, C.byref(plan)))
+    uid = (C.c_ubyte * 128)()
+    L.check(L.lib().hdg_b200_nccl_get_unique_id(uid))
+    comm = C.c_void_p()
+    L.check(L.lib().hdg_b200_nccl_comm_init(eng._ctx, 1, 0, uid, C.byref(comm)))
+    try:
+        L.check(L.lib().hdg_b200_exchange_interface(eng._ctx, plan, comm, sysH.vals.data_ptr(), sysH.b.data_ptr()))
+        eng.synchronize()
+    finally:
+        L.lib().hdg_b200_nccl_comm_destroy(comm)
+        L.lib().hdg_b200_exchange_free(plan)
+    pos = interface_positions(fb, nb, faces, d2)
+    nv = len(faces) * d2 * d2
+    want_v, want_b = v0.clone(), b0.clone()
+    want_v[torch.from_numpy(pos[:nv]).cuda()] *= 2
+    want_b[torch.from_numpy(pos[nv:]).cuda()] *= 2
+    assert torch.equal(sysH.vals, want_v) and torch.equal(sysH.b, want_b)
+    assert len(faces) > 0
