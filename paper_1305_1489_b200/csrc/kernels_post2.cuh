@@ -185,7 +185,11 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
         const double* Pd = tp.Pd + long(h) * nq * n + long(i) * nq;
         const double* Gh = G + h * nq4 * kPost2LDE;
         double acc[kPost2NT][2][2] = {};  // two chains per tile (k-step parity)
-#pragma unroll 4
+#ifndef HDG_K6_RUNROLL
+#define HDG_K6_RUNROLL 4
+#endif
+        constexpr int kRU = HDG_K6_RUNROLL;
+#pragma unroll kRU
         for (int kk = 0; kk < nq4 / 4; ++kk) {
           const int q = kk * 4 + t;
           const double a = (q < nq && i < n) ? __ldg(Pd + q) : 0.0;
