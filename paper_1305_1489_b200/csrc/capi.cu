@@ -19,6 +19,7 @@
 #include "kernels_post.cuh"
 #include "kernels_condense2.cuh"
 #include "kernels_condense3.cuh"
+#include "kernels_condense6.cuh"
 #include "kernels_condense5.cuh"
 #include "kernels_recover3.cuh"
 #include "kernels_boundary.cuh"
@@ -326,6 +327,10 @@ struct C3Launch {
   static constexpr int EPB = C3Cfg<K_>::EPB, THREADS = C3Cfg<K_>::NWT * 32;
 };
 
+struct C6Launch {  // one element per warp
+  static constexpr int EPB = C6Cfg::NW, THREADS = C6Cfg::NW * 32;
+};
+
 template <int K_>
 struct C5Launch {  // one element per CTA iteration
   static constexpr int EPB = 1, THREADS = C5Cfg<K_>::NWT * 32;
@@ -364,7 +369,13 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
 #endif
   if constexpr (K_ <= HDG_TEAM_MAXK)
     launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
-  else if constexpr (K_ <= 3)
+  else if constexpr (K_ == 3) {
+    static const bool v3 = std::getenv("HDG_K3_V3") != nullptr;  // diagnostics: the CTA-phase kernel
+    if (v3)
+      launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
+    else
+      launch_condense_impl<C6Dims, C6Launch>(c, condense6_kernel<C6Cfg::NW>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
+  } else if constexpr (K_ <= 3)
     launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
   else
     launch_condense_impl<C5Dims<K_>, C5Launch<K_>>(c, condense5_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
