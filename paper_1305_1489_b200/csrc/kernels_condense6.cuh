@@ -45,7 +45,8 @@ struct C6Dims {
   static constexpr int CH_SZ = 24 * LT, WT_SZ = D2 * LT;
   // per CTA: Chat_h row-major (rows / columns >= 20 zero), W^{l,mu} row-major, tauDD
   static constexpr int OFF_CH = 0, OFF_WT = OFF_CH + 3 * CH_SZ, OFF_DD = OFF_WT + 24 * WT_SZ;
-  static constexpr int CTA_EXTRA = round_up(OFF_DD + D2 * D2, 2);
+  static constexpr int OFF_ZR = round_up(OFF_DD + D2 * D2, 2);  // a zero row (LT)
+  static constexpr int CTA_EXTRA = OFF_ZR + LT;
   // per warp (all offsets even: 16-byte aligned)
   static constexpr int P_SQ = 0;                 // Mi (LQ), then S (LS), then Si (LQ)
   static constexpr int P_VT = P_SQ + 24 * LQ;    // V^T, M x LT; packed-Mi staging before that
@@ -65,6 +66,7 @@ static_assert(C6Dims::P_D % 2 == 0 && C6Dims::P_FG % 2 == 0 && C6Dims::PER_ELT %
 #ifndef HDG_C6_NW
 #define HDG_C6_NW 8
 #endif
+
 struct C6Cfg {
   static constexpr int NW = HDG_C6_NW;
 };
@@ -85,12 +87,11 @@ __device__ __forceinline__ int c6_kidx(int s, int t) { return s < 4 ? (s >> 1) *
 __device__ __forceinline__ void c6_rowfrag(const double* p, int t, double (&f)[5]) {
   const double2 a = *reinterpret_cast<const double2*>(p + 2 * t);
   const double2 b = *reinterpret_cast<const double2*>(p + 8 + 2 * t);
-  const double2 c = *reinterpret_cast<const double2*>(p + 16 + 2 * (t >> 1));
   f[0] = a.x;
   f[1] = a.y;
   f[2] = b.x;
   f[3] = b.y;
-  f[4] = (t & 1) ? c.y : c.x;
+  f[4] = p[16 + t];  // 2-way bank conflict: the wavefronts of a 16-byte load + select, no select
 }
 
 // the row strip x[n] (n = 0..2 column tiles over d3) of accumulator tiles as
@@ -123,6 +124,10 @@ __device__ __forceinline__ void c6_symfrag(const double* Q, int g, int t, double
   }
 }
 
+__device__ __forceinline__ void c6_sweep(double (&a)[C6Dims::D3], double* stage, int lane, double& pmin, double& pmax) {
+  gj_sweep_inverse<C6Dims::D3>(a, stage, lane, pmin, pmax);
+}
+
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
 condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
@@ -148,6 +153,8 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     WT[i] = k < D3 ? tab.Wlm[tb * D2 * D3 + r + k * D2] : 0.0;
   }
   for (int i = threadIdx.x; i < D2 * D2; i += blockDim.x) DDs[i] = tab.DD[i];
+  double* ZR = smem + Dm::OFF_ZR;
+  for (int i = threadIdx.x; i < LT; i += blockDim.x) ZR[i] = 0.0;
   __syncthreads();
 
   double* W0 = smem + Dm::CTA_EXTRA + warp * Dm::PER_ELT;
@@ -189,11 +196,49 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   const long wstride = long(gridDim.x) * NW;
   long K = long(blockIdx.x) * NW + warp;
   int cur = 0;
-  if (K < nelt) prefetch(K, 0);
-
-  for (; K < nelt; K += wstride, cur ^= 1) {
+  // packed M staged in Mp -> lane columns (lane c < D3 owns column c)
+  auto load_M = [&](double (&a)[D3], bool) {
+#pragma unroll
+    for (int i = 0; i < D3; ++i) {
+      const int r = i > lane ? i : lane, c = i > lane ? lane : i;
+      a[i] = lane < D3 ? Mp[sym_idx(r, c, D3)] : 0.0;
+    }
+  };
+  // M^-1 of element Kx (lane columns) -> SQ (stride LQ), its packed lower part
+  // -> recovery cache by one TMA bulk store (staged in VT, retired before VT
+  // is rewritten), pivot statistics
+  auto store_Mi = [&](const double (&a)[D3], long Kx, double pmin, double pmax) {
+    if (lane < D3) {
+#pragma unroll
+      for (int i = 0; i < D3; ++i) SQ[i * LQ + lane] = a[i];
+    }
+    if (factors) {
+      if (lane < D3) {
+        double* dst = VT + lane * (2 * D3 - lane + 1) / 2 - lane;
+#pragma unroll
+        for (int i = 0; i < D3; ++i)
+          if (i >= lane) dst[i] = a[i];
+      }
+      __syncwarp();
+      if (lane == 0) bulk_store(factors + Kx * Dm::FACTORS, VT, NSYM * 8);
+    }
+    if (lane == 0) store_pivstat(pivstat, Kx, 0, pmin, pmax);
+    __syncwarp();
+  };
+  if (K < nelt) {  // the first element's M^-1 on its own; later ones run inside the previous element's C phase
+    prefetch(K, 0);
     cp_async_wait_all();
     __syncwarp();
+    double a[D3];
+    load_M(a, true);
+    __syncwarp();
+    double pmin = 1e300, pmax = 0.0;
+    c6_sweep(a, ST, lane, pmin, pmax);
+    store_Mi(a, K, pmin, pmax);
+  }
+
+  for (; K < nelt; K += wstride, cur ^= 1) {
+    // (this element's inputs arrived before its M^-1)
     const double* fg = W0 + Dm::P_FG + cur * Dm::FG_SZ;
     const double* sg = fg + D3;
     // ---- derived scalars
@@ -218,40 +263,10 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
       DG[q] = v;
     }
-    __syncwarp();
-
-    // ---- M^-1: warp-register sweep (lane c owns column c)
     double mib[5][3];
-    {
-      double a[D3];
-#pragma unroll
-      for (int i = 0; i < D3; ++i) {
-        const int r = i > lane ? i : lane, c = i > lane ? lane : i;
-        a[i] = lane < D3 ? Mp[sym_idx(r, c, D3)] : 0.0;
-      }
-      __syncwarp();
-      double pmin = 1e300, pmax = 0.0;
-      gj_sweep_inverse<D3>(a, ST, lane, pmin, pmax);
-      if (lane < D3) {
-#pragma unroll
-        for (int i = 0; i < D3; ++i) SQ[i * LQ + lane] = a[i];
-      }
-      if (factors) {  // packed lower M^-1 -> recovery cache by one TMA bulk store (staged in VT)
-        if (lane < D3) {
-          double* dst = VT + lane * (2 * D3 - lane + 1) / 2 - lane;
-#pragma unroll
-          for (int i = 0; i < D3; ++i)
-            if (i >= lane) dst[i] = a[i];
-        }
-        __syncwarp();
-        if (lane == 0) bulk_store(factors + K * Dm::FACTORS, VT, NSYM * 8);
-      }
-      if (lane == 0) store_pivstat(pivstat, K, 0, pmin, pmax);
-      __syncwarp();
-      c6_symfrag(SQ, g, t, mib);
-      if (factors && lane == 0) bulk_store_wait_read();  // VT is rewritten below
-      __syncwarp();
-    }
+    c6_symfrag(SQ, g, t, mib);
+    if (factors && lane == 0) bulk_store_wait_read();  // the packed M^-1 staged in VT is read out
+    __syncwarp();
 
     // ---- per d3 row tile i: Y_h, R'_h, S row tiles, V^T column tile
     double gm[3][3];
@@ -260,7 +275,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int h2 = 0; h2 < 3; ++h2) gm[h][h2] = DG[Dm::DG_G + 3 * h + h2];
     const double vol = DG[Dm::DG_VOL];
-#pragma unroll 1
+#pragma unroll
     for (int i = 0; i < 3; ++i) {
       double y[3][3][2];
       double ca[3][5];
@@ -344,13 +359,17 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
         for (int jc = 0; jc < 5; ++jc) {
           const int c = 8 * jc + g, fc = c / D2;
-          double wa[5];
-          c6_rowfrag(WT + int(DG[Dm::DG_TB + fc]) + (c - fc * D2) * LT, t, wa);
+          const double* wr = WT + int(DG[Dm::DG_TB + fc]) + (c - fc * D2) * LT;
           double va[2] = {0.0, 0.0};
+          const int f0 = (8 * jc) / D2, f1 = (8 * jc + 7) / D2;  // faces the tile's rows span
 #pragma unroll
-          for (int f = (8 * jc) / D2; f <= (8 * jc + 7) / D2; ++f)  // faces the tile's rows span
+          for (int f = f0; f <= f1; ++f) {
+            // rows of another face read a zero row (masking by address, not by selects)
+            double wa[5];
+            c6_rowfrag(f0 == f1 || fc == f ? wr : ZR, t, wa);
 #pragma unroll
-            for (int s = 0; s < 5; ++s) dmma(va[0], va[1], fc == f ? wa[s] : 0.0, zf[f][s]);
+            for (int s = 0; s < 5; ++s) dmma(va[0], va[1], wa[s], zf[f][s]);
+          }
           const int r0 = 8 * i + 2 * t;
           if (r0 < LT) {
             const double v0 = r0 < nu ? va[0] : 0.0, v1 = r0 + 1 < nu ? va[1] : 0.0;
@@ -360,9 +379,9 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
     }
     __syncwarp();
-    // f of this element (the next prefetch reuses only the other slot)
     const long Kn = K + wstride;
-    if (Kn < nelt) prefetch(Kn, cur ^ 1);  // packed M, D of this element are dead
+    const bool has_next = Kn < nelt;
+    if (has_next) prefetch(Kn, cur ^ 1);  // packed M, D of this element are dead
 
     // ---- S^-1: sweep (S stored row-major with stride LS), then stored with stride LQ
     double sib[5][3];
@@ -372,7 +391,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       for (int i = 0; i < D3; ++i) a[i] = lane < D3 ? SQ[i * LS + lane] : 0.0;
       __syncwarp();
       double pmin = 1e300, pmax = 0.0;
-      gj_sweep_inverse<D3>(a, ST, lane, pmin, pmax);
+      c6_sweep(a, ST, lane, pmin, pmax);
       if (lane < D3) {
 #pragma unroll
         for (int i = 0; i < D3; ++i) SQ[i * LQ + lane] = a[i];
@@ -392,12 +411,13 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
 
     // ---- C, Cf and the Vs record, by m row tiles jc
-    double vfr[5][5], wfr[5][5];
+    // W rows of this lane in every m row tile (V^T and W fragments are
+    // reloaded per C tile: fewer live registers, measured faster than keeping them)
+    const double* wrow[5];
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
       const int c = 8 * j + g, fc = c / D2;
-      c6_rowfrag(VT + c * LT, t, vfr[j]);
-      c6_rowfrag(WT + int(DG[Dm::DG_TB + fc]) + (c - fc * D2) * LT, t, wfr[j]);
+      wrow[j] = WT + int(DG[Dm::DG_TB + fc]) + (c - fc * D2) * LT;
     }
     double fr[3][2];  // f at this lane's Vs rows 8n + 2t, + 1
 #pragma unroll
@@ -407,6 +427,9 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     double* Ck = Cout + K * M * M;
 #pragma unroll
     for (int jc = 0; jc < 5; ++jc) {
+      double vfr[5], wfr[5];
+      c6_rowfrag(VT + (8 * jc + g) * LT, t, vfr);
+      c6_rowfrag(wrow[jc], t, wfr);
       double vs[3][2], zp[3][2];
 #pragma unroll
       for (int n = 0; n < 3; ++n) vs[n][0] = vs[n][1] = zp[n][0] = zp[n][1] = 0.0;
@@ -414,8 +437,8 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       for (int s = 0; s < 5; ++s)
 #pragma unroll
         for (int n = 0; n < 3; ++n) {
-          dmma(vs[n][0], vs[n][1], vfr[jc][s], sib[s][n]);
-          dmma(zp[n][0], zp[n][1], wfr[jc][s], mib[s][n]);
+          dmma(vs[n][0], vs[n][1], vfr[s], sib[s][n]);
+          dmma(zp[n][0], zp[n][1], wfr[s], mib[s][n]);
         }
       const int r = 8 * jc + g;  // row of C / column of Vs
       {
@@ -439,10 +462,18 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int j = 0; j <= jc; ++j) {
         double c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
+        double wb[5], vb[5];
+        if (j < jc) {
+          c6_rowfrag(wrow[j], t, wb);
+          c6_rowfrag(VT + (8 * j + g) * LT, t, vb);
+        } else {
+#pragma unroll
+          for (int s = 0; s < 5; ++s) wb[s] = wfr[s], vb[s] = vfr[s];
+        }
 #pragma unroll
         for (int s = 0; s < 5; ++s) {
-          dmma(c1[0], c1[1], zpa[s], wfr[j][s]);
-          dmma(c2[0], c2[1], vsa[s], vfr[j][s]);
+          dmma(c1[0], c1[1], zpa[s], wb[s]);
+          dmma(c2[0], c2[1], vsa[s], vb[s]);
         }
         const int c0 = 8 * j + 2 * t;
         double val[2];
@@ -459,6 +490,16 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
     }
     __syncwarp();
+    if (has_next) {  // M^-1 of the next element (measured: interleaving its pivot steps with
+                     // this element's C tiles is slower, the sweep's DFMAs share the DMMA pipe)
+      double am[D3], pmin = 1e300, pmax = 0.0;
+      cp_async_wait_all();
+      __syncwarp();
+      load_M(am, true);
+      __syncwarp();
+      c6_sweep(am, ST, lane, pmin, pmax);
+      store_Mi(am, Kn, pmin, pmax);
+    }
   }
 }
 

@@ -10,7 +10,7 @@ build() {  # name, extra nvcc flags
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
     --expt-relaxed-constexpr $2 -c capi.cu -o /tmp/capi_$1.o
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/lib_$1.so /tmp/capi_$1.o \
-    mesh_dev.o host_tables.o host_mesh.o jit_quad.o -lcudart -lnvrtc
+    mesh_dev.o host_tables.o host_mesh.o jit_quad.o -lcudart -lnvrtc -ldl
 }
 for spec in "$@"; do
   IFS=, read name flags <<< "$spec"
