@@ -327,8 +327,9 @@ struct C3Launch {
   static constexpr int EPB = C3Cfg<K_>::EPB, THREADS = C3Cfg<K_>::NWT * 32;
 };
 
+template <int K_>
 struct C6Launch {  // one element per warp
-  static constexpr int EPB = C6Cfg::NW, THREADS = C6Cfg::NW * 32;
+  static constexpr int EPB = C6Cfg<K_>::NW, THREADS = C6Cfg<K_>::NW * 32;
 };
 
 template <int K_>
@@ -369,14 +370,14 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
 #endif
   if constexpr (K_ <= HDG_TEAM_MAXK)
     launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
-  else if constexpr (K_ == 3) {
+  else if constexpr (K_ <= 3) {
     static const bool v3 = std::getenv("HDG_K3_V3") != nullptr;  // diagnostics: the CTA-phase kernel
     if (v3)
       launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
     else
-      launch_condense_impl<C6Dims, C6Launch>(c, condense6_kernel<C6Cfg::NW>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
-  } else if constexpr (K_ <= 3)
-    launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
+      launch_condense_impl<C6Dims<K_>, C6Launch<K_>>(c, condense6_kernel<K_, C6Cfg<K_>::NW>, nelt, geo, Ms, Ds, fv,
+                                                     C, Cf, F, ps);
+  }
   else
     launch_condense_impl<C5Dims<K_>, C5Launch<K_>>(c, condense5_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
 }

@@ -1,4 +1,4 @@
-// K3 v6 (k = 3): static condensation, one warp per element, DMMA operands
+// K3 v6 (k = 2, 3): static condensation, one warp per element, DMMA operands
 // chained through registers.
 //
 // Same algebra as v3 (kernels_condense3.cuh): with Mi = M^-1 and
@@ -7,16 +7,16 @@
 //   S    = D + sum_h R'_h Chat_h^T         (= D + sum_s C_s M^-1 C_s^T)
 //   V^T  = W_l (sum_h beta_h(l) Y_h + T_l I)^T   per face l (rows of face l)
 //   Vs^T = V^T Si,   Zp^T = W Mi,   Si = S^-1
-//   C    = tauDD + (n_l1 . n_l2) o (Zp^T W^T) - Vs^T V^T^T,   Cf = Vs^T f
+//   C    = tauDD + (n_l1 . n_l2) o (Zp^T W^T) - Vs^T V,   Cf = Vs^T f
 // (C, Cf = A3 A1^-1 A2 + tauDD, A3 A1^-1 Af of local_solver.cpp:71-100).
 //
 // v3 ran every contraction as a CTA-wide phase over shared-memory operands
 // (five CTA barriers per batch, ~1.4 fragment loads per DMMA, the L1/shared
 // pipe at 71% while the DMMA pipe sat at 37%). Here one warp owns an
 // element from the packed M to the stored C, with no CTA barrier in the
-// element loop, and two warps share each SM sub-partition so one's sweep
-// inverse (DFMA-latency bound) overlaps the other's DMMA phases (one warp
-// with two independent accumulator chains already saturates its
+// element loop, and two or more warps share each SM sub-partition so one's
+// sweep inverse (DFMA-latency bound) overlaps another's DMMA phases (one
+// warp with two independent accumulator chains already saturates its
 // sub-partition's DMMA issue: 26-cycle latency, 16-cycle issue,
 // tools/microbench/dmma_lat.cu).
 //
@@ -24,51 +24,59 @@
 // (g, t); a DMMA A fragment wants A[g][k(t)], a B fragment B[k(t)][g]. So a
 // row strip of accumulator tiles IS a set of A (or, for the transposed
 // product, B) fragments if the contraction index runs in the permuted order
-// kidx: ksteps (tile 0, even), (tile 0, odd), (tile 1, even), (tile 1, odd)
-// take k = 2t, 2t + 1, 8 + 2t, 9 + 2t from the lane's own registers; the
-// fifth kstep (k = 16 + t, the last 4 of d3 = 20) is gathered by two
-// shuffles. The other operand is read in the same order from a k-fastest
-// table (row stride 24: two 16-byte loads give four ksteps, conflict-free).
-// Per element: 645 DMMA (as v3) and ~80 16-byte fragment loads + 30 8-byte
-// loads instead of ~900 8-byte loads.
+// kidx: per whole 8-column tile two ksteps k = 8n + 2t, 8n + 2t + 1 taken
+// from the lane's own registers; the d3 remainder (the last 4 of d3 = 20,
+// the last 2 of d3 = 10, zero-padded) as one natural kstep k = 8n + t
+// gathered by two shuffles. The other operand is read in the same order from
+// a k-fastest table (row stride 24: one 16-byte load gives a tile's two
+// ksteps, conflict-free).
 #pragma once
 
 #include "kernels_condense3.cuh"
 
 namespace hdgb {
 
+template <int K_>
 struct C6Dims {
-  static constexpr int D3 = 20, D2 = 10, M = 40, NSYM = 210;
+  static constexpr int D3 = cdim3(K_), D2 = cdim2(K_), M = 4 * cdim2(K_), NSYM = D3 * (D3 + 1) / 2;
+  static constexpr int NP = D3 / 8;                       // whole 8-wide tiles of d3
+  static constexpr int NT3 = (D3 + 7) / 8;                // d3 tiles (row / column)
+  static constexpr int KS = 2 * NP + (D3 % 8 ? 1 : 0);    // ksteps over d3
+  static constexpr int NTM = M / 8;                       // m tiles
   static constexpr int LT = 24;  // row stride of the k-fastest operands (Chat, W, V^T)
-  static constexpr int LQ = 26;  // Mi / Si storage: (row i, column c) at i * LQ + c
-  static constexpr int LS = 24;  // S storage for the sweep (row-major)
-  static constexpr int CH_SZ = 24 * LT, WT_SZ = D2 * LT;
-  // per CTA: Chat_h row-major (rows / columns >= 20 zero), W^{l,mu} row-major, tauDD
+  static constexpr int LQ = K_ == 3 ? 26 : 14;  // Mi / Si storage: (row i, column c) at i * LQ + c
+  static constexpr int LS = K_ == 3 ? 24 : 12;  // S storage for the sweep (row-major)
+  static constexpr int CH_SZ = NT3 * 8 * LT, WT_SZ = D2 * LT;
+  // per CTA: Chat_h row-major (rows / columns >= d3 zero), W^{l,mu} row-major, tauDD, a zero row
   static constexpr int OFF_CH = 0, OFF_WT = OFF_CH + 3 * CH_SZ, OFF_DD = OFF_WT + 24 * WT_SZ;
-  static constexpr int OFF_ZR = round_up(OFF_DD + D2 * D2, 2);  // a zero row (LT)
+  static constexpr int OFF_ZR = round_up(OFF_DD + D2 * D2, 2);
   static constexpr int CTA_EXTRA = OFF_ZR + LT;
-  // per warp (all offsets even: 16-byte aligned)
-  static constexpr int P_SQ = 0;                 // Mi (LQ), then S (LS), then Si (LQ)
-  static constexpr int P_VT = P_SQ + 24 * LQ;    // V^T, M x LT; packed-Mi staging before that
-  static constexpr int P_ST = P_VT + M * LT;     // sweep stage, 128
-  static constexpr int P_M = P_ST + 128;         // packed M of the element (cp.async)
-  static constexpr int P_D = P_M + NSYM;         // packed D
-  static constexpr int FG_SZ = 48;               // f (20) + geometry record (28)
-  static constexpr int P_FG = P_D + NSYM;        // 2 slots (current / next element)
-  static constexpr int P_DG = P_FG + 2 * FG_SZ;  // derived per-element scalars, 48
+  // per warp (every slot 16-byte aligned)
+  static constexpr int P_SQ = 0;                                 // Mi (LQ), then S (LS), then Si (LQ)
+  static constexpr int P_VT = P_SQ + round_up(D3 * LQ, 2);       // V^T, M x LT; packed-Mi staging before that
+  static constexpr int P_ST = P_VT + M * LT;                     // sweep stage, 128
+  static constexpr int P_M = P_ST + 128;                         // packed M of the element (cp.async)
+  static constexpr int P_D = P_M + round_up(NSYM, 2);            // packed D
+  static constexpr int FG_SZ = round_up(D3 + 28, 2);             // f + geometry record
+  static constexpr int P_FG = P_D + round_up(NSYM, 2);           // 2 slots (current / next element)
+  static constexpr int P_DG = P_FG + 2 * FG_SZ;                  // derived per-element scalars, 48
   static constexpr int PER_ELT = P_DG + 48;
   static constexpr int FACTORS = round_up(NSYM + D3 * M + D3, 2);
+  // the packed M^-1 record goes out by one TMA bulk store (a 16-byte multiple)
+  static constexpr bool BULK_MI = (NSYM * 8) % 16 == 0;
   // derived scalars (DG): g(h,h') 9, beta[f][h] 12, nn[l1][l2] 16, T 4, vol, table row base 4
   static constexpr int DG_G = 0, DG_B = 9, DG_NN = 21, DG_T = 37, DG_VOL = 41, DG_TB = 42;
 };
-static_assert(C6Dims::P_D % 2 == 0 && C6Dims::P_FG % 2 == 0 && C6Dims::PER_ELT % 2 == 0, "16-byte slots");
 
-#ifndef HDG_C6_NW
-#define HDG_C6_NW 8
+#ifndef HDG_C6_NW3
+#define HDG_C6_NW3 8
 #endif
-
+#ifndef HDG_C6_NW2
+#define HDG_C6_NW2 12
+#endif
+template <int K_>
 struct C6Cfg {
-  static constexpr int NW = HDG_C6_NW;
+  static constexpr int NW = K_ == 3 ? HDG_C6_NW3 : HDG_C6_NW2;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -80,62 +88,76 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) 
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem_src) : "memory");
 }
 
-// contraction index of kstep s (0..4) for lane t: the accumulator-chained order
-__device__ __forceinline__ int c6_kidx(int s, int t) { return s < 4 ? (s >> 1) * 8 + 2 * t + (s & 1) : 16 + t; }
-
-// five fragments of one k-fastest row (stride LT, 16-byte aligned) in kidx order
-__device__ __forceinline__ void c6_rowfrag(const double* p, int t, double (&f)[5]) {
-  const double2 a = *reinterpret_cast<const double2*>(p + 2 * t);
-  const double2 b = *reinterpret_cast<const double2*>(p + 8 + 2 * t);
-  f[0] = a.x;
-  f[1] = a.y;
-  f[2] = b.x;
-  f[3] = b.y;
-  f[4] = p[16 + t];  // 2-way bank conflict: the wavefronts of a 16-byte load + select, no select
+// contraction index of kstep s for lane t: the accumulator-chained order
+template <int K_>
+__device__ __forceinline__ int c6_kidx(int s, int t) {
+  constexpr int NP = C6Dims<K_>::NP;
+  return s < 2 * NP ? (s >> 1) * 8 + 2 * t + (s & 1) : 8 * NP + t;
 }
 
-// the row strip x[n] (n = 0..2 column tiles over d3) of accumulator tiles as
-// five kidx-ordered fragments (A of X, or B of X^T)
-__device__ __forceinline__ void c6_chain(const double (&x)[3][2], int lane, double (&f)[5]) {
-  f[0] = x[0][0];
-  f[1] = x[0][1];
-  f[2] = x[1][0];
-  f[3] = x[1][1];
-  const int src = (lane & ~3) | ((lane & 3) >> 1);
-  const double v0 = __shfl_sync(0xffffffffu, x[2][0], src);
-  const double v1 = __shfl_sync(0xffffffffu, x[2][1], src);
-  f[4] = (lane & 1) ? v1 : v0;
+// the KS fragments of one k-fastest row (stride LT, 16-byte aligned) in kidx order
+template <int K_>
+__device__ __forceinline__ void c6_rowfrag(const double* p, int t, double (&f)[C6Dims<K_>::KS]) {
+  using Dm = C6Dims<K_>;
+#pragma unroll
+  for (int n = 0; n < Dm::NP; ++n) {
+    const double2 a = *reinterpret_cast<const double2*>(p + 8 * n + 2 * t);
+    f[2 * n] = a.x;
+    f[2 * n + 1] = a.y;
+  }
+  // remainder kstep: a 2-way bank conflict, the wavefronts of a 16-byte load + select
+  if (Dm::KS > 2 * Dm::NP) f[2 * Dm::NP] = p[8 * Dm::NP + t];
+}
+
+// the row strip x[n] (n over the d3 column tiles) of accumulator tiles as
+// KS kidx-ordered fragments (A of X, or B of X^T)
+template <int K_>
+__device__ __forceinline__ void c6_chain(const double (&x)[C6Dims<K_>::NT3][2], int lane,
+                                         double (&f)[C6Dims<K_>::KS]) {
+  using Dm = C6Dims<K_>;
+#pragma unroll
+  for (int n = 0; n < Dm::NP; ++n) {
+    f[2 * n] = x[n][0];
+    f[2 * n + 1] = x[n][1];
+  }
+  if (Dm::KS > 2 * Dm::NP) {
+    const int src = (lane & ~3) | ((lane & 3) >> 1);
+    const double v0 = __shfl_sync(0xffffffffu, x[Dm::NT3 - 1][0], src);
+    const double v1 = __shfl_sync(0xffffffffu, x[Dm::NT3 - 1][1], src);
+    f[2 * Dm::NP] = (lane & 1) ? v1 : v0;
+  }
 }
 
 // B fragments b[s][n] = X[kidx(s)][8n + g] of a symmetric d3 x d3 inverse
 // stored by its sweep (Q[i * LQ + c] = lane c's column entry i); every
 // symmetric pair reads the lower-index lane's below-diagonal entry (the two
-// triangles of a sweep round differently, kernels_condense3.cuh)
-__device__ __forceinline__ void c6_symfrag(const double* Q, int g, int t, double (&b)[5][3]) {
+// triangles of a sweep round differently, kernels_condense3.cuh); k-padding
+// rows and columns >= d3 read as zero
+template <int K_>
+__device__ __forceinline__ void c6_symfrag(const double* Q, int g, int t,
+                                           double (&b)[C6Dims<K_>::KS][C6Dims<K_>::NT3]) {
+  using Dm = C6Dims<K_>;
 #pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const int k = c6_kidx(s, t);
+  for (int s = 0; s < Dm::KS; ++s) {
+    const int k = c6_kidx<K_>(s, t);
 #pragma unroll
-    for (int n = 0; n < 3; ++n) {
+    for (int n = 0; n < Dm::NT3; ++n) {
       const int col = 8 * n + g;
       const int hi = k > col ? k : col, lo = k > col ? col : k;
-      b[s][n] = col < C6Dims::D3 ? Q[hi * C6Dims::LQ + lo] : 0.0;
+      b[s][n] = (col < Dm::D3 && k < Dm::D3) ? Q[hi * Dm::LQ + lo] : 0.0;
     }
   }
 }
 
-__device__ __forceinline__ void c6_sweep(double (&a)[C6Dims::D3], double* stage, int lane, double& pmin, double& pmax) {
-  gj_sweep_inverse<C6Dims::D3>(a, stage, lane, pmin, pmax);
-}
-
-template <int NW>
+template <int K_, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
 condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
                  const double* __restrict__ Dsym, const double* __restrict__ fvec,
                  double* __restrict__ Cout, double* __restrict__ Cfout, double* __restrict__ factors,
                  double* __restrict__ pivstat) {
-  using Dm = C6Dims;
+  using Dm = C6Dims<K_>;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, NSYM = Dm::NSYM, LT = Dm::LT, LQ = Dm::LQ, LS = Dm::LS;
+  constexpr int KS = Dm::KS, NT3 = Dm::NT3, NTM = Dm::NTM;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -144,6 +166,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   double* CH = smem + Dm::OFF_CH;
   double* WT = smem + Dm::OFF_WT;
   double* DDs = smem + Dm::OFF_DD;
+  double* ZR = smem + Dm::OFF_ZR;
   for (int i = threadIdx.x; i < 3 * Dm::CH_SZ; i += blockDim.x) {
     const int h = i / Dm::CH_SZ, rem = i - h * Dm::CH_SZ, r = rem / LT, k = rem - r * LT;
     CH[i] = (r < D3 && k < D3) ? tab.Chat[h * D3 * D3 + r + k * D3] : 0.0;
@@ -153,7 +176,6 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     WT[i] = k < D3 ? tab.Wlm[tb * D2 * D3 + r + k * D2] : 0.0;
   }
   for (int i = threadIdx.x; i < D2 * D2; i += blockDim.x) DDs[i] = tab.DD[i];
-  double* ZR = smem + Dm::OFF_ZR;
   for (int i = threadIdx.x; i < LT; i += blockDim.x) ZR[i] = 0.0;
   __syncthreads();
 
@@ -165,8 +187,8 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   double* Dp = W0 + Dm::P_D;
   double* DG = W0 + Dm::P_DG;
   const int nu = tab.nu;
-  const bool al16 = ((reinterpret_cast<uintptr_t>(Msym) | reinterpret_cast<uintptr_t>(Dsym) |
-                      reinterpret_cast<uintptr_t>(fvec)) & 15) == 0;
+  const bool al16 = NSYM % 2 == 0 && ((reinterpret_cast<uintptr_t>(Msym) | reinterpret_cast<uintptr_t>(Dsym) |
+                                       reinterpret_cast<uintptr_t>(fvec)) & 15) == 0;
 
   // packed M, D, f and the geometry record of element K -> this warp's slot
   auto prefetch = [&](long K, int slot) {
@@ -192,12 +214,8 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     else if (lane < 30) cp_async4(reinterpret_cast<int*>(sg + 26) + (lane - 26), geo.perm + long(lane - 26) * nelt + K);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-
-  const long wstride = long(gridDim.x) * NW;
-  long K = long(blockIdx.x) * NW + warp;
-  int cur = 0;
   // packed M staged in Mp -> lane columns (lane c < D3 owns column c)
-  auto load_M = [&](double (&a)[D3], bool) {
+  auto load_M = [&](double (&a)[D3]) {
 #pragma unroll
     for (int i = 0; i < D3; ++i) {
       const int r = i > lane ? i : lane, c = i > lane ? lane : i;
@@ -205,40 +223,48 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
   };
   // M^-1 of element Kx (lane columns) -> SQ (stride LQ), its packed lower part
-  // -> recovery cache by one TMA bulk store (staged in VT, retired before VT
-  // is rewritten), pivot statistics
+  // -> recovery cache (k = 3: one TMA bulk store staged in VT, retired before
+  // VT is rewritten), pivot statistics
   auto store_Mi = [&](const double (&a)[D3], long Kx, double pmin, double pmax) {
     if (lane < D3) {
 #pragma unroll
       for (int i = 0; i < D3; ++i) SQ[i * LQ + lane] = a[i];
     }
     if (factors) {
+      double* dst = (Dm::BULK_MI ? VT : factors + Kx * Dm::FACTORS) + lane * (2 * D3 - lane + 1) / 2 - lane;
       if (lane < D3) {
-        double* dst = VT + lane * (2 * D3 - lane + 1) / 2 - lane;
 #pragma unroll
         for (int i = 0; i < D3; ++i)
           if (i >= lane) dst[i] = a[i];
       }
-      __syncwarp();
-      if (lane == 0) bulk_store(factors + Kx * Dm::FACTORS, VT, NSYM * 8);
+      if (Dm::BULK_MI) {
+        __syncwarp();
+        if (lane == 0) bulk_store(factors + Kx * Dm::FACTORS, VT, NSYM * 8);
+      }
     }
     if (lane == 0) store_pivstat(pivstat, Kx, 0, pmin, pmax);
     __syncwarp();
   };
-  if (K < nelt) {  // the first element's M^-1 on its own; later ones run inside the previous element's C phase
-    prefetch(K, 0);
+  // one M^-1: the packed M of element Kx must be in Mp
+  auto invert_M = [&](long Kx) {
+    double a[D3], pmin = 1e300, pmax = 0.0;
     cp_async_wait_all();
     __syncwarp();
-    double a[D3];
-    load_M(a, true);
+    load_M(a);
     __syncwarp();
-    double pmin = 1e300, pmax = 0.0;
-    c6_sweep(a, ST, lane, pmin, pmax);
-    store_Mi(a, K, pmin, pmax);
+    gj_sweep_inverse<D3>(a, ST, lane, pmin, pmax);
+    store_Mi(a, Kx, pmin, pmax);
+  };
+
+  const long wstride = long(gridDim.x) * NW;
+  long K = long(blockIdx.x) * NW + warp;
+  int cur = 0;
+  if (K < nelt) {  // the first element's M^-1; later ones follow the previous element's C phase
+    prefetch(K, 0);
+    invert_M(K);
   }
 
   for (; K < nelt; K += wstride, cur ^= 1) {
-    // (this element's inputs arrived before its M^-1)
     const double* fg = W0 + Dm::P_FG + cur * Dm::FG_SZ;
     const double* sg = fg + D3;
     // ---- derived scalars
@@ -263,9 +289,9 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
       DG[q] = v;
     }
-    double mib[5][3];
-    c6_symfrag(SQ, g, t, mib);
-    if (factors && lane == 0) bulk_store_wait_read();  // the packed M^-1 staged in VT is read out
+    double mib[KS][NT3];
+    c6_symfrag<K_>(SQ, g, t, mib);
+    if (Dm::BULK_MI && factors && lane == 0) bulk_store_wait_read();  // the packed M^-1 staged in VT is read out
     __syncwarp();
 
     // ---- per d3 row tile i: Y_h, R'_h, S row tiles, V^T column tile
@@ -276,49 +302,49 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       for (int h2 = 0; h2 < 3; ++h2) gm[h][h2] = DG[Dm::DG_G + 3 * h + h2];
     const double vol = DG[Dm::DG_VOL];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      double y[3][3][2];
-      double ca[3][5];
+    for (int i = 0; i < NT3; ++i) {
+      double y[3][NT3][2];
+      double ca[3][KS];
 #pragma unroll
-      for (int h = 0; h < 3; ++h) c6_rowfrag(CH + h * Dm::CH_SZ + (8 * i + g) * LT, t, ca[h]);
+      for (int h = 0; h < 3; ++h) c6_rowfrag<K_>(CH + h * Dm::CH_SZ + (8 * i + g) * LT, t, ca[h]);
 #pragma unroll
       for (int h = 0; h < 3; ++h)
 #pragma unroll
-        for (int n = 0; n < 3; ++n) y[h][n][0] = y[h][n][1] = 0.0;
+        for (int n = 0; n < NT3; ++n) y[h][n][0] = y[h][n][1] = 0.0;
 #pragma unroll
-      for (int s = 0; s < 5; ++s)
+      for (int s = 0; s < KS; ++s)
 #pragma unroll
         for (int h = 0; h < 3; ++h)
 #pragma unroll
-          for (int n = 0; n < 3; ++n) dmma(y[h][n][0], y[h][n][1], ca[h][s], mib[s][n]);
+          for (int n = 0; n < NT3; ++n) dmma(y[h][n][0], y[h][n][1], ca[h][s], mib[s][n]);
       // S row tiles j <= i: S = D + sum_h R'_h Chat_h^T
       {
-        double ra[3][5];
+        double ra[3][KS];
 #pragma unroll
         for (int h = 0; h < 3; ++h) {
-          double rp[3][2];
+          double rp[NT3][2];
 #pragma unroll
-          for (int n = 0; n < 3; ++n)
+          for (int n = 0; n < NT3; ++n)
 #pragma unroll
             for (int e = 0; e < 2; ++e)
               rp[n][e] = gm[0][h] * y[0][n][e] + gm[1][h] * y[1][n][e] + gm[2][h] * y[2][n][e];
-          c6_chain(rp, lane, ra[h]);
+          c6_chain<K_>(rp, lane, ra[h]);
         }
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
+        for (int j = 0; j < NT3; ++j) {
           if (j > i) break;
           double sa[2][2] = {{0, 0}, {0, 0}};
 #pragma unroll
           for (int h = 0; h < 3; ++h) {
-            double cb[5];
+            double cb[KS];
             if (j == i) {
 #pragma unroll
-              for (int s = 0; s < 5; ++s) cb[s] = ca[h][s];
+              for (int s = 0; s < KS; ++s) cb[s] = ca[h][s];
             } else {
-              c6_rowfrag(CH + h * Dm::CH_SZ + (8 * j + g) * LT, t, cb);
+              c6_rowfrag<K_>(CH + h * Dm::CH_SZ + (8 * j + g) * LT, t, cb);
             }
 #pragma unroll
-            for (int s = 0; s < 5; ++s) dmma(sa[s & 1][0], sa[s & 1][1], ra[h][s], cb[s]);
+            for (int s = 0; s < KS; ++s) dmma(sa[s & 1][0], sa[s & 1][1], ra[h][s], cb[s]);
           }
           // lower entries c <= r, mirrored: the sweep needs S exactly symmetric
           const int r = 8 * i + g;
@@ -336,28 +362,28 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
       // V^T column tile i: V^T[c][r] = sum_k W_l(c)[c'][k] Z_l[r][k], Z_l = sum_h beta_h(l) Y_h + T_l I
       {
-        double yb[3][5];
+        double yb[3][KS];
 #pragma unroll
         for (int h = 0; h < 3; ++h) {
-          double yy[3][2];
+          double yy[NT3][2];
 #pragma unroll
-          for (int n = 0; n < 3; ++n) yy[n][0] = y[h][n][0], yy[n][1] = y[h][n][1];
-          c6_chain(yy, lane, yb[h]);
+          for (int n = 0; n < NT3; ++n) yy[n][0] = y[h][n][0], yy[n][1] = y[h][n][1];
+          c6_chain<K_>(yy, lane, yb[h]);
         }
-        double zf[4][5];
+        double zf[4][KS];
 #pragma unroll
         for (int f = 0; f < 4; ++f) {
           const double b0 = DG[Dm::DG_B + 3 * f], b1 = DG[Dm::DG_B + 3 * f + 1], b2 = DG[Dm::DG_B + 3 * f + 2];
           const double Tf = DG[Dm::DG_T + f];
 #pragma unroll
-          for (int s = 0; s < 5; ++s) {
+          for (int s = 0; s < KS; ++s) {
             double z = b0 * yb[0][s] + b1 * yb[1][s] + b2 * yb[2][s];
-            if (c6_kidx(s, t) == 8 * i + g) z += Tf;
+            if (c6_kidx<K_>(s, t) == 8 * i + g) z += Tf;
             zf[f][s] = z;
           }
         }
 #pragma unroll
-        for (int jc = 0; jc < 5; ++jc) {
+        for (int jc = 0; jc < NTM; ++jc) {
           const int c = 8 * jc + g, fc = c / D2;
           const double* wr = WT + int(DG[Dm::DG_TB + fc]) + (c - fc * D2) * LT;
           double va[2] = {0.0, 0.0};
@@ -365,10 +391,10 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
           for (int f = f0; f <= f1; ++f) {
             // rows of another face read a zero row (masking by address, not by selects)
-            double wa[5];
-            c6_rowfrag(f0 == f1 || fc == f ? wr : ZR, t, wa);
+            double wa[KS];
+            c6_rowfrag<K_>(f0 == f1 || fc == f ? wr : ZR, t, wa);
 #pragma unroll
-            for (int s = 0; s < 5; ++s) dmma(va[0], va[1], wa[s], zf[f][s]);
+            for (int s = 0; s < KS; ++s) dmma(va[0], va[1], wa[s], zf[f][s]);
           }
           const int r0 = 8 * i + 2 * t;
           if (r0 < LT) {
@@ -384,21 +410,21 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     if (has_next) prefetch(Kn, cur ^ 1);  // packed M, D of this element are dead
 
     // ---- S^-1: sweep (S stored row-major with stride LS), then stored with stride LQ
-    double sib[5][3];
+    double sib[KS][NT3];
     {
       double a[D3];
 #pragma unroll
       for (int i = 0; i < D3; ++i) a[i] = lane < D3 ? SQ[i * LS + lane] : 0.0;
       __syncwarp();
       double pmin = 1e300, pmax = 0.0;
-      c6_sweep(a, ST, lane, pmin, pmax);
+      gj_sweep_inverse<D3>(a, ST, lane, pmin, pmax);
       if (lane < D3) {
 #pragma unroll
         for (int i = 0; i < D3; ++i) SQ[i * LQ + lane] = a[i];
       }
       if (lane == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
       __syncwarp();
-      c6_symfrag(SQ, g, t, sib);
+      c6_symfrag<K_>(SQ, g, t, sib);
       if (factors && lane < D3) {  // fs = S^-1 f (canonical entries)
         double s = 0.0;
 #pragma unroll
@@ -413,65 +439,71 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     // ---- C, Cf and the Vs record, by m row tiles jc
     // W rows of this lane in every m row tile (V^T and W fragments are
     // reloaded per C tile: fewer live registers, measured faster than keeping them)
-    const double* wrow[5];
+    const double* wrow[NTM];
 #pragma unroll
-    for (int j = 0; j < 5; ++j) {
+    for (int j = 0; j < NTM; ++j) {
       const int c = 8 * j + g, fc = c / D2;
       wrow[j] = WT + int(DG[Dm::DG_TB + fc]) + (c - fc * D2) * LT;
     }
-    double fr[3][2];  // f at this lane's Vs rows 8n + 2t, + 1
+    double fr[NT3][2];  // f at this lane's Vs rows 8n + 2t, + 1
 #pragma unroll
-    for (int n = 0; n < 3; ++n)
+    for (int n = 0; n < NT3; ++n)
 #pragma unroll
       for (int e = 0; e < 2; ++e) fr[n][e] = 8 * n + 2 * t + e < D3 ? fg[8 * n + 2 * t + e] : 0.0;
     double* Ck = Cout + K * M * M;
 #pragma unroll
-    for (int jc = 0; jc < 5; ++jc) {
-      double vfr[5], wfr[5];
-      c6_rowfrag(VT + (8 * jc + g) * LT, t, vfr);
-      c6_rowfrag(wrow[jc], t, wfr);
-      double vs[3][2], zp[3][2];
+    for (int jc = 0; jc < NTM; ++jc) {
+      double vfr[KS], wfr[KS];
+      c6_rowfrag<K_>(VT + (8 * jc + g) * LT, t, vfr);
+      c6_rowfrag<K_>(wrow[jc], t, wfr);
+      double vs[NT3][2], zp[NT3][2];
 #pragma unroll
-      for (int n = 0; n < 3; ++n) vs[n][0] = vs[n][1] = zp[n][0] = zp[n][1] = 0.0;
+      for (int n = 0; n < NT3; ++n) vs[n][0] = vs[n][1] = zp[n][0] = zp[n][1] = 0.0;
 #pragma unroll
-      for (int s = 0; s < 5; ++s)
+      for (int s = 0; s < KS; ++s)
 #pragma unroll
-        for (int n = 0; n < 3; ++n) {
+        for (int n = 0; n < NT3; ++n) {
           dmma(vs[n][0], vs[n][1], vfr[s], sib[s][n]);
           dmma(zp[n][0], zp[n][1], wfr[s], mib[s][n]);
         }
       const int r = 8 * jc + g;  // row of C / column of Vs
       {
         double p = 0.0;
+        double* rec = factors + K * Dm::FACTORS + NSYM + r * D3;
 #pragma unroll
-        for (int n = 0; n < 3; ++n) {
-          const int rr = 8 * n + 2 * t;
-          if (factors && rr < D3)
-            *reinterpret_cast<double2*>(factors + K * Dm::FACTORS + NSYM + rr + r * D3) =
-                make_double2(vs[n][0], vs[n][1]);
+        for (int n = 0; n < NT3; ++n) {
+          const int rr = 8 * n + 2 * t;  // d3 is even: a pair never straddles it
+          if (factors && rr < D3) {
+            if ((NSYM + D3) % 2 == 0) {  // 16-byte aligned pairs
+              *reinterpret_cast<double2*>(rec + rr) = make_double2(vs[n][0], vs[n][1]);
+            } else {
+              rec[rr] = vs[n][0];
+              rec[rr + 1] = vs[n][1];
+            }
+          }
           p += vs[n][0] * fr[n][0] + vs[n][1] * fr[n][1];
         }
         p += __shfl_xor_sync(FULL, p, 1);
         p += __shfl_xor_sync(FULL, p, 2);
         if (t == 0) Cfout[K * M + r] = p;
       }
-      double vsa[5], zpa[5];
-      c6_chain(vs, lane, vsa);
-      c6_chain(zp, lane, zpa);
+      double vsa[KS], zpa[KS];
+      c6_chain<K_>(vs, lane, vsa);
+      c6_chain<K_>(zp, lane, zpa);
       const int l1 = r / D2;
 #pragma unroll
       for (int j = 0; j <= jc; ++j) {
         double c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
-        double wb[5], vb[5];
+        double wb[KS], vb[KS];
         if (j < jc) {
-          c6_rowfrag(wrow[j], t, wb);
-          c6_rowfrag(VT + (8 * j + g) * LT, t, vb);
+          c6_rowfrag<K_>(wrow[j], t, wb);
+          c6_rowfrag<K_>(VT + (8 * j + g) * LT, t, vb);
         } else {
 #pragma unroll
-          for (int s = 0; s < 5; ++s) wb[s] = wfr[s], vb[s] = vfr[s];
+          for (int s = 0; s < KS; ++s) wb[s] = wfr[s], vb[s] = vfr[s];
         }
 #pragma unroll
-        for (int s = 0; s < 5; ++s) {
+        for (int s = 0; s < KS; ++s) {
           dmma(c1[0], c1[1], zpa[s], wb[s]);
           dmma(c2[0], c2[1], vsa[s], vb[s]);
         }
@@ -490,16 +522,9 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
     }
     __syncwarp();
-    if (has_next) {  // M^-1 of the next element (measured: interleaving its pivot steps with
-                     // this element's C tiles is slower, the sweep's DFMAs share the DMMA pipe)
-      double am[D3], pmin = 1e300, pmax = 0.0;
-      cp_async_wait_all();
-      __syncwarp();
-      load_M(am, true);
-      __syncwarp();
-      c6_sweep(am, ST, lane, pmin, pmax);
-      store_Mi(am, Kn, pmin, pmax);
-    }
+    // M^-1 of the next element (measured: interleaving its pivot steps with
+    // this element's C tiles is slower, the sweep's DFMAs share the DMMA pipe)
+    if (has_next) invert_M(Kn);
   }
 }
 
