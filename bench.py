@@ -623,10 +623,10 @@ def run_ours(args):
     hbm_peak, hbm_src = load_peaks()
     k3_ms = stage_ms.get("condense", float("nan"))
     achieved = k3_flops(k) * nelt / (k3_ms / 1e3) / 1e12
-    kname3 = f"condense3_kernel<{k}>" if k in (2, 3) else (f"condense2_kernel<{k}>" if k <= 1 else
-                                                           f"condense5_kernel<{k}>")
+    kname3 = f"condense6_kernel<{k}" if k in (2, 3) else (f"condense2_kernel<{k}>" if k <= 1 else
+                                                          f"condense5_kernel<{k}>")
     traffic, traffic_src = ncu_traffic(kname3)
-    roof = {"kernel": f"{kname3} (K3)", "bound": "tensor", "achieved": achieved,
+    roof = {"kernel": (kname3 + (", warps>" if k in (2, 3) else "")) + " (K3)", "bound": "tensor", "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
             "traffic": traffic if cfg.name == "C2" and world == 1 else None,
             "traffic_source": traffic_src,

@@ -18,7 +18,6 @@
 #include "kernels_misc.cuh"
 #include "kernels_post.cuh"
 #include "kernels_condense2.cuh"
-#include "kernels_condense3.cuh"
 #include "kernels_condense6.cuh"
 #include "kernels_condense5.cuh"
 #include "kernels_recover3.cuh"
@@ -321,12 +320,6 @@ int factor_doubles(int k) {
   return (d3 * (d3 + 1) / 2 + d3 * m + d3 + 1) / 2 * 2;
 }
 
-// launch shape of the CTA-batched kernel in the (NW, EPB) vocabulary
-template <int K_>
-struct C3Launch {
-  static constexpr int EPB = C3Cfg<K_>::EPB, THREADS = C3Cfg<K_>::NWT * 32;
-};
-
 template <int K_>
 struct C6Launch {  // one element per warp
   static constexpr int EPB = C6Cfg<K_>::NW, THREADS = C6Cfg<K_>::NW * 32;
@@ -359,9 +352,10 @@ void launch_condense_impl(hdg_ctx* c, Kern kern, int nelt, const GeoDev& geo, co
   CUDA_OK(cudaGetLastError());
 }
 
-// k <= 1: per-element warp teams (kernels_condense2.cuh); k = 2, 3: CTA-batched
-// phases (kernels_condense3.cuh); k = 4, 5: one element per CTA iteration
-// (kernels_condense5.cuh). All write the recovery cache {M^-1, S^-1, V, f}.
+// k <= 1: per-element warp teams (kernels_condense2.cuh); k = 2, 3: one warp
+// per element, register-chained DMMA (kernels_condense6.cuh); k = 4, 5: one
+// element per CTA iteration (kernels_condense5.cuh). All write the recovery
+// cache (factor_doubles) read by launch_recover.
 template <int K_>
 void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, const double* Ds,
                      const double* fv, double* C, double* Cf, double* F, double* ps) {
@@ -370,14 +364,9 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
 #endif
   if constexpr (K_ <= HDG_TEAM_MAXK)
     launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
-  else if constexpr (K_ <= 3) {
-    static const bool v3 = std::getenv("HDG_K3_V3") != nullptr;  // diagnostics: the CTA-phase kernel
-    if (v3)
-      launch_condense_impl<C3Dims<K_>, C3Launch<K_>>(c, condense3_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
-    else
-      launch_condense_impl<C6Dims<K_>, C6Launch<K_>>(c, condense6_kernel<K_, C6Cfg<K_>::NW>, nelt, geo, Ms, Ds, fv,
-                                                     C, Cf, F, ps);
-  }
+  else if constexpr (K_ <= 3)
+    launch_condense_impl<C6Dims<K_>, C6Launch<K_>>(c, condense6_kernel<K_, C6Cfg<K_>::NW>, nelt, geo, Ms, Ds, fv,
+                                                   C, Cf, F, ps);
   else
     launch_condense_impl<C5Dims<K_>, C5Launch<K_>>(c, condense5_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
 }

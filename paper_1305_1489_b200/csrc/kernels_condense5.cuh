@@ -24,7 +24,18 @@
 #pragma once
 
 #include "kernels_condense2.cuh"
-#include "kernels_condense3.cuh"
+
+namespace hdgb {
+// Most 8-column tiles one face's d2 columns (starting at l d2) touch.
+constexpr int face_tiles(int d2) {
+  int n = 0;
+  for (int l = 0; l < 4; ++l) {
+    const int t = (l * d2 + d2 - 1) / 8 - (l * d2) / 8 + 1;
+    n = t > n ? t : n;
+  }
+  return n;
+}
+}  // namespace hdgb
 
 namespace hdgb {
 

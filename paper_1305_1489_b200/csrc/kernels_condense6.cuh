@@ -1,7 +1,7 @@
 // K3 v6 (k = 2, 3): static condensation, one warp per element, DMMA operands
 // chained through registers.
 //
-// Same algebra as v3 (kernels_condense3.cuh): with Mi = M^-1 and
+// Same algebra as the round-1 CTA-phase kernel (v3): with Mi = M^-1 and
 //   Y_h  = Chat_h Mi                       (d3 x d3, h = reference direction)
 //   R'_h = sum_h' g(h', h) Y_h'            (g = a^T a)
 //   S    = D + sum_h R'_h Chat_h^T         (= D + sum_s C_s M^-1 C_s^T)
@@ -32,7 +32,7 @@
 // ksteps, conflict-free).
 #pragma once
 
-#include "kernels_condense3.cuh"
+#include "kernels_condense2.cuh"
 
 namespace hdgb {
 
@@ -131,7 +131,7 @@ __device__ __forceinline__ void c6_chain(const double (&x)[C6Dims<K_>::NT3][2], 
 // B fragments b[s][n] = X[kidx(s)][8n + g] of a symmetric d3 x d3 inverse
 // stored by its sweep (Q[i * LQ + c] = lane c's column entry i); every
 // symmetric pair reads the lower-index lane's below-diagonal entry (the two
-// triangles of a sweep round differently, kernels_condense3.cuh); k-padding
+// triangles of a sweep round differently); k-padding
 // rows and columns >= d3 read as zero
 template <int K_>
 __device__ __forceinline__ void c6_symfrag(const double* Q, int g, int t,

@@ -6,7 +6,7 @@ mkdir -p gpurun_out/ncu
 N="ncu --set full --clock-control none --import-source on"
 specs=("$@")
 if [ ${#specs[@]} -eq 0 ]; then
-  specs=(k3_c2:condense3_kernel:C2:none k3_c4:condense3_kernel:C4:none k3_c3:condense5_kernel:C3:none
+  specs=(k3_c2:condense6_kernel:C2:none k3_c4:condense6_kernel:C4:none k3_c3:condense5_kernel:C3:none
          k6_c5:postprocess2_kernel:C5:post k4_c2:scatter_faces:C2:scatter k7_c4:convection_kernel:C4:conv
          k2_c2:quad_build:C2:none k5_c2:recover3:C2:none)
 fi

@@ -1,5 +1,5 @@
 """One pass of a config's pipeline at full size (for ncu captures of a single
-kernel, e.g. ncu -k regex:condense3 -c 1 python tools/diag/run_config.py C4):
+kernel, e.g. ncu -k regex:condense6 -c 1 python tools/diag/run_config.py C4):
 geometry (+ upwind tau), build+condense, recover, then per config the
 postprocess (C5), the convection block (C4), and the face-ordered scatter."""
 import os
