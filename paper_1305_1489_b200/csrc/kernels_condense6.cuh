@@ -60,7 +60,12 @@ struct C6Dims {
   static constexpr int FG_SZ = round_up(D3 + 28, 2);             // f + geometry record
   static constexpr int P_FG = P_D + round_up(NSYM, 2);           // 2 slots (current / next element)
   static constexpr int P_DG = P_FG + 2 * FG_SZ;                  // derived per-element scalars, 48
-  static constexpr int PER_ELT = P_DG + 48;
+  // k = 3: M^-1 kept in its own buffer (stride d3), its fragments reloaded per
+  // row tile and for the C phase instead of held in registers (measured
+  // 4.00 -> 3.94 ms at C2; at k = 2 no gain)
+  static constexpr bool MIQ = K_ == 3;
+  static constexpr int P_MQ = P_DG + 48;
+  static constexpr int PER_ELT = P_MQ + (MIQ ? round_up(D3 * D3, 2) : 0);
   static constexpr int FACTORS = round_up(NSYM + D3 * M + D3, 2);
   // the packed M^-1 record goes out by one TMA bulk store (a 16-byte multiple)
   static constexpr bool BULK_MI = (NSYM * 8) % 16 == 0;
@@ -133,7 +138,7 @@ __device__ __forceinline__ void c6_chain(const double (&x)[C6Dims<K_>::NT3][2], 
 // symmetric pair reads the lower-index lane's below-diagonal entry (the two
 // triangles of a sweep round differently); k-padding
 // rows and columns >= d3 read as zero
-template <int K_>
+template <int K_, int LDQ = C6Dims<K_>::LQ>
 __device__ __forceinline__ void c6_symfrag(const double* Q, int g, int t,
                                            double (&b)[C6Dims<K_>::KS][C6Dims<K_>::NT3]) {
   using Dm = C6Dims<K_>;
@@ -144,7 +149,7 @@ __device__ __forceinline__ void c6_symfrag(const double* Q, int g, int t,
     for (int n = 0; n < Dm::NT3; ++n) {
       const int col = 8 * n + g;
       const int hi = k > col ? k : col, lo = k > col ? col : k;
-      b[s][n] = (col < Dm::D3 && k < Dm::D3) ? Q[hi * Dm::LQ + lo] : 0.0;
+      b[s][n] = (col < Dm::D3 && k < Dm::D3) ? Q[hi * LDQ + lo] : 0.0;
     }
   }
 }
@@ -186,6 +191,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   double* Mp = W0 + Dm::P_M;
   double* Dp = W0 + Dm::P_D;
   double* DG = W0 + Dm::P_DG;
+  double* MQ = W0 + Dm::P_MQ;
   const int nu = tab.nu;
   const bool al16 = NSYM % 2 == 0 && ((reinterpret_cast<uintptr_t>(Msym) | reinterpret_cast<uintptr_t>(Dsym) |
                                        reinterpret_cast<uintptr_t>(fvec)) & 15) == 0;
@@ -228,7 +234,10 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   auto store_Mi = [&](const double (&a)[D3], long Kx, double pmin, double pmax) {
     if (lane < D3) {
 #pragma unroll
-      for (int i = 0; i < D3; ++i) SQ[i * LQ + lane] = a[i];
+      for (int i = 0; i < D3; ++i) {
+        if (Dm::MIQ) MQ[i * D3 + lane] = a[i];
+        else SQ[i * LQ + lane] = a[i];
+      }
     }
     if (factors) {
       double* dst = (Dm::BULK_MI ? VT : factors + Kx * Dm::FACTORS) + lane * (2 * D3 - lane + 1) / 2 - lane;
@@ -264,7 +273,14 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     invert_M(K);
   }
 
+#ifdef HDG_C6_CLK  // diagnostics build: per-phase clocks of each element into Cf[K][0..5]
+  long long clk[6];
+#define C6_CLK(i) clk[i] = clock64()
+#else
+#define C6_CLK(i)
+#endif
   for (; K < nelt; K += wstride, cur ^= 1) {
+    C6_CLK(0);
     const double* fg = W0 + Dm::P_FG + cur * Dm::FG_SZ;
     const double* sg = fg + D3;
     // ---- derived scalars
@@ -290,10 +306,11 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       DG[q] = v;
     }
     double mib[KS][NT3];
-    c6_symfrag<K_>(SQ, g, t, mib);
+    if (!Dm::MIQ) c6_symfrag<K_>(SQ, g, t, mib);
     if (Dm::BULK_MI && factors && lane == 0) bulk_store_wait_read();  // the packed M^-1 staged in VT is read out
     __syncwarp();
 
+    C6_CLK(1);
     // ---- per d3 row tile i: Y_h, R'_h, S row tiles, V^T column tile
     double gm[3][3];
 #pragma unroll
@@ -303,6 +320,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     const double vol = DG[Dm::DG_VOL];
 #pragma unroll
     for (int i = 0; i < NT3; ++i) {
+      if (Dm::MIQ) c6_symfrag<K_, D3>(MQ, g, t, mib);
       double y[3][NT3][2];
       double ca[3][KS];
 #pragma unroll
@@ -405,6 +423,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
     }
     __syncwarp();
+    C6_CLK(2);
     const long Kn = K + wstride;
     const bool has_next = Kn < nelt;
     if (has_next) prefetch(Kn, cur ^ 1);  // packed M, D of this element are dead
@@ -436,6 +455,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
     }
 
+    C6_CLK(3);
     // ---- C, Cf and the Vs record, by m row tiles jc
     // W rows of this lane in every m row tile (V^T and W fragments are
     // reloaded per C tile: fewer live registers, measured faster than keeping them)
@@ -451,6 +471,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int e = 0; e < 2; ++e) fr[n][e] = 8 * n + 2 * t + e < D3 ? fg[8 * n + 2 * t + e] : 0.0;
     double* Ck = Cout + K * M * M;
+    if (Dm::MIQ) c6_symfrag<K_, D3>(MQ, g, t, mib);
 #pragma unroll
     for (int jc = 0; jc < NTM; ++jc) {
       double vfr[KS], wfr[KS];
@@ -524,7 +545,13 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     __syncwarp();
     // M^-1 of the next element (measured: interleaving its pivot steps with
     // this element's C tiles is slower, the sweep's DFMAs share the DMMA pipe)
+    C6_CLK(4);
     if (has_next) invert_M(Kn);
+#ifdef HDG_C6_CLK
+    C6_CLK(5);
+    __syncwarp();
+    if (lane < 5) Cfout[K * M + lane] = double(clk[lane + 1] - clk[lane]);
+#endif
   }
 }
 
