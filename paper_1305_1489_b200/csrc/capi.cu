@@ -279,6 +279,10 @@ struct hdg_ctx {
   int* d_adj = nullptr;     // boundary face -> 4 K + l (neumann_load)
   double* d_ksamp = nullptr;  // kappa sampled at the postprocess nodes (JIT sampler)
   size_t ksamp_len = 0;
+  double* d_bsamp = nullptr;  // program beta components sampled at the convection points (JIT sampler)
+  size_t bsamp_len = 0;
+  double* d_cbary = nullptr;  // convection points: volume nodes + element-parametrised face points (npts x 4)
+  int cbary_k = -1;
   int adj_len = 0;
   cudaEvent_t ev[2 * HDG_NSTAGES] = {};
   bool pending[HDG_NSTAGES] = {};
@@ -807,6 +811,8 @@ void hdg_b200_destroy(hdg_ctx* c) {
   if (c->d_adj) cudaFree(c->d_adj);
   if (c->d_zero_T) cudaFree(c->d_zero_T);
   if (c->d_ksamp) cudaFree(c->d_ksamp);
+  if (c->d_bsamp) cudaFree(c->d_bsamp);
+  if (c->d_cbary) cudaFree(c->d_cbary);
   if (c->d_rescue) cudaFree(c->d_rescue);
   if (c->d_bad) cudaFree(c->d_bad);
   if (c->h_bad) cudaFreeHost(c->h_bad);
@@ -1443,6 +1449,50 @@ int hdg_b200_convection_block(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_f
     const DevTab& t = c->tab[0].dev;
     if (t.Aconv) {  // k <= 3: CTA-batched, the volume block on DMMA (kernels_conv2.cuh)
       const Conv2Dims cd(t.d3, t.d2, t.nq, t.nqd);
+      // program beta components are sampled once per point by an NVRTC-compiled
+      // sampler (the volume nodes, then the element-parametrised face points),
+      // so the kernel reads samples instead of interpreting the programs
+      FieldDev fb[3] = {to_dev(bx, "bx"), to_dev(by, "by"), to_dev(bz, "bz")};
+      const hdg_field* hb[3] = {&bx, &by, &bz};
+      const int npts = t.nq + 4 * t.nqd;
+      if (c->jit && (bx.kind == HDG_FIELD_PROGRAM || by.kind == HDG_FIELD_PROGRAM || bz.kind == HDG_FIELD_PROGRAM)) {
+        if (c->cbary_k != t.k) {
+          if (c->d_cbary) cudaFree(c->d_cbary);
+          c->d_cbary = nullptr;
+          CUDA_OK(cudaMalloc(&c->d_cbary, sizeof(double) * 4 * npts));
+          conv_points_kernel<<<1, 256, 0, c->stream>>>(t, c->d_cbary);
+          CUDA_OK(cudaGetLastError());
+          c->cbary_k = t.k;
+        }
+        const size_t len = size_t(3) * npts * nelt;
+        if (c->bsamp_len < len) {
+          if (c->d_bsamp) cudaFree(c->d_bsamp);
+          c->d_bsamp = nullptr;
+          CUDA_OK(cudaMalloc(&c->d_bsamp, len * sizeof(double)));
+          c->bsamp_len = len;
+        }
+        for (int h = 0; h < 3; ++h) {
+          if (hb[h]->kind != HDG_FIELD_PROGRAM) continue;
+          std::string err;
+          CUfunction fn = jit_sample_kernel(*hb[h], &err);  // out[K * npts + p]
+          if (!fn) {
+            c->jit_error = err;
+            continue;
+          }
+          int nel = nelt, np = npts;
+          const double *bary = c->d_cbary, *V = geo.verts;
+          double* out = c->d_bsamp + size_t(h) * npts * nelt;
+          void* args[] = {&nel, &np, &bary, &V, &out};
+          const int grid = int(std::min<long>((long(npts) * nelt + 255) / 256, long(c->sms) * 16));
+          if (launch_quad_jit(fn, c->stream, grid, 256, 0, args, &err)) {
+            fb[h].kind = HDG_FIELD_SAMPLED;
+            fb[h].samples = out;
+            c->jit_error.clear();
+          } else {
+            c->jit_error = err;
+          }
+        }
+      }
       const size_t smem = size_t(cd.total) * sizeof(double);
       auto go = [&](auto kern) {
         CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1450,8 +1500,7 @@ int hdg_b200_convection_block(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_f
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kConv2Threads, smem));
         const long need = (long(nelt) + kConv2EB - 1) / kConv2EB;
         const int grid = int(std::min<long>(need, long(c->sms) * std::max(occ, 1)));
-        kern<<<grid, kConv2Threads, smem, c->stream>>>(t, nelt, geo, to_dev(bx, "bx"), to_dev(by, "by"),
-                                                       to_dev(bz, "bz"), vol, dp, dd);
+        kern<<<grid, kConv2Threads, smem, c->stream>>>(t, nelt, geo, fb[0], fb[1], fb[2], npts, vol, dp, dd);
       };
       switch (t.k) {
         case 0: go(convection2_kernel<0>); break;

@@ -297,7 +297,7 @@ CUfunction compile_cached(const std::string& src, const char* name, std::string*
   }
   char key_prefix[32];
   std::snprintf(key_prefix, sizeof key_prefix, "%p\n", static_cast<void*>(ctx));
-  const std::string key = key_prefix + src;
+  const std::string key = key_prefix + std::string(name) + "\n" + src;  // one module may hold several kernels
   auto it = C.fn.find(key);
   if (it != C.fn.end()) return it->second;
   auto bin = C.cubin.find(src);

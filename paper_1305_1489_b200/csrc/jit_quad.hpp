@@ -44,6 +44,7 @@ struct JitKernel {
 JitKernel jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_field& f, int eb, int nqp,
                           std::string* err);
 // Kernel sampling a PROGRAM field at every element node (SAMPLED layout), or nullptr.
+// A program field sampled at every point of a table (out[K * npoints + p]).
 CUfunction jit_sample_kernel(const hdg_field& f, std::string* err);
 bool launch_quad_jit(CUfunction fn, cudaStream_t stream, int grid, int block, size_t smem, void** args,
                      std::string* err);

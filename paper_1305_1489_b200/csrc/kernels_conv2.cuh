@@ -36,9 +36,36 @@ struct Conv2Dims {
   }
 };
 
+// The convection points of degree tab.k: the nq volume nodes, then face l's
+// element-parametrised points (face_points_physical, element_matrices.cpp:
+// 72-82) for l = 0..3, as barycentric weights of the element's vertices
+// (npts x 4, column-major): the JIT sampler's point table (SAMPLED beta is
+// read at K * npts + point).
+__global__ void conv_points_kernel(DevTab tab, double* __restrict__ out) {
+  const int nq = tab.nq, nqd = tab.nqd, npts = nq + 4 * nqd;
+  for (int p = threadIdx.x; p < npts; p += blockDim.x) {
+    double b[4];
+    if (p < nq) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) b[v] = tab.bary[v * nq + p];
+    } else {
+      const int l = (p - nq) / nqd, r = (p - nq) - l * nqd;
+      const double s = tab.tri_bary[nqd + r], tt = tab.tri_bary[2 * nqd + r];
+      const double px = l == 2 ? 0.0 : s, py = l == 1 ? 0.0 : (l == 2 ? s : tt),
+                   pz = l == 0 ? 0.0 : (l == 3 ? 1.0 - s - tt : tt);
+      b[0] = 1.0 - (px + py + pz);
+      b[1] = px;
+      b[2] = py;
+      b[3] = pz;
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) out[v * npts + p] = b[v];
+  }
+}
+
 template <int K_>
 __global__ void __launch_bounds__(kConv2Threads)
-convection2_kernel(DevTab tab, int nelt, GeoDev geo, FieldDev bx, FieldDev by, FieldDev bz,
+convection2_kernel(DevTab tab, int nelt, GeoDev geo, FieldDev bx, FieldDev by, FieldDev bz, int npts,
                    double* __restrict__ vol, double* __restrict__ dp, double* __restrict__ dd) {
   extern __shared__ __align__(16) double csm[];
   constexpr int d3 = cdim3(K_), d2 = cdim2(K_), m = 4 * d2, dd3 = d3 * d3;
@@ -50,6 +77,7 @@ convection2_kernel(DevTab tab, int nelt, GeoDev geo, FieldDev bx, FieldDev by, F
   double* Dps = csm + cd.off_dp;
   double* Pfs = csm + cd.off_pf;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const bool any_prog = bx.kind == HDG_FIELD_PROGRAM || by.kind == HDG_FIELD_PROGRAM || bz.kind == HDG_FIELD_PROGRAM;
   for (int i = tid; i < 6 * nqd * d2; i += kConv2Threads) Dps[i] = tab.Dperm[i];
   for (int i = tid; i < 4 * nqd * d3; i += kConv2Threads) Pfs[i] = tab.Pface[i];
   for (int i = tid; i < 3 * cd.nqp * kConv2LDE; i += kConv2Threads) gam[i] = 0.0;  // node padding stays zero
@@ -70,16 +98,19 @@ convection2_kernel(DevTab tab, int nelt, GeoDev geo, FieldDev bx, FieldDev by, F
     }
     __syncthreads();
     // beta at the volume nodes -> gamma_# (B operand), and at the element's face points
+    auto beta = [&](const FieldDev& F, double x, double y, double z, int p, long K) {
+      return eval_field(F, x, y, z, p, K, npts);
+    };
     for (int idx = tid; idx < kConv2EB * nq; idx += kConv2Threads) {
       const int e = idx / nq, q = idx - e * nq;
       const long K = K0 + e;
       double gv[3] = {0.0, 0.0, 0.0};
       if (K < nelt) {
-        double x, y, z;
-        elem_point(geo, K, nelt, __ldg(tab.bary + q), __ldg(tab.bary + nq + q), __ldg(tab.bary + 2 * nq + q),
-                   __ldg(tab.bary + 3 * nq + q), x, y, z);
-        const double b0 = eval_field(bx, x, y, z, q, K, nq), b1 = eval_field(by, x, y, z, q, K, nq),
-                     b2 = eval_field(bz, x, y, z, q, K, nq);
+        double x = 0.0, y = 0.0, z = 0.0;
+        if (any_prog)
+          elem_point(geo, K, nelt, __ldg(tab.bary + q), __ldg(tab.bary + nq + q), __ldg(tab.bary + 2 * nq + q),
+                     __ldg(tab.bary + 3 * nq + q), x, y, z);
+        const double b0 = beta(bx, x, y, z, q, K), b1 = beta(by, x, y, z, q, K), b2 = beta(bz, x, y, z, q, K);
         const double wq = __ldg(tab.w + q) / 6.0;
         const double* a9 = sg + 32 * e + 1;
 #pragma unroll
@@ -97,10 +128,10 @@ convection2_kernel(DevTab tab, int nelt, GeoDev geo, FieldDev bx, FieldDev by, F
         // face l's element-parametrised points (element_matrices.cpp:72-82)
         const double px = l == 2 ? 0.0 : s, py = l == 1 ? 0.0 : (l == 2 ? s : tt),
                      pz = l == 0 ? 0.0 : (l == 3 ? 1.0 - s - tt : tt);
-        double x, y, z;
-        elem_point(geo, K, nelt, 1.0 - (px + py + pz), px, py, pz, x, y, z);
-        const double b0 = eval_field(bx, x, y, z, r, K, nqd), b1 = eval_field(by, x, y, z, r, K, nqd),
-                     b2 = eval_field(bz, x, y, z, r, K, nqd);
+        double x = 0.0, y = 0.0, z = 0.0;
+        if (any_prog) elem_point(geo, K, nelt, 1.0 - (px + py + pz), px, py, pz, x, y, z);
+        const int pp = nq + lr;  // this face point's index in the sampled layout
+        const double b0 = beta(bx, x, y, z, pp, K), b1 = beta(by, x, y, z, pp, K), b2 = beta(bz, x, y, z, pp, K);
         const double* nrm = sg + 32 * e + 10;
         v = __ldg(tab.tri_w + r) * (b0 * nrm[3 * l] + b1 * nrm[3 * l + 1] + b2 * nrm[3 * l + 2]);
       }
