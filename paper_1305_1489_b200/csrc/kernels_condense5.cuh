@@ -68,6 +68,9 @@ struct C5Dims {
 };
 
 template <int K_> struct C5Cfg { static constexpr int NWT = 16; };
+#ifndef HDG_C5_BLOCKINV
+#define HDG_C5_BLOCKINV 1  // d3 = 56: block sweep with DMMA trailing updates (cta_block_inverse)
+#endif
 
 // Inverse of the full symmetric N x N matrix X (stride LD, shared memory) by
 // the sweep operator with 2 x 2 pivots, all NT threads of the CTA. Thread
@@ -185,6 +188,116 @@ __device__ __forceinline__ void cta_sweep_inverse(double* X, double* Y, double& 
   }
   __syncthreads();
   if (bad) pmin = 0.0;
+}
+
+// Inverse of the full symmetric positive definite N x N matrix X (stride LD,
+// shared memory; N a multiple of 8) by the block sweep operator with 8 x 8
+// pivot blocks, all NT threads of the CTA: per block p, (a) one warp inverts
+// the pivot block P = A_pp by the register sweep (gj_sweep_inverse, whose
+// |LDL^T pivots| are the matrix's own, block by block), (b) Cb_i = A_ip P^-1
+// for every other row block (DMMA), (c) A_ij -= Cb_i A_pj for i, j != p, one
+// 8 x 8 DMMA tile per warp task (2 k-steps), (d) A_ip <- Cb_i, A_pj <- Cb_j^T,
+// A_pp <- -P^-1. Sweeping every block leaves -X^-1; the lower triangle is
+// written back negated and mirrored (the consumers' canonical entries, as
+// cta_sweep_inverse). 7 block steps at N = 56 instead of 28 scalar 2 x 2
+// pivot steps, the trailing updates on the DMMA pipe. Y: >= 704 doubles of
+// scratch (16-byte aligned). pmin / pmax valid on thread 0.
+template <int N, int LD, int NT>
+__device__ __forceinline__ void cta_block_inverse(double* X, double* Y, double& pmin, double& pmax) {
+  static_assert(N % 8 == 0, "whole 8 x 8 blocks");
+  constexpr int NB = N / 8, NW = NT / 32, LC = N + 4, LP = 12;
+  double* Cb = Y;             // N x 8, column-major, stride LC
+  double* Pi = Y + 8 * LC;    // 8 x 8, stride LP
+  double* stage = Pi + 8 * LP + 8;  // gj sweep stage (128), 16-byte aligned
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  pmin = 1e300;
+  pmax = 0.0;
+  for (int p = 0; p < NB; ++p) {
+    const int p0 = 8 * p;
+    // (a) P^-1 (warp 0, lane c < 8 owns column c)
+    if (warp == 0) {
+      double a[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = lane < 8 ? X[p0 + i + (p0 + lane) * LD] : 0.0;
+      double bmin = 1e300, bmax = 0.0;
+      gj_sweep_inverse<8>(a, stage, lane, bmin, bmax);
+      pmin = fmin(pmin, bmin);
+      pmax = fmax(pmax, bmax);
+      if (lane < 8) {  // canonical entries: each pair from the lower-index lane's
+#pragma unroll      // below-diagonal half (the upper half of a sweep column is less accurate)
+        for (int i = 0; i < 8; ++i)
+          if (i >= lane) {
+            Pi[i + lane * LP] = a[i];
+            Pi[lane + i * LP] = a[i];
+          }
+      }
+    }
+    __syncthreads();
+    // (b) Cb_i = A_ip P^-1, i != p
+    for (int i = warp; i < NB; i += NW) {
+      if (i == p) continue;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int k = 4 * kk + t;
+        dmma(c0, c1, X[8 * i + g + (p0 + k) * LD], Pi[k + g * LP]);
+      }
+      Cb[8 * i + g + (2 * t) * LC] = c0;
+      Cb[8 * i + g + (2 * t + 1) * LC] = c1;
+    }
+    __syncthreads();
+    // (c) A_ij -= Cb_i A_pj, i, j != p (results held until every A_pj is read)
+    constexpr int NU = (N / 8 - 1) * (N / 8 - 1);
+    constexpr int TPW = (NU + NW - 1) / NW;
+    double acc[TPW][2];
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+      const int task = warp + u * NW;
+      acc[u][0] = acc[u][1] = 0.0;
+      if (task < NU) {
+        int i = task / (NB - 1), j = task - i * (NB - 1);
+        i += i >= p;
+        j += j >= p;
+        acc[u][0] = X[8 * i + g + (8 * j + 2 * t) * LD];
+        acc[u][1] = X[8 * i + g + (8 * j + 2 * t + 1) * LD];
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int k = 4 * kk + t;
+          dmma(acc[u][0], acc[u][1], -Cb[8 * i + g + k * LC], X[p0 + k + (8 * j + g) * LD]);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+      const int task = warp + u * NW;
+      if (task < NU) {
+        int i = task / (NB - 1), j = task - i * (NB - 1);
+        i += i >= p;
+        j += j >= p;
+        X[8 * i + g + (8 * j + 2 * t) * LD] = acc[u][0];
+        X[8 * i + g + (8 * j + 2 * t + 1) * LD] = acc[u][1];
+      }
+    }
+    // (d) the pivot block row and column
+    for (int idx = threadIdx.x; idx < 8 * N; idx += NT) {
+      const int r = idx % N, c = idx / N;  // row r of column p0 + c
+      const double v = (r >= p0 && r < p0 + 8) ? -Pi[(r - p0) + c * LP] : Cb[r + c * LC];
+      X[r + (p0 + c) * LD] = v;           // column block
+      X[p0 + c + r * LD] = v;             // row block (= its transpose)
+    }
+    __syncthreads();
+  }
+  // -X^-1 -> X^-1, lower triangle mirrored
+  for (int idx = threadIdx.x; idx < N * N; idx += NT) {
+    const int r = idx % N, c = idx / N;
+    if (r >= c) {
+      const double v = -X[r + c * LD];
+      X[r + c * LD] = v;
+      if (r > c) X[c + r * LD] = v;
+    }
+  }
+  __syncthreads();
 }
 
 template <int K_>
@@ -343,7 +456,8 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     // ---- P1: M^-1 (CTA sweep), packed lower part into the recovery cache
     {
       double pmin, pmax;
-      cta_sweep_inverse<D3, LD, NT>(Mi, T0, pmin, pmax);
+      if constexpr (D3 % 8 == 0 && HDG_C5_BLOCKINV) cta_block_inverse<D3, LD, NT>(Mi, T0, pmin, pmax);
+      else cta_sweep_inverse<D3, LD, NT>(Mi, T0, pmin, pmax);
       if (threadIdx.x == 0) store_pivstat(pivstat, K, 0, pmin, pmax);
     }
     if (factors)  // packed lower, column-major: column c at sym_idx(c, c)
@@ -441,7 +555,8 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     // ---- P6: S^-1 (CTA sweep)
     {
       double pmin, pmax;
-      cta_sweep_inverse<D3, LD, NT>(S, T1, pmin, pmax);
+      if constexpr (D3 % 8 == 0 && HDG_C5_BLOCKINV) cta_block_inverse<D3, LD, NT>(S, T1, pmin, pmax);
+      else cta_sweep_inverse<D3, LD, NT>(S, T1, pmin, pmax);
       if (threadIdx.x == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
     }
 
