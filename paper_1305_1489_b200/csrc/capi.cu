@@ -27,6 +27,7 @@
 #include "kernels_post2.cuh"
 #include "kernels_rescue.cuh"
 #include "kernels_conv2.cuh"
+#include "kernels_conv3.cuh"
 #include "exchange.cuh"
 #include "jit_quad.hpp"
 #include "mesh_dev.hpp"
@@ -1447,7 +1448,7 @@ int hdg_b200_convection_block(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_f
     const GeoDev geo = to_geo(g);
     set_device(c);
     const DevTab& t = c->tab[0].dev;
-    if (t.Aconv) {  // k <= 3: CTA-batched, the volume block on DMMA (kernels_conv2.cuh)
+    if (t.Aconv) {  // k <= 3: the DMMA kernels (kernels_conv3.cuh, k <= 2; kernels_conv2.cuh, k = 3)
       const Conv2Dims cd(t.d3, t.d2, t.nq, t.nqd);
       // program beta components are sampled once per point by an NVRTC-compiled
       // sampler (the volume nodes, then the element-parametrised face points),
@@ -1494,6 +1495,26 @@ int hdg_b200_convection_block(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_f
         }
       }
       const size_t smem = size_t(cd.total) * sizeof(double);
+      auto go3 = [&](auto kern, auto dims) -> bool {  // one warp per element (kernels_conv3.cuh)
+        using Dm = decltype(dims);
+        if (t.nq != Dm::NQ || t.nqd != Dm::NQD) return false;  // another rule: the generic kernels
+        constexpr int NW = 16;
+        const size_t smem3 = size_t(Dm::CTA_EXTRA + NW * Dm::PER_WARP) * sizeof(double);
+        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem3)));
+        const long need = (long(nelt) + NW - 1) / NW;
+        const int grid = int(std::min<long>(need, long(c->sms)));
+        kern<<<grid, NW * 32, smem3, c->stream>>>(t, nelt, geo, fb[0], fb[1], fb[2], vol, dp, dd);
+        CUDA_OK(cudaGetLastError());
+        return true;
+      };
+      bool done3 = false;
+      switch (t.k) {
+        case 0: done3 = go3(convection3_kernel<0>, Conv3Dims<0>{}); break;
+        case 1: done3 = go3(convection3_kernel<1>, Conv3Dims<1>{}); break;
+        case 2: done3 = go3(convection3_kernel<2>, Conv3Dims<2>{}); break;
+        default: break;
+      }
+      if (done3) return;
       auto go = [&](auto kern) {
         CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         int occ = 0;
