@@ -43,6 +43,9 @@ struct C6Dims {
   static constexpr int NT3 = (D3 + 7) / 8;                // d3 tiles (row / column)
   static constexpr int KS = 2 * NP + (D3 % 8 ? 1 : 0);    // ksteps over d3
   static constexpr int NTM = M / 8;                       // m tiles
+  // d3 <= 16 (k = 2): S^-1 of an element and M^-1 of the warp's next element
+  // as one sweep on the two 16-lane halves (gj_sweep_seg)
+  static constexpr bool PAIR = D3 <= 16;
   static constexpr int LT = 24;  // row stride of the k-fastest operands (Chat, W, V^T)
   static constexpr int LQ = K_ == 3 ? 26 : 14;  // Mi / Si storage: (row i, column c) at i * LQ + c
   static constexpr int LS = K_ == 3 ? 24 : 12;  // S storage for the sweep (row-major)
@@ -55,7 +58,7 @@ struct C6Dims {
   static constexpr int P_SQ = 0;                                 // Mi (LQ), then S (LS), then Si (LQ)
   static constexpr int P_VT = P_SQ + round_up(D3 * LQ, 2);       // V^T, M x LT; packed-Mi staging before that
   static constexpr int P_ST = P_VT + M * LT;                     // sweep stage, 128
-  static constexpr int P_M = P_ST + 128;                         // packed M of the element (cp.async)
+  static constexpr int P_M = P_ST + (PAIR ? 256 : 128);          // packed M of the element (cp.async)
   static constexpr int P_D = P_M + round_up(NSYM, 2);            // packed D
   static constexpr int FG_SZ = round_up(D3 + 28, 2);             // f + geometry record
   static constexpr int P_FG = P_D + round_up(NSYM, 2);           // 2 slots (current / next element)
@@ -63,9 +66,10 @@ struct C6Dims {
   // k = 3: M^-1 kept in its own buffer (stride d3), its fragments reloaded per
   // row tile and for the C phase instead of held in registers (measured
   // 4.00 -> 3.94 ms at C2; at k = 2 no gain)
-  static constexpr bool MIQ = K_ == 3;
+  static constexpr bool MIQ = K_ == 3 || PAIR;
   static constexpr int P_MQ = P_DG + 48;
-  static constexpr int PER_ELT = P_MQ + (MIQ ? round_up(D3 * D3, 2) : 0);
+  static constexpr int MQS = round_up(D3 * D3, 2);  // PAIR: two slots (this element's, the next one's)
+  static constexpr int PER_ELT = P_MQ + (MIQ ? (PAIR ? 2 : 1) * MQS : 0);
   static constexpr int FACTORS = round_up(NSYM + D3 * M + D3, 2);
   // the packed M^-1 record goes out by one TMA bulk store (a 16-byte multiple)
   static constexpr bool BULK_MI = (NSYM * 8) % 16 == 0;
@@ -196,20 +200,23 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   const bool al16 = NSYM % 2 == 0 && ((reinterpret_cast<uintptr_t>(Msym) | reinterpret_cast<uintptr_t>(Dsym) |
                                        reinterpret_cast<uintptr_t>(fvec)) & 15) == 0;
 
-  // packed M, D, f and the geometry record of element K -> this warp's slot
-  auto prefetch = [&](long K, int slot) {
+  // packed D of element K -> Dp (one cp.async group)
+  auto prefetch_D = [&](long K) {
+    if (al16) {
+      for (int q = lane; q < NSYM / 2; q += 32) cp_async16(Dp + 2 * q, Dsym + K * NSYM + 2 * q);
+    } else {
+      for (int q = lane; q < NSYM; q += 32) cp_async8(Dp + q, Dsym + K * NSYM + q);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // packed M, f and the geometry record of element K -> Mp and FG slot (one cp.async group)
+  auto prefetch_M = [&](long K, int slot) {
     double* fg = W0 + Dm::P_FG + slot * Dm::FG_SZ;
     if (al16) {
-      for (int q = lane; q < NSYM / 2; q += 32) {
-        cp_async16(Mp + 2 * q, Msym + K * NSYM + 2 * q);
-        cp_async16(Dp + 2 * q, Dsym + K * NSYM + 2 * q);
-      }
+      for (int q = lane; q < NSYM / 2; q += 32) cp_async16(Mp + 2 * q, Msym + K * NSYM + 2 * q);
       if (lane < D3 / 2) cp_async16(fg + 2 * lane, fvec + K * D3 + 2 * lane);
     } else {
-      for (int q = lane; q < NSYM; q += 32) {
-        cp_async8(Mp + q, Msym + K * NSYM + q);
-        cp_async8(Dp + q, Dsym + K * NSYM + q);
-      }
+      for (int q = lane; q < NSYM; q += 32) cp_async8(Mp + q, Msym + K * NSYM + q);
       if (lane < D3) cp_async8(fg + lane, fvec + K * D3 + lane);
     }
     double* sg = fg + D3;  // [0] volume, [1..9] a, [10..21] normals, [22..25] T, [26..27] perm (4 x int32)
@@ -269,7 +276,8 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   long K = long(blockIdx.x) * NW + warp;
   int cur = 0;
   if (K < nelt) {  // the first element's M^-1; later ones follow the previous element's C phase
-    prefetch(K, 0);
+    prefetch_M(K, 0);   //  (PAIR: beside its S^-1)
+    prefetch_D(K);
     invert_M(K);
   }
 
@@ -281,6 +289,13 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #endif
   for (; K < nelt; K += wstride, cur ^= 1) {
     C6_CLK(0);
+    const long Kn = K + wstride;
+    const bool has_next = Kn < nelt;
+    if (Dm::PAIR) {
+      cp_async_wait_all();  // this element's D (its M, f, geometry arrived long ago)
+      __syncwarp();
+      if (has_next) prefetch_M(Kn, cur ^ 1);  // Mp is free: this element's M^-1 is in MQ
+    }
     const double* fg = W0 + Dm::P_FG + cur * Dm::FG_SZ;
     const double* sg = fg + D3;
     // ---- derived scalars
@@ -320,7 +335,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     const double vol = DG[Dm::DG_VOL];
 #pragma unroll
     for (int i = 0; i < NT3; ++i) {
-      if (Dm::MIQ) c6_symfrag<K_, D3>(MQ, g, t, mib);
+      if (Dm::MIQ) c6_symfrag<K_, D3>(MQ + (Dm::PAIR ? cur * Dm::MQS : 0), g, t, mib);
       double y[3][NT3][2];
       double ca[3][KS];
 #pragma unroll
@@ -424,24 +439,61 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
     __syncwarp();
     C6_CLK(2);
-    const long Kn = K + wstride;
-    const bool has_next = Kn < nelt;
-    if (has_next) prefetch(Kn, cur ^ 1);  // packed M, D of this element are dead
+    if (has_next) {
+      if (!Dm::PAIR) prefetch_M(Kn, cur ^ 1);
+      prefetch_D(Kn);  // the packed M, D of this element are dead
+    }
 
     // ---- S^-1: sweep (S stored row-major with stride LS), then stored with stride LQ
     double sib[KS][NT3];
     {
       double a[D3];
-#pragma unroll
-      for (int i = 0; i < D3; ++i) a[i] = lane < D3 ? SQ[i * LS + lane] : 0.0;
-      __syncwarp();
       double pmin = 1e300, pmax = 0.0;
-      gj_sweep_inverse<D3>(a, ST, lane, pmin, pmax);
-      if (lane < D3) {
+      if constexpr (Dm::PAIR) {
+        // lanes 0-15: S of this element; lanes 16-31: M of the next one
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // the next M (its D may stay in flight)
+        __syncwarp();
+        const int h = lane >> 4, c = lane & 15;
 #pragma unroll
-        for (int i = 0; i < D3; ++i) SQ[i * LQ + lane] = a[i];
+        for (int i = 0; i < D3; ++i) {
+          double v = 0.0;
+          if (c < D3) {
+            if (h == 0) v = SQ[i * LS + c];
+            else if (has_next) v = Mp[i > c ? sym_idx(i, c, D3) : sym_idx(c, i, D3)];
+            else v = i == c ? 1.0 : 0.0;
+          }
+          a[i] = v;
+        }
+        __syncwarp();
+        gj_sweep_seg<D3, 16, D3>(a, ST + h * 128, c, pmin, pmax);
+        if (c < D3) {
+          if (h == 0) {
+#pragma unroll
+            for (int i = 0; i < D3; ++i) SQ[i * LQ + c] = a[i];
+          } else if (has_next) {
+#pragma unroll
+            for (int i = 0; i < D3; ++i) MQ[(cur ^ 1) * Dm::MQS + i * D3 + c] = a[i];  // the other M^-1 slot
+            if (factors) {
+              double* dst = factors + Kn * Dm::FACTORS + c * (2 * D3 - c + 1) / 2 - c;
+#pragma unroll
+              for (int i = 0; i < D3; ++i)
+                if (i >= c) dst[i] = a[i];
+            }
+          }
+        }
+        if (lane == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
+        if (lane == 16 && has_next) store_pivstat(pivstat, Kn, 0, pmin, pmax);
+      } else {
+#pragma unroll
+        for (int i = 0; i < D3; ++i) a[i] = lane < D3 ? SQ[i * LS + lane] : 0.0;
+        __syncwarp();
+        gj_sweep_inverse<D3>(a, ST, lane, pmin, pmax);
+        if (lane < D3) {
+#pragma unroll
+          for (int i = 0; i < D3; ++i) SQ[i * LQ + lane] = a[i];
+        }
+        if (lane == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
       }
-      if (lane == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
       __syncwarp();
       c6_symfrag<K_>(SQ, g, t, sib);
       if (factors && lane < D3) {  // fs = S^-1 f (canonical entries)
@@ -471,7 +523,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
       for (int e = 0; e < 2; ++e) fr[n][e] = 8 * n + 2 * t + e < D3 ? fg[8 * n + 2 * t + e] : 0.0;
     double* Ck = Cout + K * M * M;
-    if (Dm::MIQ) c6_symfrag<K_, D3>(MQ, g, t, mib);
+    if (Dm::MIQ) c6_symfrag<K_, D3>(MQ + (Dm::PAIR ? cur * Dm::MQS : 0), g, t, mib);
 #pragma unroll
     for (int jc = 0; jc < NTM; ++jc) {
       double vfr[KS], wfr[KS];
@@ -546,7 +598,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     // M^-1 of the next element (measured: interleaving its pivot steps with
     // this element's C tiles is slower, the sweep's DFMAs share the DMMA pipe)
     C6_CLK(4);
-    if (has_next) invert_M(Kn);
+    if (!Dm::PAIR && has_next) invert_M(Kn);
 #ifdef HDG_C6_CLK
     C6_CLK(5);
     __syncwarp();
