@@ -1472,26 +1472,27 @@ int hdg_b200_convection_block(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_f
           CUDA_OK(cudaMalloc(&c->d_bsamp, len * sizeof(double)));
           c->bsamp_len = len;
         }
-        for (int h = 0; h < 3; ++h) {
-          if (hb[h]->kind != HDG_FIELD_PROGRAM) continue;
-          std::string err;
-          CUfunction fn = jit_sample_kernel(*hb[h], &err);  // out[K * npts + p]
-          if (!fn) {
-            c->jit_error = err;
-            continue;
-          }
+        std::string err;
+        CUfunction fn = jit_sample3_kernel(hb, &err);  // all program components in one pass
+        if (fn) {
           int nel = nelt, np = npts;
           const double *bary = c->d_cbary, *V = geo.verts;
-          double* out = c->d_bsamp + size_t(h) * npts * nelt;
-          void* args[] = {&nel, &np, &bary, &V, &out};
+          double* o[3];
+          for (int h = 0; h < 3; ++h) o[h] = c->d_bsamp + size_t(h) * npts * nelt;
+          void* args[] = {&nel, &np, &bary, &V, &o[0], &o[1], &o[2]};
           const int grid = int(std::min<long>((long(npts) * nelt + 255) / 256, long(c->sms) * 16));
           if (launch_quad_jit(fn, c->stream, grid, 256, 0, args, &err)) {
-            fb[h].kind = HDG_FIELD_SAMPLED;
-            fb[h].samples = out;
+            for (int h = 0; h < 3; ++h)
+              if (hb[h]->kind == HDG_FIELD_PROGRAM) {
+                fb[h].kind = HDG_FIELD_SAMPLED;
+                fb[h].samples = o[h];
+              }
             c->jit_error.clear();
           } else {
             c->jit_error = err;
           }
+        } else {
+          c->jit_error = err;
         }
       }
       const size_t smem = size_t(cd.total) * sizeof(double);

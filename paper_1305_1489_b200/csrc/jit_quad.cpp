@@ -355,6 +355,26 @@ sample_field_jit(int nelt, int nq, const double* __restrict__ bary, const double
     out[idx] = FIELD_EXPR;
   }
 }
+// Up to three fields at every point of a table, one pass (shared point and
+// temporaries): out_h[K * npts + p] for the fields the host marked present.
+extern "C" __global__ void __launch_bounds__(256)
+sample_fields3_jit(int nelt, int nq, const double* __restrict__ bary, const double* __restrict__ V,
+                   double* __restrict__ out0, double* __restrict__ out1, double* __restrict__ out2) {
+  const long n = long(nelt) * nq;
+  for (long idx = long(blockIdx.x) * blockDim.x + threadIdx.x; idx < n; idx += long(gridDim.x) * blockDim.x) {
+    const long K = idx / nq;
+    const int q = int(idx - K * nq);
+    const double l0 = __ldg(bary + q), l1 = __ldg(bary + nq + q), l2 = __ldg(bary + 2 * nq + q),
+                 l3 = __ldg(bary + 3 * nq + q);
+    const double x = l0 * V[K] + l1 * V[nelt + K] + l2 * V[2L * nelt + K] + l3 * V[3L * nelt + K];
+    const double y = l0 * V[4L * nelt + K] + l1 * V[5L * nelt + K] + l2 * V[6L * nelt + K] + l3 * V[7L * nelt + K];
+    const double z = l0 * V[8L * nelt + K] + l1 * V[9L * nelt + K] + l2 * V[10L * nelt + K] + l3 * V[11L * nelt + K];
+    FIELD_STMTS3
+    FIELD_OUT0
+    FIELD_OUT1
+    FIELD_OUT2
+  }
+}
 )CUDA";
 }  // namespace
 
@@ -383,6 +403,27 @@ CUfunction jit_sample_kernel(const hdg_field& f, std::string* err) {
   const std::string e = fe.emit(f, "nullptr");
   return compile_cached("#define FIELD_STMTS " + fe.stmts() + "\n#define FIELD_EXPR " + e + "\n" + kSampleSource,
                         "sample_field_jit", err);
+}
+
+CUfunction jit_sample3_kernel(const hdg_field* const f[3], std::string* err) {
+  FieldEmitter fe;
+  std::string outs;
+  bool any = false;
+  for (int h = 0; h < 3; ++h) {
+    outs += "#define FIELD_OUT" + std::to_string(h) + " ";
+    if (f[h]->kind == HDG_FIELD_PROGRAM) {
+      outs += "out" + std::to_string(h) + "[idx] = " + fe.emit(*f[h], "nullptr") + ";";
+      any = true;
+    }
+    outs += "\n";
+  }
+  if (!any) {
+    if (err) *err = "no program field to sample";
+    return nullptr;
+  }
+  return compile_cached("#define FIELD_STMTS3 " + fe.stmts() + "\n" + outs +
+                            "#define FIELD_STMTS\n#define FIELD_EXPR 0.0\n" + kSampleSource,
+                        "sample_fields3_jit", err);
 }
 
 bool launch_quad_jit(CUfunction fn, cudaStream_t stream, int grid, int block, size_t smem, void** args,
