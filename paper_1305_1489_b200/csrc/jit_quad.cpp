@@ -355,6 +355,9 @@ sample_field_jit(int nelt, int nq, const double* __restrict__ bary, const double
     out[idx] = FIELD_EXPR;
   }
 }
+)CUDA";
+
+const char* kSample3Source = R"CUDA(
 // Up to three fields at every point of a table, one pass (shared point and
 // temporaries): out_h[K * npts + p] for the fields the host marked present.
 extern "C" __global__ void __launch_bounds__(256)
@@ -421,8 +424,7 @@ CUfunction jit_sample3_kernel(const hdg_field* const f[3], std::string* err) {
     if (err) *err = "no program field to sample";
     return nullptr;
   }
-  return compile_cached("#define FIELD_STMTS3 " + fe.stmts() + "\n" + outs +
-                            "#define FIELD_STMTS\n#define FIELD_EXPR 0.0\n" + kSampleSource,
+  return compile_cached("#define FIELD_STMTS3 " + fe.stmts() + "\n" + outs + kSample3Source,
                         "sample_fields3_jit", err);
 }
 

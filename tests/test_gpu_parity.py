@@ -404,6 +404,36 @@ def test_jit_and_interpreter_agree(k):
     assert max_slice_relerr(np_(cs_jit.Cf_cols()), np_(cs_vm.Cf_cols())) < 1e-10
 
 
+@pytest.mark.parametrize("k", [2, 3])
+def test_jit_samplers_run(k):
+    """The NVRTC samplers of the postprocess kappa and the convection beta
+    compile and run (a failure falls back silently to the interpreted
+    programs: same values, several times slower), and the sampled paths agree
+    with the interpreted ones."""
+    from test_gpu_ragged import first_tets
+    mesh = first_tets(107, 3)
+    prob = CONFIGS["C2"].problem
+    beta = CONFIGS["C4"].upwind_beta
+    eng = Engine(0)
+    eng.set_degree(k)
+    dm = eng.upload(mesh)
+    g = eng.geometry(dm, 1.0)
+    cs = eng.build_condense(g, prob.kappa, prob.c, prob.f)
+    uhat = torch.sin(torch.arange(dm.nfc * dim2(k), dtype=torch.float64, device="cuda") * 0.37)
+    ls = eng.recover(g, dm, cs, uhat)
+    eng.set_postprocess_rule()
+    us = eng.postprocess_star(g, prob.kappa, ls)
+    assert eng.jit_status == "", eng.jit_status
+    conv = eng.convection_bilinear_matrices(g, beta)
+    assert eng.jit_status == "", eng.jit_status
+    eng.set_jit(False)
+    us_vm = eng.postprocess_star(g, prob.kappa, ls)
+    conv_vm = eng.convection_bilinear_matrices(g, beta)
+    assert max_slice_relerr(np_(us), np_(us_vm)) < 1e-11
+    for a, b in zip(conv, conv_vm):
+        assert max_slice_relerr(np_(a), np_(b)) < 1e-12
+
+
 # Field programs exercising the JIT emitter's rewrites (jit_quad.cpp
 # FieldEmitter): sin/cos of exact multiples of pi as sinpi/cospi (m = 3, 1/2,
 # -2, 2, 1), a non-multiple (pi*pi stays sin), folded literal products,
