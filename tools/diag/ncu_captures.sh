@@ -3,7 +3,7 @@
 # config), exported to text on the box (reports are too large to bring back).
 # usage: ncu_captures.sh [name:regex:config:what ...]
 mkdir -p gpurun_out/ncu
-N="ncu --set full --clock-control none --import-source on"
+N="ncu -f --set full --clock-control none --import-source on"
 specs=("$@")
 if [ ${#specs[@]} -eq 0 ]; then
   specs=(k3_c2:condense6_kernel:C2:none k3_c4:condense6_kernel:C4:none k3_c3:condense5_kernel:C3:none

@@ -12,4 +12,4 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv \
   --log-file gpurun_out/r2b_launches_raw.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-sampled \
   --no-scatter > gpurun_out/r2b_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-bash tools/diag/ncu_captures.sh k3v6_c2:condense6_kernel:C2:none k3v6_c4:condense6_kernel:C4:none
+bash tools/diag/ncu_captures.sh k3v6_c2:condense6_kernel:C2:none k3v6_c4:condense6_kernel:C4:none k3v5_c3:condense5_kernel:C3:none k7v3_c4:convection3_kernel:C4:conv k6_c5:postprocess2_kernel:C5:post
