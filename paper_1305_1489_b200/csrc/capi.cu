@@ -1189,9 +1189,11 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
       const Post2Dims pd(n, tp.nq, c->tab[0].dev.d3);
       const size_t smem2 = size_t(pd.total) * sizeof(double);
       const long need2 = (long(nelt) + kPost2EB - 1) / kPost2EB;
-      const int grid2 = int(std::min<long>(need2, long(c->sms)));
       auto go = [&](auto kern) {
         CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+        int occ = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPost2Warps * 32, smem2));
+        const int grid2 = int(std::min<long>(need2, long(c->sms) * std::max(occ, 1)));
         kern<<<grid2, kPost2Warps * 32, smem2, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, qx, qy, qz, u,
                                                             ustar);
       };
