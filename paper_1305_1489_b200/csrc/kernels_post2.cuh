@@ -28,7 +28,7 @@ constexpr int kPost2LDE = kPost2EB + 4;  // [row][e] operand rows: B-fragment re
 
 struct Post2Dims {
   int n, nq, nq4, d3k, npad, ns, nsp;
-  int off_verts, off_sg, off_qc, off_gm, off_R, off_Rp, off_GS, off_ks, total;
+  int off_verts, off_sg, off_qc, off_gm, off_R, off_Rp, off_GS, off_ks, off_nx, nx, total;
   __host__ __device__ Post2Dims(int n_, int nq_, int d3k_) : n(n_), nq(nq_), d3k(d3k_) {
     nq4 = (nq + 3) / 4 * 4;
     npad = (n + 7) / 8 * 8;
@@ -44,7 +44,11 @@ struct Post2Dims {
     off_GS = off_Rp + (rp > solve ? rp : solve);      // G (3 nq4 x LDE) | S (EB x nsp)
     const int g = 3 * nq4 * kPost2LDE, sgs = kPost2EB * nsp;
     off_ks = off_GS + (g > sgs ? g : sgs);            // 2 x nq x EB: sampled kappa (double buffer)
-    total = off_ks + 2 * nq * kPost2EB;
+    // the next batch's staging (cp.async, copied into verts / sg / qc at the
+    // batch start): 12 x EB verts, 10 x EB geometry (volume, a), 3 d3k x EB q
+    off_nx = off_ks + 2 * nq * kPost2EB;
+    nx = (12 + 10 + 3 * d3k) * kPost2EB;
+    total = off_nx + nx;
   }
 };
 
@@ -78,41 +82,53 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
     for (long i = threadIdx.x; i < cnt; i += blockDim.x) cp_async8(dst + i, kap.samples + Kb * nq + i);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
+  // the inputs of batch Kb -> the staging buffer (one cp.async group with the
+  // kappa samples): element-fastest, so each source array is read coalesced
+  double* nxb = psm + dm.off_nx;
+  const bool need_x = kap.kind == HDG_FIELD_PROGRAM;  // the vertices only for an interpreted kappa
+  auto prefetch_batch = [&](long Kb) {
+    const int ne = int(nelt - Kb < kPost2EB ? nelt - Kb : kPost2EB);
+    for (int idx = threadIdx.x; idx < (22 + 3 * d3k) * kPost2EB; idx += blockDim.x) {
+      const int r = idx / kPost2EB, e = idx - r * kPost2EB;
+      if (e >= ne || (r < 12 && !need_x)) continue;
+      const long K = Kb + e;
+      const double* src;
+      if (r < 12) src = geo.verts + long(r) * nelt + K;
+      else if (r == 12) src = geo.volume + K;
+      else if (r < 22) src = geo.piola + long(r - 13) * nelt + K;
+      else {
+        const int s = (r - 22) / d3k, i = (r - 22) - s * d3k;
+        src = qs[s] + K * d3k + i;
+      }
+      cp_async8(nxb + idx, src);
+    }
+  };
   int kbuf = 0;
-  if (sampled && long(blockIdx.x) * kPost2EB < nelt) prefetch_kappa(long(blockIdx.x) * kPost2EB, 0);
+  if (long(blockIdx.x) * kPost2EB < nelt) {
+    prefetch_batch(long(blockIdx.x) * kPost2EB);
+    if (sampled) prefetch_kappa(long(blockIdx.x) * kPost2EB, 0);  // (commits the group)
+    else asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
 
   for (long K0 = long(blockIdx.x) * kPost2EB; K0 < nelt; K0 += long(gridDim.x) * kPost2EB, kbuf ^= 1) {
     const long Kn0 = K0 + long(gridDim.x) * kPost2EB;
-    if (sampled && Kn0 < nelt) prefetch_kappa(Kn0, kbuf ^ 1);
-    // ---- stage geometry, vertices, coefficients
-    for (int idx = threadIdx.x; idx < kPost2EB * 32; idx += blockDim.x) {
-      const int e = idx >> 5, i = idx & 31;
-      const long K = K0 + e;
-      double v = 0.0;
-      if (K < nelt && i < 30) {
-        if (i == 0) v = geo.volume[K];
-        else if (i < 10) v = geo.piola[long(i - 1) * nelt + K];
-        else if (i < 22) v = geo.normals[long(i - 10) * nelt + K];
-        else if (i < 26) v = geo.T[long(i - 22) * nelt + K];
-        else v = double(geo.perm[long(i - 26) * nelt + K]);
-      }
-      sg[idx] = v;
-    }
-    for (int idx = threadIdx.x; idx < 12 * kPost2EB; idx += blockDim.x) {
-      const int c = idx / kPost2EB, e = idx - c * kPost2EB;
-      const long K = K0 + e;
-      verts[idx] = K < nelt ? geo.verts[long(c) * nelt + K] : 0.0;
-    }
-    for (int idx = threadIdx.x; idx < 3 * d3k * kPost2EB; idx += blockDim.x) {
-      const int e = idx % kPost2EB, si = idx / kPost2EB, s = si / d3k, i = si - s * d3k;
-      const long K = K0 + e;
-      qc[si * kPost2LDE + e] = K < nelt ? qs[s][K * d3k + i] : 0.0;
-    }
-    if (sampled) {  // this batch's kappa samples (the next batch's group may stay in flight)
-      if (Kn0 < nelt) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    // ---- this batch's geometry, vertices, coefficients from the staging buffer
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < (22 + 3 * d3k) * kPost2EB; idx += blockDim.x) {
+      const int r = idx / kPost2EB, e = idx - r * kPost2EB;
+      const bool live = K0 + e < nelt;
+      const double v = live ? nxb[idx] : 0.0;
+      if (r < 12) verts[idx] = v;
+      else if (r < 22) sg[32 * e + (r - 12)] = v;  // [0] volume, [1..9] a
+      else qc[(r - 22) * kPost2LDE + e] = v;
     }
     __syncthreads();
+    if (Kn0 < nelt) {  // the next batch's inputs stream in while this one computes
+      prefetch_batch(Kn0);
+      if (sampled) prefetch_kappa(Kn0, kbuf ^ 1);
+      else asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
     for (int idx = threadIdx.x; idx < 12 * kPost2EB; idx += blockDim.x) {
       const int h = idx / kPost2EB, e = idx - h * kPost2EB;
       double v = 0.0;
