@@ -415,24 +415,39 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     }
   };
 
-  for (long K = blockIdx.x; K < nelt; K += gridDim.x) {
-    // ---- prologue: geometry, column data, packed M / D / f
-    if (threadIdx.x < 30) {
-      const int i = threadIdx.x;
-      double v;
-      if (i == 0) v = geo.volume[K];
-      else if (i < 10) v = geo.piola[long(i - 1) * nelt + K];
-      else if (i < 22) v = geo.normals[long(i - 10) * nelt + K];
-      else if (i < 26) v = geo.T[long(i - 22) * nelt + K];
-      else v = double(geo.perm[long(i - 26) * nelt + K]);
-      sg[i] = v;
-    }
-    for (int p = threadIdx.x; p < NSYM; p += NT) {
-      cp_async8(T1 + p, Msym + K * NSYM + p);
-      cp_async8(Dp + p, Dsym + K * NSYM + p);
-    }
-    for (int i = threadIdx.x; i < D3; i += NT) cp_async8(fv + i, fvec + K * D3 + i);
+  // the next element's inputs stream in while this one computes, each as soon
+  // as its buffer is dead: packed D after P3, packed M (into T1) after the S
+  // inverse, f after P7, the geometry record into registers
+  auto geo_value = [&](long Kx) {
+    const int i = threadIdx.x;
+    if (i == 0) return geo.volume[Kx];
+    if (i < 10) return geo.piola[long(i - 1) * nelt + Kx];
+    if (i < 22) return geo.normals[long(i - 10) * nelt + Kx];
+    if (i < 26) return geo.T[long(i - 22) * nelt + Kx];
+    return double(geo.perm[long(i - 26) * nelt + Kx]);
+  };
+  auto prefetch_packed = [&](double* dst, const double* src, long Kx) {
+    for (int p = threadIdx.x; p < NSYM; p += NT) cp_async8(dst + p, src + Kx * NSYM + p);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto prefetch_f = [&](long Kx) {
+    for (int i = threadIdx.x; i < D3; i += NT) cp_async8(fv + i, fvec + Kx * D3 + i);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  double gnext = 0.0;
+  if (long(blockIdx.x) < nelt) {
+    const long K = blockIdx.x;
+    if (threadIdx.x < 30) gnext = geo_value(K);
+    prefetch_packed(T1, Msym, K);
+    prefetch_packed(Dp, Dsym, K);
+    prefetch_f(K);
+  }
+
+  for (long K = blockIdx.x; K < nelt; K += gridDim.x) {
+    const long Kn = K + gridDim.x;
+    const bool has_next = Kn < nelt;
+    // ---- prologue: geometry, column data, packed M / D / f (prefetched)
+    if (threadIdx.x < 30) sg[threadIdx.x] = gnext;
     cp_async_wait_all();
     __syncthreads();
     if (warp == 0) {
@@ -500,6 +515,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       else t_strip(T1, 1, task - NSS);
     }
     __syncthreads();
+    if (has_next) prefetch_packed(Dp, Dsym, Kn);  // the packed D of this element is dead
     for (int task = warp; task < NSS + NTS; task += NWT) {
       if (task < NSS) s_strip(T1, 1, task, false);
       else t_strip(T0, 2, task - NSS);
@@ -559,6 +575,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       else cta_sweep_inverse<D3, LD, NT>(S, T1, pmin, pmax);
       if (threadIdx.x == 0) store_pivstat(pivstat, K, 1, pmin, pmax);
     }
+    if (has_next) prefetch_packed(T1, Msym, Kn);  // T1 (the inverse's scratch) is dead
 
     // ---- P7: Vs = S^-1 V strips | fs = S^-1 f
     for (int task = warp; task < NTM; task += NWT) {
@@ -597,6 +614,10 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       }
     }
 
+    if (has_next) {
+      prefetch_f(Kn);  // f of this element is dead after P7's fs (the barrier above)
+      if (threadIdx.x < 30) gnext = geo_value(Kn);
+    }
     // ---- P8: C (lower tile pairs, mirrored) | Cf
     for (int task = warp; task < NLP; task += NWT) {
       const int mt = int(2.0f * sqrtf(float(task) + 0.25f)) - 1;
