@@ -1156,11 +1156,14 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
     const DevTab& tp = c->tab[1].dev;
     const int n = tp.d3;
     require(n - 1 <= 96, HDG_EINVAL, "postprocess degree too high (d3(k+1) <= 97)");
+    int kap_wdiv = 0;
     if (c->jit && kappa.kind == HDG_FIELD_PROGRAM) {
       // a program kappa is sampled once at the P_{k+1} nodes by an NVRTC-compiled
       // sampler, so the postprocess reads samples instead of interpreting it per node
       std::string err;
-      CUfunction fn = jit_sample_kernel(kappa, &err);
+      // k + 1 <= 4 (postprocess2_kernel): w_q / kappa, no division in K6's epilogue
+      const bool wdiv = n <= 40;
+      CUfunction fn = wdiv ? jit_sample_wdiv_kernel(kappa, &err) : jit_sample_kernel(kappa, &err);
       if (fn) {
         const size_t len = size_t(tp.nq) * nelt;
         if (c->ksamp_len < len) {
@@ -1170,13 +1173,16 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
           c->ksamp_len = len;
         }
         int nel = nelt, nq = tp.nq;
-        const double *bary = tp.bary, *V = geo.verts;
+        const double *bary = tp.bary, *V = geo.verts, *wq = tp.w;
         double* out = c->d_ksamp;
-        void* args[] = {&nel, &nq, &bary, &V, &out};
+        void* args_w[] = {&nel, &nq, &bary, &V, &wq, &out};
+        void* args_k[] = {&nel, &nq, &bary, &V, &out};
+        void** args = wdiv ? args_w : args_k;
         const int grid = int(std::min<long>((long(len) + 255) / 256, long(c->sms) * 16));
         if (launch_quad_jit(fn, c->stream, grid, 256, 0, args, &err)) {
           fk.kind = HDG_FIELD_SAMPLED;
           fk.samples = c->d_ksamp;
+          kap_wdiv = wdiv ? 1 : 0;
           c->jit_error.clear();
         } else {
           c->jit_error = err;
@@ -1194,8 +1200,8 @@ int hdg_b200_postprocess(hdg_ctx* c, int nelt, const hdg_geometry* g, hdg_field 
         int occ = 0;
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPost2Warps * 32, smem2));
         const int grid2 = int(std::min<long>(need2, long(c->sms) * std::max(occ, 1)));
-        kern<<<grid2, kPost2Warps * 32, smem2, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, qx, qy, qz, u,
-                                                            ustar);
+        kern<<<grid2, kPost2Warps * 32, smem2, c->stream>>>(tp, c->tab[0].dev.d3, nelt, geo, fk, kap_wdiv, qx, qy,
+                                                            qz, u, ustar);
       };
       stage_begin(c, 5);
       switch (n - 1) {  // trailing system size for k + 1 = 1..4

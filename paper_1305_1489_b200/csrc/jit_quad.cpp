@@ -357,6 +357,27 @@ sample_field_jit(int nelt, int nq, const double* __restrict__ bary, const double
 }
 )CUDA";
 
+const char* kSampleWSource = R"CUDA(
+// JIT: w_q / field at every element node (K * nq + q): the postprocess's
+// kappa^-1 weights, the division done here instead of in its epilogue.
+extern "C" __global__ void __launch_bounds__(256)
+sample_wdiv_jit(int nelt, int nq, const double* __restrict__ bary, const double* __restrict__ V,
+                const double* __restrict__ wq, double* __restrict__ out) {
+  const long n = long(nelt) * nq;
+  for (long idx = long(blockIdx.x) * blockDim.x + threadIdx.x; idx < n; idx += long(gridDim.x) * blockDim.x) {
+    const long K = idx / nq;
+    const int q = int(idx - K * nq);
+    const double l0 = __ldg(bary + q), l1 = __ldg(bary + nq + q), l2 = __ldg(bary + 2 * nq + q),
+                 l3 = __ldg(bary + 3 * nq + q);
+    const double x = l0 * V[K] + l1 * V[nelt + K] + l2 * V[2L * nelt + K] + l3 * V[3L * nelt + K];
+    const double y = l0 * V[4L * nelt + K] + l1 * V[5L * nelt + K] + l2 * V[6L * nelt + K] + l3 * V[7L * nelt + K];
+    const double z = l0 * V[8L * nelt + K] + l1 * V[9L * nelt + K] + l2 * V[10L * nelt + K] + l3 * V[11L * nelt + K];
+    FIELD_STMTS
+    out[idx] = __ldg(wq + q) / (FIELD_EXPR);
+  }
+}
+)CUDA";
+
 const char* kSample3Source = R"CUDA(
 // Up to three fields at every point of a table, one pass (shared point and
 // temporaries): out_h[K * npts + p] for the fields the host marked present.
@@ -406,6 +427,17 @@ CUfunction jit_sample_kernel(const hdg_field& f, std::string* err) {
   const std::string e = fe.emit(f, "nullptr");
   return compile_cached("#define FIELD_STMTS " + fe.stmts() + "\n#define FIELD_EXPR " + e + "\n" + kSampleSource,
                         "sample_field_jit", err);
+}
+
+CUfunction jit_sample_wdiv_kernel(const hdg_field& f, std::string* err) {
+  if (f.kind != HDG_FIELD_PROGRAM) {
+    if (err) *err = "only program fields are sampled";
+    return nullptr;
+  }
+  FieldEmitter fe;
+  const std::string e = fe.emit(f, "nullptr");
+  return compile_cached("#define FIELD_STMTS " + fe.stmts() + "\n#define FIELD_EXPR " + e + "\n" + kSampleWSource,
+                        "sample_wdiv_jit", err);
 }
 
 CUfunction jit_sample3_kernel(const hdg_field* const f[3], std::string* err) {

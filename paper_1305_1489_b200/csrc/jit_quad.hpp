@@ -46,6 +46,8 @@ JitKernel jit_quad_kernel(const hdg_field& kap, const hdg_field& c, const hdg_fi
 // Kernel sampling a PROGRAM field at every element node (SAMPLED layout), or nullptr.
 // A program field sampled at every point of a table (out[K * npoints + p]).
 CUfunction jit_sample_kernel(const hdg_field& f, std::string* err);
+// w_q / f(x_q) at every element node (out[K * nq + q]; w: the rule's weights).
+CUfunction jit_sample_wdiv_kernel(const hdg_field& f, std::string* err);
 // The program fields among f[0..2] sampled in one pass at every point of a
 // table (out_h[K * npoints + p]; outputs of non-program fields untouched).
 CUfunction jit_sample3_kernel(const hdg_field* const f[3], std::string* err);

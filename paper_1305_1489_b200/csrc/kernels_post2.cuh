@@ -56,7 +56,7 @@ __device__ __forceinline__ int pk_lower(int i, int j, int n) { return j * n - j 
 
 template <int M_>  // trailing system size n - 1
 __global__ void __launch_bounds__(kPost2Warps * 32, 1)
-postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, const double* __restrict__ qx,
+postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, int kap_wdiv, const double* __restrict__ qx,
                     const double* __restrict__ qy, const double* __restrict__ qz, const double* __restrict__ u,
                     double* __restrict__ ustar) {
   extern __shared__ double psm[];
@@ -176,7 +176,7 @@ postprocess2_kernel(DevTab tp, int d3k, int nelt, GeoDev geo, FieldDev kap, cons
             }
             const double kq = sampled ? psm[dm.off_ks + kbuf * nq * kPost2EB + e * nq + qa]
                                       : eval_field(kap, x, y, z, qa, K, nq);
-            const double wk = __ldg(tp.w + qa) / kq;
+            const double wk = kap_wdiv ? kq : __ldg(tp.w + qa) / kq;  // kap_wdiv: samples are w_q / kappa
             const double* a9 = sg + 32 * e + 1;
 #pragma unroll
             for (int h = 0; h < 3; ++h)
