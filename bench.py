@@ -414,15 +414,47 @@ def run_ours(args):
         torch.cuda.synchronize()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         stage_acc = {}
+        # the step as one CUDA graph (its 8-10 launches replayed without host
+        # gaps; launch-bound configs such as C1 gain most); per-kernel times
+        # come from eager steps with stage events
+        graph = None
+        if not args.no_graph:
+            try:
+                eng.set_timing(False)
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=stream):
+                    step()
+                gr.replay()
+                stream.synchronize()
+                graph = gr
+            except Exception as exc:  # eager timing instead
+                print(f"# CUDA graph capture failed ({exc!r:.120}); timing eager launches", file=sys.stderr)
+                graph = None
+            finally:
+                eng.set_timing(True)
+                torch.cuda.synchronize()
         with ClockSampler(local) as clk:
             for i in range(args.steps):
                 flush.zero_()
                 ev[i][0].record(stream)
-                step()
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step()
                 ev[i][1].record(stream)
-                for kname, v in eng.stage_times().items():   # waits for this step
-                    stage_acc.setdefault(kname, []).append(v)
+                if graph is None:
+                    for kname, v in eng.stage_times().items():   # waits for this step
+                        stage_acc.setdefault(kname, []).append(v)
+                else:
+                    ev[i][1].synchronize()
         torch.cuda.synchronize()
+        if graph is not None:  # per-kernel stage times: eager steps (not the timed ones)
+            for _ in range(min(args.steps, 5)):
+                flush.zero_()
+                step()
+                for kname, v in eng.stage_times().items():
+                    stage_acc.setdefault(kname, []).append(v)
+            torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -671,6 +703,8 @@ def run_ours(args):
         "clocks": clk.summary(),
         "setup_s": t_setup,
     }
+    line["config"]["step_launch"] = ("one CUDA graph replay per step (the captured launches)" if graph is not None
+                                     else "eager launches")
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_line(cfg, os.cpu_count() or 1)
@@ -693,6 +727,8 @@ def main():
                     help="multi-GPU: weak = an n^3 slab per GPU, strong = the config's n^3 mesh split in z-slabs")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time the step as eager launches instead of one CUDA graph replay")
     ap.add_argument("--no-sampled", action="store_true", help="skip the HDG_FIELD_SAMPLED leg")
     ap.add_argument("--no-scatter", action="store_true",
                     help="skip the separately reported K4 scatter + interface exchange timing")
