@@ -449,12 +449,16 @@ def run_ours(args):
                     ev[i][1].synchronize()
         torch.cuda.synchronize()
         if graph is not None:  # per-kernel stage times: eager steps (not the timed ones)
+            c_graph = cs.C.clone()
             for _ in range(min(args.steps, 5)):
                 flush.zero_()
                 step()
                 for kname, v in eng.stage_times().items():
                     stage_acc.setdefault(kname, []).append(v)
             torch.cuda.synchronize()
+            # the replayed graph and the eager launches compute the same step, bit for bit
+            assert torch.equal(c_graph, cs.C), "CUDA graph replay and eager step differ"
+            del c_graph
         if world > 1:
             dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
