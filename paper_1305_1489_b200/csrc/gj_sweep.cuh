@@ -81,7 +81,7 @@ __device__ __forceinline__ void gj_sweep_step(double (&a)[N], double* stage, int
 // The trailing scalar pivot (odd N), the sign flip and the pivot reduction:
 // pmin / pmax return the extreme |LDL^T pivots| (0 for a vanished or
 // non-finite one).
-template <int N>
+template <int N, bool REDUCE = true>
 __device__ __forceinline__ void gj_sweep_finish(double (&a)[N], double* stage, int lane, double& piv,
                                                 double& pmin, double& pmax) {
   if (N % 2) {  // trailing scalar pivot
@@ -106,10 +106,12 @@ __device__ __forceinline__ void gj_sweep_finish(double (&a)[N], double* stage, i
   double d = fabs((lane & 1) && lane < N - (N % 2) ? 1.0 / piv : piv);
   if (!(d <= 1.79e308)) d = 0.0;
   double mn = lane < N ? d : 1e300, mx = lane < N ? d : 0.0;
+  if (REDUCE) {  // (else the caller reduces this lane's pivot later, off the critical path)
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
   }
   pmin = fmin(pmin, mn);
   pmax = fmax(pmax, mx);

@@ -200,8 +200,8 @@ __device__ __forceinline__ void cta_sweep_inverse(double* X, double* Y, double& 
 // A_pp <- -P^-1. Sweeping every block leaves -X^-1; the lower triangle is
 // written back negated and mirrored (the consumers' canonical entries, as
 // cta_sweep_inverse). 7 block steps at N = 56 instead of 28 scalar 2 x 2
-// pivot steps, the trailing updates on the DMMA pipe. Y: >= 704 doubles of
-// scratch (16-byte aligned). pmin / pmax valid on thread 0.
+// pivot steps, the trailing updates on the DMMA pipe. Y: >= 712 + 2 N doubles
+// of scratch (16-byte aligned). pmin / pmax valid on thread 0.
 template <int N, int LD, int NT>
 __device__ __forceinline__ void cta_block_inverse(double* X, double* Y, double& pmin, double& pmax) {
   static_assert(N % 8 == 0, "whole 8 x 8 blocks");
@@ -209,6 +209,7 @@ __device__ __forceinline__ void cta_block_inverse(double* X, double* Y, double& 
   double* Cb = Y;             // N x 8, column-major, stride LC
   double* Pi = Y + 8 * LC;    // 8 x 8, stride LP
   double* stage = Pi + 8 * LP + 8;  // gj sweep stage (128), 16-byte aligned
+  double* pst = stage + 128;        // |LDL^T pivots| (min, max) of each block's 8 lanes, reduced at the end
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   pmin = 1e300;
   pmax = 0.0;
@@ -219,10 +220,14 @@ __device__ __forceinline__ void cta_block_inverse(double* X, double* Y, double& 
       double a[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) a[i] = lane < 8 ? X[p0 + i + (p0 + lane) * LD] : 0.0;
-      double bmin = 1e300, bmax = 0.0;
-      gj_sweep_inverse<8>(a, stage, lane, bmin, bmax);
-      pmin = fmin(pmin, bmin);
-      pmax = fmax(pmax, bmax);
+      double bmin = 1e300, bmax = 0.0, piv = 1.0;
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) gj_sweep_step<8>(a, stage, lane, k, piv);
+      gj_sweep_finish<8, false>(a, stage, lane, piv, bmin, bmax);  // this lane's pivot: no reduction here
+      if (lane < 8) {
+        pst[16 * p + lane] = bmin;
+        pst[16 * p + 8 + lane] = bmax;
+      }
       if (lane < 8) {  // canonical entries: each pair from the lower-index lane's
 #pragma unroll      // below-diagonal half (the upper half of a sweep column is less accurate)
         for (int i = 0; i < 8; ++i)
@@ -287,6 +292,12 @@ __device__ __forceinline__ void cta_block_inverse(double* X, double* Y, double& 
       X[p0 + c + r * LD] = v;             // row block (= its transpose)
     }
     __syncthreads();
+  }
+  if (threadIdx.x == 0) {  // every block's pivots (the stats were kept off the block steps' chains)
+    for (int i = 0; i < 16 * NB; ++i) {
+      if ((i & 15) < 8) pmin = fmin(pmin, pst[i]);
+      else pmax = fmax(pmax, pst[i]);
+    }
   }
   // -X^-1 -> X^-1, lower triangle mirrored
   for (int idx = threadIdx.x; idx < N * N; idx += NT) {
