@@ -60,7 +60,10 @@ struct Rec3Dims {
   static constexpr int REC = round_up(FACTORS, 2);       // 16-byte multiple
   static constexpr int SCR = round_up(M, 2) + 2 * 32 + 3 * D3 + 32;  // lambda, t, u, r_s, geometry
   static constexpr int PER_WARP = Rec3Cfg<K_>::BUFS * REC + SCR;
-  static constexpr int TABLES = 3 * D3 * D3 + 24 * D2 * D3;  // per CTA
+  static constexpr int D2P = round_up(D2, 2);
+  // per CTA, row-pair interleaved: [h][i / 2][j][i % 2] (Chat^T), [l, perm][i / 2][j][i % 2] (W^T, rows
+  // padded to D2P), so that lane j reads rows i, i + 1 of its column with one 16-byte load
+  static constexpr int TABLES = 3 * D3 * D3 + 24 * D2P * D3;
   static_assert((FACTORS * 8) % 16 == 0, "cache record must be a 16-byte multiple for cp.async.bulk");
 };
 
@@ -83,10 +86,18 @@ recover3_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ faceby
   double* uu = tv + 32;
   double* rs = uu + 32;
   double* sg = rs + 3 * D3;
-  double* ChT = rsm + kRec3Warps * Rd::PER_WARP;  // CTA copies of Chat^T, Wlm^T
+  constexpr int D2P = Rd::D2P;
+  static_assert(D3 % 2 == 0 && M % 2 == 0, "row pairs");
+  double* ChT = rsm + kRec3Warps * Rd::PER_WARP;  // CTA copies of Chat^T, Wlm^T (row-pair interleaved)
   double* WT = ChT + 3 * D3 * D3;
-  for (int i = threadIdx.x; i < 3 * D3 * D3; i += blockDim.x) ChT[i] = tab.ChatT[i];
-  for (int i = threadIdx.x; i < 24 * D2 * D3; i += blockDim.x) WT[i] = tab.WlmT[i];
+  for (int x = threadIdx.x; x < 3 * D3 * D3; x += blockDim.x) {
+    const int h = x / (D3 * D3), r = x - h * D3 * D3, i = r / D3, j = r - i * D3;
+    ChT[h * D3 * D3 + (i >> 1) * 2 * D3 + 2 * j + (i & 1)] = tab.ChatT[x];
+  }
+  for (int x = threadIdx.x; x < 24 * D2P * D3; x += blockDim.x) {
+    const int b = x / (D2P * D3), r = x - b * D2P * D3, i = r / D3, j = r - i * D3;
+    WT[b * D2P * D3 + (i >> 1) * 2 * D3 + 2 * j + (i & 1)] = i < D2 ? tab.WlmT[(b * D2 + i) * D3 + j] : 0.0;
+  }
   __syncthreads();
   if (lane == 0) {
     for (int i = 0; i < kRec3Bufs; ++i) mbar_init(&bars[warp][i], 1);
@@ -156,8 +167,9 @@ recover3_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ faceby
       double s0 = fs[lane], s1 = 0.0;
 #pragma unroll
       for (int c = 0; c < M; c += 2) {
-        s0 = fma(Vs[lane + c * D3], lam[c], s0);
-        if (c + 1 < M) s1 = fma(Vs[lane + (c + 1) * D3], lam[c + 1], s1);
+        const double2 lc = *reinterpret_cast<const double2*>(lam + c);  // broadcast pair
+        s0 = fma(Vs[lane + c * D3], lc.x, s0);
+        s1 = fma(Vs[lane + (c + 1) * D3], lc.y, s1);
       }
       const double u = s0 + s1;
       uu[lane] = u;
@@ -166,26 +178,37 @@ recover3_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ faceby
     __syncwarp();
     if (lane < D3) {  // r_s(j) = sum_# a(s,#) (Chat_# u)(j) - sum_l n_l,s (W_l lambda_l)(j)
       const int j = lane;
-      double p[3];
+      double p[3] = {0.0, 0.0, 0.0}, p1[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-      for (int h = 0; h < 3; ++h) {
-        const double* C = ChT + h * D3 * D3 + j;
-        double a0 = 0.0, a1 = 0.0;
+      for (int i = 0; i < D3; i += 2) {
+        const double2 ui = *reinterpret_cast<const double2*>(uu + i);
 #pragma unroll
-        for (int i = 0; i < D3; ++i) {
-          if (i & 1) a1 = fma(C[i * D3], uu[i], a1);
-          else a0 = fma(C[i * D3], uu[i], a0);
+        for (int h = 0; h < 3; ++h) {
+          const double2 c = *reinterpret_cast<const double2*>(ChT + h * D3 * D3 + i * D3 + 2 * j);
+          p[h] = fma(c.x, ui.x, p[h]);
+          p1[h] = fma(c.y, ui.y, p1[h]);
         }
-        p[h] = a0 + a1;
       }
+#pragma unroll
+      for (int h = 0; h < 3; ++h) p[h] += p1[h];
       double w[4];
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
-        const double* W = WT + (6 * l + int(sg[26 + l]) - 1) * D2 * D3 + j;
-        double acc = 0.0;
+        const double* W = WT + (6 * l + int(sg[26 + l]) - 1) * D2P * D3 + 2 * j;
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < D2; ++i) acc = fma(W[i * D3], lam[l * D2 + i], acc);
-        w[l] = acc;
+        for (int i = 0; i < D2P; i += 2) {
+          const double2 c = *reinterpret_cast<const double2*>(W + i * D3);
+          if constexpr (D2 % 2 == 0) {
+            const double2 li = *reinterpret_cast<const double2*>(lam + l * D2 + i);
+            a0 = fma(c.x, li.x, a0);
+            a1 = fma(c.y, li.y, a1);
+          } else {
+            a0 = fma(c.x, lam[l * D2 + i], a0);
+            if (i + 1 < D2) a1 = fma(c.y, lam[l * D2 + i + 1], a1);
+          }
+        }
+        w[l] = a0 + a1;
       }
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
@@ -200,11 +223,15 @@ recover3_kernel(DevTab tab, int nelt, GeoDev geo, const int* __restrict__ faceby
       const int i = lane;
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
-      for (int j = 0; j < D3; ++j) {
-        const double m = Mi[j >= i ? sym_idx(j, i, D3) : sym_idx(i, j, D3)];
-        a0 = fma(m, rs[j], a0);
-        a1 = fma(m, rs[D3 + j], a1);
-        a2 = fma(m, rs[2 * D3 + j], a2);
+      for (int j = 0; j < D3; j += 2) {
+        const double m0 = Mi[j >= i ? sym_idx(j, i, D3) : sym_idx(i, j, D3)];
+        const double m1 = Mi[j + 1 >= i ? sym_idx(j + 1, i, D3) : sym_idx(i, j + 1, D3)];
+        const double2 r0 = *reinterpret_cast<const double2*>(rs + j);
+        const double2 r1 = *reinterpret_cast<const double2*>(rs + D3 + j);
+        const double2 r2 = *reinterpret_cast<const double2*>(rs + 2 * D3 + j);
+        a0 = fma(m1, r0.y, fma(m0, r0.x, a0));
+        a1 = fma(m1, r1.y, fma(m0, r1.x, a1));
+        a2 = fma(m1, r2.y, fma(m0, r2.x, a2));
       }
       qx[K * D3 + i] = a0;
       qy[K * D3 + i] = a1;
