@@ -4,6 +4,7 @@
 #pragma once
 
 #include <climits>
+#include <type_traits>
 
 #include "dev_common.cuh"
 #include "kernels_local.cuh"
@@ -292,7 +293,7 @@ __global__ void face_sides_fix_kernel(int nfc, int* __restrict__ sides) {
 // atomics and no zero fill; b = sum of the sides' Cf rows the same way.
 constexpr int kFaceRowWarps = 8;
 template <int D2>
-__global__ void __launch_bounds__(kFaceRowWarps * 32)
+__global__ void __launch_bounds__(kFaceRowWarps * 32, D2 <= 10 ? 4 : 1)  // k <= 3: 4 CTAs per SM fit
 scatter_faces_kernel(int nfc, const int* __restrict__ sides, const uint8_t* __restrict__ slot,
                      const int64_t* __restrict__ facebase, const double* __restrict__ C,
                      const double* __restrict__ Cf, double* __restrict__ vals, double* __restrict__ b, int nwarps) {
@@ -341,20 +342,36 @@ scatter_faces_kernel(int nfc, const int* __restrict__ sides, const uint8_t* __re
     __syncwarp();
     const int l0 = s0 & 3, l1 = s1 & 3;
     double* dst = vals + base * D2 * D2;
-#pragma unroll 1
-    for (int i = 0; i < D2; ++i) {
-      for (int p = lane; p < W; p += 32) {
-        const int q = p / D2, j = p - q * D2;
-        const int src = inv[q];
-        double v;
-        if (src == 8) {
-          v = ch[l0 * D2 + j + i * m];
-          if (ns == 2) v += ch[md + l1 * D2 + j + i * m];
-        } else {
-          v = ch[(src >> 2) * md + (src & 3) * D2 + j + i * m];
+    // the D2 x W block row as one flat run of (row, column) units, 16-byte
+    // units for even D2 (column pairs never straddle a block): every lane busy
+    // and half the stores; the row of a unit from a float reciprocal (exact
+    // here: t < 2^12, the nearest row boundary >= 1 / (2 W) away)
+    constexpr int U = D2 % 2 == 0 ? 2 : 1, H = D2 / U;
+    using vec = typename std::conditional<U == 2, double2, double>::type;
+    const int WU = W / U;
+    const float rW = 1.0f / float(WU);
+#pragma unroll 2
+    for (int t = lane; t < D2 * WU; t += 32) {
+      const int i = __float2int_rz((float(t) + 0.5f) * rW), p = t - i * WU;
+      const int q = p / H, j = U * (p - q * H);
+      const int src = inv[q];
+      const int o = j + i * m;
+      vec v;
+      if (src == 8) {
+        v = *reinterpret_cast<const vec*>(ch + l0 * D2 + o);
+        if (ns == 2) {
+          const vec w = *reinterpret_cast<const vec*>(ch + md + l1 * D2 + o);
+          if constexpr (U == 2) {
+            v.x += w.x;
+            v.y += w.y;
+          } else {
+            v += w;
+          }
         }
-        dst[i * W + p] = v;
+      } else {
+        v = *reinterpret_cast<const vec*>(ch + (src >> 2) * md + (src & 3) * D2 + o);
       }
+      *reinterpret_cast<vec*>(dst + i * W + U * p) = v;
     }
     if (lane < D2) {
       double v = Cf[long(s0 >> 2) * m + l0 * D2 + lane];
