@@ -286,14 +286,16 @@ int hdg_b200_neumann_load(hdg_ctx* ctx, int nver, const double* d_coords, int nf
                           hdg_field gy, hdg_field gz, double alpha, double* d_b);
 
 /* ------------------------------------------------- K9: skeleton solve
- * Replaces solve_skeleton (global_system.cpp:106-165), SPD branch: Dirichlet
- * dofs (faces [0, ndir)) fixed to d_ub (ndir x d2, hdg_b200_dirichlet_project),
- * the free dofs from H_ff x = b_f - H_fD u_D by block-Jacobi preconditioned CG
- * (d2 x d2 face blocks) on the block CSR of hdg_b200_scatter, iterated until
- * ||r|| <= rtol ||r_0|| or maxit. A system failing the reference's symmetry
- * test (sum|H - H^T| >= 1e-12 sum|H| over the free block) returns HDG_EINVAL
- * (the reference's SparseLU branch is not implemented); a non-SPD diagonal
- * block or no convergence returns HDG_ESOLVE. d_uhat: nfc x d2.            */
+ * Replaces solve_skeleton (global_system.cpp:106-165): Dirichlet dofs (faces
+ * [0, ndir)) fixed to d_ub (ndir x d2, hdg_b200_dirichlet_project), the free
+ * dofs from H_ff x = b_f - H_fD u_D on the block CSR of hdg_b200_scatter,
+ * iterated until ||r|| <= rtol ||r_0|| or maxit. A system passing the
+ * reference's symmetry test (sum|H - H^T| < 1e-12 sum|H| over the free block,
+ * :144-148) is solved by block-Jacobi preconditioned CG (the SimplicialLDLT
+ * branch); any other by block-Jacobi preconditioned BiCGStab restarted on the
+ * true residual (the SparseLU branch, :155-162). A non-SPD (CG) or singular
+ * (BiCGStab) diagonal block, or no convergence, returns HDG_ESOLVE
+ * (GlobalSolverError). d_uhat: nfc x d2.                                   */
 typedef struct {
   int iterations;
   int converged;

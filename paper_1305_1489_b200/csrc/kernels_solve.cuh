@@ -1,6 +1,8 @@
 // Skeleton solve on the GPU (replaces solve_skeleton,
-// global_system.cpp:106-165, SPD branch): block-Jacobi preconditioned CG on
-// the free dofs, Dirichlet dofs fixed to their projected values.
+// global_system.cpp:106-165): block-Jacobi preconditioned CG on the free dofs
+// for a symmetric system (the reference's SimplicialLDLT branch), block-Jacobi
+// preconditioned BiCGStab otherwise (its SparseLU branch); Dirichlet dofs
+// fixed to their projected values.
 //
 // The reference eliminates the Dirichlet rows/columns into Hff and moves
 // H_fD u_D to the right-hand side. Here the operator is the full CSR H
@@ -242,6 +244,131 @@ __global__ void asym_kernel(int nfc, int ndir, const int64_t* __restrict__ fb, c
   if (threadIdx.x == 0) {
     pa[blockIdx.x] = A;
     ps[blockIdx.x] = S;
+  }
+}
+
+// ---- nonsymmetric branch (the reference's SparseLU branch,
+// global_system.cpp:155-162): right-preconditioned BiCGStab with a general
+// block-Jacobi preconditioner. Off the timed path; host-driven scalars.
+
+// Inverse of each free face's diagonal block by Gauss-Jordan with partial
+// pivoting: one warp per face on the augmented [A | I] in shared memory,
+// stored row-major (d2 x d2 doubles per face). A vanished pivot column
+// reports the face in `bad`.
+template <int D2>
+__global__ void __launch_bounds__(128)
+block_inverse_general_kernel(int nfc, int ndir, const int64_t* __restrict__ fb, const int* __restrict__ nbr,
+                             const double* __restrict__ vals, double* __restrict__ binv,
+                             unsigned long long* __restrict__ bad) {
+  constexpr int W = 2 * D2, LD = W + 1;
+  __shared__ double aug[4][D2 * LD];
+  __shared__ double colp[4][D2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* A = aug[warp];
+  double* cp = colp[warp];
+  for (long f = long(blockIdx.x) * 4 + warp; f < nfc; f += long(gridDim.x) * 4) {
+    if (f < ndir) {
+      for (int q = lane; q < D2 * D2; q += 32) binv[f * D2 * D2 + q] = (q / D2 == q % D2) ? 1.0 : 0.0;
+      continue;
+    }
+    const int64_t b0 = fb[f];
+    const int n1 = int(fb[f + 1] - b0);
+    int ss = 0;
+    while (ss < n1 && nbr[8 * f + ss] != int(f)) ++ss;
+    const double* v = vals + b0 * D2 * D2;
+    for (int q = lane; q < D2 * W; q += 32) {
+      const int i = q / W, j = q - i * W;
+      A[i * LD + j] = j < D2 ? v[long(i) * n1 * D2 + ss * D2 + j] : (j - D2 == i ? 1.0 : 0.0);
+    }
+    __syncwarp();
+    bool ok = true;
+    for (int p = 0; p < D2; ++p) {
+      // pivot row: largest |A[r][p]|, r >= p (lowest row on ties)
+      double best = (lane >= p && lane < D2) ? fabs(A[lane * LD + p]) : -1.0;
+      int row = lane;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int orow = __shfl_xor_sync(0xffffffffu, row, o);
+        if (ob > best || (ob == best && orow < row)) { best = ob; row = orow; }
+      }
+      if (!(best > 0.0) || !isfinite(best)) { ok = false; break; }
+      if (row != p)
+        for (int j = lane; j < W; j += 32) {
+          const double tmp = A[p * LD + j];
+          A[p * LD + j] = A[row * LD + j];
+          A[row * LD + j] = tmp;
+        }
+      __syncwarp();
+      const double ip = 1.0 / A[p * LD + p];
+      if (lane < D2) cp[lane] = A[lane * LD + p];
+      __syncwarp();
+      for (int j = lane; j < W; j += 32) A[p * LD + j] *= ip;
+      __syncwarp();
+      for (int j = lane; j < W; j += 32) {
+        const double pj = A[p * LD + j];
+        for (int r = 0; r < D2; ++r)
+          if (r != p) A[r * LD + j] = fma(-cp[r], pj, A[r * LD + j]);
+      }
+      __syncwarp();
+    }
+    if (!ok && lane == 0) atomicMin(bad, static_cast<unsigned long long>(f));
+    for (int q = lane; q < D2 * D2; q += 32) {
+      const int i = q / D2, j = q - i * D2;
+      binv[f * D2 * D2 + q] = ok ? A[i * LD + D2 + j] : (i == j ? 1.0 : 0.0);
+    }
+    __syncwarp();
+  }
+}
+
+// out = Binv in per face (zero on the Dirichlet faces); one thread per row
+template <int D2>
+__global__ void __launch_bounds__(kSolveThreads)
+precond_general_kernel(int nfc, int ndir, const double* __restrict__ binv, const double* __restrict__ in,
+                       double* __restrict__ out) {
+  const long rows = long(nfc) * D2;
+  for (long row = long(blockIdx.x) * blockDim.x + threadIdx.x; row < rows; row += long(gridDim.x) * blockDim.x) {
+    const long f = row / D2;
+    const int i = int(row - f * D2);
+    double z = 0.0;
+    if (f >= ndir) {
+      const double* B = binv + f * D2 * D2 + i * D2;
+#pragma unroll
+      for (int j = 0; j < D2; ++j) z = fma(B[j], in[f * D2 + j], z);
+    }
+    out[row] = z;
+  }
+}
+
+// up to three dot products a_i . b_i (null pairs skipped), per-block partials
+__global__ void __launch_bounds__(kSolveThreads)
+dots_kernel(long n, const double* a0, const double* b0, const double* a1, const double* b1, const double* a2,
+            const double* b2, double* __restrict__ partial) {
+  __shared__ double red[kSolveThreads / 32];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+    if (a0) s0 = fma(a0[i], b0[i], s0);
+    if (a1) s1 = fma(a1[i], b1[i], s1);
+    if (a2) s2 = fma(a2[i], b2[i], s2);
+  }
+  const double r0 = block_sum(s0, red);
+  const double r1 = block_sum(s1, red);
+  const double r2 = block_sum(s2, red);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = r0;
+    partial[gridDim.x + blockIdx.x] = r1;
+    partial[2 * gridDim.x + blockIdx.x] = r2;
+  }
+}
+
+// out = alpha x + beta y + gamma z (null vectors skipped; out may alias any of them)
+__global__ void lincomb_kernel(long n, double* out, double alpha, const double* x, double beta, const double* y,
+                               double gamma, const double* z) {
+  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+    double v = alpha * x[i];
+    if (y) v = fma(beta, y[i], v);
+    if (z) v = fma(gamma, z[i], v);
+    out[i] = v;
   }
 }
 

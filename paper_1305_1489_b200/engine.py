@@ -529,8 +529,9 @@ class Engine:
     # ---------------------------------------------------------------- K9
     def solve_skeleton(self, dm: DeviceMesh, pat: DevicePattern, sys: SkeletonSystem, ub: torch.Tensor,
                        rtol: float = 1e-13, maxit: int = 200000, out: Optional[torch.Tensor] = None):
-        """solve_skeleton (global_system.cpp:106-165), SPD branch, on the GPU: Dirichlet dofs
-        = ub, free dofs by block-Jacobi CG to ||r|| <= rtol ||r0||. Returns (uhat, info)."""
+        """solve_skeleton (global_system.cpp:106-165) on the GPU: Dirichlet dofs = ub, free dofs
+        by block-Jacobi CG (symmetric system) or BiCGStab (any other, the reference's SparseLU
+        branch) to ||r|| <= rtol ||r0||. Returns (uhat, info)."""
         d2 = sys.d2
         if out is None:
             out = torch.empty(dm.nfc * d2, dtype=torch.float64, device=self.device)

@@ -291,14 +291,45 @@ def test_solve_skeleton(k):
     assert np.array_equal(np_(uhat)[:ub.numel()], np_(ub).ravel())
 
 
-def test_solve_skeleton_rejects_nonsymmetric():
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_solve_skeleton_nonsymmetric(k):
+    """The reference's SparseLU branch (global_system.cpp:155-162): a system
+    failing the symmetry test (here the assembled H with every value scaled by
+    a smooth, non-symmetric factor, as an upwinded convection term would) is
+    solved by the GPU BiCGStab and compared with the reference's direct solve."""
+    prob = CONFIGS["C2"].problem
+    mesh = HostMesh.box(3, bc=prob.bc, perturb=0.1)
+    em = oracle_mesh(mesh)
+    eng, dm, g, cs = gpu_pipeline(mesh, k, prob.kappa, prob.c, prob.f)
+    pat = eng.pattern_device(dm)
+    sys = eng.assemble(dm, pat, cs)
+    idx = torch.arange(sys.vals.numel(), dtype=torch.float64, device="cuda")
+    sys.vals.mul_(1.0 + 0.2 * torch.sin(0.7 * idx))
+    ub = eng.dirichlet_project(dm, prob.u)
+    uhat, info = eng.solve_skeleton(dm, pat, sys, ub, rtol=1e-12)
+    assert info["converged"] and info["asym"] > 1e-3 * info["scale"]
+    import scipy.sparse as sp
+    nd = sys.b.numel()
+    H = sp.csr_matrix((np_(sys.vals), np_(sys.colidx), np_(sys.rowptr)), shape=(nd, nd)).tocsc()
+    want = solve_skeleton(em, H.indptr, H.indices, H.data, np_(sys.b), np_(ub).ravel(), dim2(k))
+    assert relerr(np_(uhat), want) < 1e-9
+    assert np.array_equal(np_(uhat)[:ub.numel()], np_(ub).ravel())
+
+
+def test_solve_skeleton_singular_block_reported():
+    """A vanished diagonal block of a nonsymmetric system: HDG_ESOLVE
+    (GlobalSolverError, global_system.cpp:157-158)."""
     from paper_1305_1489_b200._lib import HdgError
     mesh = HostMesh.box(2, bc="dirichlet_x")
     eng, dm, g, cs = gpu_pipeline(mesh, 1, KAP, CC, FF)
     pat = eng.pattern_device(dm)
     sys = eng.assemble(dm, pat, cs)
-    sys.vals[-2] += 1.0  # off-diagonal entry of the last (interior) face: breaks H = H^T
-    with pytest.raises(HdgError, match="not symmetric"):
+    sys.vals[-2] += 1.0  # breaks H = H^T
+    d2 = dim2(1)
+    f = dm.nfc - 1  # last (interior) face: zero its whole block row
+    fbase = pat.facebase.cpu().numpy()
+    sys.vals[int(fbase[f]) * d2 * d2:int(fbase[f + 1]) * d2 * d2] = 0.0
+    with pytest.raises(HdgError, match="factorization"):
         eng.solve_skeleton(dm, pat, sys, eng.dirichlet_project(dm, "x"))
 
 
