@@ -2,6 +2,10 @@
 // condensation kernel, kernels_condense3.cuh). Self-contained: no includes.
 #pragma once
 
+#ifndef HDG_GJ_EARLY
+#define HDG_GJ_EARLY 1
+#endif
+
 // 1/x to full double precision: MUFU reciprocal seed + two Newton steps.
 __device__ __forceinline__ double gj_rcp(double x) {
   double r;
@@ -30,6 +34,23 @@ __device__ __forceinline__ void gj_sweep_step(double (&a)[N], double* stage, int
     st[lane] = a[k];
     st[32 + lane] = a[k + 1];
   }
+#if HDG_GJ_EARLY
+  // barrier right after the stage stores: the pivot block, the next pivot
+  // rows and the update's stage loads all issue under the reciprocal chain
+  __syncwarp();
+  const double2 pk0 = *reinterpret_cast<const double2*>(st + k);       // a[k] of lanes k, k + 1
+  const double2 pk1 = *reinterpret_cast<const double2*>(st + 32 + k);  // a[k + 1] of lanes k, k + 1
+  const double p00 = pk0.x, p01 = pk1.x, p11 = pk1.y;
+  double n0x = 0.0, n0y = 0.0, n1x = 0.0, n1y = 0.0;
+  if (k + 2 < N) {
+    n0x = st[k + 2];
+    n1x = st[32 + k + 2];
+    if (k + 3 < N) {
+      n0y = st[k + 3];
+      n1y = st[32 + k + 3];
+    }
+  }
+#else
   const double p00 = __shfl_sync(0xffffffffu, a[k], k);
   const double p01 = __shfl_sync(0xffffffffu, a[k + 1], k);
   const double p11 = __shfl_sync(0xffffffffu, a[k + 1], k + 1);
@@ -44,6 +65,7 @@ __device__ __forceinline__ void gj_sweep_step(double (&a)[N], double* stage, int
       n1y = __shfl_sync(0xffffffffu, a[k + 1], k + 3);
     }
   }
+#endif
   const double det = fma(p00, p11, -p01 * p01);
   const bool m0 = lane == k, m1 = lane == k + 1;
   const double ak0 = m0 ? a[k] - 1.0 : a[k];
@@ -65,7 +87,9 @@ __device__ __forceinline__ void gj_sweep_step(double (&a)[N], double* stage, int
   const double w0 = u0 * id, w1 = u1 * id;
   if (m0) piv = p00;
   if (m1) piv = p00 * id;
+#if !HDG_GJ_EARLY
   __syncwarp();
+#endif
 #pragma unroll
   for (int i0 = 0; i0 < N; i0 += 2) {
     if (i0 == k || i0 == k + 2) continue;
@@ -151,6 +175,18 @@ __device__ __forceinline__ void gj_sweep_seg(double (&a)[R], double* stage, int 
       st[c] = a[k];
       st[32 + c] = a[k + 1];
     }
+#if HDG_GJ_EARLY
+    __syncwarp();
+    const double2 pk0 = *reinterpret_cast<const double2*>(st + k);
+    const double2 pk1 = *reinterpret_cast<const double2*>(st + 32 + k);
+    const double p00 = pk0.x, p01 = pk1.x, p11 = pk1.y;
+    double n0x = 0.0, n0y = 0.0, n1x = 0.0, n1y = 0.0;
+    if (k + 2 < N) {
+      const double2 q0 = *reinterpret_cast<const double2*>(st + k + 2);
+      const double2 q1 = *reinterpret_cast<const double2*>(st + 32 + k + 2);
+      n0x = q0.x, n0y = q0.y, n1x = q1.x, n1y = q1.y;
+    }
+#else
     const double p00 = __shfl_sync(FULL, a[k], k, W);
     const double p01 = __shfl_sync(FULL, a[k + 1], k, W);
     const double p11 = __shfl_sync(FULL, a[k + 1], k + 1, W);
@@ -161,6 +197,7 @@ __device__ __forceinline__ void gj_sweep_seg(double (&a)[R], double* stage, int 
       n0y = __shfl_sync(FULL, a[k], k + 3, W);
       n1y = __shfl_sync(FULL, a[k + 1], k + 3, W);
     }
+#endif
     const double det = fma(p00, p11, -p01 * p01);
     const bool m0 = c == k, m1 = c == k + 1;
     const double ak0 = m0 ? a[k] - 1.0 : a[k];
@@ -180,7 +217,9 @@ __device__ __forceinline__ void gj_sweep_seg(double (&a)[R], double* stage, int 
     const double w0 = u0 * id, w1 = u1 * id;
     if (m0) piv = p00;
     if (m1) piv = p00 * id;
+#if !HDG_GJ_EARLY
     __syncwarp();
+#endif
 #pragma unroll
     for (int i0 = 0; i0 < N; i0 += 2) {
       if (i0 == k || i0 == k + 2) continue;
