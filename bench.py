@@ -69,6 +69,11 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def c_sms(dev) -> int:
+    import torch
+    return torch.cuda.get_device_properties(dev).multi_processor_count
+
+
 # --------------------------------------------------------------- flop model
 def k3_flops(k: int) -> float:
     """Algorithmic fp64 flops per element of the condense kernel as executed
@@ -669,6 +674,19 @@ def run_ours(args):
             "peak_source": FP64_PEAK_SOURCE, "flops_per_element": k3_flops(k),
             "flops_per_launch": k3_flops(k) * nelt, "launch_ms": k3_ms,
             "pipe": "fp64 (DMMA mma.sync m8n8k4)"}
+    if k == 3:
+        # Explains frac (not a second claim): how busy the fp64 pipe is with the
+        # instructions K3 v6 executes per element (ncu instruction counts of the
+        # committed capture: 645 DMMA.8x8x4 at one per 16 sub-partition cycles,
+        # 1690 DFMA/DMUL/DADD at one per 2), over the measured launch time at the
+        # sampled SM clock. Padding (d3 = 20 in 24-wide tiles) and the sweeps'
+        # DFMAs are pipe time that frac, counted on algorithmic flops, leaves out.
+        sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+        pipe_cycles = 645 * 16 + 1690 * 2
+        roof["fp64_pipe"] = {"dmma_per_element": 645, "fp64_alu_per_element": 1690,
+                             "pipe_cycles_per_element": pipe_cycles,
+                             "busy_frac": pipe_cycles * nelt / (c_sms(dev) * 4 * (k3_ms / 1e3) * sm_mhz * 1e6),
+                             "source": "profiles/r02c_ncu_k3v6_c2.txt (executed instruction counts)"}
     # SURVEY §8(d) compulsory HBM bytes of the whole step (mesh + geometry for
     # build and for recover, coefficient samples when SAMPLED, C + Cf written,
     # lambda gathered, q + u written); caches and intermediates are not
