@@ -99,6 +99,32 @@ std::vector<double> to_fragments(const std::vector<double>& A, int rows, int col
   return out;
 }
 
+// K3 v6 (k = 2, 3) skips the 8 x 4 blocks of Chat_h that c6_ch_nz declares
+// structurally zero (rows of top-degree modes, the lower triangle): verify the
+// claim on the tables actually built, entry by entry, and fail loudly if a
+// skipped block holds anything above rounding.
+void check_chat_pattern(const HostTables& h) {
+  const int k = h.k, d3 = h.d3;
+  if (k != 2 && k != 3) return;
+  const int np = d3 / 8, ks = 2 * np + (d3 % 8 ? 1 : 0), nt3 = (d3 + 7) / 8;
+  double mx = 0.0;
+  for (int hh = 0; hh < 3; ++hh)
+    for (double v : h.Chat[hh]) mx = std::max(mx, std::fabs(v));
+  for (int hh = 0; hh < 3; ++hh)
+    for (int tile = 0; tile < nt3; ++tile)
+      for (int s = 0; s < ks; ++s) {
+        if (c6_ch_nz(k, hh, tile, s)) continue;
+        for (int r = 8 * tile; r < std::min(8 * tile + 8, d3); ++r)
+          for (int t = 0; t < 4; ++t) {
+            const int kk = s < 2 * np ? (s >> 1) * 8 + 2 * t + (s & 1) : 8 * np + t;
+            if (kk < d3 && std::fabs(h.Chat[hh][r + size_t(kk) * d3]) > 1e-13 * mx)
+              throw HdgError{HDG_ESTATE, "reference convection table Chat_" + std::to_string(hh) + " is not zero at (" +
+                                             std::to_string(r) + ", " + std::to_string(kk) +
+                                             "): the condensation kernel's sparsity pattern does not hold"};
+          }
+      }
+}
+
 void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
   if (ts.buf) { cudaFree(ts.buf); ts.buf = nullptr; }
   ts.ready = false;
@@ -957,6 +983,7 @@ int hdg_b200_set_degree(hdg_ctx* c, int k, int tet_deg, int tri_deg) {
     require(k >= 0 && k <= 5, HDG_EINVAL, "degree must be in 0..5");
     set_device(c);
     upload_tables(c->tab[0], k, tet_deg, tri_deg);
+    check_chat_pattern(c->tab[0].host);
     c->tri_deg = tri_deg;
     c->tab[1].ready = false;
     if (c->post_tet_deg >= 0) upload_tables(c->tab[1], k + 1, c->post_tet_deg, tri_deg);

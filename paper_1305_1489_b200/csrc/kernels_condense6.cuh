@@ -97,6 +97,34 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) 
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem_src) : "memory");
 }
 
+// Structural zeros of the reference convection matrices. In the
+// degree-graded orthonormal basis Chat_h[i][j] = (1/6) int P_i d_h P_j
+// vanishes unless deg P_i < deg P_j: its rows i >= dim P_{k-1} are zero and the
+// rest is strictly upper triangular. c6_ch_nz says whether the 8 x 4 block
+// (row tile, kstep s in the kidx order) of Chat_h holds any nonzero; the
+// blocks it denies are skipped as DMMA operands. hdg_b200_set_degree checks
+// the pattern against the tables it uploads (capi.cu, check_chat_pattern).
+#ifndef HDG_C6_SPARSE
+#define HDG_C6_SPARSE 1
+#endif
+constexpr bool c6_ch_nz(int k, int h, int tile, int s) {
+  if (!HDG_C6_SPARSE) return true;
+  if (k == 3) {
+    if (tile == 0) return !(h == 0 && s == 0);
+    if (tile == 1) return s == 4 || (h == 2 && s == 3);
+    return false;
+  }
+  if (k == 2) return tile == 0 && !(h == 0 && s == 0);
+  return true;
+}
+// any nonzero block in the row tile (else Y_h and R'_h vanish on it for every h)
+constexpr bool c6_tile_nz(int k, int tile) {
+  for (int h = 0; h < 3; ++h)
+    for (int s = 0; s < 8; ++s)
+      if (c6_ch_nz(k, h, tile, s)) return true;
+  return false;
+}
+
 // contraction index of kstep s for lane t: the accumulator-chained order
 template <int K_>
 __device__ __forceinline__ int c6_kidx(int s, int t) {
@@ -335,6 +363,37 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     const double vol = DG[Dm::DG_VOL];
 #pragma unroll
     for (int i = 0; i < NT3; ++i) {
+      if (!c6_tile_nz(K_, i)) {
+        // Chat_h vanishes on these rows for every h: Y_h = R'_h = 0 there, so S
+        // keeps D on the tile's rows and V^T[c][r] = T_l(c) W_l(c)[c'][r] on its columns
+        const int r = 8 * i + g;
+#pragma unroll
+        for (int j = 0; j < NT3; ++j) {
+          if (j > i) break;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = 8 * j + 2 * t + e;
+            if (r < D3 && c <= r) {
+              const double v = (r >= nu || c >= nu) ? (r == c ? 6.0 * vol : 0.0) : Dp[sym_idx(r, c, D3)];
+              SQ[r * LS + c] = v;
+              SQ[c * LS + r] = v;
+            }
+          }
+        }
+        const int r0 = 8 * i + 2 * t;
+        if (r0 < LT) {
+#pragma unroll
+          for (int jc = 0; jc < NTM; ++jc) {
+            const int c = 8 * jc + g, fc = c / D2;
+            const double* wr = WT + int(DG[Dm::DG_TB + fc]) + (c - fc * D2) * LT;
+            const double Tf = DG[Dm::DG_T + fc];
+            const double2 w2 = *reinterpret_cast<const double2*>(wr + r0);
+            const double v0 = r0 < nu ? Tf * w2.x : 0.0, v1 = r0 + 1 < nu ? Tf * w2.y : 0.0;
+            *reinterpret_cast<double2*>(VT + c * LT + r0) = make_double2(v0, v1);
+          }
+        }
+        continue;
+      }
       if (Dm::MIQ) c6_symfrag<K_, D3>(MQ + (Dm::PAIR ? cur * Dm::MQS : 0), g, t, mib);
       double y[3][NT3][2];
       double ca[3][KS];
@@ -349,7 +408,8 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
         for (int h = 0; h < 3; ++h)
 #pragma unroll
-          for (int n = 0; n < NT3; ++n) dmma(y[h][n][0], y[h][n][1], ca[h][s], mib[s][n]);
+          for (int n = 0; n < NT3; ++n)
+            if (c6_ch_nz(K_, h, i, s)) dmma(y[h][n][0], y[h][n][1], ca[h][s], mib[s][n]);
       // S row tiles j <= i: S = D + sum_h R'_h Chat_h^T
       {
         double ra[3][KS];
@@ -377,7 +437,8 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
               c6_rowfrag<K_>(CH + h * Dm::CH_SZ + (8 * j + g) * LT, t, cb);
             }
 #pragma unroll
-            for (int s = 0; s < KS; ++s) dmma(sa[s & 1][0], sa[s & 1][1], ra[h][s], cb[s]);
+            for (int s = 0; s < KS; ++s)
+              if (c6_ch_nz(K_, h, j, s)) dmma(sa[s & 1][0], sa[s & 1][1], ra[h][s], cb[s]);
           }
           // lower entries c <= r, mirrored: the sweep needs S exactly symmetric
           const int r = 8 * i + g;
