@@ -69,6 +69,12 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# executed fp64 instructions per element of condense6_kernel<3> (ncu instruction
+# counts of the committed capture profiles/r02d_ncu_k3v6_c2.txt)
+K3_DMMA_PER_ELT = 466
+K3_FP64_ALU_PER_ELT = 1564
+
+
 def c_sms(dev) -> int:
     import torch
     return torch.cuda.get_device_properties(dev).multi_processor_count
@@ -77,16 +83,21 @@ def c_sms(dev) -> int:
 # --------------------------------------------------------------- flop model
 def k3_flops(k: int) -> float:
     """Algorithmic fp64 flops per element of the condense kernel as executed
-    (kernels_condense2.cuh; unpadded counts, symmetric products counted once;
-    DESIGN.md §K3)."""
+    (unpadded counts, symmetric products counted once). The
+    k = 2, 3 kernel (kernels_condense6.cuh) skips the rows of Chat_h that
+    vanish structurally (modes of top degree: only the first n1 = dim P_{k-1}
+    rows are nonzero), so Y_h, R'_h and the S update are counted on those rows
+    only (the count of the algorithm actually executed, never a
+    larger one); its skipping of zero blocks inside those rows is not counted."""
     n = (k + 1) * (k + 2) * (k + 3) // 6
     m = 2 * (k + 1) * (k + 2)
+    n1 = k * (k + 1) * (k + 2) // 6 if k in (2, 3) else n   # nonzero rows of Chat_h
     f = 0.0
     f += 2 * 2.0 * n ** 3                 # two Gauss-Jordan inverses (M, S)
     f += 2.0 * n * n * m                  # Zp = Mi W^T
-    f += 3 * 2.0 * n ** 3 + 3 * 3 * 2.0 * n * n   # Q_# = Mi Chat_#^T, R_# = g Q
-    f += 3 * 2.0 * n * n * (n + 1) / 2    # S += sum_# Chat_# R_# (lower)
-    f += 2.0 * n * n * m + 4 * 3 * 2.0 * n * n    # V: per-face Chat_l Zp_l (+ Chat_l combos)
+    f += 3 * 2.0 * n1 * n * n + 3 * 3 * 2.0 * n1 * n   # Y_# = Chat_# Mi, R'_# = g Y
+    f += 3 * 2.0 * n * n1 * (n1 + 1) / 2  # S += sum_# R'_# Chat_#^T (lower, n1 x n1)
+    f += 2.0 * n1 * n * m + 4 * 3 * 2.0 * n1 * n + (n - n1) * m   # V: W_l Z_l^T on the dense rows, T W on the rest
     f += 2.0 * n * n * m + 2.0 * n * n    # Vs = Si V, fs
     f += 2 * 2.0 * n * m * (m + 1) / 2    # W Zp and V^T Vs (lower)
     f += 2.0 * m * n                      # Cf
@@ -677,16 +688,16 @@ def run_ours(args):
     if k == 3:
         # Explains frac (not a second claim): how busy the fp64 pipe is with the
         # instructions K3 v6 executes per element (ncu instruction counts of the
-        # committed capture: 645 DMMA.8x8x4 at one per 16 sub-partition cycles,
-        # 1690 DFMA/DMUL/DADD at one per 2), over the measured launch time at the
+        # committed capture: K3_DMMA_PER_ELT DMMA.8x8x4 at one per 16 sub-partition
+        # cycles, K3_FP64_ALU_PER_ELT DFMA/DMUL/DADD at one per 2), over the measured launch time at the
         # sampled SM clock. Padding (d3 = 20 in 24-wide tiles) and the sweeps'
         # DFMAs are pipe time that frac, counted on algorithmic flops, leaves out.
         sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
-        pipe_cycles = 645 * 16 + 1690 * 2
-        roof["fp64_pipe"] = {"dmma_per_element": 645, "fp64_alu_per_element": 1690,
+        pipe_cycles = K3_DMMA_PER_ELT * 16 + K3_FP64_ALU_PER_ELT * 2
+        roof["fp64_pipe"] = {"dmma_per_element": K3_DMMA_PER_ELT, "fp64_alu_per_element": K3_FP64_ALU_PER_ELT,
                              "pipe_cycles_per_element": pipe_cycles,
                              "busy_frac": pipe_cycles * nelt / (c_sms(dev) * 4 * (k3_ms / 1e3) * sm_mhz * 1e6),
-                             "source": "profiles/r02c_ncu_k3v6_c2.txt (executed instruction counts)"}
+                             "source": "profiles/r02d_ncu_k3v6_c2.txt (executed instruction counts)"}
     # SURVEY §8(d) compulsory HBM bytes of the whole step (mesh + geometry for
     # build and for recover, coefficient samples when SAMPLED, C + Cf written,
     # lambda gathered, q + u written); caches and intermediates are not
