@@ -84,14 +84,14 @@ def c_sms(dev) -> int:
 def k3_flops(k: int) -> float:
     """Algorithmic fp64 flops per element of the condense kernel as executed
     (unpadded counts, symmetric products counted once). The
-    k = 2, 3 kernel (kernels_condense6.cuh) skips the rows of Chat_h that
+    k >= 2 kernels (kernels_condense6.cuh, kernels_condense5.cuh) skip the rows of Chat_h that
     vanish structurally (modes of top degree: only the first n1 = dim P_{k-1}
     rows are nonzero), so Y_h, R'_h and the S update are counted on those rows
     only (the count of the algorithm actually executed, never a
     larger one); its skipping of zero blocks inside those rows is not counted."""
     n = (k + 1) * (k + 2) * (k + 3) // 6
     m = 2 * (k + 1) * (k + 2)
-    n1 = k * (k + 1) * (k + 2) // 6 if k in (2, 3) else n   # nonzero rows of Chat_h
+    n1 = k * (k + 1) * (k + 2) // 6 if k >= 2 else n   # nonzero rows of Chat_h (k <= 1: the dense kernel)
     f = 0.0
     f += 2 * 2.0 * n ** 3                 # two Gauss-Jordan inverses (M, S)
     f += 2.0 * n * n * m                  # Zp = Mi W^T

@@ -100,11 +100,26 @@ std::vector<double> to_fragments(const std::vector<double>& A, int rows, int col
 }
 
 // K3 v6 (k = 2, 3) skips the 8 x 4 blocks of Chat_h that c6_ch_nz declares
-// structurally zero (rows of top-degree modes, the lower triangle): verify the
+// structurally zero (rows of top-degree modes, the lower triangle), K3 v5
+// (k = 4, 5) the zero row tiles and the ksteps below a row tile: verify the
 // claim on the tables actually built, entry by entry, and fail loudly if a
 // skipped block holds anything above rounding.
 void check_chat_pattern(const HostTables& h) {
   const int k = h.k, d3 = h.d3;
+  if (k >= 4) {  // kernels_condense5.cuh: rows >= dim P_{k-1} and, per 8-row tile, the columns below the tile
+    const int n1 = pdim3(k - 1);
+    double mx = 0.0;
+    for (int hh = 0; hh < 3; ++hh)
+      for (double v : h.Chat[hh]) mx = std::max(mx, std::fabs(v));
+    for (int hh = 0; hh < 3; ++hh)
+      for (int r = 0; r < d3; ++r)
+        for (int kk = 0; kk < d3; ++kk)
+          if ((r >= n1 || kk < 8 * (r / 8)) && std::fabs(h.Chat[hh][r + size_t(kk) * d3]) > 1e-13 * mx)
+            throw HdgError{HDG_ESTATE, "reference convection table Chat_" + std::to_string(hh) + " is not zero at (" +
+                                           std::to_string(r) + ", " + std::to_string(kk) +
+                                           "): the condensation kernel's sparsity pattern does not hold"};
+    return;
+  }
   if (k != 2 && k != 3) return;
   const int np = d3 / 8, ks = 2 * np + (d3 % 8 ? 1 : 0), nt3 = (d3 + 7) / 8;
   double mx = 0.0;

@@ -23,6 +23,10 @@
 // and a free product buffer (one barrier per pivot pair).
 #pragma once
 
+#ifndef HDG_C5_SPARSE  // skip the structurally zero row tiles / ksteps of Chat_h
+#define HDG_C5_SPARSE 1
+#endif
+
 #include "kernels_condense2.cuh"
 
 namespace hdgb {
@@ -324,6 +328,13 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   constexpr int NTF = face_tiles(D2);
   constexpr int NLP = (NTM / 2 + 1) * ((NTM + 1) / 2);  // C tile pairs (rows' pairs and singles)
   constexpr bool PAD = Dm::D34 != D3;                    // k-padding present (k = 4)
+  // Structural zeros of Chat_h (kernels_condense6.cuh; checked on the host by
+  // check_chat_pattern): rows >= dim P_{k-1} vanish and the rest is strictly
+  // upper triangular, Chat_h(r, k) = 0 for k <= r. Row tiles >= NT1 of Chat_h
+  // are skipped, and a row tile's ksteps start at its first row.
+  constexpr int N1 = HDG_C5_SPARSE ? cdim3(K_ - 1) : D3;
+  constexpr int NT1 = (N1 + 7) / 8;
+  constexpr int KSKIP = HDG_C5_SPARSE ? 2 : 0;           // ksteps below row tile nt: 2 * nt
   extern __shared__ double smem[];
   for (int i = threadIdx.x; i < Dm::TOTAL; i += NT) smem[i] = 0.0;
   __syncthreads();
@@ -357,7 +368,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   // (three row groups per column): the Chat fragment of a k-step (L1/L2)
   // feeds every row tile of the group
   constexpr int TSG = 3;                           // row groups per column strip
-  constexpr int NTS = MT * TSG;                    // T strip tasks
+  constexpr int NTS = NT1 * TSG;                   // T strip tasks (column tiles < NT1: the nonzero rows of Chat_h)
   auto t_strip = [&](double* Tb, int h, int task) {
     const int nt = task / TSG, part = task - nt * TSG;
     const int lo = part * MT / TSG, hi = (part + 1) * MT / TSG;
@@ -366,7 +377,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
     for (int u = 0; u < (MT + TSG - 1) / TSG; ++u) acc[u][0] = acc[u][1] = 0.0;
 #pragma unroll 2
-    for (int kk = 0; kk < KS; ++kk) {
+    for (int kk = KSKIP * nt; kk < KS; ++kk) {
       const int k = kk * 4 + t;
       const double b = chat(h, c, k);
 #pragma unroll
@@ -388,9 +399,9 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   // (rows split into chunks of <= 3 lower tiles): the combined Chat'_h
   // fragment (3 L1/L2 loads + FMAs) of a k-step feeds the whole chunk
   constexpr int SCH = 3;                           // lower tiles per S task at most
-  constexpr int NSS = [] {
+  constexpr int NSS = [] {                         // row tiles < NT1 only: Chat'_h vanishes below
     int n = 0;
-    for (int mt = 0; mt < MT; ++mt) n += (mt + SCH) / SCH;
+    for (int mt = 0; mt < NT1; ++mt) n += (mt + SCH) / SCH;
     return n;
   }();
   auto s_strip = [&](const double* Tb, int h, int task, bool first) {
@@ -404,7 +415,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
 #pragma unroll
     for (int u = 0; u < SCH; ++u) acc[u][0] = acc[u][1] = 0.0;
 #pragma unroll 2
-    for (int kk = 0; kk < KS; ++kk) {
+    for (int kk = KSKIP * mt; kk < KS; ++kk) {
       const int k = kk * 4 + t;
       const double a = g0 * chat(0, r, k) + g1 * chat(1, r, k) + g2 * chat(2, r, k);
 #pragma unroll
@@ -525,6 +536,15 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       if (task < NSS) s_strip(T0, 0, task, true);
       else t_strip(T1, 1, task - NSS);
     }
+    // rows >= 8 NT1 of S are D alone (Chat'_h vanishes there)
+    for (int idx = threadIdx.x; idx < (D3 - NT1 * 8) * D3; idx += NT) {
+      const int r = NT1 * 8 + idx / D3, c = idx - (idx / D3) * D3;
+      if (c <= r) {
+        const double v = Dp[sym_idx(r, c, D3)];
+        S[r + c * LD] = v;
+        S[c + r * LD] = v;
+      }
+    }
     __syncthreads();
     if (has_next) prefetch_packed(Dp, Dsym, Kn);  // the packed D of this element is dead
     for (int task = warp; task < NSS + NTS; task += NWT) {
@@ -532,7 +552,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
       else t_strip(T0, 2, task - NSS);
     }
     __syncthreads();
-    for (int task = warp; task < NSS + 4 * MT; task += NWT) {
+    for (int task = warp; task < NSS + 4 * NT1; task += NWT) {  // V: row tiles < NT1 (below, V keeps the staged T_l W_l^T)
       if (task < NSS) {
         s_strip(T0, 2, task, false);
       } else {  // V rows of row tile mt, face l
@@ -542,7 +562,7 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         const double b0 = beta[cl0], b1 = beta[MP + cl0], b2 = beta[2 * MP + cl0];
         double acc[NTF][2] = {};
 #pragma unroll 2
-        for (int kk = 0; kk < KS; ++kk) {
+        for (int kk = KSKIP * mt; kk < KS; ++kk) {
           const int k = kk * 4 + t;
           const double a = b0 * chat(0, r, k) + b1 * chat(1, r, k) + b2 * chat(2, r, k);
 #pragma unroll
