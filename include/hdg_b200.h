@@ -374,6 +374,14 @@ int hdg_b200_set_jit(hdg_ctx* ctx, int enabled);
 /* k = 1..3 recovery kernel: 3 = TMA-streamed cache records (default), 2 = one warp
  * per element with direct loads (equivalent; kept for comparison). */
 int hdg_b200_set_recover_variant(hdg_ctx* ctx, int variant);
+/* K3 (k >= 2) skips the operand blocks of the reference convection matrices
+ * Chat_# (element_matrices.cpp:117-122) that vanish structurally in the
+ * degree-graded orthonormal basis (rows of top-degree modes, the lower
+ * triangle). set_degree verifies the pattern on the tables it builds and
+ * otherwise (a tet rule too coarse for it) runs the dense kernel; this knob
+ * forces the dense kernel (enabled = 0) for comparison. Call after
+ * set_degree; returns the setting through *active if not NULL.            */
+int hdg_b200_set_chat_sparsity(hdg_ctx* ctx, int enabled, int* active);
 /* Singular elements. The condensation eliminates A1 by blocks (sweep
  * inverses of M and of its Schur complement S, no pivoting) and records their
  * extreme |pivots|. An element whose combined pivot ratio falls below

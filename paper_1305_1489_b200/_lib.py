@@ -116,6 +116,7 @@ _SIGS = {
     "hdg_b200_stage_times": (C.c_int, [P, DP]),
     "hdg_b200_set_jit": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_recover_variant": (C.c_int, [P, C.c_int]),
+    "hdg_b200_set_chat_sparsity": (C.c_int, [P, C.c_int, C.POINTER(C.c_int)]),
     "hdg_b200_set_bdm": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_tau_allow_zero": (C.c_int, [P, C.c_int]),
     "hdg_b200_set_rescue_screen": (C.c_int, [P, C.c_double]),

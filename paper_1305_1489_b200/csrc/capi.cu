@@ -80,6 +80,7 @@ void require(bool cond, int code, const std::string& msg) {
 // Device copy of one degree's tables (one allocation, offsets into it).
 struct TabSet {
   bool ready = false;
+  bool chat_sparse = false;  // Chat_h has the structural zeros K3 skips (check_chat_pattern)
   HostTables host;
   DevTab dev{};
   double* buf = nullptr;
@@ -101,30 +102,25 @@ std::vector<double> to_fragments(const std::vector<double>& A, int rows, int col
 
 // K3 v6 (k = 2, 3) skips the 8 x 4 blocks of Chat_h that c6_ch_nz declares
 // structurally zero (rows of top-degree modes, the lower triangle), K3 v5
-// (k = 4, 5) the zero row tiles and the ksteps below a row tile: verify the
-// claim on the tables actually built, entry by entry, and fail loudly if a
-// skipped block holds anything above rounding.
-void check_chat_pattern(const HostTables& h) {
+// (k = 4, 5) the zero row tiles and the ksteps below a row tile. The claim is
+// verified on the tables actually built, entry by entry; if a skipped block
+// holds anything above rounding (a quadrature rule too coarse to integrate
+// P_i d_h P_j exactly), the dense instantiation of the kernel runs instead.
+bool check_chat_pattern(const HostTables& h) {
   const int k = h.k, d3 = h.d3;
-  if (k >= 4) {  // kernels_condense5.cuh: rows >= dim P_{k-1} and, per 8-row tile, the columns below the tile
-    const int n1 = pdim3(k - 1);
-    double mx = 0.0;
-    for (int hh = 0; hh < 3; ++hh)
-      for (double v : h.Chat[hh]) mx = std::max(mx, std::fabs(v));
-    for (int hh = 0; hh < 3; ++hh)
-      for (int r = 0; r < d3; ++r)
-        for (int kk = 0; kk < d3; ++kk)
-          if ((r >= n1 || kk < 8 * (r / 8)) && std::fabs(h.Chat[hh][r + size_t(kk) * d3]) > 1e-13 * mx)
-            throw HdgError{HDG_ESTATE, "reference convection table Chat_" + std::to_string(hh) + " is not zero at (" +
-                                           std::to_string(r) + ", " + std::to_string(kk) +
-                                           "): the condensation kernel's sparsity pattern does not hold"};
-    return;
-  }
-  if (k != 2 && k != 3) return;
-  const int np = d3 / 8, ks = 2 * np + (d3 % 8 ? 1 : 0), nt3 = (d3 + 7) / 8;
+  if (k < 2) return false;
   double mx = 0.0;
   for (int hh = 0; hh < 3; ++hh)
     for (double v : h.Chat[hh]) mx = std::max(mx, std::fabs(v));
+  if (k >= 4) {  // kernels_condense5.cuh: rows >= dim P_{k-1} and, per 8-row tile, the columns below the tile
+    const int n1 = pdim3(k - 1);
+    for (int hh = 0; hh < 3; ++hh)
+      for (int r = 0; r < d3; ++r)
+        for (int kk = 0; kk < d3; ++kk)
+          if ((r >= n1 || kk < 8 * (r / 8)) && std::fabs(h.Chat[hh][r + size_t(kk) * d3]) > 1e-13 * mx) return false;
+    return true;
+  }
+  const int np = d3 / 8, ks = 2 * np + (d3 % 8 ? 1 : 0), nt3 = (d3 + 7) / 8;
   for (int hh = 0; hh < 3; ++hh)
     for (int tile = 0; tile < nt3; ++tile)
       for (int s = 0; s < ks; ++s) {
@@ -132,17 +128,16 @@ void check_chat_pattern(const HostTables& h) {
         for (int r = 8 * tile; r < std::min(8 * tile + 8, d3); ++r)
           for (int t = 0; t < 4; ++t) {
             const int kk = s < 2 * np ? (s >> 1) * 8 + 2 * t + (s & 1) : 8 * np + t;
-            if (kk < d3 && std::fabs(h.Chat[hh][r + size_t(kk) * d3]) > 1e-13 * mx)
-              throw HdgError{HDG_ESTATE, "reference convection table Chat_" + std::to_string(hh) + " is not zero at (" +
-                                             std::to_string(r) + ", " + std::to_string(kk) +
-                                             "): the condensation kernel's sparsity pattern does not hold"};
+            if (kk < d3 && std::fabs(h.Chat[hh][r + size_t(kk) * d3]) > 1e-13 * mx) return false;
           }
       }
+  return true;
 }
 
 void upload_tables(TabSet& ts, int k, int tet_deg, int tri_deg) {
   if (ts.buf) { cudaFree(ts.buf); ts.buf = nullptr; }
   ts.ready = false;
+  ts.chat_sparse = false;
   ts.host = build_host_tables(k, tet_deg, tri_deg);
   const HostTables& h = ts.host;
   const int d3 = h.d3, d2 = h.d2, nq = h.nq, nqd = h.nqd;
@@ -410,11 +405,21 @@ void launch_condense(hdg_ctx* c, int nelt, const GeoDev& geo, const double* Ms, 
 #endif
   if constexpr (K_ <= HDG_TEAM_MAXK)
     launch_condense_impl<C2Dims<K_>, C2Launch<K_>>(c, condense2_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
-  else if constexpr (K_ <= 3)
-    launch_condense_impl<C6Dims<K_>, C6Launch<K_>>(c, condense6_kernel<K_, C6Cfg<K_>::NW>, nelt, geo, Ms, Ds, fv,
-                                                   C, Cf, F, ps);
-  else
-    launch_condense_impl<C5Dims<K_>, C5Launch<K_>>(c, condense5_kernel<K_>, nelt, geo, Ms, Ds, fv, C, Cf, F, ps);
+  else if constexpr (K_ <= 3) {
+    if (c->tab[0].chat_sparse)
+      launch_condense_impl<C6Dims<K_>, C6Launch<K_>>(c, condense6_kernel<K_, C6Cfg<K_>::NW, true>, nelt, geo, Ms, Ds,
+                                                     fv, C, Cf, F, ps);
+    else
+      launch_condense_impl<C6Dims<K_>, C6Launch<K_>>(c, condense6_kernel<K_, C6Cfg<K_>::NW, false>, nelt, geo, Ms,
+                                                     Ds, fv, C, Cf, F, ps);
+  } else {
+    if (c->tab[0].chat_sparse)
+      launch_condense_impl<C5Dims<K_>, C5Launch<K_>>(c, condense5_kernel<K_, true>, nelt, geo, Ms, Ds, fv, C, Cf, F,
+                                                     ps);
+    else
+      launch_condense_impl<C5Dims<K_>, C5Launch<K_>>(c, condense5_kernel<K_, false>, nelt, geo, Ms, Ds, fv, C, Cf,
+                                                     F, ps);
+  }
 }
 
 // K3b: screen the pivot statistics, re-solve the flagged elements by the
@@ -998,7 +1003,7 @@ int hdg_b200_set_degree(hdg_ctx* c, int k, int tet_deg, int tri_deg) {
     require(k >= 0 && k <= 5, HDG_EINVAL, "degree must be in 0..5");
     set_device(c);
     upload_tables(c->tab[0], k, tet_deg, tri_deg);
-    check_chat_pattern(c->tab[0].host);
+    c->tab[0].chat_sparse = check_chat_pattern(c->tab[0].host);
     c->tri_deg = tri_deg;
     c->tab[1].ready = false;
     if (c->post_tet_deg >= 0) upload_tables(c->tab[1], k + 1, c->post_tet_deg, tri_deg);
@@ -1806,6 +1811,14 @@ int hdg_b200_set_recover_variant(hdg_ctx* c, int variant) {
   return guarded([&] {
     require(c != nullptr && (variant == 2 || variant == 3), HDG_EINVAL, "recover variant must be 2 or 3");
     c->recover_variant = variant;
+  });
+}
+
+int hdg_b200_set_chat_sparsity(hdg_ctx* c, int enabled, int* active) {
+  return guarded([&] {
+    require(c && c->tab[0].ready, HDG_ESTATE, "set_degree first");
+    c->tab[0].chat_sparse = enabled != 0 && check_chat_pattern(c->tab[0].host);
+    if (active) *active = c->tab[0].chat_sparse ? 1 : 0;
   });
 }
 

@@ -315,7 +315,7 @@ __device__ __forceinline__ void cta_block_inverse(double* X, double* Y, double& 
   __syncthreads();
 }
 
-template <int K_>
+template <int K_, bool SP = true>
 __global__ void __launch_bounds__(C5Cfg<K_>::NWT * 32, 1)
 condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
                  const double* __restrict__ Dsym, const double* __restrict__ fvec,
@@ -332,9 +332,9 @@ condense5_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   // check_chat_pattern): rows >= dim P_{k-1} vanish and the rest is strictly
   // upper triangular, Chat_h(r, k) = 0 for k <= r. Row tiles >= NT1 of Chat_h
   // are skipped, and a row tile's ksteps start at its first row.
-  constexpr int N1 = HDG_C5_SPARSE ? cdim3(K_ - 1) : D3;
+  constexpr int N1 = (HDG_C5_SPARSE && SP) ? cdim3(K_ - 1) : D3;
   constexpr int NT1 = (N1 + 7) / 8;
-  constexpr int KSKIP = HDG_C5_SPARSE ? 2 : 0;           // ksteps below row tile nt: 2 * nt
+  constexpr int KSKIP = (HDG_C5_SPARSE && SP) ? 2 : 0;           // ksteps below row tile nt: 2 * nt
   extern __shared__ double smem[];
   for (int i = threadIdx.x; i < Dm::TOTAL; i += NT) smem[i] = 0.0;
   __syncthreads();

@@ -186,7 +186,10 @@ __device__ __forceinline__ void c6_symfrag(const double* Q, int g, int t,
   }
 }
 
-template <int K_, int NW>
+// SP: the tables passed check_chat_pattern (capi.cu) and the zero blocks of
+// Chat_h are skipped; otherwise (a rule too coarse to integrate P_i d_h P_j
+// exactly) every block is contracted.
+template <int K_, int NW, bool SP = true>
 __global__ void __launch_bounds__(NW * 32, 1)
 condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Msym,
                  const double* __restrict__ Dsym, const double* __restrict__ fvec,
@@ -195,6 +198,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
   using Dm = C6Dims<K_>;
   constexpr int D3 = Dm::D3, D2 = Dm::D2, M = Dm::M, NSYM = Dm::NSYM, LT = Dm::LT, LQ = Dm::LQ, LS = Dm::LS;
   constexpr int KS = Dm::KS, NT3 = Dm::NT3, NTM = Dm::NTM;
+  constexpr int KSP = SP ? K_ : -1;  // degree handed to the block masks (-1: nothing skipped)
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -363,7 +367,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
     const double vol = DG[Dm::DG_VOL];
 #pragma unroll
     for (int i = 0; i < NT3; ++i) {
-      if (!c6_tile_nz(K_, i)) {
+      if (!c6_tile_nz(KSP, i)) {
         // Chat_h vanishes on these rows for every h: Y_h = R'_h = 0 there, so S
         // keeps D on the tile's rows and V^T[c][r] = T_l(c) W_l(c)[c'][r] on its columns
         const int r = 8 * i + g;
@@ -409,7 +413,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
         for (int h = 0; h < 3; ++h)
 #pragma unroll
           for (int n = 0; n < NT3; ++n)
-            if (c6_ch_nz(K_, h, i, s)) dmma(y[h][n][0], y[h][n][1], ca[h][s], mib[s][n]);
+            if (c6_ch_nz(KSP, h, i, s)) dmma(y[h][n][0], y[h][n][1], ca[h][s], mib[s][n]);
       // S row tiles j <= i: S = D + sum_h R'_h Chat_h^T
       {
         double ra[3][KS];
@@ -438,7 +442,7 @@ condense6_kernel(DevTab tab, int nelt, GeoDev geo, const double* __restrict__ Ms
             }
 #pragma unroll
             for (int s = 0; s < KS; ++s)
-              if (c6_ch_nz(K_, h, j, s)) dmma(sa[s & 1][0], sa[s & 1][1], ra[h][s], cb[s]);
+              if (c6_ch_nz(KSP, h, j, s)) dmma(sa[s & 1][0], sa[s & 1][1], ra[h][s], cb[s]);
           }
           // lower entries c <= r, mirrored: the sweep needs S exactly symmetric
           const int r = 8 * i + g;

@@ -345,6 +345,13 @@ class Engine:
         """BDM variant (bdm_blocks, local_solver.cpp:65-69): u truncated to P_{k-1}, tau ignored."""
         L.check(L.lib().hdg_b200_set_bdm(self._ctx, int(enabled)))
 
+    def set_chat_sparsity(self, enabled: bool) -> bool:
+        """K3 skips the structurally zero blocks of Chat_# (default, verified at set_degree);
+        False forces the dense kernel. Returns whether the sparse kernel will run."""
+        active = C.c_int(0)
+        L.check(L.lib().hdg_b200_set_chat_sparsity(self._ctx, int(bool(enabled)), C.byref(active)))
+        return bool(active.value)
+
     def set_recover_variant(self, variant: int) -> None:
         """k = 1..3 recovery kernel: 3 = TMA-streamed cache (default), 2 = direct loads."""
         L.check(L.lib().hdg_b200_set_recover_variant(self._ctx, int(variant)))

@@ -138,3 +138,32 @@ def test_full_size_properties_c2():
     assert abs(float(sysH.vals.sum()) - float(C.sum())) < 1e-12 * sum_abs
     Cf = cs.Cf_cols()
     assert abs(float(sysH.b.sum()) - float(Cf.sum())) < 1e-12 * float(Cf.abs().sum())
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+def test_chat_sparsity_kernels_agree(k):
+    """K3 with the structurally zero blocks of Chat_# skipped (default) against
+    the dense instantiation of the same kernel (hdg_b200_set_chat_sparsity 0)
+    and against the oracle, on a perturbed mesh with every perm code in play:
+    both within the parity tolerance, and within rounding of each other."""
+    n = 2 if k < 4 else 1
+    mesh = HostMesh.box(n, bc="dirichlet_x", perturb=0.1, seed=9)
+    em = oracle_mesh(mesh)
+    eng, dm, g, cs = gpu_pipeline(mesh, k, KAP, CC, FF)
+    assert eng.set_chat_sparsity(True) is True  # the tables have the pattern
+    d2 = dim2(k)
+    rng = np.random.default_rng(3)
+    uhat = torch.from_numpy(rng.standard_normal(dm.nfc * d2)).cuda()
+    ls = eng.recover(g, dm, cs, uhat)
+    sparse = [cs.C.clone(), cs.Cf.clone(), ls.u.clone(), ls.qx.clone()]
+    assert eng.set_chat_sparsity(False) is False
+    cs2 = eng.build_condense(g, KAP, CC, FF)
+    ls2 = eng.recover(g, dm, cs2, uhat)
+    dense = [cs2.C, cs2.Cf, ls2.u, ls2.qx]
+    for a, b in zip(sparse, dense):
+        assert float((a - b).abs().max()) <= 1e-12 * float(b.abs().max())
+    _, _, lb, C, Cf = oracle_condense(em, k, KAP, CC, FF, 1.0)
+    from oracle_util import max_slice_relerr
+    for got in (cs, cs2):
+        assert max_slice_relerr(np_(got.C_slices()), C) < 1e-10
+        assert max_slice_relerr(np_(got.Cf_cols()), Cf.T) < 1e-10

@@ -125,6 +125,52 @@ def test_tables_match_oracle(k):
             assert np.max(np.abs(W[6 * l + mu] - ref)) < 1e-13
 
 
+def _c6_ch_nz(k, h, tile, s):
+    """The condensation kernel's block mask (kernels_condense6.cuh, c6_ch_nz), restated."""
+    if k == 3:
+        if tile == 0:
+            return not (h == 0 and s == 0)
+        if tile == 1:
+            return s == 4 or (h == 2 and s == 3)
+        return False
+    if k == 2:
+        return tile == 0 and not (h == 0 and s == 0)
+    return True
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_chat_structural_zeros(k):
+    """The sparsity K3 relies on, on the reference's own tables (oracle) and on the
+    product's host tables: Chat_h[i][j] = (1/6) int P_i d_h P_j (element_matrices.cpp:
+    117-122) vanishes for i >= dim P_{k-1} and for j <= i; at k = 2, 3 every 8 x 4 operand
+    block the kernel skips (c6_ch_nz, kidx kstep order) is zero, and every block it keeps
+    is needed (the mask is tight)."""
+    qd = 2 * k + 2
+    t = core.tables(k, qd, qd)
+    d3 = t.d3
+    n1 = k * (k + 1) * (k + 2) // 6
+    ref = [(np.diag(t.tet_w) @ t.P).T @ Pd / 6 for Pd in (t.Px, t.Py, t.Pz)]
+    host = _host_table(k, qd, "Chat", 3 * d3 * d3).reshape(3, d3, d3).transpose(0, 2, 1)
+    for Ch in (ref, host):
+        mx = max(np.abs(c).max() for c in Ch)
+        for c in Ch:
+            assert np.abs(c[n1:, :]).max(initial=0.0) < 1e-13 * mx
+            assert np.abs(np.tril(c)).max() < 1e-13 * mx
+            # K3 v5 (k = 4, 5): a row tile's columns below its first row
+            for tile in range((d3 + 7) // 8):
+                assert np.abs(c[8 * tile:8 * tile + 8, :8 * tile]).max(initial=0.0) < 1e-13 * mx
+        if k in (2, 3):
+            npair = d3 // 8
+            ks = 2 * npair + (1 if d3 % 8 else 0)
+            for h, c in enumerate(Ch):
+                for tile in range((d3 + 7) // 8):
+                    for s in range(ks):
+                        cols = [(s >> 1) * 8 + 2 * tt + (s & 1) if s < 2 * npair else 8 * npair + tt for tt in range(4)]
+                        cols = [q for q in cols if q < d3]
+                        blk = np.abs(c[8 * tile:min(8 * tile + 8, d3)][:, cols]).max(initial=0.0)
+                        assert (blk > 1e-13 * mx) == _c6_ch_nz(k, h, tile, s), (h, tile, s, blk)
+
+
 def test_field_compiler_roundtrip():
     for expr in ("1 + 0.5*sin(2*pi*x)*cos(2*pi*y)", "exp(x + y)*sin(pi*z)",
                  "(1 + 0.25*sin(2*pi*x)*sin(2*pi*y))*(100 - 99*lt(z, 0.5))", "x**2 - abs(y)/sqrt(2 + z)"):
