@@ -1,5 +1,6 @@
 """Every element of the bench configuration C2 (k = 3, 32^3 Kuhn box,
-196,608 tets) against the oracle's reference path, streamed over
+196,608 tets) and of C4 (k = 2, 48^3, upwind tau; C3 and C5 on request)
+against the oracle's reference path, streamed over
 16,384-element ranges of the full mesh (oracle.core.pipeline_range on all
 host cores): C, Cf, and q, u recovered from the same lambda, within the
 1e-10 contract; the pivot screen rescues nothing on this healthy mesh."""
@@ -24,7 +25,12 @@ def _rel(got, want):
     return np.linalg.norm(got - want, axis=1) / np.maximum(np.linalg.norm(want, axis=1), 1e-300)
 
 
-@pytest.mark.parametrize("cfg_name", ["C2"])
+# C2 and C4 always; HDG_FULLSIZE_CONFIGS=C3,C5 adds the other BASELINE meshes (about a minute of oracle
+# time each on 16 cores; profiles/r02e_fullsize_parity.txt holds a run of all of them)
+_CONFIGS = ["C2", "C4"] + [c for c in os.environ.get("HDG_FULLSIZE_CONFIGS", "").split(",") if c in ("C3", "C5")]
+
+
+@pytest.mark.parametrize("cfg_name", _CONFIGS)
 def test_every_element_matches_oracle(cfg_name):
     cfg = CONFIGS[cfg_name]
     prob = cfg.problem
@@ -34,6 +40,9 @@ def test_every_element_matches_oracle(cfg_name):
     eng.set_degree(k)
     dm = eng.upload(mesh)
     g = eng.geometry(dm, cfg.tau)
+    tau_dev = eng.upwind_tau(g, cfg.upwind_beta) if cfg.upwind_beta else None   # C4: tau = 1 + |beta . nu|
+    if tau_dev is not None:
+        g = eng.geometry(dm, tau_dev)
     cs = eng.build_condense(g, prob.kappa, prob.c, prob.f)
     assert eng.rescued_elements() == 0
     d2 = dim2(k)
@@ -42,7 +51,8 @@ def test_every_element_matches_oracle(cfg_name):
     torch.cuda.synchronize()
     em = oracle_mesh(mesh)
     t = core.tables(k, 2 * k + 2, 2 * k + 2)
-    tau = core.Stabilization(np.full((em.n_elements, 4), float(cfg.tau)))
+    tau = core.Stabilization(np.asfortranarray(np_(tau_dev).T) if tau_dev is not None
+                             else np.full((em.n_elements, 4), float(cfg.tau)))
     kap, c, f = field(prob.kappa), field(prob.c), field(prob.f)
     lam = np.asfortranarray(core.gather_traces(em, d2, np_(uhat)))
     nelt, chunk = dm.nelt, 16384
