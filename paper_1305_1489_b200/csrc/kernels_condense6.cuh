@@ -46,7 +46,15 @@ struct C6Dims {
   // d3 <= 16 (k = 2): S^-1 of an element and M^-1 of the warp's next element
   // as one sweep on the two 16-lane halves (gj_sweep_seg)
   static constexpr bool PAIR = D3 <= 16;
-  static constexpr int LT = 24;  // row stride of the k-fastest operands (Chat, W, V^T)
+#ifndef HDG_C6_LT3
+#define HDG_C6_LT3 20
+#endif
+#ifndef HDG_C6_LT2
+#define HDG_C6_LT2 24
+#endif
+  // row stride of the k-fastest operands (Chat, W, V^T): the fragments read columns < 8 NP + 4 only
+  static constexpr int LT = K_ == 3 ? HDG_C6_LT3 : HDG_C6_LT2;
+  static_assert(LT % 2 == 0 && LT >= 8 * (D3 / 8) + (D3 % 8 ? 4 : 0), "row stride covers every kstep");
   static constexpr int LQ = K_ == 3 ? 26 : 14;  // Mi / Si storage: (row i, column c) at i * LQ + c
   static constexpr int LS = K_ == 3 ? 24 : 12;  // S storage for the sweep (row-major)
   static constexpr int CH_SZ = NT3 * 8 * LT, WT_SZ = D2 * LT;
