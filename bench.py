@@ -70,7 +70,7 @@ def load_peaks():
 
 
 # executed fp64 instructions per element of condense6_kernel<3> (ncu instruction
-# counts of the committed capture profiles/r02e_ncu_k3v6_c2.txt)
+# counts of the committed capture profiles/r02f_ncu_k3v6_c2.txt)
 K3_DMMA_PER_ELT = 466
 K3_FP64_ALU_PER_ELT = 1564
 
@@ -697,7 +697,7 @@ def run_ours(args):
         roof["fp64_pipe"] = {"dmma_per_element": K3_DMMA_PER_ELT, "fp64_alu_per_element": K3_FP64_ALU_PER_ELT,
                              "pipe_cycles_per_element": pipe_cycles,
                              "busy_frac": pipe_cycles * nelt / (c_sms(dev) * 4 * (k3_ms / 1e3) * sm_mhz * 1e6),
-                             "source": "profiles/r02e_ncu_k3v6_c2.txt (executed instruction counts)"}
+                             "source": "profiles/r02f_ncu_k3v6_c2.txt (executed instruction counts)"}
     # SURVEY §8(d) compulsory HBM bytes of the whole step (mesh + geometry for
     # build and for recover, coefficient samples when SAMPLED, C + Cf written,
     # lambda gathered, q + u written); caches and intermediates are not

@@ -28,8 +28,8 @@
 // from the lane's own registers; the d3 remainder (the last 4 of d3 = 20,
 // the last 2 of d3 = 10, zero-padded) as one natural kstep k = 8n + t
 // gathered by two shuffles. The other operand is read in the same order from
-// a k-fastest table (row stride 24: one 16-byte load gives a tile's two
-// ksteps, conflict-free).
+// a k-fastest table (row stride LT = 20 at k = 3, 24 at k = 2, measured: one
+// 16-byte load gives a tile's two ksteps).
 #pragma once
 
 #include "kernels_condense2.cuh"

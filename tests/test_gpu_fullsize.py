@@ -26,7 +26,7 @@ def _rel(got, want):
 
 
 # C2 and C4 always; HDG_FULLSIZE_CONFIGS=C3,C5 adds the other BASELINE meshes (about a minute of oracle
-# time each on 16 cores; profiles/r02e_fullsize_parity.txt holds a run of all of them)
+# time each on 16 cores; profiles/r02f_fullsize_parity.txt holds a run of all of them)
 _CONFIGS = ["C2", "C4"] + [c for c in os.environ.get("HDG_FULLSIZE_CONFIGS", "").split(",") if c in ("C3", "C5")]
 
 
